@@ -1,0 +1,274 @@
+"""fp64 CPU oracle for the MRFMap hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package.  It shares no code with paper_2006_03512_b200 (the
+CUDA path) and the product never imports it.  The arithmetic lives in
+mrf_oracle.c (plain C, fp64, no FMA contraction); this module only marshals
+numpy arrays to it and assembles the per-frame CSR in canonical order
+(frame add order, pixel index v*W+u, position along the ray).
+
+Every function cites the SURVEY §8(c) step (B1..B7) / PAPER.md lines it follows;
+the pins that tie it to the paper are in tests/test_oracle_*.py.  Parity status:
+  B1 ray setup, B2 DDA, B3 offsets/LUT, B5 single-ray messages, B5+B6 on tree
+  graphs: pinned.  B5+B6 on loopy graphs (several overlapping rays): parity
+  unpinned beyond the invariants (loopy BP has no closed form).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "mrf_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+STATUS_KEPT, STATUS_INVALID, STATUS_DROPPED, STATUS_OTHER_RANK = 0, 1, 2, 3
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-O2 -ffp-contract=off -fopenmp)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math",
+                               "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _P(t):
+    return ctypes.POINTER(t)
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            i32p, i64p, dp, fp = _P(ctypes.c_int32), _P(ctypes.c_int64), _P(ctypes.c_double), _P(ctypes.c_float)
+            i16p, i8p = _P(ctypes.c_int16), _P(ctypes.c_int8)
+            i32, i64, d = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+            L.orc_ray_setup.argtypes = [i32p, dp, dp, dp, dp, i32, i32, ctypes.c_float, i64p, i64p, dp, dp]
+            L.orc_ray_setup.restype = ctypes.c_int
+            L.orc_dda.argtypes = [i32p, i64p, i64p, d, d, i32p, i16p, dp, dp, i64]
+            L.orc_dda.restype = i64
+            L.orc_log_nu.argtypes = [fp, i32, i32, dp, d, i32]
+            L.orc_log_nu.restype = d
+            L.orc_ray_messages.argtypes = [i64, dp, dp, dp, dp, dp]
+            L.orc_ray_messages.restype = None
+            L.orc_ray_pass.argtypes = [i64, i64p, i32p, i16p, dp, fp, i32, i32, dp, d, dp, dp]
+            L.orc_ray_pass.restype = None
+            L.orc_accumulate.argtypes = [i64, i32p, dp, i64, dp]
+            L.orc_accumulate.restype = None
+            L.orc_bp.argtypes = [i64, i64p, i32p, i16p, dp, fp, i32, i32, dp, d, i64, i32, dp, dp]
+            L.orc_bp.restype = None
+            L.orc_marginals.argtypes = [i64, d, dp, dp]
+            L.orc_marginals.restype = None
+            L.orc_frame_count.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32, i8p, i64p, dp, dp]
+            L.orc_frame_count.restype = None
+            L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p]
+            L.orc_frame_fill.restype = None
+            _lib = L
+    return _lib
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+class Params:
+    """Grid + noise model, as plain arrays for the C entry points."""
+
+    def __init__(self, dims, res, origin, prior, log_nu, z_lo, z_hi, off_lo, off_hi,
+                 margin_min, margin_k, sigma_c):
+        self.dims = _c(dims, np.int32)
+        self.geo = _c([res, origin[0], origin[1], origin[2]], np.float64)
+        self.par = _c([z_lo, z_hi, off_lo, off_hi, margin_min, margin_k,
+                       sigma_c[0], sigma_c[1], sigma_c[2]], np.float64)
+        self.lut = _c(log_nu, np.float32)
+        self.prior = float(prior)
+        self.L0 = math.log(prior / (1.0 - prior))  # prior log-odds of Eq.2
+        self.V = int(np.prod(self.dims.astype(np.int64)))
+
+    @classmethod
+    def from_workload(cls, w):
+        return cls(w.dims, w.res, w.origin, w.prior, w.log_nu, w.z_lo, w.z_hi, w.off_lo, w.off_hi,
+                   w.margin_min, w.margin_k, w.sigma_c)
+
+
+# --------------------------------------------------------------------------- B1..B3
+
+def ray_setup(p: Params, K, T_wc, u, v, z):
+    """B1 for one pixel -> (status, G0[3], G1[3], Z, L)."""
+    G0 = np.zeros(3, np.int64)
+    G1 = np.zeros(3, np.int64)
+    Z = ctypes.c_double(0.0)
+    L = ctypes.c_double(0.0)
+    K = _c(K, np.float64)
+    T = _c(T_wc, np.float64)
+    s = lib().orc_ray_setup(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double),
+                            _ptr(p.par, ctypes.c_double), _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double),
+                            int(u), int(v), float(z), _ptr(G0, ctypes.c_int64), _ptr(G1, ctypes.c_int64),
+                            ctypes.byref(Z), ctypes.byref(L))
+    return s, G0, G1, Z.value, L.value
+
+
+def dda(dims, G0, G1, Z=0.0, L=1.0):
+    """B2+B3 for one fixed-point segment -> (vid, off_q, t_in, t_out)."""
+    dims = _c(dims, np.int32)
+    G0 = _c(G0, np.int64)
+    G1 = _c(G1, np.int64)
+    L_ = lib()
+    n = L_.orc_dda(_ptr(dims, ctypes.c_int32), _ptr(G0, ctypes.c_int64), _ptr(G1, ctypes.c_int64),
+                   float(Z), float(L), None, None, None, None, 0)
+    vid = np.zeros(n, np.int32)
+    off = np.zeros(n, np.int16)
+    tin = np.zeros(n, np.float64)
+    tout = np.zeros(n, np.float64)
+    L_.orc_dda(_ptr(dims, ctypes.c_int32), _ptr(G0, ctypes.c_int64), _ptr(G1, ctypes.c_int64),
+               float(Z), float(L), _ptr(vid, ctypes.c_int32), _ptr(off, ctypes.c_int16),
+               _ptr(tin, ctypes.c_double), _ptr(tout, ctypes.c_double), n)
+    return vid, off, tin, tout
+
+
+def log_nu(p: Params, Z, off_q):
+    return lib().orc_log_nu(_ptr(p.lut, ctypes.c_float), p.lut.shape[0], p.lut.shape[1],
+                            _ptr(p.par, ctypes.c_double), float(Z), int(off_q))
+
+
+# --------------------------------------------------------------------------- graph
+
+class Graph:
+    """Canonical-order CSR of one rank's rays: row_ptr over kept rays, vid, off_q,
+    plus per-ray range Z and the flat pixel id (frame, v*W+u)."""
+
+    def __init__(self, row_ptr, vid, off_q, Z, frame, pixel, n_invalid, n_dropped):
+        self.row_ptr, self.vid, self.off_q, self.Z = row_ptr, vid, off_q, Z
+        self.frame, self.pixel = frame, pixel
+        self.n_invalid, self.n_dropped = n_invalid, n_dropped
+
+    @property
+    def n_rays(self):
+        return len(self.row_ptr) - 1
+
+    @property
+    def E(self):
+        return int(self.row_ptr[-1])
+
+
+def build_graph(p: Params, frames, rank: int = 0, world: int = 1) -> Graph:
+    """B1-B3 over every frame; keeps pixels of rows v % world == rank."""
+    L_ = lib()
+    parts = []
+    total = 0
+    n_inv = n_drop = 0
+    for fi, fr in enumerate(frames):
+        H, W = fr.depth.shape
+        depth = _c(fr.depth, np.float32)
+        K = _c(fr.K, np.float64)
+        T = _c(fr.T_wc, np.float64)
+        status = np.zeros(H * W, np.int8)
+        count = np.zeros(H * W, np.int64)
+        Z = np.zeros(H * W, np.float64)
+        Lr = np.zeros(H * W, np.float64)
+        L_.orc_frame_count(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
+                           _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
+                           rank, world, _ptr(status, ctypes.c_int8), _ptr(count, ctypes.c_int64),
+                           _ptr(Z, ctypes.c_double), _ptr(Lr, ctypes.c_double))
+        kept = np.nonzero(status == STATUS_KEPT)[0]
+        n_inv += int(np.sum(status == STATUS_INVALID))
+        n_drop += int(np.sum(status == STATUS_DROPPED))
+        parts.append((fi, depth, K, T, W, H, kept, count[kept], Z[kept]))
+        total += int(count[kept].sum())
+    vid = np.zeros(total, np.int32)
+    off_q = np.zeros(total, np.int16)
+    row_ptr = [np.zeros(1, np.int64)]
+    Zs, fids, pix = [], [], []
+    base = 0
+    for fi, depth, K, T, W, H, kept, cnt, Z in parts:
+        offs = np.full(H * W, -1, np.int64)
+        starts = base + np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64) if len(cnt) else np.zeros(0, np.int64)
+        offs[kept] = starts
+        L_.orc_frame_fill(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
+                          _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
+                          _ptr(offs, ctypes.c_int64), _ptr(vid, ctypes.c_int32), _ptr(off_q, ctypes.c_int16))
+        row_ptr.append(base + np.cumsum(cnt).astype(np.int64))
+        base += int(cnt.sum())
+        Zs.append(Z)
+        fids.append(np.full(len(kept), fi, np.int32))
+        pix.append(kept.astype(np.int64))
+    return Graph(np.concatenate(row_ptr), vid, off_q, np.concatenate(Zs) if Zs else np.zeros(0),
+                 np.concatenate(fids) if fids else np.zeros(0, np.int32),
+                 np.concatenate(pix) if pix else np.zeros(0, np.int64), n_inv, n_drop)
+
+
+# --------------------------------------------------------------------------- B4..B6
+
+def ray_messages(c, lnu):
+    """B5 core for one ray: (lpos, lneg) = log of Eq.13 / Eq.14 messages."""
+    c = _c(c, np.float64)
+    lnu = _c(lnu, np.float64)
+    n = len(c)
+    lpos = np.zeros(n)
+    lneg = np.zeros(n)
+    work = np.zeros(5 * max(n, 1))
+    lib().orc_ray_messages(n, _ptr(c, ctypes.c_double), _ptr(lnu, ctypes.c_double), _ptr(lpos, ctypes.c_double),
+                           _ptr(lneg, ctypes.c_double), _ptr(work, ctypes.c_double))
+    return lpos, lneg
+
+
+def ray_pass(p: Params, g: Graph, T, lam):
+    """One flooding pass (B5) in place on lam (float64[E]) from snapshot T (float64[V])."""
+    T = _c(T, np.float64)
+    assert lam.dtype == np.float64 and lam.flags.c_contiguous
+    lib().orc_ray_pass(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
+                       _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
+                       _ptr(p.lut, ctypes.c_float), p.lut.shape[0], p.lut.shape[1], _ptr(p.par, ctypes.c_double),
+                       p.L0, _ptr(T, ctypes.c_double), _ptr(lam, ctypes.c_double))
+    return lam
+
+
+def accumulate(p: Params, g: Graph, lam):
+    T = np.zeros(p.V)
+    lib().orc_accumulate(g.E, _ptr(g.vid, ctypes.c_int32), _ptr(_c(lam, np.float64), ctypes.c_double),
+                         p.V, _ptr(T, ctypes.c_double))
+    return T
+
+
+def bp(p: Params, g: Graph, n_iter: int, lam=None):
+    """B4 (lam = 0) + n flooding iterations (B5, B7) -> (lam, T)."""
+    lam = np.zeros(g.E) if lam is None else _c(lam, np.float64).copy()
+    T = np.zeros(p.V)
+    lib().orc_bp(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
+                 _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
+                 _ptr(p.lut, ctypes.c_float), p.lut.shape[0], p.lut.shape[1], _ptr(p.par, ctypes.c_double),
+                 p.L0, p.V, int(n_iter), _ptr(lam, ctypes.c_double), _ptr(T, ctypes.c_double))
+    return lam, T
+
+
+def marginals(p: Params, T):
+    """B6: p_v = sigma(L0 + T_v) (Eq.8)."""
+    T = _c(T, np.float64)
+    out = np.zeros(len(T))
+    lib().orc_marginals(len(T), p.L0, _ptr(T, ctypes.c_double), _ptr(out, ctypes.c_double))
+    return out
+
+
+def run(workload, n_iter=None, rank=0, world=1):
+    """Convenience: graph + BP + marginals for a synth.Workload."""
+    p = Params.from_workload(workload)
+    g = build_graph(p, workload.frames, rank, world)
+    lam, T = bp(p, g, workload.n_iter if n_iter is None else n_iter)
+    return p, g, lam, T, marginals(p, T)

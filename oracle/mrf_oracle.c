@@ -1,0 +1,319 @@
+/*
+ * mrf_oracle.c -- plain, slow, fp64 CPU oracle for the MRFMap hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or helper with the CUDA path (paper_2006_03512_b200/csrc) and is
+ * written from PAPER.md and the readings listed in DESIGN.md ("Readings").
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; B1..B7 = the oracle steps
+ * of SURVEY.md §8(c), restated in DESIGN.md.  Build:
+ *     gcc -O2 -ffp-contract=off -fopenmp -shared -fPIC  (no FMA contraction, so the
+ *     fp64 ray setup rounds exactly as written, op by op)
+ *
+ * Functions and their pins (tests/test_oracle_*.py):
+ *   orc_ray_setup   B1 pixel -> fixed-point segment        pinned: closed-form rays, round trip
+ *   orc_dda         B2 fixed-point 3D-DDA (+B3 offsets)    pinned: exact rational brute force
+ *   orc_log_nu      B3 bilinear LUT lookup                 pinned: bin centres / edge clamp
+ *   orc_ray_messages B5 single-ray messages (Eq.13/14)     pinned: 2^N enumeration of Eq.12
+ *   orc_ray_pass + orc_accumulate  B5 flooding iteration   pinned: exact marginals on trees
+ *   orc_marginals   B6 (Eq.8)                              pinned: unseen voxel = prior
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define FIX_ONE 65536LL /* 16 fractional bits of the fixed-point grid coordinates (B1) */
+
+/* ------------------------------------------------------------------ B1: pixel -> segment */
+/* par[9] = {z_lo, z_hi, off_lo, off_hi, margin_min, margin_k, c0, c1, c2}
+ * geo[4] = {res, ox, oy, oz}.  Returns 0 = ray kept, 1 = invalid pixel, 2 = dropped
+ * (measured point outside the grid, reading R11). */
+int orc_ray_setup(const int32_t dims[3], const double geo[4], const double par[9],
+                  const double K[4], const double Twc[12], int32_t u, int32_t v, float zf,
+                  int64_t G0[3], int64_t G1[3], double* Z_out, double* L_out) {
+    const double z = (double)zf;
+    if (!isfinite(z) || !(z > 0.0)) return 1;
+    const double xc = ((double)u - K[2]) / K[0];
+    const double yc = ((double)v - K[3]) / K[1];
+    const double rho = sqrt((xc * xc + yc * yc) + 1.0);
+    const double Z = z * rho;                                 /* range along the ray */
+    const double sZ = (par[6] + par[7] * Z) + (par[8] * Z) * Z; /* sigma(Z) */
+    double m = par[5] * sZ;                                   /* 3 sigma beyond the depth */
+    if (m < par[4]) m = par[4];
+    const double L = Z + m;
+    const double res = geo[0];
+    for (int k = 0; k < 3; ++k) {
+        const double Ck = Twc[4 * k + 3];
+        const double Dk = (Twc[4 * k + 0] * xc + Twc[4 * k + 1] * yc) + Twc[4 * k + 2];
+        const double pk = ((Ck + z * Dk) - geo[1 + k]) / res; /* measured point, grid units */
+        if (pk < 0.0 || pk >= (double)dims[k]) return 2;
+        const double Ek = Ck + (L / rho) * Dk;
+        const double g0 = (Ck - geo[1 + k]) / res;
+        const double g1 = (Ek - geo[1 + k]) / res;
+        G0[k] = llrint(g0 * 65536.0); /* round half to even (default rounding mode) */
+        G1[k] = llrint(g1 * 65536.0);
+    }
+    *Z_out = Z;
+    *L_out = L;
+    return 0;
+}
+
+/* ------------------------------------------------------------------ B2 + B3: fixed-point DDA */
+static int64_t floor_div(int64_t a, int64_t b) { /* b > 0 */
+    int64_t q = a / b;
+    if ((a % b) != 0 && a < 0) q -= 1;
+    return q;
+}
+
+/* Walk the segment G0 -> G1 (grid units x 65536) and emit, in order, every cell whose
+ * intersection with the segment has positive length ("standard 3DDA",
+ * Amanatides-Woo; tie rule of reading R13).  For each emitted cell: vid = x + nx(y + ny z),
+ * and off_q = clamp(llrint((0.5 (t_in + t_out) L - Z) * 32768), +-32767) (B3, reading R6).
+ * Pointers may be NULL (count only).  Returns the number of cells (all of them, even
+ * beyond cap; only the first cap are written). */
+int64_t orc_dda(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3], double Z, double L,
+                int32_t* vid, int16_t* off_q, double* t_in_out, double* t_out_out, int64_t cap) {
+    int64_t c[3], num[3], den[3];
+    int step[3];
+    for (int k = 0; k < 3; ++k) {
+        const int64_t dG = G1[k] - G0[k];
+        c[k] = floor_div(G0[k], FIX_ONE);
+        if (dG < 0 && G0[k] == c[k] * FIX_ONE) c[k] -= 1; /* cell containing t = 0+ */
+        if (dG > 0) {
+            step[k] = 1;
+            num[k] = (c[k] + 1) * FIX_ONE - G0[k];
+            den[k] = dG;
+        } else if (dG < 0) {
+            step[k] = -1;
+            num[k] = G0[k] - c[k] * FIX_ONE;
+            den[k] = -dG;
+        } else {
+            step[k] = 0;
+            num[k] = 0;
+            den[k] = 1;
+        }
+    }
+    int64_t n = 0;
+    double t_in = 0.0;
+    for (;;) {
+        int inside = 1;
+        for (int k = 0; k < 3; ++k)
+            if (c[k] < 0 || c[k] >= dims[k]) inside = 0;
+        if (!inside) break; /* grid exit */
+        /* smallest next crossing, by exact cross-multiplication */
+        int amin = -1;
+        for (int k = 0; k < 3; ++k) {
+            if (step[k] == 0) continue;
+            if (amin < 0 || num[k] * den[amin] < num[amin] * den[k]) amin = k;
+        }
+        const int last = (amin < 0) || (num[amin] >= den[amin]);
+        const double t_out = last ? 1.0 : (double)num[amin] / (double)den[amin];
+        if (n < cap) {
+            if (vid) vid[n] = (int32_t)(c[0] + (int64_t)dims[0] * (c[1] + (int64_t)dims[1] * c[2]));
+            if (off_q) {
+                const double d_mid = (0.5 * (t_in + t_out)) * L;
+                const double delta = d_mid - Z;
+                long long q = llrint(delta * 32768.0);
+                if (q > 32767) q = 32767;
+                if (q < -32767) q = -32767;
+                off_q[n] = (int16_t)q;
+            }
+            if (t_in_out) t_in_out[n] = t_in;
+            if (t_out_out) t_out_out[n] = t_out;
+        }
+        ++n;
+        if (last) break;
+        const int64_t na = num[amin], da = den[amin];
+        for (int k = 0; k < 3; ++k) { /* step every axis tied at t_min, simultaneously */
+            if (step[k] == 0) continue;
+            if (num[k] * da == na * den[k]) {
+                c[k] += step[k];
+                num[k] += FIX_ONE;
+            }
+        }
+        t_in = t_out;
+    }
+    return n;
+}
+
+/* ------------------------------------------------------------------ B3: log nu lookup */
+/* Bilinear interpolation of log nu at (Z, off_q / 32768) over bin centres, with the
+ * coordinates clamped to the edge centres (reading R6/R9). */
+double orc_log_nu(const float* lut, int32_t n_z, int32_t n_off, const double par[9], double Z,
+                  int32_t off_q) {
+    const double off = (double)off_q / 32768.0;
+    double fz = (Z - par[0]) / (par[1] - par[0]) * (double)n_z - 0.5;
+    double fo = (off - par[2]) / (par[3] - par[2]) * (double)n_off - 0.5;
+    if (fz < 0.0) fz = 0.0;
+    if (fz > (double)(n_z - 1)) fz = (double)(n_z - 1);
+    if (fo < 0.0) fo = 0.0;
+    if (fo > (double)(n_off - 1)) fo = (double)(n_off - 1);
+    int iz = (int)floor(fz), io = (int)floor(fo);
+    if (iz > n_z - 2) iz = n_z - 2;
+    if (io > n_off - 2) io = n_off - 2;
+    const double wz = fz - iz, wo = fo - io;
+    const double a = lut[(int64_t)iz * n_off + io], b = lut[(int64_t)iz * n_off + io + 1];
+    const double cc = lut[(int64_t)(iz + 1) * n_off + io], d = lut[(int64_t)(iz + 1) * n_off + io + 1];
+    return (1.0 - wz) * ((1.0 - wo) * a + wo * b) + wz * ((1.0 - wo) * cc + wo * d);
+}
+
+/* ------------------------------------------------------------------ B5: one ray */
+static double softplus(double x) { return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
+
+static double lse(double a, double b) {
+    if (a == -INFINITY) return b;
+    if (b == -INFINITY) return a;
+    const double m = a > b ? a : b;
+    return m + log1p(exp(-fabs(a - b)));
+}
+
+/* Factor->occupancy messages of one ray, in the log domain.
+ * Input: cavity log-odds c[i] (voxel->factor message, Eq.6) and log nu[i].
+ * Output: lpos[i] = log mu_{psi->o_i}(1) (Eq.13) and
+ *         lneg[i] = log mu_{psi->o_i}(0) (Eq.14 in the division-free form of P:524),
+ * both relative to the normalised incoming messages mu(o_k) = sigma(+-c_k).
+ *   lV_i = sum_{k<i} log mu(o_k=0)                          (prod_{k<i} mu(o_k=0))
+ *   lP_i = lse_{j<i} [log mu(o_j=1) + log nu_j + lV_j]      (first sums of Eq.13/14)
+ *   lR_i = lse_{j>i} [log mu(o_j=1) + log nu_j + sum_{i<k<j} log mu(o_k=0)]
+ *        (suffix recurrence lR_{i-1} = lse(lb_i + lnu_i, la_i + lR_i); V_i R_i is the
+ *         second term of P:524)
+ *   lpos_i = lse(lP_i, lV_i + lnu_i),  lneg_i = lse(lP_i, lV_i + lR_i). */
+void orc_ray_messages(int64_t N, const double* c, const double* lnu, double* lpos, double* lneg,
+                      double* work /* 5N doubles */) {
+    double* la = work;
+    double* lb = work + N;
+    double* lV = work + 2 * N;
+    double* lP = work + 3 * N;
+    double* lR = work + 4 * N;
+    for (int64_t i = 0; i < N; ++i) {
+        la[i] = -softplus(c[i]);  /* log sigma(-c) = log mu(o_i = 0) */
+        lb[i] = -softplus(-c[i]); /* log sigma(+c) = log mu(o_i = 1) */
+    }
+    if (N == 0) return;
+    lV[0] = 0.0;
+    lP[0] = -INFINITY;
+    for (int64_t i = 0; i + 1 < N; ++i) {
+        lV[i + 1] = lV[i] + la[i];
+        lP[i + 1] = lse(lP[i], lb[i] + lnu[i] + lV[i]);
+    }
+    lR[N - 1] = -INFINITY;
+    for (int64_t i = N - 1; i >= 1; --i) lR[i - 1] = lse(lb[i] + lnu[i], la[i] + lR[i]);
+    for (int64_t i = 0; i < N; ++i) {
+        lpos[i] = lse(lP[i], lV[i] + lnu[i]);
+        lneg[i] = lse(lP[i], lV[i] + lR[i]);
+    }
+}
+
+static double clip256(double x) {
+    if (!(x < 256.0)) return 256.0; /* also lneg = -inf (N = 1) */
+    if (x < -256.0) return -256.0;
+    return x;
+}
+
+/* One flooding pass over all rays from the same snapshot T (reading R4):
+ * c_e = L0 + T[v_e] - lambda_e (Eq.6 excluding the ray's own message),
+ * lambda_e <- clip(lpos - lneg, +-256) (reading R9).  lambda is updated in place (each
+ * ray reads only its own old messages).  Z_ray[r] is the ray's measured range. */
+void orc_ray_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
+                  const double* Z_ray, const float* lut, int32_t n_z, int32_t n_off, const double par[9],
+                  double L0, const double* T, double* lambda) {
+#pragma omp parallel
+    {
+        int64_t cap = 0;
+        double* buf = NULL;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t r = 0; r < n_rays; ++r) {
+            const int64_t e0 = row_ptr[r], N = row_ptr[r + 1] - e0;
+            if (N <= 0) continue;
+            if (N > cap) {
+                free(buf);
+                cap = N * 2;
+                buf = (double*)malloc(sizeof(double) * 9 * cap);
+            }
+            double* c = buf;
+            double* lnu = buf + N;
+            double* lpos = buf + 2 * N;
+            double* lneg = buf + 3 * N;
+            double* work = buf + 4 * N;
+            for (int64_t i = 0; i < N; ++i) {
+                c[i] = L0 + T[vid[e0 + i]] - lambda[e0 + i];
+                lnu[i] = orc_log_nu(lut, n_z, n_off, par, Z_ray[r], off_q[e0 + i]);
+            }
+            orc_ray_messages(N, c, lnu, lpos, lneg, work);
+            for (int64_t i = 0; i < N; ++i) lambda[e0 + i] = clip256(lpos[i] - lneg[i]);
+        }
+        free(buf);
+    }
+}
+
+/* T_v = sum_e lambda_e over the incidences of v, fp64 in incidence order (B5: "any fixed
+ * order"); T is zeroed first.  This is the incoming-belief accumulation of P:200. */
+void orc_accumulate(int64_t E, const int32_t* vid, const double* lambda, int64_t V, double* T) {
+    memset(T, 0, sizeof(double) * (size_t)V);
+    for (int64_t e = 0; e < E; ++e) T[vid[e]] += lambda[e];
+}
+
+/* n flooding iterations (B7) starting from lambda (in/out); T returned for the final lambda. */
+void orc_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
+            const double* Z_ray, const float* lut, int32_t n_z, int32_t n_off, const double par[9],
+            double L0, int64_t V, int32_t n_iter, double* lambda, double* T) {
+    const int64_t E = row_ptr[n_rays];
+    orc_accumulate(E, vid, lambda, V, T);
+    for (int32_t it = 0; it < n_iter; ++it) {
+        orc_ray_pass(n_rays, row_ptr, vid, off_q, Z_ray, lut, n_z, n_off, par, L0, T, lambda);
+        orc_accumulate(E, vid, lambda, V, T);
+    }
+}
+
+/* B6: p_v = sigma(L0 + T_v) (Eq.8); an unobserved voxel (T_v = 0) gives gamma. */
+void orc_marginals(int64_t V, double L0, const double* T, double* p) {
+    for (int64_t v = 0; v < V; ++v) p[v] = 1.0 / (1.0 + exp(-(L0 + T[v])));
+}
+
+/* ------------------------------------------------------------------ frames -> CSR */
+/* Pass 1 over one frame: per pixel status (0 kept, 1 invalid, 2 dropped), cell count and
+ * range Z.  Only rows with v % world == rank are visited (others get status 3). */
+void orc_frame_count(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+                     const double Twc[12], int32_t W, int32_t H, const float* depth, int32_t rank,
+                     int32_t world, int8_t* status, int64_t* count, double* Z_out, double* L_out) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int32_t v = 0; v < H; ++v) {
+        for (int32_t u = 0; u < W; ++u) {
+            const int64_t p = (int64_t)v * W + u;
+            count[p] = 0;
+            Z_out[p] = 0.0;
+            L_out[p] = 0.0;
+            if (v % world != rank) {
+                status[p] = 3;
+                continue;
+            }
+            int64_t G0[3], G1[3];
+            double Z = 0.0, L = 0.0;
+            const int s = orc_ray_setup(dims, geo, par, K, Twc, u, v, depth[p], G0, G1, &Z, &L);
+            status[p] = (int8_t)s;
+            if (s != 0) continue;
+            Z_out[p] = Z;
+            L_out[p] = L;
+            count[p] = orc_dda(dims, G0, G1, Z, L, NULL, NULL, NULL, NULL, 0);
+        }
+    }
+}
+
+/* Pass 2: write vid/off_q of every kept pixel at offset[p] (offset < 0: skip). */
+void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+                    const double Twc[12], int32_t W, int32_t H, const float* depth, const int64_t* offset,
+                    int32_t* vid, int16_t* off_q) {
+#pragma omp parallel for schedule(dynamic, 4)
+    for (int32_t v = 0; v < H; ++v) {
+        for (int32_t u = 0; u < W; ++u) {
+            const int64_t p = (int64_t)v * W + u;
+            if (offset[p] < 0) continue;
+            int64_t G0[3], G1[3];
+            double Z = 0.0, L = 0.0;
+            if (orc_ray_setup(dims, geo, par, K, Twc, u, v, depth[p], G0, G1, &Z, &L) != 0) continue;
+            orc_dda(dims, G0, G1, Z, L, vid + offset[p], off_q + offset[p], NULL, NULL, INT64_MAX);
+        }
+    }
+}
