@@ -1,0 +1,313 @@
+"""bench.py -- MRFMap hot path on B200: ray-voxel message updates/s (BASELINE.json metric).
+
+One step = the whole hot path over one batch of synthetic input:
+  reset; add_frame x F (raygen + DDA count, scan, DDA fill); bp_iterate(n) (transpose build,
+  then n x [K5 ray messages, K6 voxel reduction, (K7 all-reduce)]); marginals.
+Units per step = E * n (message updates), E = incidences of all ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config frames30] [--impl ours|reference]
+
+N > 1: launched by torch.distributed.run, one rank per GPU, rays sharded by pixel row
+(v % world == rank) with an NCCL all-reduce of the int64 voxel sums every iteration.
+--impl reference: the fp64 CPU oracle (oracle/) timed on the host cores on a bounded sample
+of the same workload (this tier has no reference implementation to install).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ray-voxel message updates/sec"
+UNIT = "updates/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 4 + i and r[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def _oracle_sample(w, max_frames=1):
+    """The oracle as it stands on a bounded sample: the first `max_frames` frames of the
+    workload, graph build + n iterations.  Returns (updates, seconds, E)."""
+    import oracle
+    p = oracle.Params.from_workload(w)
+    t0 = time.perf_counter()
+    g = oracle.build_graph(p, w.frames[:max_frames])
+    oracle.bp(p, g, w.n_iter)
+    dt = time.perf_counter() - t0
+    return g.E * w.n_iter, dt, g.E
+
+
+def run_reference(args, rank, world):
+    import synth
+    if rank != 0:
+        return
+    w = synth.make_workload(args.config)
+    for _ in range(args.warmup):
+        _oracle_sample(w, 1)
+    tot_u = tot_t = 0.0
+    for _ in range(args.steps):
+        u, dt, E = _oracle_sample(w, 1)
+        tot_u += u
+        tot_t += dt
+    v = tot_u / tot_t
+    cores = _cores()
+    sample = f"first frame of {args.config} (E={E}), graph build + {w.n_iter} BP iterations per step"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": args.config, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    import paper_2006_03512_b200 as pkg
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = synth.make_workload(args.config)
+    n_iter = w.n_iter if args.iters is None else args.iters
+
+    kw = {}
+    if world > 1:
+        ids = [pkg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        kw = dict(rank=rank, world=world, comm=pkg.MRF_COMM_NCCL, nccl_id=ids[0])
+    m = pkg.MRFMap.from_workload(w, **kw)
+    stream = torch.cuda.current_stream(dev)
+    m.set_stream(stream.cuda_stream)
+
+    depth_dev = [torch.from_numpy(fr.depth).to(dev) for fr in w.frames]
+    depth_host = [torch.from_numpy(fr.depth).pin_memory() for fr in w.frames]
+    marg_dev = torch.empty(w.n_voxels, dtype=torch.float32, device=dev)
+    marg_host = torch.empty(w.n_voxels, dtype=torch.float32).pin_memory()
+
+    def step(host_io=False):
+        m.reset()
+        for fr, dd, dh in zip(w.frames, depth_dev, depth_host):
+            m.add_frame(dh if host_io else dd, fr.K, fr.T_wc)
+        m.bp_iterate(n_iter)
+        if host_io:
+            m.marginals(marg_host.numpy())
+        else:
+            m.marginals(marg_dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also sizes every buffer)
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    sizes = m.graph_sizes()
+    E_local = sizes["E"]
+    t = torch.tensor([E_local, sizes["n_rays"]], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(t)
+    E_all, R_all = int(t[0]), int(t[1])
+
+    # ---- timed region (device-resident inputs)
+    m.set_profiling(True)
+    m.profile_read()
+    launches0 = m.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = m.launch_count() - launches0
+    prof = m.profile_read()
+    m.set_profiling(False)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t)
+    units = E_all * n_iter * args.steps
+    value = units / (ms / 1e3)
+
+    # ---- end to end through the public API: host depth in, host marginals out
+    e2e_steps = max(1, min(args.steps, 3))
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step(host_io=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_e2e, op=dist.ReduceOp.MAX)
+    e2e_value = E_all * n_iter * e2e_steps / (float(ms_e2e) / 1e3)
+    h2d = sum(fr.depth.nbytes for fr in w.frames)
+    d2h = w.n_voxels * 4
+
+    # ---- roofline of the dominant kernel (K5 = ray messages, one launch group per iteration)
+    peak, peak_kind = _peaks()
+    V = w.n_voxels
+    n_k5, ms_k5 = prof["ray_messages"]
+    n_k6, ms_k6 = prof["voxel_sum"]
+    per_iter_k5 = ms_k5 / max(1, args.steps * n_iter)
+    per_iter_k6 = ms_k6 / max(1, args.steps * n_iter)
+    bytes_k5 = 14 * E_local + 8 * V      # vid 4 + off_q 2 + lambda r/w 8 per incidence; T gather per voxel
+    bytes_k6 = 8 * E_local + 8 * V       # tr 4 + lambda 4 per incidence; T write per voxel
+    ach_k5 = bytes_k5 / (per_iter_k5 / 1e3) / 1e9 if per_iter_k5 > 0 else 0.0
+    ach_k6 = bytes_k6 / (per_iter_k6 / 1e3) / 1e9 if per_iter_k6 > 0 else 0.0
+    ach_bp = (bytes_k5 + bytes_k6) / ((per_iter_k5 + per_iter_k6) / 1e3) / 1e9 if per_iter_k5 > 0 else 0.0
+    dominant = "ray_messages" if ms_k5 >= ms_k6 else "voxel_sum"
+    ach = ach_k5 if dominant == "ray_messages" else ach_k6
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_json):
+        try:
+            d = json.load(open(prof_json))
+            k = d.get("kernels", {}).get(dominant)
+            if k and k.get("config") == args.config and k.get("E") == E_local:
+                traffic = k.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+
+    if rank == 0:
+        kernel_ms = {k: round(v[1] / max(1, args.steps), 4) for k, v in prof.items() if v[0]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": args.config, "frames": len(w.frames), "bp_iterations": n_iter,
+                       "incidences": E_all, "rays": R_all, "voxels": V, "grid": list(w.dims), "res_m": w.res,
+                       "parallelism": f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else "1 GPU",
+                       "l2": f"inputs larger than L2: messages {4 * E_all / 1e9:.2f} GB, graph {10 * E_all / 1e9:.2f} GB"},
+            "ms_per_bp_iteration": (ms_k5 + ms_k6 + prof["allreduce"][1]) / max(1, args.steps * n_iter),
+            "kernel_ms_per_step": kernel_ms,
+            "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": peak, "unit": "GB/s",
+                         "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": bytes_k5 if dominant == "ray_messages" else bytes_k6,
+                         "bp_iteration_frac": ach_bp / peak, "k5_frac": ach_k5 / peak, "k6_frac": ach_k6 / peak},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            u, dt, Es = _oracle_sample(w, 1)
+            line["cpu_baseline"] = {"value": u / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
+                                    "sample": f"first frame of {args.config} (E={Es}), graph build + "
+                                              f"{w.n_iter} BP iterations, fp64"}
+        print(json.dumps(line), flush=True)
+    m.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="frames30")
+    ap.add_argument("--iters", type=int, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,188 @@
+/*
+ * mrf.h -- C ABI of the B200-native MRFMap hot path (arxiv 2006.03512).
+ *
+ * The library builds the ray-voxel factor graph of posed depth images and runs
+ * loopy sum-product belief propagation over it on one B200 (or on N B200s, one
+ * process per GPU, rays sharded by pixel row).  Citations: P:n = line n of the
+ * paper; DESIGN.md restates every step and every reading R1..R15.
+ *
+ *   mrf_create      grid + prior + forward sensor model       (Eq.1, Eq.2, Eq.4)
+ *   mrf_add_frame   depth image + intrinsics + pose -> rays -> 3D-DDA -> ray->voxel CSR
+ *                                                             ("ray traced ... 3DDA", P:205 3-sigma cutoff)
+ *   mrf_bp_iterate  n flooding iterations: per-ray factor->voxel messages (Eq.13 P:153-156,
+ *                   Eq.14 P:158-161 / P:524) and voxel beliefs as a deterministic segmented
+ *                   reduction over the voxel->ray transpose (Eq.6)
+ *   mrf_marginals   p_v = sigma(L0 + T_v) (Eq.8)
+ *
+ * Conventions shared by every entry point
+ *   - Status codes only; nothing throws across the ABI.  CUDA and NCCL failures are sticky:
+ *     once one is returned every later call on the ctx returns the same code.
+ *   - Ownership: every input buffer is read (copied to the device or consumed) before the
+ *     call returns; the caller keeps ownership.  Outputs go to caller-allocated buffers.
+ *   - Pointers marked "host or device" are classified with cudaPointerGetAttributes.
+ *   - A ctx is bound to the CUDA device that was current at mrf_create and is not
+ *     thread-safe.  All device work is ordered on the ctx stream (mrf_set_stream).
+ *   - Voxel index v = x + nx*(y + ny*z) (x fastest).  Canonical incidence order is
+ *     (frame add order, pixel index v*W+u, position along the ray).
+ *   - Messages are stored as int32 fixed point lambda*2^23 (clipped to +-256 nats, reading
+ *     R9) and beliefs as int64 sums T_v = sum_e q_e, so every reduction is exact and
+ *     independent of order, rank count and scheduling.
+ */
+#ifndef MRF_H
+#define MRF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mrf_ctx mrf_ctx; /* opaque; owned by the caller from mrf_create to mrf_destroy */
+
+typedef enum {
+    MRF_OK = 0,
+    MRF_ERR_INVALID_ARG = 1,   /* argument rejected; state unchanged */
+    MRF_ERR_OUT_OF_MEMORY = 2, /* device allocation failed; state unchanged */
+    MRF_ERR_CAPACITY = 3,      /* frame would exceed an index limit (E >= 2^31, rays >= 2^31); state unchanged */
+    MRF_ERR_CUDA = 4,          /* sticky */
+    MRF_ERR_NCCL = 5,          /* sticky */
+    MRF_ERR_STATE = 6          /* call not valid in the current state (e.g. comm mode mismatch) */
+} mrf_status;
+
+/* Forward sensor model nu(Z | d) (Eq.4; learnt aggregate model P:230) as a table of
+ * log densities.  Row i is the measured range Z_i = z_lo + (i+0.5)(z_hi-z_lo)/n_z, column j the
+ * offset delta_j = off_lo + (j+0.5)(off_hi-off_lo)/n_off of the voxel depth d = Z + delta.
+ * Lookups interpolate bilinearly between bin centres and clamp to the edge centres.
+ * Traversal margin past the measured range: margin(Z) = max(margin_min, margin_k*sigma(Z)),
+ * sigma(Z) = (c0 + c1 Z) + c2 Z^2  (3 sigma beyond the depth; reading R5). */
+typedef struct {
+    const float* log_nu;   /* [n_z][n_off] row-major, finite, host memory; copied at create */
+    int32_t n_z, n_off;    /* >= 2 each */
+    double z_lo, z_hi;     /* metres, z_hi > z_lo */
+    double off_lo, off_hi; /* metres, -1 <= off_lo < off_hi <= 1 (span of the int16 offset code) */
+    double margin_min;     /* metres, >= 0 */
+    double margin_k;       /* >= 0 */
+    double sigma_c[3];     /* c0, c1, c2 */
+} mrf_noise_desc;
+
+/* Data-parallel sharding: rank keeps the rays of pixel rows v % world == rank.
+ * comm = MRF_COMM_NCCL: an NCCL communicator is created from nccl_id (all ranks pass the same
+ *   id, from mrf_nccl_unique_id on rank 0) and mrf_bp_iterate all-reduces the per-voxel int64
+ *   partial sums every iteration.
+ * comm = MRF_COMM_EXTERNAL: no communicator; the caller reduces the partials itself with
+ *   mrf_bp_partial / mrf_bp_finish (used to emulate ranks on one GPU, and by tests). */
+enum { MRF_COMM_NCCL = 0, MRF_COMM_EXTERNAL = 1 };
+typedef struct {
+    int32_t rank, world; /* 0 <= rank < world */
+    int32_t comm;        /* MRF_COMM_NCCL or MRF_COMM_EXTERNAL */
+    unsigned char nccl_id[128];
+} mrf_dist_desc;
+
+/* Create a dense nx*ny*nz grid of voxel side resolution_m at origin_m (metres), with the
+ * Bernoulli prior gamma (Eq.2) and sensor model noise.  dist == NULL -> one GPU.
+ * Errors: INVALID_ARG for dims <= 0 or > 8192, V >= 2^31, resolution not finite or <= 0,
+ * prior not in (0,1), bad noise table; OUT_OF_MEMORY; NCCL on communicator failure. */
+mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double origin_m[3], float prior,
+                      const mrf_noise_desc* noise, const mrf_dist_desc* dist, mrf_ctx** out);
+
+/* Add one keyframe: depth is H*W z-depth in metres (row-major, host or device; 0, NaN or <= 0
+ * = invalid pixel, skipped and counted); K = {fx, fy, cx, cy} with pixel centres at integer
+ * (u, v); T_wc = 3x4 row-major world-from-camera [R | C], OpenCV camera axes.
+ * Each kept pixel becomes a ray traced by the fixed-point 3D-DDA from C to the measured range
+ * plus margin(Z); a ray whose measured point lies outside the grid is dropped and counted
+ * (reading R11).  New messages start at 0 (warm start of the existing ones).
+ * Errors: INVALID_ARG for width/height <= 0, non-finite K, fx or fy <= 0, non-finite T_wc,
+ * ||R^T R - I||_max > 1e-6, camera centre outside the grid; CAPACITY when the graph would
+ * exceed the index limits (the frame is not added); OUT_OF_MEMORY (not added).
+ * frame_id_out (nullable) receives the 0-based frame index. */
+mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_t height, const double K[4],
+                         const double T_wc[12], int64_t* frame_id_out);
+
+/* Run n >= 0 synchronous flooding iterations (reading R4): every ray computes its
+ * factor->voxel messages from the same belief snapshot T, then T is rebuilt by the segmented
+ * reduction over the voxel->ray transpose (and all-reduced across ranks).  Asynchronous on the
+ * ctx stream.  Errors: INVALID_ARG for n < 0; STATE in MRF_COMM_EXTERNAL mode with world > 1. */
+mrf_status mrf_bp_iterate(mrf_ctx* ctx, int32_t n);
+
+/* Occupancy marginals p_v = sigma(L0 + T_v 2^-23) for all V voxels, x fastest, float32; out is
+ * a host (out_is_device = 0) or device (1) buffer of V floats.  Voxels seen by no ray return
+ * the prior.  Synchronises the ctx stream. */
+mrf_status mrf_marginals(mrf_ctx* ctx, float* out, int32_t out_is_device);
+
+/* Free everything (also valid on a ctx in a sticky error state).  NULL is a no-op. */
+mrf_status mrf_destroy(mrf_ctx* ctx);
+
+/* Last error message of the ctx (or of the last failed mrf_create when ctx == NULL); the
+ * string stays valid until the next call on the ctx. */
+const char* mrf_last_error(const mrf_ctx* ctx);
+
+/* ------------------------------------------------------------------ runtime / introspection */
+
+/* Use cuda_stream (a cudaStream_t, or NULL for the ctx's own stream) for all later work. */
+mrf_status mrf_set_stream(mrf_ctx* ctx, void* cuda_stream);
+
+/* Drop every frame, ray, incidence and message (buffers are kept for reuse); T = 0. */
+mrf_status mrf_reset(mrf_ctx* ctx);
+
+/* Pre-allocate room for n_rays rays (pixels owned by this rank) and n_incidences incidences. */
+mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences);
+
+/* Graph sizes of this rank: kept rays, incidences E, voxels touched by >= 1 incidence,
+ * invalid pixels and dropped rays.  Any pointer may be NULL.  Synchronises. */
+mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences, int64_t* n_active_vox,
+                           int64_t* n_invalid, int64_t* n_dropped);
+
+/* Copy this rank's graph to host buffers in canonical order: ray_pixel[n_rays] = frame*2^32 +
+ * (v*W + u) of each kept ray, row_ptr[n_rays+1], vid[E], off_q[E] (metres * 32768).  Any pointer
+ * may be NULL.  Synchronises. */
+mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, int32_t* vid, int16_t* off_q);
+
+/* Voxel->ray transpose: col_ptr[V+1] and, per voxel, the incidence indices tr[E] (order inside a
+ * voxel is unspecified).  Builds the transpose if needed.  Synchronises. */
+mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr);
+
+/* Messages lambda_e (nats) of this rank in canonical order, host buffer of E floats. */
+mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda);
+
+/* Replace the messages (host buffer of E floats, nats; quantised to 2^-23 and clipped to
+ * +-256) and rebuild T from them (summed over ranks in MRF_COMM_NCCL mode; left to the caller
+ * in MRF_COMM_EXTERNAL mode with world > 1, see mrf_bp_partial). */
+mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda);
+
+/* Beliefs T_v (int64, units 2^-23 nats; the global sum over ranks) into a host buffer of V. */
+mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T);
+
+/* MRF_COMM_EXTERNAL mode, one iteration split in two: mrf_bp_partial (iterate = 1) computes
+ * this rank's messages from the current T and writes its partial voxel sums to partial_out
+ * (device pointer, V int64); the caller sums the partials of all ranks and hands the total
+ * back with mrf_bp_finish (device pointer, V int64), which becomes T.  iterate = 0 only sums
+ * the current messages (e.g. after mrf_import_messages, which in this mode leaves T alone). */
+mrf_status mrf_bp_partial(mrf_ctx* ctx, int32_t iterate, int64_t* partial_out_device);
+mrf_status mrf_bp_finish(mrf_ctx* ctx, const int64_t* total_device);
+
+/* 128-byte ncclUniqueId for MRF_COMM_NCCL (call on rank 0, broadcast to the others). */
+mrf_status mrf_nccl_unique_id(unsigned char out[128]);
+
+/* Per-kernel timing with CUDA events on the ctx stream (off by default). */
+enum {
+    MRF_K_RAYGEN_COUNT = 0, /* K1: pixel -> segment + DDA count */
+    MRF_K_DDA_FILL = 1,     /* K3: DDA fill of vid/off_q + voxel histogram */
+    MRF_K_SCAN = 2,         /* K2: exclusive scans */
+    MRF_K_TRANSPOSE = 3,    /* K4: voxel->ray transpose fill + work lists */
+    MRF_K_RAY_MSG = 4,      /* K5: factor->voxel messages (all length classes) */
+    MRF_K_VOXEL_SUM = 5,    /* K6: segmented reduction over the transpose */
+    MRF_K_ALLREDUCE = 6,    /* K7: NCCL all-reduce of T */
+    MRF_K_MARGINALS = 7,    /* K8 */
+    MRF_K_COUNT = 8
+};
+mrf_status mrf_set_profiling(mrf_ctx* ctx, int32_t on);
+/* Synchronise, then return (and clear) per-kernel launch counts and summed event time (ms),
+ * arrays of MRF_K_COUNT entries (nullable). */
+mrf_status mrf_profile_read(mrf_ctx* ctx, int64_t* launches, double* total_ms);
+/* Total kernels launched by this ctx since create (all kinds). */
+int64_t mrf_launch_count(const mrf_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRF_H */

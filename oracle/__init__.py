@@ -214,6 +214,33 @@ def build_graph(p: Params, frames, rank: int = 0, world: int = 1) -> Graph:
                  np.concatenate(pix) if pix else np.zeros(0, np.int64), n_inv, n_drop)
 
 
+def trace_pixels(p: Params, frame, pixels, frame_index: int = 0) -> Graph:
+    """B1-B3 for selected pixel ids (v*W+u) of one frame, one by one (sampled parity at full
+    size).  Only kept pixels (status 0) become rays, in the order given."""
+    H, W = frame.depth.shape
+    row_ptr = [0]
+    vids, offs, Zs, pix = [], [], [], []
+    n_inv = n_drop = 0
+    for px in pixels:
+        v, u = divmod(int(px), W)
+        s, G0, G1, Z, L = ray_setup(p, frame.K, frame.T_wc, u, v, float(frame.depth[v, u]))
+        if s == STATUS_INVALID:
+            n_inv += 1
+            continue
+        if s == STATUS_DROPPED:
+            n_drop += 1
+            continue
+        vid, off, _, _ = dda(p.dims, G0, G1, Z, L)
+        vids.append(vid)
+        offs.append(off)
+        row_ptr.append(row_ptr[-1] + len(vid))
+        Zs.append(Z)
+        pix.append(int(px))
+    cat = lambda a, t: np.concatenate(a).astype(t) if a else np.zeros(0, t)  # noqa: E731
+    return Graph(np.array(row_ptr, np.int64), cat(vids, np.int32), cat(offs, np.int16), np.array(Zs),
+                 np.full(len(pix), frame_index, np.int32), np.array(pix, np.int64), n_inv, n_drop)
+
+
 # --------------------------------------------------------------------------- B4..B6
 
 def ray_messages(c, lnu):

@@ -1,0 +1,376 @@
+// graph.cu -- ray-voxel factor graph construction on sm_100a (K1, K3, K4 + work lists).
+//
+// "all keyframe images are ray traced ... The ray traversal is done via the
+// standard 3DDA traversal algorithm"; traverse "until a 3 sigma distance beyond the
+// measured depth".  Here each pixel's segment is quantised to 16-fractional-bit grid
+// coordinates and walked with an integer-only DDA (DESIGN.md §Graph build, readings R5, R6,
+// R11, R13), so the ray->voxel index lists are bit-exact across implementations.
+//
+// Layout: one thread per owned pixel; a warp holds 32 neighbouring pixels of one image row,
+// so the warp's rays start in the same voxel and fan out slowly -- voxel-histogram and
+// transpose-cursor atomics are aggregated per warp with __match_any_sync.
+#include "internal.cuh"
+
+namespace mrf {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------- B1: pixel -> segment
+// All fp64 steps use explicitly rounded intrinsics (no FMA contraction), in the order
+// stated in DESIGN.md §Graph build, so the quantised end points are reproducible.
+struct Segment {
+    long long g0[3], g1[3];
+    double Z, L;
+};
+
+// 0 = kept, 1 = invalid pixel, 2 = dropped (measured point outside the grid)
+__device__ __forceinline__ int pixel_segment(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, int u,
+                                             int v, float zf, Segment& sg) {
+    const double z = (double)zf;
+    if (!(z > 0.0) || isinf(z)) return 1;
+    const double xc = __ddiv_rn(__dsub_rn((double)u, f.cx), f.fx);
+    const double yc = __ddiv_rn(__dsub_rn((double)v, f.cy), f.fy);
+    const double rho = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xc, xc), __dmul_rn(yc, yc)), 1.0));
+    const double Z = __dmul_rn(z, rho);
+    const double sig = __dadd_rn(__dadd_rn(n.c0, __dmul_rn(n.c1, Z)), __dmul_rn(__dmul_rn(n.c2, Z), Z));
+    double margin = __dmul_rn(n.margin_k, sig);
+    if (margin < n.margin_min) margin = n.margin_min;
+    const double L = __dadd_rn(Z, margin);
+    const double l_over_rho = __ddiv_rn(L, rho);
+    const double org[3] = {g.ox, g.oy, g.oz};
+    const int dims[3] = {g.nx, g.ny, g.nz};
+    for (int k = 0; k < 3; ++k) {
+        const double d = __dadd_rn(__dadd_rn(__dmul_rn(f.R[3 * k], xc), __dmul_rn(f.R[3 * k + 1], yc)), f.R[3 * k + 2]);
+        const double hit = __ddiv_rn(__dsub_rn(__dadd_rn(f.C[k], __dmul_rn(z, d)), org[k]), g.res);
+        if (hit < 0.0 || hit >= (double)dims[k]) return 2;
+        const double end = __dadd_rn(f.C[k], __dmul_rn(l_over_rho, d));
+        const double a = __ddiv_rn(__dsub_rn(f.C[k], org[k]), g.res);
+        const double b = __ddiv_rn(__dsub_rn(end, org[k]), g.res);
+        sg.g0[k] = __double2ll_rn(__dmul_rn(a, 65536.0));
+        sg.g1[k] = __double2ll_rn(__dmul_rn(b, 65536.0));
+    }
+    sg.Z = Z;
+    sg.L = L;
+    return 0;
+}
+
+// ---------------------------------------------------------------- B2: integer 3D-DDA
+// State of the walk: current cell, per-axis step direction, and the exact crossing parameter
+// of the next boundary on each axis as the rational num/den (den = |dG| > 0).
+struct Walker {
+    long long num[3], den[3];
+    int cell[3], dir[3];
+    double t_in;
+
+    __device__ __forceinline__ void start(const Segment& sg) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const long long d = sg.g1[k] - sg.g0[k];
+            long long c = sg.g0[k] >> kFixShift;  // arithmetic shift == floor
+            const bool on_face = (sg.g0[k] & (kFixOne - 1)) == 0;
+            if (d < 0 && on_face) c -= 1;         // cell that contains t = 0+
+            cell[k] = (int)c;
+            if (d > 0) {
+                dir[k] = 1;
+                num[k] = ((c + 1) << kFixShift) - sg.g0[k];
+                den[k] = d;
+            } else if (d < 0) {
+                dir[k] = -1;
+                num[k] = sg.g0[k] - (c << kFixShift);
+                den[k] = -d;
+            } else {
+                dir[k] = 0;
+                num[k] = 1;
+                den[k] = 0;
+            }
+        }
+        t_in = 0.0;
+    }
+    __device__ __forceinline__ bool inside(const GridDesc& g) const {
+        return (unsigned)cell[0] < (unsigned)g.nx && (unsigned)cell[1] < (unsigned)g.ny &&
+               (unsigned)cell[2] < (unsigned)g.nz;
+    }
+    // Axis of the earliest next crossing (-1 if none); exact comparison of num/den.
+    __device__ __forceinline__ int earliest() const {
+        int a = -1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (dir[k] == 0) continue;
+            if (a < 0) {
+                a = k;
+            } else if (num[k] * den[a] < num[a] * den[k]) {
+                a = k;
+            }
+        }
+        return a;
+    }
+    // Advance every axis whose crossing ties with axis a (simultaneous steps on corners/edges).
+    __device__ __forceinline__ void advance(int a) {
+        const long long na = num[a], da = den[a];
+        bool tie[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tie[k] = dir[k] != 0 && num[k] * da == na * den[k];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (tie[k]) {
+                cell[k] += dir[k];
+                num[k] += kFixOne;
+            }
+        }
+    }
+};
+
+__device__ __forceinline__ double crossing_t(const Walker& w, int a, bool& last) {
+    last = (a < 0) || (w.num[a] >= w.den[a]);
+    return last ? 1.0 : __ddiv_rn((double)w.num[a], (double)w.den[a]);
+}
+
+__device__ __forceinline__ void owned_pixel(const FrameDesc& f, long long i, int& u, int& v) {
+    const int lr = (int)(i / f.W);
+    u = (int)(i - (long long)lr * f.W);
+    v = f.rank + lr * f.world;
+}
+
+// ---------------------------------------------------------------- K1
+__global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
+                                                           const float* __restrict__ depth, int32_t* n_r,
+                                                           int8_t* status, RayZ* ray_z,
+                                                           unsigned long long* counters) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n_pix = (long long)f.rows_owned * f.W;
+    int st = 3;
+    if (i < n_pix) {
+        int u, v;
+        owned_pixel(f, i, u, v);
+        Segment sg;
+        st = pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg);
+        int count = 0;
+        RayZ rz{0, 0.f};
+        if (st == 0) {
+            Walker w;
+            w.start(sg);
+            while (w.inside(g)) {
+                ++count;
+                const int a = w.earliest();
+                if (a < 0 || w.num[a] >= w.den[a]) break;  // end point inside this cell
+                w.advance(a);
+            }
+            // LUT row of the measured range (bin centres, clamped to the edge centres)
+            double fz = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(sg.Z, n.z_lo), __dsub_rn(n.z_hi, n.z_lo)),
+                                            (double)n.n_z), 0.5);
+            if (fz < 0.0) fz = 0.0;
+            if (fz > (double)(n.n_z - 1)) fz = (double)(n.n_z - 1);
+            int iz = (int)floor(fz);
+            if (iz > n.n_z - 2) iz = n.n_z - 2;
+            rz.iz = iz;
+            rz.wz = (float)(fz - (double)iz);
+        }
+        n_r[f.ray_base + i] = count;
+        status[f.ray_base + i] = (int8_t)st;
+        ray_z[f.ray_base + i] = rz;
+    }
+    const unsigned inv = __ballot_sync(kFull, st == 1);
+    const unsigned drp = __ballot_sync(kFull, st == 2);
+    if ((threadIdx.x & 31) == 0) {
+        if (inv) atomicAdd(&counters[0], (unsigned long long)__popc(inv));
+        if (drp) atomicAdd(&counters[1], (unsigned long long)__popc(drp));
+    }
+}
+
+// ---------------------------------------------------------------- K3
+// B3: off_q = clamp(rint((0.5 (t_in + t_out) L - Z) * 32768), +-32767), the span midpoint
+// relative to the measured range (reading R6).
+__global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
+                                                       const float* __restrict__ depth,
+                                                       const long long* __restrict__ row_ptr, int32_t* vid,
+                                                       int16_t* off_q, int32_t* vox_count) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n_pix = (long long)f.rows_owned * f.W;
+    const int lane = threadIdx.x & 31;
+    bool alive = false;
+    Segment sg;
+    Walker w;
+    long long e = 0;
+    if (i < n_pix) {
+        int u, v;
+        owned_pixel(f, i, u, v);
+        if (pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg) == 0) {
+            w.start(sg);
+            alive = w.inside(g);
+            e = row_ptr[f.ray_base + i];
+        }
+    }
+    for (;;) {
+        const unsigned am = __ballot_sync(kFull, alive);
+        if (am == 0) break;
+        if (alive) {
+            bool last;
+            const int a = w.earliest();
+            const double t_out = crossing_t(w, a, last);
+            const int vx = w.cell[0] + g.nx * (w.cell[1] + g.ny * w.cell[2]);
+            const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
+            long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
+            q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
+            vid[e] = vx;
+            off_q[e] = (int16_t)q;
+            ++e;
+            const unsigned peers = __match_any_sync(am, vx);
+            if (lane == __ffs(peers) - 1) atomicAdd(&vox_count[vx], __popc(peers));
+            if (last) {
+                alive = false;
+            } else {
+                w.advance(a);
+                w.t_in = t_out;
+                alive = w.inside(g);
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K4
+// Thread per ray walking its incidences in lock step with its warp neighbours; incidences
+// that land in the same voxel at the same step share one cursor atomic.
+__global__ void __launch_bounds__(256) transpose_fill_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                                             const int32_t* __restrict__ vid,
+                                                             const long long* __restrict__ col_ptr,
+                                                             int32_t* cursor, int32_t* tr) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    long long e = 0, e1 = 0;
+    if (r < n_rays) {
+        e = row_ptr[r];
+        e1 = row_ptr[r + 1];
+    }
+    for (;;) {
+        const bool alive = e < e1;
+        const unsigned am = __ballot_sync(kFull, alive);
+        if (am == 0) break;
+        if (alive) {
+            const int v = vid[e];
+            const unsigned peers = __match_any_sync(am, v);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (lane == leader) base = atomicAdd(&cursor[v], __popc(peers));
+            base = __shfl_sync(peers, base, leader);
+            const int rank = __popc(peers & ((1u << lane) - 1u));
+            tr[col_ptr[v] + base + rank] = (int32_t)e;
+            ++e;
+        }
+    }
+}
+
+__global__ void item_counts_kernel(long long V, const int32_t* __restrict__ cnt, int32_t* n_items) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < V) n_items[v] = (cnt[v] + kVoxelChunk - 1) / kVoxelChunk;
+}
+
+__global__ void item_fill_kernel(long long V, const int32_t* __restrict__ n_items,
+                                 const long long* __restrict__ item_ptr, int2* items) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= V) return;
+    const long long b = item_ptr[v];
+    for (int j = 0; j < n_items[v]; ++j) items[b + j] = make_int2((int)v, j);
+}
+
+__global__ void active_flags_kernel(long long V, const int32_t* __restrict__ cnt, int32_t* flags) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < V) flags[v] = cnt[v] > 0 ? 1 : 0;
+}
+
+__global__ void class_flags_kernel(long long n_rays, const long long* __restrict__ row_ptr, int cls,
+                                   int32_t* flags) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays) return;
+    const long long e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    int c = -1;
+    if (e1 > e0) {
+        c = 3;
+        for (int k = 0; k < 3; ++k) {
+            const long long K = 4LL << k;  // 4, 8, 16 elements per lane
+            if (e1 - (e0 & ~(K - 1)) <= 32 * K) {
+                c = k;
+                break;
+            }
+        }
+    }
+    flags[r] = (c == cls) ? 1 : 0;
+}
+
+__global__ void compact_kernel(long long n, const int32_t* __restrict__ flags, const long long* __restrict__ pos,
+                               int32_t* out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && flags[i]) out[pos[i]] = (int32_t)i;
+}
+
+__global__ void span_max_kernel(long long n, const int32_t* __restrict__ rays, const long long* __restrict__ row_ptr,
+                                unsigned long long* out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned long long m = 0;
+    if (i < n) {
+        const long long r = rays[i];
+        m = (unsigned long long)(row_ptr[r + 1] - (row_ptr[r] & ~7LL));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long x = __shfl_xor_sync(kFull, m, o);
+        m = x > m ? x : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+
+}  // namespace
+
+void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
+                         int32_t* n_r, int8_t* status, RayZ* ray_z, unsigned long long* counters,
+                         cudaStream_t s) {
+    const long long n_pix = (long long)f.rows_owned * f.W;
+    if (n_pix == 0) return;
+    raygen_count_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, n_r, status, ray_z, counters);
+}
+
+void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
+                     const long long* row_ptr, int32_t* vid, int16_t* off_q, int32_t* vox_count,
+                     cudaStream_t s) {
+    const long long n_pix = (long long)f.rows_owned * f.W;
+    if (n_pix == 0) return;
+    dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q, vox_count);
+}
+
+void launch_transpose_fill(long long n_rays, const long long* row_ptr, const int32_t* vid,
+                           const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s) {
+    if (n_rays == 0) return;
+    transpose_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, vid, col_ptr, cursor, tr);
+}
+
+void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, cudaStream_t s) {
+    item_counts_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, n_items);
+}
+
+void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
+                      cudaStream_t s) {
+    item_fill_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, n_items, item_ptr, items);
+}
+
+void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, cudaStream_t s) {
+    active_flags_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, flags);
+}
+
+void launch_class_flags(long long n_rays, const long long* row_ptr, int cls, int32_t* flags, cudaStream_t s) {
+    if (n_rays == 0) return;
+    class_flags_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, cls, flags);
+}
+
+void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s) {
+    if (n == 0) return;
+    compact_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, flags, pos, out);
+}
+
+void launch_span_max(long long n, const int32_t* rays, const long long* row_ptr, unsigned long long* out,
+                     cudaStream_t s) {
+    if (n == 0) return;
+    span_max_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, rays, row_ptr, out);
+}
+
+}  // namespace mrf

@@ -1,0 +1,100 @@
+// internal.cuh -- shared declarations of the CUDA path (sm_100a).  Not part of the ABI.
+//
+// The product path: mrf_api.cu (host runtime behind include/mrf.h) drives the kernels of
+// graph.cu (K1 raygen+DDA count, K3 DDA fill, K4 transpose, work lists), scan.cu (K2) and
+// bp.cu (K5 ray messages, K6 voxel reduction, K8 marginals).  Nothing here is shared with
+// oracle/ (the fp64 CPU checker), which is written independently from the paper.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mrf {
+
+// ---- fixed-point conventions (DESIGN.md §Data layout)
+constexpr int kFixShift = 16;                 // grid coordinates carry 16 fractional bits
+constexpr long long kFixOne = 1LL << kFixShift;
+constexpr float kQScale = 8388608.0f;         // messages: int32 q = round(lambda * 2^23)
+constexpr float kQInv = 1.0f / 8388608.0f;
+constexpr double kQInvD = 1.0 / 8388608.0;
+constexpr float kLambdaClip = 256.0f;         // reading R9
+constexpr int kPadElems = 64;                 // slack after incidence arrays (aligned over-reads)
+constexpr int kVoxelChunk = 4096;             // K6 work item: <= 4096 transpose entries
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr float kLn2 = 0.6931471805599453f;
+
+struct GridDesc {
+    int nx, ny, nz;
+    double res, ox, oy, oz;
+};
+
+struct NoiseDesc {
+    double z_lo, z_hi, off_lo, off_hi, margin_min, margin_k, c0, c1, c2;
+    int n_z, n_off;
+};
+
+struct FrameDesc {
+    double fx, fy, cx, cy;
+    double R[9];
+    double C[3];
+    int W, H, rank, world;
+    int rows_owned;           // number of pixel rows v with v % world == rank
+    long long ray_base;       // index of this frame's first ray
+};
+
+// Per-ray LUT row information: row iz (<= n_z-2) and weight wz in [0,1].
+struct RayZ {
+    int iz;
+    float wz;
+};
+
+// K5 parameters (log2 units).
+struct MsgParams {
+    const float2* lutp;       // pair table [n_z][n_off-1] of (L[i][j], L[i][j+1]) * log2(e)
+    int n_offm1;              // n_off - 1
+    float s_off, b_off;       // fo = off_q * s_off + b_off
+    float fo_max;             // n_off - 1
+    float L0_2;               // prior log-odds * log2(e)
+};
+
+// ---- launchers (all asynchronous on `s`)
+// K1: per owned pixel -> status, ray length, LUT row; counters[0] += invalid, counters[1] += dropped
+void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
+                         int32_t* n_r, int8_t* status, RayZ* ray_z, unsigned long long* counters,
+                         cudaStream_t s);
+// K3: walk again, write vid/off_q at row_ptr offsets, histogram voxel degrees
+void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
+                     const long long* row_ptr, int32_t* vid, int16_t* off_q, int32_t* vox_count,
+                     cudaStream_t s);
+// K2: out[i] = offset + sum_{j<i} in[j] for i in [0, n]; out has n+1 entries.
+void launch_exclusive_scan(const int32_t* in, long long* out, long long n, long long offset,
+                           long long* scratch, cudaStream_t s);
+long long scan_scratch_elems(long long n);
+// K4: tr[col_ptr[v] + slot] = e for every incidence e (cursor zeroed by caller)
+void launch_transpose_fill(long long n_rays, const long long* row_ptr, const int32_t* vid,
+                           const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s);
+// K6 work list: n_items[v] = ceil(deg/kVoxelChunk); items from item_ptr
+void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, cudaStream_t s);
+void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
+                      cudaStream_t s);
+// K5 ray length classes: flags[r] = (class(r) == c)
+void launch_class_flags(long long n_rays, const long long* row_ptr, int cls, int32_t* flags, cudaStream_t s);
+void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s);
+// misc
+void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, cudaStream_t s);
+void launch_span_max(long long n, const int32_t* rays, const long long* row_ptr, unsigned long long* out,
+                     cudaStream_t s);
+
+// ---- BP kernels (bp.cu)
+constexpr int kNumClasses = 4;      // K = 4, 8, 16 single-tile warps; class 3 = long rays (tiled)
+int class_capacity(int cls);        // max span handled by class cls (class 3: unbounded)
+void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+                         const RayZ* ray_z, const int32_t* vid, const int16_t* off_q, int32_t* lam,
+                         const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
+                         int n_warps_long, cudaStream_t s);
+void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
+                         const int32_t* lam, long long* T, cudaStream_t s);
+void launch_marginals(long long V, const long long* T, double L0, float* out, cudaStream_t s);
+void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s);
+
+}  // namespace mrf

@@ -1,0 +1,766 @@
+// mrf_api.cu -- host runtime behind include/mrf.h (C ABI), one ctx per GPU/rank.
+//
+// Owns the device buffers (HBM layout in DESIGN.md §Data layout), the stream, the NCCL
+// communicator and the graph state; every step of the hot path runs in the kernels of
+// graph.cu / scan.cu / bp.cu.  There is no CPU fallback: any CUDA failure is returned as a
+// sticky MRF_ERR_CUDA.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+#include "mrf.h"
+
+using namespace mrf;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    // Grow to at least n elements (x1.5 geometric); copies the first `used` elements.
+    cudaError_t ensure(size_t n, size_t used, cudaStream_t s) {
+        if (n <= cap) return cudaSuccess;
+        size_t nc = std::max(n, cap + cap / 2);
+        T* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, nc * sizeof(T));
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return e;
+        }
+        if (p) {
+            if (used) {
+                e = cudaMemcpyAsync(q, p, used * sizeof(T), cudaMemcpyDeviceToDevice, s);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                if (e != cudaSuccess) {
+                    cudaFree(q);
+                    return e;
+                }
+            }
+            cudaFree(p);
+        }
+        p = q;
+        cap = nc;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct FrameRec {
+    int W, H, rows_owned;
+    long long ray_base, n_rays;
+};
+
+struct ProfEvent {
+    int kind;
+    cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct mrf_ctx {
+    int device = 0;
+    GridDesc grid{};
+    NoiseDesc noise{};
+    long long V = 0;
+    float prior = 0.5f;
+    double L0 = 0.0;
+    MsgParams mp{};
+    int rank = 0, world = 1, comm_mode = MRF_COMM_NCCL;
+    ncclComm_t comm = nullptr;
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    std::string err;
+    mrf_status sticky = MRF_OK;
+
+    long long R = 0, E = 0;
+    long long n_invalid = 0, n_dropped = 0, n_kept = 0;
+    DBuf<int32_t> n_r;
+    DBuf<int8_t> status;
+    DBuf<RayZ> ray_z;
+    DBuf<long long> row_ptr;
+    DBuf<int32_t> vid;
+    DBuf<int16_t> off_q;
+    DBuf<int32_t> lam;
+    DBuf<int32_t> tr;
+    DBuf<int32_t> vox_count, cursor, n_items, flags;
+    DBuf<long long> col_ptr, item_ptr, pos;
+    DBuf<int2> items;
+    long long n_items_total = 0;
+    DBuf<long long> T, T_part;
+    DBuf<float2> lutp;
+    DBuf<float> depth_stage, marg;
+    DBuf<long long> scan_scratch;
+    DBuf<unsigned long long> counters;
+    DBuf<int32_t> class_rays[kNumClasses];
+    long long class_n[kNumClasses] = {0, 0, 0, 0};
+    DBuf<float> long_scratch;
+    long long long_scratch_per_warp = 0;
+    int n_warps_long = 0;
+    long long* pinned = nullptr;  // small readbacks
+    std::vector<FrameRec> frames;
+    bool dirty = true;
+
+    bool prof = false;
+    std::vector<ProfEvent> events;
+    long long prof_launch[MRF_K_COUNT] = {};
+    double prof_ms[MRF_K_COUNT] = {};
+    long long launches = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+mrf_status set_err(mrf_ctx* c, mrf_status st, const std::string& msg) {
+    c->err = msg;
+    if (st == MRF_ERR_CUDA || st == MRF_ERR_NCCL) c->sticky = st;
+    return st;
+}
+
+mrf_status cuda_fail(mrf_ctx* c, cudaError_t e, const char* what, int line) {
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        return set_err(c, MRF_ERR_OUT_OF_MEMORY, std::string("out of device memory: ") + what);
+    }
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %s (%s) at mrf_api.cu:%d in %s", cudaGetErrorName(e),
+             cudaGetErrorString(e), line, what);
+    return set_err(c, MRF_ERR_CUDA, buf);
+}
+
+#define CK(call)                                                      \
+    do {                                                              \
+        cudaError_t e_ = (call);                                      \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, #call, __LINE__); \
+    } while (0)
+
+#define CK_LAUNCH(kind_, nk_)                                                   \
+    do {                                                                        \
+        c->launches += (nk_);                                                   \
+        c->prof_launch[kind_] += (nk_);                                         \
+        cudaError_t e_ = cudaGetLastError();                                    \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, "kernel launch", __LINE__); \
+    } while (0)
+
+#define NCK(call)                                                                              \
+    do {                                                                                       \
+        ncclResult_t r_ = (call);                                                              \
+        if (r_ != ncclSuccess)                                                                 \
+            return set_err(c, MRF_ERR_NCCL, std::string("NCCL error: ") + ncclGetErrorString(r_) + " in " #call); \
+    } while (0)
+
+#define ENTER(ctx)                                                   \
+    if (!(ctx)) return MRF_ERR_INVALID_ARG;                          \
+    mrf_ctx* c = (ctx);                                              \
+    if (c->sticky != MRF_OK) return c->sticky;                       \
+    DeviceGuard guard_(c->device)
+
+bool finite_all(const double* a, int n) {
+    for (int i = 0; i < n; ++i)
+        if (!std::isfinite(a[i])) return false;
+    return true;
+}
+
+// Event pair around a group of launches when profiling is on.
+struct ProfScope {
+    mrf_ctx* c;
+    int kind;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(mrf_ctx* c_, int k) : c(c_), kind(k) {
+        if (!c->prof) return;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, c->stream);
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEventRecord(b, c->stream);
+        c->events.push_back({kind, a, b});
+    }
+};
+
+mrf_status scan(mrf_ctx* c, const int32_t* in, long long* out, long long n, long long offset) {
+    CK(c->scan_scratch.ensure((size_t)scan_scratch_elems(n), 0, c->stream));
+    ProfScope ps(c, MRF_K_SCAN);
+    launch_exclusive_scan(in, out, n, offset, c->scan_scratch.p, c->stream);
+    CK_LAUNCH(MRF_K_SCAN, n > 0 ? 3 : 1);
+    return MRF_OK;
+}
+
+mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
+    CK(cudaMemcpyAsync(c->pinned, dev, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    *out = c->pinned[0];
+    return MRF_OK;
+}
+
+// Build the voxel->ray transpose, the K6 work list and the K5 length classes (on graph change).
+mrf_status prepare(mrf_ctx* c) {
+    if (!c->dirty) return MRF_OK;
+    const long long V = c->V;
+    mrf_status st;
+    // K4: col_ptr = scan(degrees); tr by cursor atomics
+    if ((st = scan(c, c->vox_count.p, c->col_ptr.p, V, 0)) != MRF_OK) return st;
+    CK(c->tr.ensure((size_t)c->E + kPadElems, 0, c->stream));
+    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * V, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_transpose_fill(c->R, c->row_ptr.p, c->vid.p, c->col_ptr.p, c->cursor.p, c->tr.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        launch_item_counts(V, c->vox_count.p, c->n_items.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+    }
+    if ((st = scan(c, c->n_items.p, c->item_ptr.p, V, 0)) != MRF_OK) return st;
+    if ((st = read_ll(c, c->item_ptr.p + V, &c->n_items_total)) != MRF_OK) return st;
+    CK(c->items.ensure((size_t)std::max(1LL, c->n_items_total), 0, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_item_fill(V, c->n_items.p, c->item_ptr.p, c->items.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+    }
+    // K5 classes by span (stable compaction keeps pixel order inside a class)
+    CK(c->flags.ensure((size_t)std::max(c->R, V) + 1, 0, c->stream));
+    CK(c->pos.ensure((size_t)std::max(c->R, V) + 1, 0, c->stream));
+    for (int k = 0; k < kNumClasses; ++k) {
+        launch_class_flags(c->R, c->row_ptr.p, k, c->flags.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        if ((st = scan(c, c->flags.p, c->pos.p, c->R, 0)) != MRF_OK) return st;
+        if ((st = read_ll(c, c->pos.p + c->R, &c->class_n[k])) != MRF_OK) return st;
+        CK(c->class_rays[k].ensure((size_t)std::max(1LL, c->class_n[k]), 0, c->stream));
+        launch_compact(c->R, c->flags.p, c->pos.p, c->class_rays[k].p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    }
+    // scratch for the tiled long-ray kernel
+    if (c->class_n[3] > 0) {
+        CK(cudaMemsetAsync(c->counters.p + 4, 0, sizeof(unsigned long long), c->stream));
+        launch_span_max(c->class_n[3], c->class_rays[3].p, c->row_ptr.p, c->counters.p + 4, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+        long long span = 0;
+        if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 4), &span)) != MRF_OK) return st;
+        const long long tile = 256;
+        c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
+        c->n_warps_long = (int)std::min<long long>(c->class_n[3], 148LL * 16);
+        CK(c->long_scratch.ensure((size_t)(c->long_scratch_per_warp * c->n_warps_long), 0, c->stream));
+    }
+    c->dirty = false;
+    return MRF_OK;
+}
+
+// K6 over the current messages into `out` (zeroed first).
+mrf_status voxel_sums(mrf_ctx* c, long long* out) {
+    ProfScope ps(c, MRF_K_VOXEL_SUM);
+    CK(cudaMemsetAsync(out, 0, sizeof(long long) * c->V, c->stream));
+    launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
+    CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
+    return MRF_OK;
+}
+
+mrf_status ray_messages(mrf_ctx* c) {
+    ProfScope ps(c, MRF_K_RAY_MSG);
+    for (int k = 0; k < kNumClasses; ++k) {
+        if (c->class_n[k] == 0) continue;
+        launch_ray_messages(k, c->class_n[k], c->class_rays[k].p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
+                            c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long,
+                            c->stream);
+        CK_LAUNCH(MRF_K_RAY_MSG, 1);
+    }
+    return MRF_OK;
+}
+
+mrf_status allreduce_T(mrf_ctx* c) {
+    ProfScope ps(c, MRF_K_ALLREDUCE);
+    NCK(ncclAllReduce(c->T_part.p, c->T.p, (size_t)c->V, ncclInt64, ncclSum, c->comm, c->stream));
+    c->prof_launch[MRF_K_ALLREDUCE] += 1;
+    return MRF_OK;
+}
+
+// Rebuild T from the current messages (all ranks).
+mrf_status rebuild_T(mrf_ctx* c) {
+    mrf_status st;
+    if ((st = prepare(c)) != MRF_OK) return st;
+    if (c->world == 1) return voxel_sums(c, c->T.p);
+    if ((st = voxel_sums(c, c->T_part.p)) != MRF_OK) return st;
+    if (c->comm_mode == MRF_COMM_NCCL) return allreduce_T(c);
+    return MRF_OK;  // external mode: caller reduces (mrf_bp_partial / mrf_bp_finish)
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+
+extern "C" {
+
+mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double origin_m[3], float prior,
+                      const mrf_noise_desc* noise, const mrf_dist_desc* dist, mrf_ctx** out) {
+    g_create_error.clear();
+    auto reject = [](const char* m) {
+        g_create_error = m;
+        return MRF_ERR_INVALID_ARG;
+    };
+    if (!out) return reject("out is NULL");
+    *out = nullptr;
+    if (!dims || !origin_m || !noise) return reject("NULL argument");
+    for (int k = 0; k < 3; ++k)
+        if (dims[k] <= 0 || dims[k] > 8192) return reject("dims must be in [1, 8192]");
+    const long long V = (long long)dims[0] * dims[1] * dims[2];
+    if (V >= (1LL << 31)) return reject("nx*ny*nz must be < 2^31");
+    if (!std::isfinite(resolution_m) || !(resolution_m > 0)) return reject("resolution must be finite and > 0");
+    if (!finite_all(origin_m, 3)) return reject("origin must be finite");
+    if (!(prior > 0.f && prior < 1.f)) return reject("prior must be in (0, 1)");
+    if (!noise->log_nu || noise->n_z < 2 || noise->n_off < 2) return reject("noise table must be at least 2x2");
+    const double np_[9] = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min,
+                           noise->margin_k, noise->sigma_c[0], noise->sigma_c[1], noise->sigma_c[2]};
+    if (!finite_all(np_, 9)) return reject("noise parameters must be finite");
+    if (!(noise->z_hi > noise->z_lo)) return reject("z_hi must exceed z_lo");
+    if (!(noise->off_hi > noise->off_lo) || noise->off_lo < -1.0 || noise->off_hi > 1.0)
+        return reject("offset axis must satisfy -1 <= off_lo < off_hi <= 1");
+    if (noise->margin_min < 0 || noise->margin_k < 0) return reject("margin parameters must be >= 0");
+    const long long nlut = (long long)noise->n_z * noise->n_off;
+    for (long long i = 0; i < nlut; ++i)
+        if (!std::isfinite(noise->log_nu[i])) return reject("noise table has non-finite entries");
+    int rank = 0, world = 1, comm_mode = MRF_COMM_NCCL;
+    if (dist) {
+        rank = dist->rank;
+        world = dist->world;
+        comm_mode = dist->comm;
+        if (world < 1 || rank < 0 || rank >= world) return reject("bad rank/world");
+        if (comm_mode != MRF_COMM_NCCL && comm_mode != MRF_COMM_EXTERNAL) return reject("bad comm mode");
+    }
+
+    mrf_ctx* c = new mrf_ctx();
+    cudaGetDevice(&c->device);
+    c->grid = {dims[0], dims[1], dims[2], resolution_m, origin_m[0], origin_m[1], origin_m[2]};
+    c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
+                noise->sigma_c[0], noise->sigma_c[1], noise->sigma_c[2], noise->n_z, noise->n_off};
+    c->V = V;
+    c->prior = prior;
+    c->L0 = std::log((double)prior / (1.0 - (double)prior));
+    c->rank = rank;
+    c->world = world;
+    c->comm_mode = comm_mode;
+    auto fail = [&](mrf_status st) {
+        g_create_error = c->err.empty() ? "mrf_create failed" : c->err;
+        mrf_destroy(c);
+        return st;
+    };
+    if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        c->err = "cudaStreamCreate failed (no CUDA device?)";
+        cudaGetLastError();
+        return fail(MRF_ERR_CUDA);
+    }
+    c->stream = c->own_stream;
+    mrf_status st = MRF_OK;
+    auto alloc = [&]() -> mrf_status {
+        CK(c->T.ensure((size_t)V, 0, c->stream));
+        if (world > 1) CK(c->T_part.ensure((size_t)V, 0, c->stream));
+        CK(c->vox_count.ensure((size_t)V, 0, c->stream));
+        CK(c->cursor.ensure((size_t)V, 0, c->stream));
+        CK(c->n_items.ensure((size_t)V, 0, c->stream));
+        CK(c->col_ptr.ensure((size_t)V + 1, 0, c->stream));
+        CK(c->item_ptr.ensure((size_t)V + 1, 0, c->stream));
+        CK(c->counters.ensure(8, 0, c->stream));
+        CK(c->row_ptr.ensure(1, 0, c->stream));
+        CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * V, c->stream));
+        CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * V, c->stream));
+        CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
+        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 8, c->stream));
+        CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
+        // LUT as (L[i][j], L[i][j+1]) pairs in log2 units: one 8-byte load per LUT row in K5
+        const int nz = noise->n_z, no = noise->n_off;
+        std::vector<float2> h((size_t)nz * (no - 1));
+        for (int i = 0; i < nz; ++i)
+            for (int j = 0; j < no - 1; ++j)
+                h[(size_t)i * (no - 1) + j] = make_float2(noise->log_nu[(size_t)i * no + j] * kLog2e,
+                                                          noise->log_nu[(size_t)i * no + j + 1] * kLog2e);
+        CK(c->lutp.ensure(h.size(), 0, c->stream));
+        CK(cudaMemcpyAsync(c->lutp.p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const double span = noise->off_hi - noise->off_lo;
+        c->mp.lutp = c->lutp.p;
+        c->mp.n_offm1 = no - 1;
+        c->mp.s_off = (float)((double)no / (32768.0 * span));
+        c->mp.b_off = (float)(-noise->off_lo * (double)no / span - 0.5);
+        c->mp.fo_max = (float)(no - 1);
+        c->mp.L0_2 = (float)(c->L0 * (double)kLog2e);
+        return MRF_OK;
+    };
+    if ((st = alloc()) != MRF_OK) return fail(st);
+    if (world > 1 && comm_mode == MRF_COMM_NCCL) {
+        ncclUniqueId id;
+        static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
+        memcpy(id.internal, dist->nccl_id, 128);
+        ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+        if (r != ncclSuccess) {
+            c->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+            c->comm = nullptr;
+            return fail(MRF_ERR_NCCL);
+        }
+    }
+    *out = c;
+    return MRF_OK;
+}
+
+mrf_status mrf_destroy(mrf_ctx* ctx) {
+    if (!ctx) return MRF_OK;
+    mrf_ctx* c = ctx;
+    DeviceGuard guard(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm) ncclCommDestroy(c->comm);
+    for (auto& e : c->events) {
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    c->n_r.release(); c->status.release(); c->ray_z.release(); c->row_ptr.release();
+    c->vid.release(); c->off_q.release(); c->lam.release(); c->tr.release();
+    c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
+    c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release();
+    c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
+    for (auto& b : c->class_rays) b.release();
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return MRF_OK;
+}
+
+const char* mrf_last_error(const mrf_ctx* ctx) {
+    if (!ctx) return g_create_error.c_str();
+    return ctx->err.c_str();
+}
+
+mrf_status mrf_set_stream(mrf_ctx* ctx, void* cuda_stream) {
+    ENTER(ctx);
+    CK(cudaStreamSynchronize(c->stream));
+    c->stream = cuda_stream ? (cudaStream_t)cuda_stream : c->own_stream;
+    return MRF_OK;
+}
+
+mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences) {
+    ENTER(ctx);
+    if (n_rays < 0 || n_incidences < 0) return set_err(c, MRF_ERR_INVALID_ARG, "negative reservation");
+    CK(c->n_r.ensure((size_t)n_rays, (size_t)c->R, c->stream));
+    CK(c->status.ensure((size_t)n_rays, (size_t)c->R, c->stream));
+    CK(c->ray_z.ensure((size_t)n_rays, (size_t)c->R, c->stream));
+    CK(c->row_ptr.ensure((size_t)n_rays + 1, (size_t)c->R + 1, c->stream));
+    CK(c->flags.ensure((size_t)std::max<long long>(n_rays, c->V) + 1, 0, c->stream));
+    CK(c->pos.ensure((size_t)std::max<long long>(n_rays, c->V) + 1, 0, c->stream));
+    const size_t ne = (size_t)n_incidences + kPadElems;
+    CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->lam.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->tr.ensure(ne, 0, c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_reset(mrf_ctx* ctx) {
+    ENTER(ctx);
+    c->R = c->E = 0;
+    c->n_invalid = c->n_dropped = c->n_kept = 0;
+    c->frames.clear();
+    CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * c->V, c->stream));
+    CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * c->V, c->stream));
+    CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
+    c->dirty = true;
+    return MRF_OK;
+}
+
+mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_t height, const double K[4],
+                         const double T_wc[12], int64_t* frame_id_out) {
+    ENTER(ctx);
+    if (!depth || !K || !T_wc) return set_err(c, MRF_ERR_INVALID_ARG, "NULL argument");
+    if (width <= 0 || height <= 0) return set_err(c, MRF_ERR_INVALID_ARG, "width/height must be > 0");
+    if (!finite_all(K, 4) || !(K[0] > 0) || !(K[1] > 0))
+        return set_err(c, MRF_ERR_INVALID_ARG, "K must be finite with fx, fy > 0");
+    if (!finite_all(T_wc, 12)) return set_err(c, MRF_ERR_INVALID_ARG, "T_wc must be finite");
+    // rotation must be orthonormal
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+            double d = 0;
+            for (int k = 0; k < 3; ++k) d += T_wc[4 * k + a] * T_wc[4 * k + b];
+            if (std::fabs(d - (a == b ? 1.0 : 0.0)) > 1e-6)
+                return set_err(c, MRF_ERR_INVALID_ARG, "rotation of T_wc is not orthonormal");
+        }
+    const double org[3] = {c->grid.ox, c->grid.oy, c->grid.oz};
+    const int dims[3] = {c->grid.nx, c->grid.ny, c->grid.nz};
+    for (int k = 0; k < 3; ++k) {
+        const double g = (T_wc[4 * k + 3] - org[k]) / c->grid.res;
+        if (!(g >= 0.0 && g < (double)dims[k]))
+            return set_err(c, MRF_ERR_INVALID_ARG, "camera centre lies outside the grid");
+    }
+    const int rows_owned = height > c->rank ? (height - c->rank + c->world - 1) / c->world : 0;
+    const long long Rf = (long long)rows_owned * width;
+    if (c->R + Rf >= (1LL << 31)) return set_err(c, MRF_ERR_CAPACITY, "ray count would exceed 2^31");
+
+    // depth: device pointer used in place, host memory staged
+    const float* d_depth = depth;
+    cudaPointerAttributes attr;
+    cudaError_t pe = cudaPointerGetAttributes(&attr, depth);
+    if (pe != cudaSuccess) cudaGetLastError();
+    const bool on_device = pe == cudaSuccess && (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
+    const size_t npix = (size_t)width * height;
+    if (!on_device) {
+        CK(c->depth_stage.ensure(npix, 0, c->stream));
+        CK(cudaMemcpyAsync(c->depth_stage.p, depth, npix * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        d_depth = c->depth_stage.p;
+    }
+    CK(c->n_r.ensure((size_t)(c->R + Rf), (size_t)c->R, c->stream));
+    CK(c->status.ensure((size_t)(c->R + Rf), (size_t)c->R, c->stream));
+    CK(c->ray_z.ensure((size_t)(c->R + Rf), (size_t)c->R, c->stream));
+    CK(c->row_ptr.ensure((size_t)(c->R + Rf + 1), (size_t)(c->R + 1), c->stream));
+
+    FrameDesc f{};
+    f.fx = K[0]; f.fy = K[1]; f.cx = K[2]; f.cy = K[3];
+    for (int k = 0; k < 3; ++k) {
+        for (int j = 0; j < 3; ++j) f.R[3 * k + j] = T_wc[4 * k + j];
+        f.C[k] = T_wc[4 * k + 3];
+    }
+    f.W = width; f.H = height; f.rank = c->rank; f.world = c->world;
+    f.rows_owned = rows_owned;
+    f.ray_base = c->R;
+    mrf_status st;
+    CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+    {
+        ProfScope ps(c, MRF_K_RAYGEN_COUNT);
+        launch_raygen_count(f, c->grid, c->noise, d_depth, c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2,
+                            c->stream);
+        CK_LAUNCH(MRF_K_RAYGEN_COUNT, Rf > 0 ? 1 : 0);
+    }
+    if ((st = scan(c, c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->E)) != MRF_OK) return st;
+    CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R + Rf, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2];
+    if (E_new >= (1LL << 31) - kPadElems)
+        return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
+    const size_t ne = (size_t)E_new + kPadElems;
+    CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->lam.ensure(ne, (size_t)c->E, c->stream));
+    CK(cudaMemsetAsync(c->lam.p + c->E, 0, sizeof(int32_t) * (size_t)(E_new - c->E), c->stream));
+    {
+        ProfScope ps(c, MRF_K_DDA_FILL);
+        launch_dda_fill(f, c->grid, c->noise, d_depth, c->row_ptr.p, c->vid.p, c->off_q.p, c->vox_count.p, c->stream);
+        CK_LAUNCH(MRF_K_DDA_FILL, Rf > 0 ? 1 : 0);
+    }
+    if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
+    c->frames.push_back({width, height, rows_owned, c->R, Rf});
+    c->R += Rf;
+    c->E = E_new;
+    c->n_invalid += inv;
+    c->n_dropped += drp;
+    c->n_kept += Rf - inv - drp;
+    c->dirty = true;
+    if (!on_device) CK(cudaStreamSynchronize(c->stream));  // staging buffer reused by the next frame
+    return MRF_OK;
+}
+
+mrf_status mrf_bp_iterate(mrf_ctx* ctx, int32_t n) {
+    ENTER(ctx);
+    if (n < 0) return set_err(c, MRF_ERR_INVALID_ARG, "n must be >= 0");
+    if (c->world > 1 && c->comm_mode != MRF_COMM_NCCL)
+        return set_err(c, MRF_ERR_STATE, "external comm mode: use mrf_bp_partial / mrf_bp_finish");
+    mrf_status st;
+    if ((st = prepare(c)) != MRF_OK) return st;
+    for (int it = 0; it < n; ++it) {
+        if ((st = ray_messages(c)) != MRF_OK) return st;
+        if (c->world == 1) {
+            if ((st = voxel_sums(c, c->T.p)) != MRF_OK) return st;
+        } else {
+            if ((st = voxel_sums(c, c->T_part.p)) != MRF_OK) return st;
+            if ((st = allreduce_T(c)) != MRF_OK) return st;
+        }
+    }
+    return MRF_OK;
+}
+
+mrf_status mrf_bp_partial(mrf_ctx* ctx, int32_t iterate, int64_t* partial_out_device) {
+    ENTER(ctx);
+    if (!partial_out_device) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    mrf_status st;
+    if ((st = prepare(c)) != MRF_OK) return st;
+    if (iterate && (st = ray_messages(c)) != MRF_OK) return st;
+    return voxel_sums(c, reinterpret_cast<long long*>(partial_out_device));
+}
+
+mrf_status mrf_bp_finish(mrf_ctx* ctx, const int64_t* total_device) {
+    ENTER(ctx);
+    if (!total_device) return set_err(c, MRF_ERR_INVALID_ARG, "NULL input");
+    CK(cudaMemcpyAsync(c->T.p, total_device, sizeof(long long) * c->V, cudaMemcpyDeviceToDevice, c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_marginals(mrf_ctx* ctx, float* out, int32_t out_is_device) {
+    ENTER(ctx);
+    if (!out) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    float* dst = out;
+    if (!out_is_device) {
+        CK(c->marg.ensure((size_t)c->V, 0, c->stream));
+        dst = c->marg.p;
+    }
+    {
+        ProfScope ps(c, MRF_K_MARGINALS);
+        launch_marginals(c->V, c->T.p, c->L0, dst, c->stream);
+        CK_LAUNCH(MRF_K_MARGINALS, 1);
+    }
+    if (!out_is_device)
+        CK(cudaMemcpyAsync(out, dst, sizeof(float) * c->V, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences, int64_t* n_active_vox,
+                           int64_t* n_invalid, int64_t* n_dropped) {
+    ENTER(ctx);
+    if (n_rays) *n_rays = c->n_kept;
+    if (n_incidences) *n_incidences = c->E;
+    if (n_invalid) *n_invalid = c->n_invalid;
+    if (n_dropped) *n_dropped = c->n_dropped;
+    if (n_active_vox) {
+        CK(c->flags.ensure((size_t)c->V + 1, 0, c->stream));
+        CK(c->pos.ensure((size_t)c->V + 1, 0, c->stream));
+        launch_active_flags(c->V, c->vox_count.p, c->flags.p, c->stream);
+        CK_LAUNCH(MRF_K_SCAN, 1);
+        mrf_status st;
+        if ((st = scan(c, c->flags.p, c->pos.p, c->V, 0)) != MRF_OK) return st;
+        long long a = 0;
+        if ((st = read_ll(c, c->pos.p + c->V, &a)) != MRF_OK) return st;
+        *n_active_vox = a;
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, int32_t* vid, int16_t* off_q) {
+    ENTER(ctx);
+    if (ray_pixel || row_ptr) {
+        std::vector<long long> rp((size_t)c->R + 1);
+        std::vector<int8_t> stv((size_t)c->R);
+        CK(cudaMemcpyAsync(rp.data(), c->row_ptr.p, sizeof(long long) * (c->R + 1), cudaMemcpyDeviceToHost, c->stream));
+        if (c->R) CK(cudaMemcpyAsync(stv.data(), c->status.p, c->R, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        long long k = 0;
+        for (size_t fi = 0; fi < c->frames.size(); ++fi) {
+            const FrameRec& fr = c->frames[fi];
+            for (long long i = 0; i < fr.n_rays; ++i) {
+                const long long r = fr.ray_base + i;
+                if (stv[r] != 0) continue;
+                const long long lr = i / fr.W, u = i % fr.W, v = c->rank + lr * c->world;
+                if (ray_pixel) ray_pixel[k] = ((long long)fi << 32) | (v * fr.W + u);
+                if (row_ptr) row_ptr[k] = rp[r];
+                ++k;
+            }
+        }
+        if (row_ptr) row_ptr[k] = c->E;
+    }
+    if (vid && c->E) CK(cudaMemcpyAsync(vid, c->vid.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+    if (off_q && c->E) CK(cudaMemcpyAsync(off_q, c->off_q.p, sizeof(int16_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr) {
+    ENTER(ctx);
+    mrf_status st;
+    if ((st = prepare(c)) != MRF_OK) return st;
+    if (col_ptr) CK(cudaMemcpyAsync(col_ptr, c->col_ptr.p, sizeof(long long) * (c->V + 1), cudaMemcpyDeviceToHost, c->stream));
+    if (tr && c->E) CK(cudaMemcpyAsync(tr, c->tr.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda) {
+    ENTER(ctx);
+    if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    if (!c->E) return MRF_OK;
+    std::vector<int32_t> q((size_t)c->E);
+    CK(cudaMemcpyAsync(q.data(), c->lam.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (long long e = 0; e < c->E; ++e) lambda[e] = (float)((double)q[e] * kQInvD);
+    return MRF_OK;
+}
+
+mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda) {
+    ENTER(ctx);
+    if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL input");
+    std::vector<int32_t> q((size_t)c->E);
+    for (long long e = 0; e < c->E; ++e) {
+        double x = lambda[e];
+        if (!std::isfinite(x)) return set_err(c, MRF_ERR_INVALID_ARG, "non-finite message");
+        x = std::min(256.0, std::max(-256.0, x)) * 8388608.0;
+        const double r = std::nearbyint(x);
+        q[e] = r >= 2147483647.0 ? 2147483647 : (int32_t)r;
+    }
+    if (c->E) CK(cudaMemcpyAsync(c->lam.p, q.data(), sizeof(int32_t) * c->E, cudaMemcpyHostToDevice, c->stream));
+    mrf_status st = rebuild_T(c);
+    CK(cudaStreamSynchronize(c->stream));
+    return st;
+}
+
+mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T) {
+    ENTER(ctx);
+    if (!T) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    CK(cudaMemcpyAsync(T, c->T.p, sizeof(long long) * c->V, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_nccl_unique_id(unsigned char out[128]) {
+    if (!out) return MRF_ERR_INVALID_ARG;
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MRF_ERR_NCCL;
+    memcpy(out, id.internal, 128);
+    return MRF_OK;
+}
+
+mrf_status mrf_set_profiling(mrf_ctx* ctx, int32_t on) {
+    ENTER(ctx);
+    c->prof = on != 0;
+    return MRF_OK;
+}
+
+mrf_status mrf_profile_read(mrf_ctx* ctx, int64_t* launches, double* total_ms) {
+    ENTER(ctx);
+    CK(cudaStreamSynchronize(c->stream));
+    for (auto& e : c->events) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e.a, e.b));
+        c->prof_ms[e.kind] += ms;
+        cudaEventDestroy(e.a);
+        cudaEventDestroy(e.b);
+    }
+    c->events.clear();
+    for (int k = 0; k < MRF_K_COUNT; ++k) {
+        if (launches) launches[k] = c->prof_launch[k];
+        if (total_ms) total_ms[k] = c->prof_ms[k];
+        c->prof_launch[k] = 0;
+        c->prof_ms[k] = 0.0;
+    }
+    return MRF_OK;
+}
+
+int64_t mrf_launch_count(const mrf_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,331 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle.
+
+Bars (BASELINE.json north_star): ray->voxel index lists and offsets bit-exact; messages
+|dlambda| <= 1e-3 * max(1, |lambda|); marginals within 1e-4 absolute.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2006_03512_b200 as pkg  # noqa: E402
+from synth.scenes import Frame  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MSG_TOL = 1e-3
+MARG_TOL = 1e-4
+
+
+def _gpu_map(w, frames=None, **kw):
+    m = pkg.MRFMap.from_workload(w, **kw)
+    for fr in (w.frames if frames is None else frames):
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+    return m
+
+
+def _assert_graph_equal(gg, g):
+    assert np.array_equal(gg["row_ptr"], g.row_ptr)
+    assert np.array_equal(gg["frame"], g.frame)
+    assert np.array_equal(gg["pixel"], g.pixel)
+    assert np.array_equal(gg["vid"], g.vid)
+    assert np.array_equal(gg["off_q"], g.off_q)
+
+
+def _assert_msgs_close(lam_gpu, lam_ref):
+    err = np.abs(lam_gpu.astype(np.float64) - lam_ref) / np.maximum(1.0, np.abs(lam_ref))
+    assert err.max() <= MSG_TOL, f"max rel msg err {err.max():.3e} at {int(err.argmax())}"
+    return float(err.max())
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    return synth.tiny()
+
+
+@pytest.fixture(scope="module")
+def frame1():
+    return synth.single_frame()
+
+
+def test_tiny_graph_bitexact(tiny):
+    p = oracle.Params.from_workload(tiny)
+    g = oracle.build_graph(p, tiny.frames)
+    with _gpu_map(tiny) as m:
+        _assert_graph_equal(m.export_graph(), g)
+        s = m.graph_sizes()
+        assert s["n_invalid"] == g.n_invalid and s["n_dropped"] == g.n_dropped and s["E"] == g.E
+        assert s["n_active"] == len(np.unique(g.vid))
+
+
+def test_tiny_transpose_is_exact_permutation(tiny):
+    p = oracle.Params.from_workload(tiny)
+    g = oracle.build_graph(p, tiny.frames)
+    with _gpu_map(tiny) as m:
+        col_ptr, tr = m.export_transpose()
+    deg = np.bincount(g.vid, minlength=p.V)
+    assert np.array_equal(col_ptr, np.concatenate([[0], np.cumsum(deg)]))
+    assert np.array_equal(g.vid[tr], np.repeat(np.arange(p.V), deg))          # every entry in its column
+    assert np.array_equal(np.sort(tr), np.arange(g.E))                         # each incidence once
+
+
+@pytest.mark.parametrize("n_iter", [1, 3, 10])
+def test_tiny_bp_parity(tiny, n_iter):
+    p = oracle.Params.from_workload(tiny)
+    g = oracle.build_graph(p, tiny.frames)
+    lam_ref, T_ref = oracle.bp(p, g, n_iter)
+    with _gpu_map(tiny) as m:
+        m.bp_iterate(n_iter)
+        lam = m.export_messages()
+        marg = m.marginals()
+    _assert_msgs_close(lam, lam_ref)
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+def test_frame1_graph_and_bp_parity(frame1):
+    w = frame1
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    lam_ref, T_ref = oracle.bp(p, g, w.n_iter)
+    with _gpu_map(w) as m:
+        _assert_graph_equal(m.export_graph(), g)
+        m.bp_iterate(w.n_iter)
+        lam = m.export_messages()
+        marg = m.marginals()
+    _assert_msgs_close(lam, lam_ref)
+    d = np.abs(marg - oracle.marginals(p, T_ref))
+    assert d.max() <= MARG_TOL, f"max marginal err {d.max():.3e}"
+
+
+def test_one_step_parity_from_gpu_state(frame1):
+    """T3: both sides start from the same messages (GPU state after 4 iterations)."""
+    w = frame1
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    with _gpu_map(w) as m:
+        m.bp_iterate(4)
+        lam0 = m.export_messages()
+        m.import_messages(lam0)        # quantise exactly as the GPU holds it
+        lam0 = m.export_messages()
+        m.bp_iterate(1)
+        lam1 = m.export_messages()
+    lam = lam0.astype(np.float64)
+    T = oracle.accumulate(p, g, lam)
+    oracle.ray_pass(p, g, T, lam)
+    _assert_msgs_close(lam1, lam)
+
+
+def test_determinism(frame1):
+    outs = []
+    for _ in range(2):
+        with _gpu_map(frame1) as m:
+            m.bp_iterate(3)
+            outs.append((m.export_beliefs(), m.export_messages(), m.marginals()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+def test_warm_start_matches_oracle(frame1):
+    """A frame added after iterations starts with lambda = 0 (warm start of the others)."""
+    w = synth.frames30(n_frames=2)
+    p = oracle.Params.from_workload(w)
+    g1 = oracle.build_graph(p, w.frames[:1])
+    g2 = oracle.build_graph(p, w.frames)
+    lam1, _ = oracle.bp(p, g1, 3)
+    lam_start = np.concatenate([lam1, np.zeros(g2.E - g1.E)])
+    lam2, T2 = oracle.bp(p, g2, 3, lam=lam_start)
+    with _gpu_map(w, frames=w.frames[:1]) as m:
+        m.bp_iterate(3)
+        m.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
+        m.bp_iterate(3)
+        _assert_graph_equal(m.export_graph(), g2)
+        _assert_msgs_close(m.export_messages(), lam2)
+        assert np.max(np.abs(m.marginals() - oracle.marginals(p, T2))) <= MARG_TOL
+
+
+def _corridor(n_vox=1100, res=0.01, wall_vox=1050.3):
+    """Long rays (> 512 cells -> tiled class) down a 1-D corridor grid."""
+    dims = (n_vox, 8, 8)
+    C = np.array([0.002, 0.04, 0.04])
+    R = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
+    W, H, K = 6, 4, (2000.0, 2000.0, 2.5, 1.5)
+    depth = np.full((H, W), wall_vox * res - C[0], np.float32)
+    depth[0, 0] = 0.0
+    lut = synth.build_log_nu_lut(32, 128, 0.0, 12.0, -1.0, 1.0, (0.005, 0.0, 0.0), 0.0)
+    w = synth.Workload("corridor", dims, res, (0, 0, 0), 0.1, lut, 0.0, 12.0, -1.0, 1.0, 0.1, 3.0,
+                       (0.005, 0.0, 0.0), 5, [Frame(depth, np.array(K), np.concatenate([R, C[:, None]], 1).reshape(-1))])
+    return w
+
+
+def test_long_rays_tiled_class():
+    w = _corridor()
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    assert np.diff(g.row_ptr).max() > 512
+    lam_ref, T_ref = oracle.bp(p, g, w.n_iter)
+    with _gpu_map(w) as m:
+        _assert_graph_equal(m.export_graph(), g)
+        m.bp_iterate(w.n_iter)
+        _assert_msgs_close(m.export_messages(), lam_ref)
+        assert np.max(np.abs(m.marginals() - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+@pytest.mark.parametrize("wall_vox", [130.4, 250.7, 400.2])
+def test_medium_rays_k8_k16_classes(wall_vox):
+    w = _corridor(n_vox=480, wall_vox=wall_vox)
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    lam_ref, T_ref = oracle.bp(p, g, w.n_iter)
+    with _gpu_map(w) as m:
+        m.bp_iterate(w.n_iter)
+        _assert_msgs_close(m.export_messages(), lam_ref)
+        assert np.max(np.abs(m.marginals() - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+def test_rays_leaving_the_grid_and_invalid_frames(tiny):
+    """Margin past the far face: the walk stops at the grid exit; all-invalid frame adds nothing."""
+    fr = tiny.frames[0]
+    depth = fr.depth.copy()
+    depth[depth > 0] = np.float32(1.58 - 0.8)  # wall 2 cm inside the far face; margin 0.1 m leaves the grid
+    frames = [Frame(depth, fr.K, fr.T_wc), Frame(np.zeros_like(depth), fr.K, fr.T_wc),
+              Frame(np.full_like(depth, np.nan), fr.K, fr.T_wc)]
+    p = oracle.Params.from_workload(tiny)
+    g = oracle.build_graph(p, frames)
+    lam_ref, T_ref = oracle.bp(p, g, 4)
+    with _gpu_map(tiny, frames=frames) as m:
+        _assert_graph_equal(m.export_graph(), g)
+        assert m.graph_sizes()["n_invalid"] == g.n_invalid
+        m.bp_iterate(4)
+        _assert_msgs_close(m.export_messages(), lam_ref)
+
+
+def test_empty_map_returns_prior(tiny):
+    with pkg.MRFMap.from_workload(tiny) as m:
+        m.bp_iterate(3)
+        assert np.all(m.marginals() == np.float32(tiny.prior))
+
+
+def test_invalid_frames_are_rejected_without_state_change(tiny):
+    fr = tiny.frames[0]
+    with _gpu_map(tiny) as m:
+        before = m.graph_sizes()
+        bad = fr.T_wc.copy()
+        bad[0] = 2.0  # not a rotation
+        with pytest.raises(pkg.MrfError):
+            m.add_frame(fr.depth, fr.K, bad)
+        outside = fr.T_wc.copy()
+        outside[3] = -1.0  # camera outside the grid
+        with pytest.raises(pkg.MrfError):
+            m.add_frame(fr.depth, fr.K, outside)
+        with pytest.raises(pkg.MrfError):
+            m.add_frame(fr.depth, (0.0, 60.0, 32.0, 24.0), fr.T_wc)
+        with pytest.raises(pkg.MrfError):
+            m.bp_iterate(-1)
+        assert m.graph_sizes() == before
+        m.bp_iterate(2)  # still usable
+
+
+def test_device_and_host_inputs_agree(tiny):
+    fr = tiny.frames[0]
+    with pkg.MRFMap.from_workload(tiny) as a, pkg.MRFMap.from_workload(tiny) as b:
+        a.add_frame(fr.depth, fr.K, fr.T_wc)
+        b.add_frame(torch.from_numpy(fr.depth).cuda(), fr.K, fr.T_wc)
+        a.bp_iterate(3)
+        b.bp_iterate(3)
+        out = torch.empty(tiny.n_voxels, device="cuda")
+        b.marginals(out)
+        assert np.array_equal(a.marginals(), out.cpu().numpy())
+
+
+def test_virtual_ranks_bit_identical_beliefs(frame1):
+    """T5: rows sharded over 2 and 3 emulated ranks (external reduce) give bit-identical T."""
+    w = synth.frames30(n_frames=2)
+    with _gpu_map(w) as m:
+        m.bp_iterate(3)
+        T1 = m.export_beliefs()
+        marg1 = m.marginals()
+    for world in (2, 3):
+        maps = [_gpu_map(w, rank=r, world=world, comm=pkg.MRF_COMM_EXTERNAL) for r in range(world)]
+        parts = [torch.empty(w.n_voxels, dtype=torch.int64, device="cuda") for _ in range(world)]
+        for _ in range(3):
+            for m, part in zip(maps, parts):
+                m.bp_partial(part, iterate=True)
+            total = torch.stack(parts).sum(0)
+            for m in maps:
+                m.bp_finish(total)
+        for m in maps:
+            assert np.array_equal(m.export_beliefs(), T1)
+            assert np.array_equal(m.marginals(), marg1)
+        E = sum(m.graph_sizes()["E"] for m in maps)
+        for m in maps:
+            m.close()
+        p = oracle.Params.from_workload(w)
+        assert E == oracle.build_graph(p, w.frames).E
+
+
+def test_profiling_and_launch_counts(tiny):
+    with _gpu_map(tiny) as m:
+        m.set_profiling(True)
+        n0 = m.launch_count()
+        m.bp_iterate(2)
+        prof = m.profile_read()
+        assert prof["ray_messages"][0] >= 2 and prof["voxel_sum"][0] == 2
+        assert prof["ray_messages"][1] > 0
+        assert m.launch_count() > n0
+
+
+# ------------------------------------------------------------------ full size (bench config)
+
+@pytest.fixture(scope="module")
+def f30():
+    return synth.frames30()
+
+
+def test_frames30_sampled_graph_and_one_step(f30):
+    """Full 30-frame config as bench.py runs it: sampled rays traced one by one by the oracle
+    (bit-exact), and a one-step message update on those rays from the GPU state."""
+    w = f30
+    p = oracle.Params.from_workload(w)
+    rng = np.random.default_rng(0)
+    with _gpu_map(w) as m:
+        gg = m.export_graph()
+        m.bp_iterate(5)
+        lam0 = m.export_messages()
+        m.import_messages(lam0)
+        lam0 = m.export_messages()
+        m.bp_iterate(1)
+        lam1 = m.export_messages()
+        marg = m.marginals()
+        s = m.graph_sizes()
+    n_rays = len(gg["row_ptr"]) - 1
+    sel = np.sort(rng.choice(n_rays, 4000, replace=False))
+    # graph: per sampled ray, trace with the oracle and compare
+    subs = []
+    for fi in np.unique(gg["frame"][sel]):
+        rs = sel[gg["frame"][sel] == fi]
+        sub = oracle.trace_pixels(p, w.frames[fi], gg["pixel"][rs], fi)
+        assert sub.n_rays == len(rs)
+        for k, r in enumerate(rs):
+            a, b = gg["row_ptr"][r], gg["row_ptr"][r + 1]
+            assert np.array_equal(gg["vid"][a:b], sub.vid[sub.row_ptr[k]:sub.row_ptr[k + 1]])
+            assert np.array_equal(gg["off_q"][a:b], sub.off_q[sub.row_ptr[k]:sub.row_ptr[k + 1]])
+        subs.append((rs, sub))
+    # one step on the sampled rays from the same state
+    full = oracle.Graph(gg["row_ptr"], gg["vid"], gg["off_q"], np.zeros(n_rays), gg["frame"], gg["pixel"], 0, 0)
+    T = oracle.accumulate(p, full, lam0.astype(np.float64))
+    for rs, sub in subs:
+        lam_sub = np.concatenate([lam0[gg["row_ptr"][r]:gg["row_ptr"][r + 1]] for r in rs]).astype(np.float64)
+        oracle.ray_pass(p, sub, T, lam_sub)
+        got = np.concatenate([lam1[gg["row_ptr"][r]:gg["row_ptr"][r + 1]] for r in rs])
+        _assert_msgs_close(got, lam_sub)
+    # properties at full size
+    assert np.all((marg >= 0) & (marg <= 1))
+    seen = np.zeros(p.V, bool)
+    seen[gg["vid"]] = True
+    assert np.all(marg[~seen] == np.float32(w.prior))
+    assert s["E"] == len(gg["vid"]) and s["n_active"] == int(seen.sum())
