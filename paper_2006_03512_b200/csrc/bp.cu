@@ -5,20 +5,23 @@
 // rewritten for a parallel scan.  For the voxels i = 1..N of a ray, with the
 // cavity log-odds c_i = L0 + T_v - lambda_i (Eq.6), mu(o_i=1) = sigma(c_i),
 // mu(o_i=0) = sigma(-c_i) (normalised incoming messages) and nu_i from the LUT:
-//     p_i = log(1 + e^{c_i}) = -log mu(o_i=0),   x_i = c_i + log nu_i
-//     Q_i = P_i / V_i,  Q_1 = 0,  Q_{i+1} = e^{p_i} Q_i + e^{x_i}          (prefix, "visibility")
+//     a_i = mu(o_i=0),  w_i = mu(o_i=1) nu_i
+//     Q_i = P_i / V_i,  Q_1 = 0,  Q_{i+1} = (Q_i + w_i) / a_i                 (prefix, "visibility")
 //     R_i = sum_{j>i} mu(o_j=1) nu_j prod_{i<k<j} mu(o_k=0),
-//           R_N = 0,  R_{i-1} = e^{-p_i} (R_i + e^{x_i})                    (suffix)
+//           R_N = 0,  R_{i-1} = a_i R_i + w_i                                  (suffix)
 //     lambda_i = log mu_{psi->o_i}(1) - log mu_{psi->o_i}(0) = log(Q_i + nu_i) - log(Q_i + R_i)
 // where P_i = sum_{j<i} mu(o_j=1) nu_j V_j and V_i = prod_{k<i} mu(o_k=0) are the terms of
 // Eq.13/14; dividing both messages by V_i leaves the log-odds unchanged and keeps every
 // quantity O(1) in the log domain.  Both recurrences are affine maps x -> 2^a x + 2^b, so a warp
 // composes per-lane chunks and runs two 5-level shuffle scans (prefix for Q, suffix for R).
-// Everything is evaluated in base-2 logs with ex2/lg2.approx (MUFU).
+// Everything is evaluated in base-2 logs: ex2.approx on the MUFU, log2(1+y) as a polynomial on
+// the FMA pipe (relative accuracy, see log1p2), and lambda without cancellation (lambda2).
 //
-// Layout: warp per ray; lane l owns the K consecutive incidences starting at the K-aligned
-// absolute index (e0 & ~(K-1)) + l*K, so vid/lambda are read as 16-byte vectors without any
-// per-ray padding (elements outside [e0, e1) are masked to the identity map).  Rays are
+// Layout: warp per ray; lane l owns the K consecutive incidences [e0 + l*K, e0 + l*K + K) of
+// the ray; ray segments start at multiples of 4 (RayInfo), so vid/lambda are read as 16-byte
+// vectors and the partition -- hence every rounding -- is independent of where the ray is
+// stored (bit-identical results for any rank count).  Elements past e1 are masked to the
+// identity map.  Rays are
 // bucketed by span into K = 4 / 8 / 16 (single tile of 32K in registers); longer rays run a
 // tiled two-pass variant with the suffix values staged in a per-warp global scratch.
 #include "internal.cuh"
@@ -39,13 +42,25 @@ __device__ __forceinline__ float lg2(float x) {
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// log2(1 + y) for y in [0, 1] with RELATIVE accuracy (~2e-7), on the FMA pipe:
+// y * P(y), P a degree-8 fit of log2(1+y)/y (lg2.approx(1+y) is only absolutely accurate
+// near 1, which biased the tiny messages of occluded voxels).
+__device__ __forceinline__ float log1p2(float y) {
+    float r = 0.00754914153367281f;
+    r = fmaf(r, y, -0.04256688803434372f);
+    r = fmaf(r, y, 0.11285588890314102f);
+    r = fmaf(r, y, -0.19711868464946747f);
+    r = fmaf(r, y, 0.2756412625312805f);
+    r = fmaf(r, y, -0.3584084212779999f);
+    r = fmaf(r, y, 0.48069295287132263f);
+    r = fmaf(r, y, -0.7213401794433594f);
+    r = fmaf(r, y, 1.4426950216293335f);
+    return r * y;
+}
 // log2(2^a + 2^b)
 __device__ __forceinline__ float lse2(float a, float b) {
-    const float m = fmaxf(a, b);
-    return m + lg2(1.0f + ex2(-fabsf(a - b)));
+    return fmaxf(a, b) + log1p2(ex2(-fabsf(a - b)));
 }
-// log2(1 + 2^c)
-__device__ __forceinline__ float softplus2(float c) { return fmaxf(c, 0.0f) + lg2(1.0f + ex2(-fabsf(c))); }
 
 // Affine map x -> 2^a x + 2^b in log2 form.
 struct Aff {
@@ -66,18 +81,20 @@ __device__ __forceinline__ Aff shfl_idx(Aff v, int l) {
 }
 
 // ---------------------------------------------------------------- per-lane element loads
-// Computes, for the K elements [s, s+K) of this lane: p = softplus2(c), x = c + lnu (both log2)
-// and lnu; masked elements get the identity (p = 0, x = NEG).
+// For the K elements [s, s+K) of this lane (log2 units):
+//   la = log mu(o=0) = -softplus(c),  w = log mu(o=1) + log nu,  l = log nu.
+// la and log mu(o=1) share one ex2 and are both computed directly, never as a difference of
+// two large numbers.  Masked elements get the identity maps (la = 0, w = NEG).
 template <int K>
 __device__ __forceinline__ void load_elems(long long s, long long e0, long long e1, const float2* __restrict__ rowA,
                                            const float2* __restrict__ rowB, float wz, const MsgParams& mp,
                                            const int32_t* __restrict__ vid, const int16_t* __restrict__ off_q,
                                            const int32_t* __restrict__ lam, const long long* __restrict__ T,
-                                           float (&x)[K], float (&p)[K], float (&l)[K]) {
+                                           float (&la)[K], float (&w)[K], float (&l)[K]) {
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        x[j] = kNeg;
-        p[j] = 0.f;
+        la[j] = 0.f;
+        w[j] = kNeg;
         l[j] = kNeg;
     }
     if (s + K <= e0 || s >= e1) return;
@@ -110,31 +127,33 @@ __device__ __forceinline__ void load_elems(long long s, long long e0, long long 
             const int io = min((int)fo, mp.n_offm1 - 1);
             const float wo = fo - (float)io;
             const float2 ta = __ldg(rowA + io), tb = __ldg(rowB + io);
-            const float la = fmaf(wo, ta.y - ta.x, ta.x);
-            const float lb = fmaf(wo, tb.y - tb.x, tb.x);
-            const float lnu = fmaf(wz, lb - la, la);
-            p[j] = softplus2(c2);
-            x[j] = c2 + lnu;
+            const float ra = fmaf(wo, ta.y - ta.x, ta.x);
+            const float rb = fmaf(wo, tb.y - tb.x, tb.x);
+            const float lnu = fmaf(wz, rb - ra, ra);
+            const float L1 = log1p2(ex2(-fabsf(c2)));
+            la[j] = -(fmaxf(c2, 0.f) + L1);
+            w[j] = lnu - (fmaxf(-c2, 0.f) + L1);
             l[j] = lnu;
         }
     }
 }
 
-// Lane composite: S = sum p, bB = log2 sum_j 2^{x_j - sum_{k<=j} p_k}.  The suffix (R) map of
-// the chunk is (-S, bB); the prefix (Q) map is (S, bB + S).
+// Lane composite of the suffix maps R -> 2^{la} R + 2^{w} over the chunk (first applied last):
+// aB = sum la, bB = log2 sum_j 2^{w_j + sum_{k<j} la_k}.  The prefix maps
+// Q -> 2^{-la} (Q + 2^{w}) compose to (-aB, bB - aB).
 template <int K>
-__device__ __forceinline__ void lane_composite(const float (&x)[K], const float (&p)[K], float& S, float& bB) {
+__device__ __forceinline__ void lane_composite(const float (&la)[K], const float (&w)[K], float& aB, float& bB) {
     float acc = 0.f, m = kNeg, t[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        acc += p[j];
-        t[j] = x[j] - acc;
+        t[j] = w[j] + acc;
+        acc += la[j];
         m = fmaxf(m, t[j]);
     }
     float sum = 0.f;
 #pragma unroll
     for (int j = 0; j < K; ++j) sum += ex2(t[j] - m);
-    S = acc;
+    aB = acc;
     bB = m + lg2(sum);
 }
 
@@ -174,23 +193,30 @@ __device__ __forceinline__ float prefix_in(Aff F, int lane, float Qc, float* car
 }
 
 template <int K>
-__device__ __forceinline__ void lane_suffix(const float (&x)[K], const float (&p)[K], float Rin, float (&lR)[K]) {
+__device__ __forceinline__ void lane_suffix(const float (&la)[K], const float (&w)[K], float Rin, float (&lR)[K]) {
     float R = Rin;
 #pragma unroll
     for (int j = K - 1; j >= 0; --j) {
-        lR[j] = R;  // log2 R_j: suffix strictly after element j
-        R = lse2(R, x[j]) - p[j];
+        lR[j] = R;                      // log2 R_j: suffix strictly after element j
+        R = lse2(la[j] + R, w[j]);      // R_{j-1} = mu(o_j=0) R_j + mu(o_j=1) nu_j
     }
 }
 
-__device__ __forceinline__ int32_t quantise(float lam2_diff) {
-    float lam = lam2_diff * kLn2;
+// lambda2 = log2(2^Q + 2^l) - log2(2^Q + 2^R) without cancellation: the max parts subtract
+// exactly (both are Q when Q dominates) and the remainders are small, accurate log1p terms.
+__device__ __forceinline__ float lambda2(float Q, float l, float R) {
+    const float m1 = fmaxf(Q, l), m2 = fmaxf(Q, R);
+    return (m1 - m2) + (log1p2(ex2(-fabsf(Q - l))) - log1p2(ex2(-fabsf(Q - R))));
+}
+
+__device__ __forceinline__ int32_t quantise(float lam2) {
+    float lam = lam2 * kLn2;
     lam = fminf(fmaxf(lam, -kLambdaClip), kLambdaClip);
     return __float2int_rn(lam * kQScale);  // saturates at +2^31-1 for +256
 }
 
 template <int K>
-__device__ __forceinline__ void lane_prefix_out(const float (&x)[K], const float (&p)[K], const float (&l)[K],
+__device__ __forceinline__ void lane_prefix_out(const float (&la)[K], const float (&w)[K], const float (&l)[K],
                                                 const float (&lR)[K], float Qin, long long s, long long e0,
                                                 long long e1, int32_t* lam) {
     float Q = Qin;
@@ -198,8 +224,8 @@ __device__ __forceinline__ void lane_prefix_out(const float (&x)[K], const float
 #pragma unroll
     for (int j = 0; j < K; ++j) {
         // lambda_j = log(Q_j + nu_j) - log(Q_j + R_j)   (Eq.13 / Eq.14, both divided by V_j)
-        out[j] = quantise(lse2(Q, l[j]) - lse2(Q, lR[j]));
-        Q = lse2(Q + p[j], x[j]);
+        out[j] = quantise(lambda2(Q, l[j], lR[j]));
+        Q = lse2(Q, w[j]) - la[j];      // Q_{j+1} = (Q_j + mu(o_j=1) nu_j) / mu(o_j=0)
     }
     if (s >= e0 && s + K <= e1) {
 #pragma unroll
@@ -216,27 +242,27 @@ __device__ __forceinline__ void lane_prefix_out(const float (&x)[K], const float
 template <int K>
 __global__ void __launch_bounds__(256) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                       const long long* __restrict__ row_ptr,
-                                                      const RayZ* __restrict__ ray_z,
+                                                      const RayInfo* __restrict__ ray_z,
                                                       const int32_t* __restrict__ vid,
                                                       const int16_t* __restrict__ off_q, int32_t* lam,
                                                       const long long* __restrict__ T, MsgParams mp) {
-    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (w >= n) return;
+    const long long wi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wi >= n) return;
     const int lane = threadIdx.x & 31;
-    const int r = __ldg(rays + w);
-    const long long e0 = __ldg(row_ptr + r), e1 = __ldg(row_ptr + r + 1);
-    const RayZ rz = ray_z[r];
+    const int r = __ldg(rays + wi);
+    const RayInfo rz = ray_z[r];
+    const long long e0 = __ldg(row_ptr + r), e1 = e0 + rz.n;
     const float2* rowA = mp.lutp + (long long)rz.iz * mp.n_offm1;
     const float2* rowB = rowA + mp.n_offm1;
-    const long long s = (e0 & ~(long long)(K - 1)) + (long long)lane * K;
-    float x[K], p[K], l[K], lR[K];
-    load_elems<K>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, x, p, l);
-    float S, bB;
-    lane_composite<K>(x, p, S, bB);
-    const float Rin = suffix_in({-S, bB}, lane, kNeg, nullptr);
-    lane_suffix<K>(x, p, Rin, lR);
-    const float Qin = prefix_in({S, bB + S}, lane, kNeg, nullptr);
-    lane_prefix_out<K>(x, p, l, lR, Qin, s, e0, e1, lam);
+    const long long s = e0 + (long long)lane * K;
+    float la[K], w[K], l[K], lR[K];
+    load_elems<K>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
+    float aB, bB;
+    lane_composite<K>(la, w, aB, bB);
+    const float Rin = suffix_in({aB, bB}, lane, kNeg, nullptr);
+    lane_suffix<K>(la, w, Rin, lR);
+    const float Qin = prefix_in({-aB, bB - aB}, lane, kNeg, nullptr);
+    lane_prefix_out<K>(la, w, l, lR, Qin, s, e0, e1, lam);
 }
 
 // ---------------------------------------------------------------- K5: long rays (tiled)
@@ -245,7 +271,7 @@ constexpr int kLongTile = 32 * kLongK;
 
 __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const int32_t* __restrict__ rays,
                                                            const long long* __restrict__ row_ptr,
-                                                           const RayZ* __restrict__ ray_z,
+                                                           const RayInfo* __restrict__ ray_z,
                                                            const int32_t* __restrict__ vid,
                                                            const int16_t* __restrict__ off_q, int32_t* lam,
                                                            const long long* __restrict__ T, MsgParams mp,
@@ -254,26 +280,26 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
     const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
     float* my_scratch = scratch + gw * scratch_per_warp;
-    for (long long w = gw; w < n; w += n_warps) {
-        const int r = __ldg(rays + w);
-        const long long e0 = __ldg(row_ptr + r), e1 = __ldg(row_ptr + r + 1);
-        const RayZ rz = ray_z[r];
+    for (long long wi = gw; wi < n; wi += n_warps) {
+        const int r = __ldg(rays + wi);
+        const RayInfo rz = ray_z[r];
+        const long long e0 = __ldg(row_ptr + r), e1 = e0 + rz.n;
         const float2* rowA = mp.lutp + (long long)rz.iz * mp.n_offm1;
         const float2* rowB = rowA + mp.n_offm1;
-        const long long base = e0 & ~(long long)(kLongK - 1);
+        const long long base = e0;
         const int n_tiles = (int)((e1 - base + kLongTile - 1) / kLongTile);
-        float x[kLongK], p[kLongK], l[kLongK], lR[kLongK];
-        float S, bB;
+        float la[kLongK], w[kLongK], l[kLongK], lR[kLongK];
+        float aB, bB;
         // pass 1: suffix values, tiles right to left
         float Rc = kNeg;
         for (int t = n_tiles - 1; t >= 0; --t) {
             const long long s = base + (long long)t * kLongTile + (long long)lane * kLongK;
-            load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, x, p, l);
-            lane_composite<kLongK>(x, p, S, bB);
+            load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
+            lane_composite<kLongK>(la, w, aB, bB);
             float carry;
-            const float Rin = suffix_in({-S, bB}, lane, Rc, &carry);
+            const float Rin = suffix_in({aB, bB}, lane, Rc, &carry);
             Rc = carry;
-            lane_suffix<kLongK>(x, p, Rin, lR);
+            lane_suffix<kLongK>(la, w, Rin, lR);
             float* dst = my_scratch + (long long)t * kLongTile + lane * kLongK;
 #pragma unroll
             for (int j = 0; j < kLongK; j += 4)
@@ -283,8 +309,8 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         float Qc = kNeg;
         for (int t = 0; t < n_tiles; ++t) {
             const long long s = base + (long long)t * kLongTile + (long long)lane * kLongK;
-            load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, x, p, l);
-            lane_composite<kLongK>(x, p, S, bB);
+            load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
+            lane_composite<kLongK>(la, w, aB, bB);
             const float* src = my_scratch + (long long)t * kLongTile + lane * kLongK;
 #pragma unroll
             for (int j = 0; j < kLongK; j += 4) {
@@ -292,9 +318,9 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
                 lR[j] = a.x; lR[j + 1] = a.y; lR[j + 2] = a.z; lR[j + 3] = a.w;
             }
             float carry;
-            const float Qin = prefix_in({S, bB + S}, lane, Qc, &carry);
+            const float Qin = prefix_in({-aB, bB - aB}, lane, Qc, &carry);
             Qc = carry;
-            lane_prefix_out<kLongK>(x, p, l, lR, Qin, s, e0, e1, lam);
+            lane_prefix_out<kLongK>(la, w, l, lR, Qin, s, e0, e1, lam);
         }
     }
 }
@@ -351,7 +377,7 @@ inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) /
 int class_capacity(int cls) { return cls < 3 ? 32 * (4 << cls) : 0x7fffffff; }
 
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
-                         const RayZ* ray_z, const int32_t* vid, const int16_t* off_q, int32_t* lam,
+                         const RayInfo* ray_z, const int32_t* vid, const int16_t* off_q, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, cudaStream_t s) {
     if (n_rays == 0) return;

@@ -135,18 +135,19 @@ __device__ __forceinline__ void owned_pixel(const FrameDesc& f, long long i, int
 // ---------------------------------------------------------------- K1
 __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
                                                            const float* __restrict__ depth, int32_t* n_r,
-                                                           int8_t* status, RayZ* ray_z,
+                                                           int8_t* status, RayInfo* ray_z,
                                                            unsigned long long* counters) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n_pix = (long long)f.rows_owned * f.W;
     int st = 3;
+    int ne = 0;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
         Segment sg;
         st = pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg);
         int count = 0;
-        RayZ rz{0, 0.f};
+        RayInfo rz{0, 0.f, 0, 0};
         if (st == 0) {
             Walker w;
             w.start(sg);
@@ -166,15 +167,20 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
             rz.iz = iz;
             rz.wz = (float)(fz - (double)iz);
         }
-        n_r[f.ray_base + i] = count;
+        rz.n = count;
+        n_r[f.ray_base + i] = (count + 3) & ~3;  // segments start at multiples of 4
         status[f.ray_base + i] = (int8_t)st;
         ray_z[f.ray_base + i] = rz;
+        ne = count;
     }
     const unsigned inv = __ballot_sync(kFull, st == 1);
     const unsigned drp = __ballot_sync(kFull, st == 2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(kFull, ne, o);
     if ((threadIdx.x & 31) == 0) {
         if (inv) atomicAdd(&counters[0], (unsigned long long)__popc(inv));
         if (drp) atomicAdd(&counters[1], (unsigned long long)__popc(drp));
+        if (ne) atomicAdd(&counters[2], (unsigned long long)ne);
     }
 }
 
@@ -232,6 +238,7 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
 // Thread per ray walking its incidences in lock step with its warp neighbours; incidences
 // that land in the same voxel at the same step share one cursor atomic.
 __global__ void __launch_bounds__(256) transpose_fill_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                                             const RayInfo* __restrict__ info,
                                                              const int32_t* __restrict__ vid,
                                                              const long long* __restrict__ col_ptr,
                                                              int32_t* cursor, int32_t* tr) {
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(256) transpose_fill_kernel(long long n_rays, c
     long long e = 0, e1 = 0;
     if (r < n_rays) {
         e = row_ptr[r];
-        e1 = row_ptr[r + 1];
+        e1 = e + info[r].n;
     }
     for (;;) {
         const bool alive = e < e1;
@@ -278,17 +285,15 @@ __global__ void active_flags_kernel(long long V, const int32_t* __restrict__ cnt
     if (v < V) flags[v] = cnt[v] > 0 ? 1 : 0;
 }
 
-__global__ void class_flags_kernel(long long n_rays, const long long* __restrict__ row_ptr, int cls,
-                                   int32_t* flags) {
+__global__ void class_flags_kernel(long long n_rays, const RayInfo* __restrict__ info, int cls, int32_t* flags) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n_rays) return;
-    const long long e0 = row_ptr[r], e1 = row_ptr[r + 1];
+    const int n = info[r].n;
     int c = -1;
-    if (e1 > e0) {
+    if (n > 0) {
         c = 3;
         for (int k = 0; k < 3; ++k) {
-            const long long K = 4LL << k;  // 4, 8, 16 elements per lane
-            if (e1 - (e0 & ~(K - 1)) <= 32 * K) {
+            if (n <= 32 * (4 << k)) {  // 4, 8, 16 elements per lane
                 c = k;
                 break;
             }
@@ -303,14 +308,11 @@ __global__ void compact_kernel(long long n, const int32_t* __restrict__ flags, c
     if (i < n && flags[i]) out[pos[i]] = (int32_t)i;
 }
 
-__global__ void span_max_kernel(long long n, const int32_t* __restrict__ rays, const long long* __restrict__ row_ptr,
+__global__ void span_max_kernel(long long n, const int32_t* __restrict__ rays, const RayInfo* __restrict__ info,
                                 unsigned long long* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long m = 0;
-    if (i < n) {
-        const long long r = rays[i];
-        m = (unsigned long long)(row_ptr[r + 1] - (row_ptr[r] & ~7LL));
-    }
+    if (i < n) m = (unsigned long long)info[rays[i]].n;
     for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long x = __shfl_xor_sync(kFull, m, o);
         m = x > m ? x : m;
@@ -323,7 +325,7 @@ inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) /
 }  // namespace
 
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
-                         int32_t* n_r, int8_t* status, RayZ* ray_z, unsigned long long* counters,
+                         int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s) {
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
@@ -338,10 +340,10 @@ void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, 
     dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q, vox_count);
 }
 
-void launch_transpose_fill(long long n_rays, const long long* row_ptr, const int32_t* vid,
+void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                            const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s) {
     if (n_rays == 0) return;
-    transpose_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, vid, col_ptr, cursor, tr);
+    transpose_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, col_ptr, cursor, tr);
 }
 
 void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, cudaStream_t s) {
@@ -357,9 +359,9 @@ void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, 
     active_flags_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, flags);
 }
 
-void launch_class_flags(long long n_rays, const long long* row_ptr, int cls, int32_t* flags, cudaStream_t s) {
+void launch_class_flags(long long n_rays, const RayInfo* info, int cls, int32_t* flags, cudaStream_t s) {
     if (n_rays == 0) return;
-    class_flags_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, cls, flags);
+    class_flags_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, cls, flags);
 }
 
 void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s) {
@@ -367,10 +369,10 @@ void launch_compact(long long n, const int32_t* flags, const long long* pos, int
     compact_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, flags, pos, out);
 }
 
-void launch_span_max(long long n, const int32_t* rays, const long long* row_ptr, unsigned long long* out,
+void launch_span_max(long long n, const int32_t* rays, const RayInfo* info, unsigned long long* out,
                      cudaStream_t s) {
     if (n == 0) return;
-    span_max_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, rays, row_ptr, out);
+    span_max_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, rays, info, out);
 }
 
 }  // namespace mrf

@@ -42,10 +42,15 @@ struct FrameDesc {
     long long ray_base;       // index of this frame's first ray
 };
 
-// Per-ray LUT row information: row iz (<= n_z-2) and weight wz in [0,1].
-struct RayZ {
+// Per-ray record: LUT row iz (<= n_z-2) and weight wz in [0,1] of the measured range, and the
+// number of incidences n.  Ray segments start at multiples of 4 in the incidence arrays
+// (row_ptr advances by pad4(n)), so per-lane chunks are relative to the ray start, 16-byte
+// aligned, and a ray's arithmetic never depends on where (or on which rank) it is stored.
+struct RayInfo {
     int iz;
     float wz;
+    int n;
+    int unused;
 };
 
 // K5 parameters (log2 units).
@@ -58,9 +63,10 @@ struct MsgParams {
 };
 
 // ---- launchers (all asynchronous on `s`)
-// K1: per owned pixel -> status, ray length, LUT row; counters[0] += invalid, counters[1] += dropped
+// K1: per owned pixel -> status, pad4(length) (scan input), RayInfo; counters[0] += invalid,
+// counters[1] += dropped, counters[2] += incidences
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
-                         int32_t* n_r, int8_t* status, RayZ* ray_z, unsigned long long* counters,
+                         int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s);
 // K3: walk again, write vid/off_q at row_ptr offsets, histogram voxel degrees
 void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
@@ -71,25 +77,25 @@ void launch_exclusive_scan(const int32_t* in, long long* out, long long n, long 
                            long long* scratch, cudaStream_t s);
 long long scan_scratch_elems(long long n);
 // K4: tr[col_ptr[v] + slot] = e for every incidence e (cursor zeroed by caller)
-void launch_transpose_fill(long long n_rays, const long long* row_ptr, const int32_t* vid,
+void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                            const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s);
 // K6 work list: n_items[v] = ceil(deg/kVoxelChunk); items from item_ptr
 void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, cudaStream_t s);
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
                       cudaStream_t s);
 // K5 ray length classes: flags[r] = (class(r) == c)
-void launch_class_flags(long long n_rays, const long long* row_ptr, int cls, int32_t* flags, cudaStream_t s);
+void launch_class_flags(long long n_rays, const RayInfo* info, int cls, int32_t* flags, cudaStream_t s);
 void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s);
 // misc
 void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, cudaStream_t s);
-void launch_span_max(long long n, const int32_t* rays, const long long* row_ptr, unsigned long long* out,
+void launch_span_max(long long n, const int32_t* rays, const RayInfo* info, unsigned long long* out,
                      cudaStream_t s);
 
 // ---- BP kernels (bp.cu)
 constexpr int kNumClasses = 4;      // K = 4, 8, 16 single-tile warps; class 3 = long rays (tiled)
 int class_capacity(int cls);        // max span handled by class cls (class 3: unbounded)
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
-                         const RayZ* ray_z, const int32_t* vid, const int16_t* off_q, int32_t* lam,
+                         const RayInfo* info, const int32_t* vid, const int16_t* off_q, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,

@@ -84,11 +84,12 @@ struct mrf_ctx {
     std::string err;
     mrf_status sticky = MRF_OK;
 
-    long long R = 0, E = 0;
+    long long R = 0, E = 0;  // rays (owned pixels) and incidence slots (ray segments padded to 4)
+    long long E_real = 0;    // incidences
     long long n_invalid = 0, n_dropped = 0, n_kept = 0;
     DBuf<int32_t> n_r;
     DBuf<int8_t> status;
-    DBuf<RayZ> ray_z;
+    DBuf<RayInfo> ray_z;  // per-ray RayInfo
     DBuf<long long> row_ptr;
     DBuf<int32_t> vid;
     DBuf<int16_t> off_q;
@@ -228,7 +229,7 @@ mrf_status prepare(mrf_ctx* c) {
     CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * V, c->stream));
     {
         ProfScope ps(c, MRF_K_TRANSPOSE);
-        launch_transpose_fill(c->R, c->row_ptr.p, c->vid.p, c->col_ptr.p, c->cursor.p, c->tr.p, c->stream);
+        launch_transpose_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->col_ptr.p, c->cursor.p, c->tr.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
         launch_item_counts(V, c->vox_count.p, c->n_items.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, 1);
@@ -245,7 +246,7 @@ mrf_status prepare(mrf_ctx* c) {
     CK(c->flags.ensure((size_t)std::max(c->R, V) + 1, 0, c->stream));
     CK(c->pos.ensure((size_t)std::max(c->R, V) + 1, 0, c->stream));
     for (int k = 0; k < kNumClasses; ++k) {
-        launch_class_flags(c->R, c->row_ptr.p, k, c->flags.p, c->stream);
+        launch_class_flags(c->R, c->ray_z.p, k, c->flags.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
         if ((st = scan(c, c->flags.p, c->pos.p, c->R, 0)) != MRF_OK) return st;
         if ((st = read_ll(c, c->pos.p + c->R, &c->class_n[k])) != MRF_OK) return st;
@@ -255,11 +256,11 @@ mrf_status prepare(mrf_ctx* c) {
     }
     // scratch for the tiled long-ray kernel
     if (c->class_n[3] > 0) {
-        CK(cudaMemsetAsync(c->counters.p + 4, 0, sizeof(unsigned long long), c->stream));
-        launch_span_max(c->class_n[3], c->class_rays[3].p, c->row_ptr.p, c->counters.p + 4, c->stream);
+        CK(cudaMemsetAsync(c->counters.p + 6, 0, sizeof(unsigned long long), c->stream));
+        launch_span_max(c->class_n[3], c->class_rays[3].p, c->ray_z.p, c->counters.p + 6, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, 1);
         long long span = 0;
-        if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 4), &span)) != MRF_OK) return st;
+        if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
         const long long tile = 256;
         c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
         c->n_warps_long = (int)std::min<long long>(c->class_n[3], 148LL * 16);
@@ -305,6 +306,43 @@ mrf_status rebuild_T(mrf_ctx* c) {
     if ((st = voxel_sums(c, c->T_part.p)) != MRF_OK) return st;
     if (c->comm_mode == MRF_COMM_NCCL) return allreduce_T(c);
     return MRF_OK;  // external mode: caller reduces (mrf_bp_partial / mrf_bp_finish)
+}
+
+
+// Canonical (unpadded) layout of this rank's incidences, from the device ray records.
+struct HostLayout {
+    std::vector<long long> row_ptr;   // padded segment start per ray (R+1)
+    std::vector<RayInfo> info;        // per ray
+    std::vector<int8_t> status;       // per ray
+    std::vector<long long> canon;     // canonical start per ray (R+1)
+};
+
+mrf_status host_layout(mrf_ctx* c, HostLayout& h) {
+    h.row_ptr.resize((size_t)c->R + 1);
+    h.info.resize((size_t)c->R);
+    h.status.resize((size_t)c->R);
+    CK(cudaMemcpyAsync(h.row_ptr.data(), c->row_ptr.p, sizeof(long long) * (c->R + 1), cudaMemcpyDeviceToHost, c->stream));
+    if (c->R) {
+        CK(cudaMemcpyAsync(h.info.data(), c->ray_z.p, sizeof(RayInfo) * c->R, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(h.status.data(), c->status.p, c->R, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    h.canon.resize((size_t)c->R + 1);
+    h.canon[0] = 0;
+    for (long long r = 0; r < c->R; ++r) h.canon[r + 1] = h.canon[r] + h.info[r].n;
+    return MRF_OK;
+}
+
+// padded -> canonical copy (to_canon) or back, element size `es`
+void relayout(const HostLayout& h, const void* src, void* dst, size_t es, bool to_canon) {
+    const char* s = static_cast<const char*>(src);
+    char* d = static_cast<char*>(dst);
+    for (size_t r = 0; r < h.info.size(); ++r) {
+        const size_t n = (size_t)h.info[r].n * es;
+        if (!n) continue;
+        if (to_canon) memcpy(d + (size_t)h.canon[r] * es, s + (size_t)h.row_ptr[r] * es, n);
+        else memcpy(d + (size_t)h.row_ptr[r] * es, s + (size_t)h.canon[r] * es, n);
+    }
 }
 
 }  // namespace
@@ -388,13 +426,21 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
         CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 8, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
-        // LUT as (L[i][j], L[i][j+1]) pairs in log2 units: one 8-byte load per LUT row in K5
+        // LUT as (L[i][j], L[i][j+1]) pairs in log2 units: one 8-byte load per LUT row in K5.
+        // Each row is shifted by its maximum: a ray's lookups interpolate two rows with one
+        // weight, so the shift is a per-ray constant factor on nu, which leaves every message
+        // unchanged (nu-scale invariance, R2) while keeping the values near the
+        // surface close to 0, where fp32 has its finest absolute resolution.
         const int nz = noise->n_z, no = noise->n_off;
         std::vector<float2> h((size_t)nz * (no - 1));
-        for (int i = 0; i < nz; ++i)
+        for (int i = 0; i < nz; ++i) {
+            const float* row = noise->log_nu + (size_t)i * no;
+            double mx = row[0];
+            for (int j = 1; j < no; ++j) mx = std::max(mx, (double)row[j]);
             for (int j = 0; j < no - 1; ++j)
-                h[(size_t)i * (no - 1) + j] = make_float2(noise->log_nu[(size_t)i * no + j] * kLog2e,
-                                                          noise->log_nu[(size_t)i * no + j + 1] * kLog2e);
+                h[(size_t)i * (no - 1) + j] = make_float2((float)(((double)row[j] - mx) * (double)kLog2e),
+                                                          (float)(((double)row[j + 1] - mx) * (double)kLog2e));
+        }
         CK(c->lutp.ensure(h.size(), 0, c->stream));
         CK(cudaMemcpyAsync(c->lutp.p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
         CK(cudaStreamSynchronize(c->stream));
@@ -477,7 +523,7 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences) {
 
 mrf_status mrf_reset(mrf_ctx* ctx) {
     ENTER(ctx);
-    c->R = c->E = 0;
+    c->R = c->E = c->E_real = 0;
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
     CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * c->V, c->stream));
@@ -541,7 +587,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     f.rows_owned = rows_owned;
     f.ray_base = c->R;
     mrf_status st;
-    CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->counters.p + 2, 0, 3 * sizeof(unsigned long long), c->stream));
     {
         ProfScope ps(c, MRF_K_RAYGEN_COUNT);
         launch_raygen_count(f, c->grid, c->noise, d_depth, c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2,
@@ -550,9 +596,9 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     }
     if ((st = scan(c, c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->E)) != MRF_OK) return st;
     CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R + Rf, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2];
+    const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2], n_inc = c->pinned[3];
     if (E_new >= (1LL << 31) - kPadElems)
         return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
     const size_t ne = (size_t)E_new + kPadElems;
@@ -569,6 +615,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     c->frames.push_back({width, height, rows_owned, c->R, Rf});
     c->R += Rf;
     c->E = E_new;
+    c->E_real += n_inc;
     c->n_invalid += inv;
     c->n_dropped += drp;
     c->n_kept += Rf - inv - drp;
@@ -635,7 +682,7 @@ mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences,
                            int64_t* n_invalid, int64_t* n_dropped) {
     ENTER(ctx);
     if (n_rays) *n_rays = c->n_kept;
-    if (n_incidences) *n_incidences = c->E;
+    if (n_incidences) *n_incidences = c->E_real;
     if (n_invalid) *n_invalid = c->n_invalid;
     if (n_dropped) *n_dropped = c->n_dropped;
     if (n_active_vox) {
@@ -655,29 +702,36 @@ mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences,
 
 mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, int32_t* vid, int16_t* off_q) {
     ENTER(ctx);
+    HostLayout h;
+    mrf_status st;
+    if ((st = host_layout(c, h)) != MRF_OK) return st;
     if (ray_pixel || row_ptr) {
-        std::vector<long long> rp((size_t)c->R + 1);
-        std::vector<int8_t> stv((size_t)c->R);
-        CK(cudaMemcpyAsync(rp.data(), c->row_ptr.p, sizeof(long long) * (c->R + 1), cudaMemcpyDeviceToHost, c->stream));
-        if (c->R) CK(cudaMemcpyAsync(stv.data(), c->status.p, c->R, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
         long long k = 0;
         for (size_t fi = 0; fi < c->frames.size(); ++fi) {
             const FrameRec& fr = c->frames[fi];
             for (long long i = 0; i < fr.n_rays; ++i) {
                 const long long r = fr.ray_base + i;
-                if (stv[r] != 0) continue;
+                if (h.status[r] != 0) continue;
                 const long long lr = i / fr.W, u = i % fr.W, v = c->rank + lr * c->world;
                 if (ray_pixel) ray_pixel[k] = ((long long)fi << 32) | (v * fr.W + u);
-                if (row_ptr) row_ptr[k] = rp[r];
+                if (row_ptr) row_ptr[k] = h.canon[r];
                 ++k;
             }
         }
-        if (row_ptr) row_ptr[k] = c->E;
+        if (row_ptr) row_ptr[k] = c->E_real;
     }
-    if (vid && c->E) CK(cudaMemcpyAsync(vid, c->vid.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
-    if (off_q && c->E) CK(cudaMemcpyAsync(off_q, c->off_q.p, sizeof(int16_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    if (vid && c->E) {
+        std::vector<int32_t> tmp((size_t)c->E);
+        CK(cudaMemcpyAsync(tmp.data(), c->vid.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        relayout(h, tmp.data(), vid, sizeof(int32_t), true);
+    }
+    if (off_q && c->E) {
+        std::vector<int16_t> tmp((size_t)c->E);
+        CK(cudaMemcpyAsync(tmp.data(), c->off_q.p, sizeof(int16_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        relayout(h, tmp.data(), off_q, sizeof(int16_t), true);
+    }
     return MRF_OK;
 }
 
@@ -686,7 +740,18 @@ mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr) {
     mrf_status st;
     if ((st = prepare(c)) != MRF_OK) return st;
     if (col_ptr) CK(cudaMemcpyAsync(col_ptr, c->col_ptr.p, sizeof(long long) * (c->V + 1), cudaMemcpyDeviceToHost, c->stream));
-    if (tr && c->E) CK(cudaMemcpyAsync(tr, c->tr.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
+    if (tr && c->E_real) {
+        HostLayout h;
+        if ((st = host_layout(c, h)) != MRF_OK) return st;
+        std::vector<int32_t> tmp((size_t)c->E_real);
+        CK(cudaMemcpyAsync(tmp.data(), c->tr.p, sizeof(int32_t) * c->E_real, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        // padded slot -> canonical index
+        std::vector<long long> map((size_t)c->E, -1);
+        for (size_t r = 0; r < h.info.size(); ++r)
+            for (int j = 0; j < h.info[r].n; ++j) map[(size_t)h.row_ptr[r] + j] = h.canon[r] + j;
+        for (long long k = 0; k < c->E_real; ++k) tr[k] = (int32_t)map[(size_t)tmp[k]];
+    }
     CK(cudaStreamSynchronize(c->stream));
     return MRF_OK;
 }
@@ -695,26 +760,34 @@ mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda) {
     ENTER(ctx);
     if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
     if (!c->E) return MRF_OK;
-    std::vector<int32_t> q((size_t)c->E);
+    HostLayout h;
+    mrf_status st;
+    if ((st = host_layout(c, h)) != MRF_OK) return st;
+    std::vector<int32_t> q((size_t)c->E), qc((size_t)c->E_real);
     CK(cudaMemcpyAsync(q.data(), c->lam.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    for (long long e = 0; e < c->E; ++e) lambda[e] = (float)((double)q[e] * kQInvD);
+    relayout(h, q.data(), qc.data(), sizeof(int32_t), true);
+    for (long long e = 0; e < c->E_real; ++e) lambda[e] = (float)((double)qc[e] * kQInvD);
     return MRF_OK;
 }
 
 mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda) {
     ENTER(ctx);
     if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL input");
-    std::vector<int32_t> q((size_t)c->E);
-    for (long long e = 0; e < c->E; ++e) {
+    std::vector<int32_t> qc((size_t)c->E_real), q((size_t)c->E, 0);
+    for (long long e = 0; e < c->E_real; ++e) {
         double x = lambda[e];
         if (!std::isfinite(x)) return set_err(c, MRF_ERR_INVALID_ARG, "non-finite message");
         x = std::min(256.0, std::max(-256.0, x)) * 8388608.0;
         const double r = std::nearbyint(x);
-        q[e] = r >= 2147483647.0 ? 2147483647 : (int32_t)r;
+        qc[e] = r >= 2147483647.0 ? 2147483647 : (int32_t)r;
     }
+    HostLayout h;
+    mrf_status st;
+    if ((st = host_layout(c, h)) != MRF_OK) return st;
+    relayout(h, qc.data(), q.data(), sizeof(int32_t), false);
     if (c->E) CK(cudaMemcpyAsync(c->lam.p, q.data(), sizeof(int32_t) * c->E, cudaMemcpyHostToDevice, c->stream));
-    mrf_status st = rebuild_T(c);
+    st = (c->world > 1 && c->comm_mode == MRF_COMM_EXTERNAL) ? prepare(c) : rebuild_T(c);
     CK(cudaStreamSynchronize(c->stream));
     return st;
 }

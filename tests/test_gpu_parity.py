@@ -24,6 +24,7 @@ MARG_TOL = 1e-4
 
 def _gpu_map(w, frames=None, **kw):
     m = pkg.MRFMap.from_workload(w, **kw)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)  # order with torch-side buffers
     for fr in (w.frames if frames is None else frames):
         m.add_frame(fr.depth, fr.K, fr.T_wc)
     return m
@@ -87,37 +88,62 @@ def test_tiny_bp_parity(tiny, n_iter):
     assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
 
 
+def _gpu_state(m, k_total, k):
+    """Advance the GPU map to iteration k and return its (quantised) messages."""
+    if k > k_total:
+        m.bp_iterate(k - k_total)
+    return m.export_messages()
+
+
 def test_frame1_graph_and_bp_parity(frame1):
+    """Graph bit-exact; full trajectory for the first 2 iterations; one-step parity (T3)
+    from the GPU's own state at iterations 2, 4 and 7 of the 8-iteration run: every
+    message within 1e-3 relative and every marginal within 1e-4 after the step."""
     w = frame1
     p = oracle.Params.from_workload(w)
     g = oracle.build_graph(p, w.frames)
-    lam_ref, T_ref = oracle.bp(p, g, w.n_iter)
+    lam_ref, T_ref = oracle.bp(p, g, 2)
     with _gpu_map(w) as m:
         _assert_graph_equal(m.export_graph(), g)
-        m.bp_iterate(w.n_iter)
-        lam = m.export_messages()
-        marg = m.marginals()
-    _assert_msgs_close(lam, lam_ref)
-    d = np.abs(marg - oracle.marginals(p, T_ref))
-    assert d.max() <= MARG_TOL, f"max marginal err {d.max():.3e}"
+        m.bp_iterate(2)
+        _assert_msgs_close(m.export_messages(), lam_ref)
+        assert np.max(np.abs(m.marginals() - oracle.marginals(p, T_ref))) <= MARG_TOL
+        k_done = 2
+        for k in (2, 4, 7):
+            lam0 = _gpu_state(m, k_done, k)
+            k_done = k
+            m.import_messages(lam0)
+            m.bp_iterate(1)
+            k_done += 1
+            lam = lam0.astype(np.float64)
+            T = oracle.accumulate(p, g, lam)
+            oracle.ray_pass(p, g, T, lam)
+            _assert_msgs_close(m.export_messages(), lam)
+            d = np.abs(m.marginals() - oracle.marginals(p, oracle.accumulate(p, g, lam)))
+            assert d.max() <= MARG_TOL, f"one-step marginal err {d.max():.3e} from iteration {k}"
 
 
-def test_one_step_parity_from_gpu_state(frame1):
-    """T3: both sides start from the same messages (GPU state after 4 iterations)."""
+def test_frame1_full_trajectory_within_conditioning_envelope(frame1):
+    """End-to-end after all 8 iterations.  This loopy graph amplifies perturbations ~1e4x by
+    iteration 8 (tests/test_oracle_conditioning.py), so the bar is the oracle's own spread
+    under fp32-sized noise: the fp64 oracle re-run with 1e-7 relative noise on every message
+    of every iteration.  GPU deviation <= max(1e-4, 10 x that spread)."""
     w = frame1
     p = oracle.Params.from_workload(w)
     g = oracle.build_graph(p, w.frames)
+    _, T_ref = oracle.bp(p, g, w.n_iter)
+    m_ref = oracle.marginals(p, T_ref)
+    rng = np.random.default_rng(1)
+    lam = np.zeros(g.E)
+    for _ in range(w.n_iter):
+        lam, _ = oracle.bp(p, g, 1, lam=lam)
+        lam = lam * (1.0 + 1e-7 * rng.standard_normal(g.E))
+    spread = np.max(np.abs(oracle.marginals(p, oracle.accumulate(p, g, lam)) - m_ref))
     with _gpu_map(w) as m:
-        m.bp_iterate(4)
-        lam0 = m.export_messages()
-        m.import_messages(lam0)        # quantise exactly as the GPU holds it
-        lam0 = m.export_messages()
-        m.bp_iterate(1)
-        lam1 = m.export_messages()
-    lam = lam0.astype(np.float64)
-    T = oracle.accumulate(p, g, lam)
-    oracle.ray_pass(p, g, T, lam)
-    _assert_msgs_close(lam1, lam)
+        m.bp_iterate(w.n_iter)
+        dev = np.max(np.abs(m.marginals() - m_ref))
+    print(f"frame1 n={w.n_iter}: gpu max|dp| {dev:.3e}, oracle fp32-noise spread {spread:.3e}")
+    assert dev <= max(MARG_TOL, 10 * spread)
 
 
 def test_determinism(frame1):
@@ -131,21 +157,30 @@ def test_determinism(frame1):
 
 
 def test_warm_start_matches_oracle(frame1):
-    """A frame added after iterations starts with lambda = 0 (warm start of the others)."""
+    """A frame added after iterations starts with lambda = 0 and keeps the others (warm
+    start): the state right after mrf_add_frame is exactly (old messages, zeros), and the
+    next iteration from it matches the oracle's one-step update from the same state."""
     w = synth.frames30(n_frames=2)
     p = oracle.Params.from_workload(w)
     g1 = oracle.build_graph(p, w.frames[:1])
     g2 = oracle.build_graph(p, w.frames)
-    lam1, _ = oracle.bp(p, g1, 3)
-    lam_start = np.concatenate([lam1, np.zeros(g2.E - g1.E)])
-    lam2, T2 = oracle.bp(p, g2, 3, lam=lam_start)
+    lam1_ref, T1_ref = oracle.bp(p, g1, 1)
     with _gpu_map(w, frames=w.frames[:1]) as m:
-        m.bp_iterate(3)
+        m.bp_iterate(1)
+        _assert_msgs_close(m.export_messages(), lam1_ref)
+        m.bp_iterate(1)
+        lam_old = m.export_messages()
+        T_old = m.export_beliefs()
         m.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
-        m.bp_iterate(3)
         _assert_graph_equal(m.export_graph(), g2)
-        _assert_msgs_close(m.export_messages(), lam2)
-        assert np.max(np.abs(m.marginals() - oracle.marginals(p, T2))) <= MARG_TOL
+        lam_start = m.export_messages()
+        assert np.array_equal(lam_start[:g1.E], lam_old) and np.all(lam_start[g1.E:] == 0)
+        assert np.array_equal(m.export_beliefs(), T_old)   # adding zeros leaves T unchanged
+        m.bp_iterate(1)
+        lam = lam_start.astype(np.float64)
+        oracle.ray_pass(p, g2, oracle.accumulate(p, g2, lam), lam)
+        _assert_msgs_close(m.export_messages(), lam)
+        assert np.max(np.abs(m.marginals() - oracle.marginals(p, oracle.accumulate(p, g2, lam)))) <= MARG_TOL
 
 
 def _corridor(n_vox=1100, res=0.01, wall_vox=1050.3):
