@@ -149,16 +149,23 @@ mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda);
  * in MRF_COMM_EXTERNAL mode with world > 1, see mrf_bp_partial). */
 mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda);
 
-/* Beliefs T_v (int64, units 2^-23 nats; the global sum over ranks) into a host buffer of V. */
+/* Beliefs T_v (int64, units 2^-23 nats; the global sum over ranks) into a host buffer of V,
+ * x fastest. */
 mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T);
 
 /* MRF_COMM_EXTERNAL mode, one iteration split in two: mrf_bp_partial (iterate = 1) computes
- * this rank's messages from the current T and writes its partial voxel sums to partial_out
- * (device pointer, V int64); the caller sums the partials of all ranks and hands the total
- * back with mrf_bp_finish (device pointer, V int64), which becomes T.  iterate = 0 only sums
- * the current messages (e.g. after mrf_import_messages, which in this mode leaves T alone). */
+ * this rank's messages from the current T and writes its partial sums to partial_out (device
+ * pointer, mrf_belief_slots() int64 in the library's internal brick-major slot order); the
+ * caller sums the partials of all ranks element-wise and hands the total back with
+ * mrf_bp_finish (device pointer, same size), which becomes T.  iterate = 0 only sums the
+ * current messages (e.g. after mrf_import_messages, which in this mode leaves T alone).
+ * Device buffers are accessed on the ctx stream (see mrf_set_stream). */
 mrf_status mrf_bp_partial(mrf_ctx* ctx, int32_t iterate, int64_t* partial_out_device);
 mrf_status mrf_bp_finish(mrf_ctx* ctx, const int64_t* total_device);
+
+/* Number of int64 belief slots (nx, ny, nz rounded up to multiples of 8, times each other):
+ * voxels are stored brick-major in 8^3 bricks internally (cf. the paper's GVDB bricks). */
+int64_t mrf_belief_slots(const mrf_ctx* ctx);
 
 /* 128-byte ncclUniqueId for MRF_COMM_NCCL (call on rank 0, broadcast to the others). */
 mrf_status mrf_nccl_unique_id(unsigned char out[128]);

@@ -182,6 +182,9 @@ class MRFMap:
     def bp_partial(self, partial_out, iterate=True):
         self._chk(self._L.mrf_bp_partial(self._h, 1 if iterate else 0, _ptr(partial_out)))
 
+    def belief_slots(self) -> int:
+        return int(self._L.mrf_belief_slots(self._h))
+
     def bp_finish(self, total):
         self._chk(self._L.mrf_bp_finish(self._h, _ptr(total)))
 

@@ -29,8 +29,8 @@ MRF_K_COUNT = len(KERNEL_NAMES)
 EXPORTS = ["mrf_create", "mrf_add_frame", "mrf_bp_iterate", "mrf_marginals", "mrf_destroy", "mrf_last_error",
            "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_export_graph",
            "mrf_export_transpose", "mrf_export_messages", "mrf_import_messages", "mrf_export_beliefs",
-           "mrf_bp_partial", "mrf_bp_finish", "mrf_nccl_unique_id", "mrf_set_profiling", "mrf_profile_read",
-           "mrf_launch_count"]
+           "mrf_bp_partial", "mrf_bp_finish", "mrf_belief_slots", "mrf_nccl_unique_id", "mrf_set_profiling",
+           "mrf_profile_read", "mrf_launch_count"]
 
 
 class MrfError(RuntimeError):
@@ -82,6 +82,7 @@ def load(build: bool = True):
                 "mrf_export_beliefs": (st, [vp, vp]),
                 "mrf_bp_partial": (st, [vp, i32, vp]),
                 "mrf_bp_finish": (st, [vp, vp]),
+                "mrf_belief_slots": (i64, [vp]),
                 "mrf_nccl_unique_id": (st, [P(ctypes.c_ubyte)]),
                 "mrf_set_profiling": (st, [vp, i32]),
                 "mrf_profile_read": (st, [vp, P(i64), P(f64)]),

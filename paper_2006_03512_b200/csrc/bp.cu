@@ -29,6 +29,10 @@
 namespace mrf {
 namespace {
 
+#ifndef MRF_ACCURATE_RECURRENCES
+#define MRF_ACCURATE_RECURRENCES 1
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr float kNeg = -1e30f;  // log2(0); finite so that NEG - NEG = 0 stays NaN-free
 
@@ -57,9 +61,19 @@ __device__ __forceinline__ float log1p2(float y) {
     r = fmaf(r, y, 1.4426950216293335f);
     return r * y;
 }
-// log2(2^a + 2^b)
+// log2(2^a + 2^b), relative-accurate remainder (used where results are differenced)
 __device__ __forceinline__ float lse2(float a, float b) {
     return fmaxf(a, b) + log1p2(ex2(-fabsf(a - b)));
+}
+// log2(2^a + 2^b) on the MUFU (lg2.approx: ~2^-22 absolute in log2, i.e. ~1.7e-7 relative in
+// the linear quantity).  Used for the Q/R recurrences, the cavity softplus and the scans, whose
+// results are only ever used through differences that are O(1) or through lambda2.
+__device__ __forceinline__ float lse2f(float a, float b) {
+#if MRF_ACCURATE_RECURRENCES
+    return lse2(a, b);
+#else
+    return fmaxf(a, b) + lg2(1.0f + ex2(-fabsf(a - b)));
+#endif
 }
 
 // Affine map x -> 2^a x + 2^b in log2 form.
@@ -68,16 +82,19 @@ struct Aff {
 };
 // outer o inner (inner applied first)
 __device__ __forceinline__ Aff compose(Aff outer, Aff inner) {
-    return {outer.a + inner.a, lse2(outer.a + inner.b, outer.b)};
+    return {outer.a + inner.a, lse2f(outer.a + inner.b, outer.b)};
 }
+template <int G>
 __device__ __forceinline__ Aff shfl_up(Aff v, int d) {
-    return {__shfl_up_sync(kFull, v.a, d), __shfl_up_sync(kFull, v.b, d)};
+    return {__shfl_up_sync(kFull, v.a, d, G), __shfl_up_sync(kFull, v.b, d, G)};
 }
+template <int G>
 __device__ __forceinline__ Aff shfl_down(Aff v, int d) {
-    return {__shfl_down_sync(kFull, v.a, d), __shfl_down_sync(kFull, v.b, d)};
+    return {__shfl_down_sync(kFull, v.a, d, G), __shfl_down_sync(kFull, v.b, d, G)};
 }
+template <int G>
 __device__ __forceinline__ Aff shfl_idx(Aff v, int l) {
-    return {__shfl_sync(kFull, v.a, l), __shfl_sync(kFull, v.b, l)};
+    return {__shfl_sync(kFull, v.a, l, G), __shfl_sync(kFull, v.b, l, G)};
 }
 
 // ---------------------------------------------------------------- per-lane element loads
@@ -97,7 +114,7 @@ __device__ __forceinline__ void load_elems(long long s, long long e0, long long 
         w[j] = kNeg;
         l[j] = kNeg;
     }
-    if (s + K <= e0 || s >= e1) return;
+    if (s >= e1) return;
     int v[K], q[K];
     short o[K];
 #pragma unroll
@@ -112,14 +129,10 @@ __device__ __forceinline__ void load_elems(long long s, long long e0, long long 
     }
     long long t[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-        const long long e = s + j;
-        t[j] = (e >= e0 && e < e1) ? __ldg(T + v[j]) : 0;
-    }
+    for (int j = 0; j < K; ++j) t[j] = (s + j < e1) ? __ldg(T + v[j]) : 0;
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-        const long long e = s + j;
-        if (e >= e0 && e < e1) {
+        if (s + j < e1) {
             // cavity (Eq.6): prior + every other incoming message, exact in fixed point
             const float c2 = fmaf(__ll2float_rn(t[j] - (long long)q[j]), kQInv * kLog2e, mp.L0_2);
             float fo = fmaf((float)o[j], mp.s_off, mp.b_off);
@@ -130,7 +143,7 @@ __device__ __forceinline__ void load_elems(long long s, long long e0, long long 
             const float ra = fmaf(wo, ta.y - ta.x, ta.x);
             const float rb = fmaf(wo, tb.y - tb.x, tb.x);
             const float lnu = fmaf(wz, rb - ra, ra);
-            const float L1 = log1p2(ex2(-fabsf(c2)));
+            const float L1 = lse2f(0.f, -fabsf(c2));  // log2(1 + 2^-|c|)
             la[j] = -(fmaxf(c2, 0.f) + L1);
             w[j] = lnu - (fmaxf(-c2, 0.f) + L1);
             l[j] = lnu;
@@ -157,53 +170,55 @@ __device__ __forceinline__ void lane_composite(const float (&la)[K], const float
     bB = m + lg2(sum);
 }
 
-// Suffix scan over lanes: returns R entering this lane from the right given the carry Rc
-// (log2 R after the tile); *carry_out = R leaving the tile on the left.
-__device__ __forceinline__ float suffix_in(Aff G, int lane, float Rc, float* carry_out) {
-    Aff H = G;
+// Both lane scans of a ray's G lanes at once (two independent shuffle chains per level):
+// returns R entering this lane from the right and Q entering it from the left, given the tile
+// carries Rc (log2 R after the tile) and Qc (log2 Q before it); optional carries out.
+template <int G>
+__device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc, float Qc, float& Rin, float& Qin,
+                                           float* Rc_out, float* Qc_out) {
+    Aff H = {aB, bB};          // suffix maps R -> 2^{la} R + 2^{w}
+    Aff P = {-aB, bB - aB};    // prefix maps Q -> 2^{-la} (Q + 2^{w})
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const Aff o = shfl_down(H, d);
-        if (lane + d < 32) H = compose(H, o);
+    for (int d = 1; d < G; d <<= 1) {
+        const Aff oh = shfl_down<G>(H, d);
+        const Aff op = shfl_up<G>(P, d);
+        if (sl + d < G) H = compose(H, oh);
+        if (sl >= d) P = compose(P, op);
     }
-    Aff Hx = shfl_down(H, 1);
-    if (lane == 31) Hx = {0.f, kNeg};
-    if (carry_out) {
-        const Aff H0 = shfl_idx(H, 0);
-        *carry_out = lse2(H0.a + Rc, H0.b);
+    Aff Hx = shfl_down<G>(H, 1);
+    Aff Px = shfl_up<G>(P, 1);
+    if (sl == G - 1) Hx = {0.f, kNeg};
+    if (sl == 0) Px = {0.f, kNeg};
+    if (Rc_out) {
+        const Aff H0 = shfl_idx<G>(H, 0);
+        const Aff Pl = shfl_idx<G>(P, G - 1);
+        *Rc_out = lse2f(H0.a + Rc, H0.b);
+        *Qc_out = lse2f(Pl.a + Qc, Pl.b);
     }
-    return lse2(Hx.a + Rc, Hx.b);
+    Rin = lse2f(Hx.a + Rc, Hx.b);
+    Qin = lse2f(Px.a + Qc, Px.b);
 }
 
-// Prefix scan over lanes: returns Q entering this lane from the left given carry Qc.
-__device__ __forceinline__ float prefix_in(Aff F, int lane, float Qc, float* carry_out) {
-    Aff P = F;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const Aff o = shfl_up(P, d);
-        if (lane >= d) P = compose(P, o);
-    }
-    Aff Px = shfl_up(P, 1);
-    if (lane == 0) Px = {0.f, kNeg};
-    if (carry_out) {
-        const Aff P31 = shfl_idx(P, 31);
-        *carry_out = lse2(P31.a + Qc, P31.b);
-    }
-    return lse2(Px.a + Qc, Px.b);
-}
-
+// The two per-lane recurrences, interleaved (independent chains):
+//   lR[j] = log2 R_j (suffix strictly after j),  R_{j-1} = mu(o_j=0) R_j + mu(o_j=1) nu_j
+//   lQ[j] = log2 Q_j (prefix strictly before j), Q_{j+1} = (Q_j + mu(o_j=1) nu_j) / mu(o_j=0)
 template <int K>
-__device__ __forceinline__ void lane_suffix(const float (&la)[K], const float (&w)[K], float Rin, float (&lR)[K]) {
-    float R = Rin;
+__device__ __forceinline__ void lane_recurrences(const float (&la)[K], const float (&w)[K], float Rin, float Qin,
+                                                 float (&lR)[K], float (&lQ)[K]) {
+    float R = Rin, Q = Qin;
 #pragma unroll
-    for (int j = K - 1; j >= 0; --j) {
-        lR[j] = R;                      // log2 R_j: suffix strictly after element j
-        R = lse2(la[j] + R, w[j]);      // R_{j-1} = mu(o_j=0) R_j + mu(o_j=1) nu_j
+    for (int i = 0; i < K; ++i) {
+        const int jb = K - 1 - i;
+        lR[jb] = R;
+        lQ[i] = Q;
+        R = lse2f(la[jb] + R, w[jb]);
+        Q = lse2f(Q, w[i]) - la[i];
     }
 }
 
 // lambda2 = log2(2^Q + 2^l) - log2(2^Q + 2^R) without cancellation: the max parts subtract
-// exactly (both are Q when Q dominates) and the remainders are small, accurate log1p terms.
+// exactly (both are Q when Q dominates) and the remainders are small, relative-accurate log1p
+// terms.
 __device__ __forceinline__ float lambda2(float Q, float l, float R) {
     const float m1 = fmaxf(Q, l), m2 = fmaxf(Q, R);
     return (m1 - m2) + (log1p2(ex2(-fabsf(Q - l))) - log1p2(ex2(-fabsf(Q - R))));
@@ -215,58 +230,63 @@ __device__ __forceinline__ int32_t quantise(float lam2) {
     return __float2int_rn(lam * kQScale);  // saturates at +2^31-1 for +256
 }
 
+// lambda_j = log(Q_j + nu_j) - log(Q_j + R_j)   (Eq.13 / Eq.14, both divided by V_j)
 template <int K>
-__device__ __forceinline__ void lane_prefix_out(const float (&la)[K], const float (&w)[K], const float (&l)[K],
-                                                const float (&lR)[K], float Qin, long long s, long long e0,
-                                                long long e1, int32_t* lam) {
-    float Q = Qin;
+__device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[K], const float (&lQ)[K], long long s,
+                                         long long e1, int32_t* lam) {
     int32_t out[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-        // lambda_j = log(Q_j + nu_j) - log(Q_j + R_j)   (Eq.13 / Eq.14, both divided by V_j)
-        out[j] = quantise(lambda2(Q, l[j], lR[j]));
-        Q = lse2(Q, w[j]) - la[j];      // Q_{j+1} = (Q_j + mu(o_j=1) nu_j) / mu(o_j=0)
-    }
-    if (s >= e0 && s + K <= e1) {
+    for (int j = 0; j < K; ++j) out[j] = quantise(lambda2(lQ[j], l[j], lR[j]));
+    if (s + K <= e1) {
 #pragma unroll
         for (int j = 0; j < K; j += 4)
             *reinterpret_cast<int4*>(lam + s + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
     } else {
 #pragma unroll
         for (int j = 0; j < K; ++j)
-            if (s + j >= e0 && s + j < e1) lam[s + j] = out[j];
+            if (s + j < e1) lam[s + j] = out[j];
     }
 }
 
 // ---------------------------------------------------------------- K5: single-tile classes
-template <int K>
-__global__ void __launch_bounds__(256) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
+// G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.
+#ifndef MRF_K5_MIN_BLOCKS
+#define MRF_K5_MIN_BLOCKS 3
+#endif
+template <int G, int K>
+__global__ void __launch_bounds__(256, MRF_K5_MIN_BLOCKS) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                       const long long* __restrict__ row_ptr,
                                                       const RayInfo* __restrict__ ray_z,
                                                       const int32_t* __restrict__ vid,
                                                       const int16_t* __restrict__ off_q, int32_t* lam,
                                                       const long long* __restrict__ T, MsgParams mp) {
+    constexpr int RPW = 32 / G;
     const long long wi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (wi >= n) return;
-    const int lane = threadIdx.x & 31;
-    const int r = __ldg(rays + wi);
-    const RayInfo rz = ray_z[r];
-    const long long e0 = __ldg(row_ptr + r), e1 = e0 + rz.n;
+    if (wi * RPW >= n) return;  // warp-uniform
+    const int lane = threadIdx.x & 31, sl = lane & (G - 1);
+    const long long ri = wi * RPW + lane / G;
+    RayInfo rz{0, 0.f, 0, 0};
+    long long e0 = 0;
+    if (ri < n) {
+        const int r = __ldg(rays + ri);
+        rz = ray_z[r];
+        e0 = __ldg(row_ptr + r);
+    }
+    const long long e1 = e0 + rz.n;
     const float2* rowA = mp.lutp + (long long)rz.iz * mp.n_offm1;
     const float2* rowB = rowA + mp.n_offm1;
-    const long long s = e0 + (long long)lane * K;
-    float la[K], w[K], l[K], lR[K];
+    const long long s = e0 + (long long)sl * K;
+    float la[K], w[K], l[K], lR[K], lQ[K];
     load_elems<K>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
-    float aB, bB;
+    float aB, bB, Rin, Qin;
     lane_composite<K>(la, w, aB, bB);
-    const float Rin = suffix_in({aB, bB}, lane, kNeg, nullptr);
-    lane_suffix<K>(la, w, Rin, lR);
-    const float Qin = prefix_in({-aB, bB - aB}, lane, kNeg, nullptr);
-    lane_prefix_out<K>(la, w, l, lR, Qin, s, e0, e1, lam);
+    lane_scans<G>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
+    lane_recurrences<K>(la, w, Rin, Qin, lR, lQ);
+    if (s < e1) lane_out<K>(l, lR, lQ, s, e1, lam);
 }
 
 // ---------------------------------------------------------------- K5: long rays (tiled)
-constexpr int kLongK = 8;
+constexpr int kLongK = 16;
 constexpr int kLongTile = 32 * kLongK;
 
 __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const int32_t* __restrict__ rays,
@@ -286,20 +306,18 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         const long long e0 = __ldg(row_ptr + r), e1 = e0 + rz.n;
         const float2* rowA = mp.lutp + (long long)rz.iz * mp.n_offm1;
         const float2* rowB = rowA + mp.n_offm1;
-        const long long base = e0;
-        const int n_tiles = (int)((e1 - base + kLongTile - 1) / kLongTile);
-        float la[kLongK], w[kLongK], l[kLongK], lR[kLongK];
-        float aB, bB;
+        const int n_tiles = (int)((e1 - e0 + kLongTile - 1) / kLongTile);
+        float la[kLongK], w[kLongK], l[kLongK], lR[kLongK], lQ[kLongK];
+        float aB, bB, Rin, Qin, Rc_out, Qc_out;
         // pass 1: suffix values, tiles right to left
         float Rc = kNeg;
         for (int t = n_tiles - 1; t >= 0; --t) {
-            const long long s = base + (long long)t * kLongTile + (long long)lane * kLongK;
+            const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
-            float carry;
-            const float Rin = suffix_in({aB, bB}, lane, Rc, &carry);
-            Rc = carry;
-            lane_suffix<kLongK>(la, w, Rin, lR);
+            lane_scans<32>(aB, bB, lane, Rc, kNeg, Rin, Qin, &Rc_out, &Qc_out);
+            Rc = Rc_out;
+            lane_recurrences<kLongK>(la, w, Rin, kNeg, lR, lQ);
             float* dst = my_scratch + (long long)t * kLongTile + lane * kLongK;
 #pragma unroll
             for (int j = 0; j < kLongK; j += 4)
@@ -308,19 +326,19 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         // pass 2: prefix values and messages, tiles left to right
         float Qc = kNeg;
         for (int t = 0; t < n_tiles; ++t) {
-            const long long s = base + (long long)t * kLongTile + (long long)lane * kLongK;
+            const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
+            lane_scans<32>(aB, bB, lane, kNeg, Qc, Rin, Qin, &Rc_out, &Qc_out);
+            Qc = Qc_out;
+            lane_recurrences<kLongK>(la, w, kNeg, Qin, lR, lQ);
             const float* src = my_scratch + (long long)t * kLongTile + lane * kLongK;
 #pragma unroll
             for (int j = 0; j < kLongK; j += 4) {
                 const float4 a = *reinterpret_cast<const float4*>(src + j);
                 lR[j] = a.x; lR[j + 1] = a.y; lR[j + 2] = a.z; lR[j + 3] = a.w;
             }
-            float carry;
-            const float Qin = prefix_in({-aB, bB - aB}, lane, Qc, &carry);
-            Qc = carry;
-            lane_prefix_out<kLongK>(la, w, l, lR, Qin, s, e0, e1, lam);
+            if (s < e1) lane_out<kLongK>(l, lR, lQ, s, e1, lam);
         }
     }
 }
@@ -357,11 +375,76 @@ __global__ void __launch_bounds__(256) voxel_reduce_kernel(long long n_items, co
     }
 }
 
+// ---------------------------------------------------------------- K6 (tile-run transpose)
+// Same sums, over the tile->ray-run transpose: a CTA (1024 threads) takes a work item (tile t,
+// <= kRunsPerItem of its runs).  Groups of 8 lanes read one run's vid/q contiguously and add q
+// into the tile's 16384 slots in shared memory, split into 16-bit halves held in two int32
+// arrays (native 32-bit shared atomics; a slot gets at most one contribution per run, so the
+// halves cannot overflow within an item).  The slots then go to T with one int64 atomic each
+// (a tile spans several items).  Integer sums: exact, independent of order and scheduling.
+constexpr int kK6Threads = 1024;
+
+__global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
+                                                                   const long long* __restrict__ tile_ptr,
+                                                                   const Run* __restrict__ runs,
+                                                                   const int32_t* __restrict__ vid,
+                                                                   const int32_t* __restrict__ lam, long long* T) {
+    extern __shared__ int smem[];
+    int* acc_lo = smem;                 // sum of (q & 0xffff)
+    int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane >> 3, sl = lane & 7;
+    constexpr int kWarps = kK6Threads / 32;
+    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int2 item = __ldg(items + it);
+        for (int i = threadIdx.x; i < 2 * kTileSlots; i += kK6Threads) smem[i] = 0;
+        __syncthreads();
+        const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * kRunsPerItem;
+        long long r1 = __ldg(tile_ptr + item.x + 1);
+        if (r1 > r0 + kRunsPerItem) r1 = r0 + kRunsPerItem;
+        for (long long rb = r0 + 4 * wid; rb < r1; rb += 4 * kWarps) {
+            Run run{0u, 0u};
+            if (rb + sub < r1) {
+                const uint2 rr = __ldg(reinterpret_cast<const uint2*>(runs + rb + sub));
+                run = Run{rr.x, rr.y};
+            }
+            for (int k = sl; k < (int)run.n; k += 32) {
+                int v[4], q[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool ok = k + 8 * u < (int)run.n;
+                    const long long e = (long long)run.e + k + 8 * u;
+                    v[u] = ok ? __ldg(vid + e) : -1;
+                    q[u] = ok ? __ldg(lam + e) : 0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (v[u] >= 0) {
+                        const int slot = v[u] & (kTileSlots - 1);
+                        atomicAdd(acc_lo + slot, q[u] & 0xffff);
+                        atomicAdd(acc_hi + slot, q[u] >> 16);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        long long* Tt = T + ((long long)item.x << kTileShift);
+        for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
+            const long long sum = (long long)acc_hi[i] * 65536 + (long long)acc_lo[i];
+            if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- K8
-__global__ void marginals_kernel(long long V, const long long* __restrict__ T, double L0, float* out) {
+__global__ void marginals_kernel(GridDesc g, const long long* __restrict__ T, double L0, float* out) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long V = (long long)g.nx * g.ny * g.nz;
     if (v >= V) return;
-    const double a = L0 + (double)T[v] * kQInvD;  // Eq.8: prior times all incoming messages
+    const int x = (int)(v % g.nx);
+    const int y = (int)((v / g.nx) % g.ny);
+    const int z = (int)(v / ((long long)g.nx * g.ny));
+    const double a = L0 + (double)T[voxel_slot(g, x, y, z)] * kQInvD;  // Eq.8: prior x all incoming messages
     out[v] = (float)(1.0 / (1.0 + exp(-a)));
 }
 
@@ -374,18 +457,20 @@ inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) /
 
 }  // namespace
 
-int class_capacity(int cls) { return cls < 3 ? 32 * (4 << cls) : 0x7fffffff; }
+int class_capacity(int cls) { return cls < kNumClasses - 1 ? kLaneK * (kMinGroup << cls) : 0x7fffffff; }
 
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
                          const RayInfo* ray_z, const int32_t* vid, const int16_t* off_q, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, cudaStream_t s) {
     if (n_rays == 0) return;
-    const unsigned grid = blocks_for(n_rays * 32, 256);
+    auto grid = [&](int G) { return blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256); };
+    constexpr int G0 = kMinGroup, K = kLaneK;
     switch (cls) {
-        case 0: ray_msg_kernel<4><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
-        case 1: ray_msg_kernel<8><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
-        case 2: ray_msg_kernel<16><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
+        case 0: ray_msg_kernel<G0, K><<<grid(G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
+        case 1: ray_msg_kernel<2 * G0, K><<<grid(2 * G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
+        case 2: ray_msg_kernel<4 * G0, K><<<grid(4 * G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
+        case 3: ray_msg_kernel<8 * G0, K><<<grid(8 * G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
         default: {
             const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
             ray_msg_long_kernel<<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp, scratch,
@@ -401,8 +486,23 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
     voxel_reduce_kernel<<<blocks_for(warps * 32, 256), 256, 0, s>>>(n_items, items, col_ptr, tr, lam, T);
 }
 
-void launch_marginals(long long V, const long long* T, double L0, float* out, cudaStream_t s) {
-    marginals_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, T, L0, out);
+void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
+                        const int32_t* vid, const int32_t* lam, long long* T, cudaStream_t s) {
+    if (n_items == 0) return;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(tile_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             2 * kTileSlots * (int)sizeof(int));
+        configured = true;
+    }
+    const long long grid = n_items < 148LL ? n_items : 148LL;
+    tile_reduce_kernel<<<(unsigned)grid, kK6Threads, 2 * kTileSlots * sizeof(int), s>>>(n_items, items, tile_ptr, runs,
+                                                                                     vid, lam, T);
+}
+
+void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s) {
+    const long long V = (long long)g.nx * g.ny * g.nz;
+    marginals_kernel<<<blocks_for(V, 256), 256, 0, s>>>(g, T, L0, out);
 }
 
 void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s) {

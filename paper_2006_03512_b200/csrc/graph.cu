@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             bool last;
             const int a = w.earliest();
             const double t_out = crossing_t(w, a, last);
-            const int vx = w.cell[0] + g.nx * (w.cell[1] + g.ny * w.cell[2]);
+            const int vx = voxel_slot(g, w.cell[0], w.cell[1], w.cell[2]);
             const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
             long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
             q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
@@ -267,9 +267,84 @@ __global__ void __launch_bounds__(256) transpose_fill_kernel(long long n_rays, c
     }
 }
 
-__global__ void item_counts_kernel(long long V, const int32_t* __restrict__ cnt, int32_t* n_items) {
+__global__ void item_counts_kernel(long long V, const int32_t* __restrict__ cnt, int32_t* n_items, int chunk) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < V) n_items[v] = (cnt[v] + kVoxelChunk - 1) / kVoxelChunk;
+    if (v < V) n_items[v] = (cnt[v] + chunk - 1) / chunk;
+}
+
+// K4b: tile-run transpose.  Thread per ray; a run starts at the ray's first incidence and
+// wherever the tile changes (a ray crosses a convex tile once, so (ray, tile) -> one run).
+__global__ void __launch_bounds__(256) run_count_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                                        const RayInfo* __restrict__ info,
+                                                        const int32_t* __restrict__ vid, int32_t* tile_runs) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    long long e = 0, e1 = 0;
+    if (r < n_rays) {
+        e = row_ptr[r];
+        e1 = e + info[r].n;
+    }
+    int prev = -1;
+    for (;;) {
+        const bool alive = e < e1;
+        const unsigned am = __ballot_sync(kFull, alive);
+        if (am == 0) break;
+        if (alive) {
+            const int b = vid[e] >> kTileShift;
+            const bool start = b != prev;
+            prev = b;
+            const unsigned sm = __ballot_sync(am, start);
+            if (start) {
+                const unsigned peers = __match_any_sync(sm, b);
+                if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[b], __popc(peers));
+            }
+            ++e;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                                       const RayInfo* __restrict__ info,
+                                                       const int32_t* __restrict__ vid,
+                                                       const long long* __restrict__ tile_ptr, int32_t* cursor,
+                                                       Run* runs) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    long long e = 0, e1 = 0, start = 0;
+    if (r < n_rays) {
+        e = row_ptr[r];
+        e1 = e + info[r].n;
+    }
+    bool alive = e < e1;
+    int cur = -1;
+    for (;;) {
+        const unsigned am = __ballot_sync(kFull, alive);
+        if (am == 0) break;
+        if (alive) {
+            const bool at_end = e == e1;
+            const int b = at_end ? -1 : (vid[e] >> kTileShift);
+            const bool emit = cur >= 0 && b != cur;  // the run in tile `cur` ends before e
+            const unsigned em = __ballot_sync(am, emit);
+            if (emit) {
+                const unsigned peers = __match_any_sync(em, cur);
+                const int leader = __ffs(peers) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(&cursor[cur], __popc(peers));
+                base = __shfl_sync(peers, base, leader);
+                const int rank = __popc(peers & ((1u << lane) - 1u));
+                runs[tile_ptr[cur] + base + rank] = Run{(unsigned)start, (unsigned)(e - start)};
+            }
+            if (at_end) {
+                alive = false;
+            } else {
+                if (b != cur) {
+                    cur = b;
+                    start = e;
+                }
+                ++e;
+            }
+        }
+    }
 }
 
 __global__ void item_fill_kernel(long long V, const int32_t* __restrict__ n_items,
@@ -291,9 +366,9 @@ __global__ void class_flags_kernel(long long n_rays, const RayInfo* __restrict__
     const int n = info[r].n;
     int c = -1;
     if (n > 0) {
-        c = 3;
-        for (int k = 0; k < 3; ++k) {
-            if (n <= 32 * (4 << k)) {  // 4, 8, 16 elements per lane
+        c = kNumClasses - 1;
+        for (int k = 0; k < kNumClasses - 1; ++k) {
+            if (n <= kLaneK * (kMinGroup << k)) {  // groups of G lanes of kLaneK incidences
                 c = k;
                 break;
             }
@@ -346,8 +421,20 @@ void launch_transpose_fill(long long n_rays, const long long* row_ptr, const Ray
     transpose_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, col_ptr, cursor, tr);
 }
 
-void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, cudaStream_t s) {
-    item_counts_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, n_items);
+void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, int chunk, cudaStream_t s) {
+    item_counts_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, n_items, chunk);
+}
+
+void launch_run_count(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                      int32_t* tile_runs, cudaStream_t s) {
+    if (n_rays == 0) return;
+    run_count_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, tile_runs);
+}
+
+void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                     const long long* tile_ptr, int32_t* cursor, Run* runs, cudaStream_t s) {
+    if (n_rays == 0) return;
+    run_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, tile_ptr, cursor, runs);
 }
 
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,

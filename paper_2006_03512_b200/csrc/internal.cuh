@@ -19,13 +19,40 @@ constexpr float kQInv = 1.0f / 8388608.0f;
 constexpr double kQInvD = 1.0 / 8388608.0;
 constexpr float kLambdaClip = 256.0f;         // reading R9
 constexpr int kPadElems = 64;                 // slack after incidence arrays (aligned over-reads)
-constexpr int kVoxelChunk = 4096;             // K6 work item: <= 4096 transpose entries
+constexpr int kVoxelChunk = 4096;             // per-voxel K6 work item: <= 4096 transpose entries
+// Internal voxel layout: 32 x 32 x 16 tiles (16384 slots), tile-major.  K6 accumulates one tile
+// at a time in shared memory, so a tile's slots must fit one CTA (2 x int32 x 16384 = 128 KB).
+constexpr int kTileShift = 14;                // slot = tile << 14 | (z&15) << 10 | (y&31) << 5 | (x&31)
+constexpr int kTileSlots = 1 << kTileShift;
+constexpr int kRunsPerItem = 16384;           // K6 work item: <= 16384 runs of one tile (int32 halves never overflow)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
+// Dense grid; internally voxels are stored tile-major in 32 x 32 x 16 tiles (the paper's GVDB
+// stores 8^3 bricks; the larger tile here is the unit of the K6 shared-memory reduction):
+// slot = tile * 16384 + (x&31) + 32 (y&31) + 1024 (z&15), tile = tx + ntx (ty + nty tz).
 struct GridDesc {
     int nx, ny, nz;
+    int ntx, nty, ntz;
     double res, ox, oy, oz;
+};
+
+__host__ __device__ __forceinline__ int voxel_slot(const GridDesc& g, int x, int y, int z) {
+    return ((((z >> 4) * g.nty + (y >> 5)) * g.ntx + (x >> 5)) << kTileShift) | ((z & 15) << 10) | ((y & 31) << 5) |
+           (x & 31);
+}
+__host__ __device__ __forceinline__ void slot_xyz(const GridDesc& g, long long s, int& x, int& y, int& z) {
+    const long long t = s >> kTileShift;
+    const int l = (int)(s & (kTileSlots - 1));
+    x = (int)(t % g.ntx) * 32 + (l & 31);
+    y = (int)((t / g.ntx) % g.nty) * 32 + ((l >> 5) & 31);
+    z = (int)(t / ((long long)g.ntx * g.nty)) * 16 + (l >> 10);
+}
+
+// A run: the contiguous incidences [e, e + n) of one ray inside one tile.
+struct Run {
+    unsigned e;
+    unsigned n;
 };
 
 struct NoiseDesc {
@@ -79,8 +106,13 @@ long long scan_scratch_elems(long long n);
 // K4: tr[col_ptr[v] + slot] = e for every incidence e (cursor zeroed by caller)
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                            const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s);
-// K6 work list: n_items[v] = ceil(deg/kVoxelChunk); items from item_ptr
-void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, cudaStream_t s);
+// tile-run transpose (K4b): runs per tile, then the run list grouped by tile
+void launch_run_count(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                      int32_t* tile_runs, cudaStream_t s);
+void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                     const long long* tile_ptr, int32_t* cursor, Run* runs, cudaStream_t s);
+// K6 work list: n_items[i] = ceil(count[i] / chunk); items (i, j) from item_ptr
+void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, int chunk, cudaStream_t s);
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
                       cudaStream_t s);
 // K5 ray length classes: flags[r] = (class(r) == c)
@@ -92,7 +124,12 @@ void launch_span_max(long long n, const int32_t* rays, const RayInfo* info, unsi
                      cudaStream_t s);
 
 // ---- BP kernels (bp.cu)
-constexpr int kNumClasses = 4;      // K = 4, 8, 16 single-tile warps; class 3 = long rays (tiled)
+#ifndef MRF_LANE_K
+#define MRF_LANE_K 8
+#endif
+constexpr int kLaneK = MRF_LANE_K;              // incidences per lane in K5
+constexpr int kMinGroup = 32 / MRF_LANE_K;      // classes: G = kMinGroup << k lanes, capacity 32 << k
+constexpr int kNumClasses = 5;      // 4 group widths (capacity kLaneK * G) + class 4 = long rays (tiled)
 int class_capacity(int cls);        // max span handled by class cls (class 3: unbounded)
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
                          const RayInfo* info, const int32_t* vid, const int16_t* off_q, int32_t* lam,
@@ -100,7 +137,9 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
                          int n_warps_long, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
-void launch_marginals(long long V, const long long* T, double L0, float* out, cudaStream_t s);
+void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
+                         const int32_t* vid, const int32_t* lam, long long* T, cudaStream_t s);
+void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s);
 void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s);
 
 }  // namespace mrf

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,7 +75,11 @@ struct mrf_ctx {
     int device = 0;
     GridDesc grid{};
     NoiseDesc noise{};
-    long long V = 0;
+    long long V = 0;   // voxels (nx*ny*nz)
+    long long VI = 0;  // internal belief slots: tiles * 16384 (tile-major, DESIGN.md §Data layout)
+    long long NT = 0;  // tiles
+    bool k6_voxel = false;  // ablation: per-voxel transpose K6 instead of the tile-run K6 (MRF_K6=voxel)
+    bool vtr_valid = false; // per-voxel transpose built for the current graph
     float prior = 0.5f;
     double L0 = 0.0;
     MsgParams mp{};
@@ -99,13 +104,18 @@ struct mrf_ctx {
     DBuf<long long> col_ptr, item_ptr, pos;
     DBuf<int2> items;
     long long n_items_total = 0;
+    DBuf<int32_t> tile_runs, tile_cursor, tile_nitems;
+    DBuf<long long> tile_ptr, bitem_ptr;
+    DBuf<Run> runs;
+    DBuf<int2> bitems;
+    long long n_runs = 0, n_bitems = 0;
     DBuf<long long> T, T_part;
     DBuf<float2> lutp;
     DBuf<float> depth_stage, marg;
     DBuf<long long> scan_scratch;
     DBuf<unsigned long long> counters;
     DBuf<int32_t> class_rays[kNumClasses];
-    long long class_n[kNumClasses] = {0, 0, 0, 0};
+    long long class_n[kNumClasses] = {};
     DBuf<float> long_scratch;
     long long long_scratch_per_warp = 0;
     int n_warps_long = 0;
@@ -218,33 +228,80 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
     return MRF_OK;
 }
 
-// Build the voxel->ray transpose, the K6 work list and the K5 length classes (on graph change).
-mrf_status prepare(mrf_ctx* c) {
-    if (!c->dirty) return MRF_OK;
-    const long long V = c->V;
+// Per-voxel transpose (col_ptr over belief slots, tr) + its K6 work list.  Built by prepare()
+// only for the per-voxel K6 ablation, and lazily for mrf_export_transpose.
+mrf_status build_voxel_transpose(mrf_ctx* c) {
+    if (c->vtr_valid) return MRF_OK;
+    const long long VI = c->VI;
     mrf_status st;
-    // K4: col_ptr = scan(degrees); tr by cursor atomics
-    if ((st = scan(c, c->vox_count.p, c->col_ptr.p, V, 0)) != MRF_OK) return st;
+    if ((st = scan(c, c->vox_count.p, c->col_ptr.p, VI, 0)) != MRF_OK) return st;
     CK(c->tr.ensure((size_t)c->E + kPadElems, 0, c->stream));
-    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * V, c->stream));
+    CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * VI, c->stream));
     {
         ProfScope ps(c, MRF_K_TRANSPOSE);
         launch_transpose_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->col_ptr.p, c->cursor.p, c->tr.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
-        launch_item_counts(V, c->vox_count.p, c->n_items.p, c->stream);
+        launch_item_counts(VI, c->vox_count.p, c->n_items.p, kVoxelChunk, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, 1);
     }
-    if ((st = scan(c, c->n_items.p, c->item_ptr.p, V, 0)) != MRF_OK) return st;
-    if ((st = read_ll(c, c->item_ptr.p + V, &c->n_items_total)) != MRF_OK) return st;
+    if ((st = scan(c, c->n_items.p, c->item_ptr.p, VI, 0)) != MRF_OK) return st;
+    if ((st = read_ll(c, c->item_ptr.p + VI, &c->n_items_total)) != MRF_OK) return st;
     CK(c->items.ensure((size_t)std::max(1LL, c->n_items_total), 0, c->stream));
     {
         ProfScope ps(c, MRF_K_TRANSPOSE);
-        launch_item_fill(V, c->n_items.p, c->item_ptr.p, c->items.p, c->stream);
+        launch_item_fill(VI, c->n_items.p, c->item_ptr.p, c->items.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, 1);
     }
-    // K5 classes by span (stable compaction keeps pixel order inside a class)
-    CK(c->flags.ensure((size_t)std::max(c->R, V) + 1, 0, c->stream));
-    CK(c->pos.ensure((size_t)std::max(c->R, V) + 1, 0, c->stream));
+    c->vtr_valid = true;
+    return MRF_OK;
+}
+
+// Tile-run transpose (runs grouped by tile) + its K6 work list.
+mrf_status build_tile_runs(mrf_ctx* c) {
+    const long long NT = c->NT;
+    mrf_status st;
+    CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_run_count(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_runs.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    }
+    if ((st = scan(c, c->tile_runs.p, c->tile_ptr.p, NT, 0)) != MRF_OK) return st;
+    if ((st = read_ll(c, c->tile_ptr.p + NT, &c->n_runs)) != MRF_OK) return st;
+    CK(c->runs.ensure((size_t)std::max(1LL, c->n_runs), 0, c->stream));
+    CK(cudaMemsetAsync(c->tile_cursor.p, 0, sizeof(int32_t) * NT, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p, c->runs.p,
+                        c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        launch_item_counts(NT, c->tile_runs.p, c->tile_nitems.p, kRunsPerItem, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+    }
+    if ((st = scan(c, c->tile_nitems.p, c->bitem_ptr.p, NT, 0)) != MRF_OK) return st;
+    if ((st = read_ll(c, c->bitem_ptr.p + NT, &c->n_bitems)) != MRF_OK) return st;
+    CK(c->bitems.ensure((size_t)std::max(1LL, c->n_bitems), 0, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_item_fill(NT, c->tile_nitems.p, c->bitem_ptr.p, c->bitems.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+    }
+    return MRF_OK;
+}
+
+// Build the transpose used by K6, its work list and the K5 length classes (on graph change).
+mrf_status prepare(mrf_ctx* c) {
+    if (!c->dirty) return MRF_OK;
+    mrf_status st;
+    c->vtr_valid = false;
+    if (c->k6_voxel) {
+        if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
+    } else {
+        if ((st = build_tile_runs(c)) != MRF_OK) return st;
+    }
+    // K5 classes by ray length (stable compaction keeps pixel order inside a class)
+    CK(c->flags.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
+    CK(c->pos.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
     for (int k = 0; k < kNumClasses; ++k) {
         launch_class_flags(c->R, c->ray_z.p, k, c->flags.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
@@ -255,15 +312,16 @@ mrf_status prepare(mrf_ctx* c) {
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     }
     // scratch for the tiled long-ray kernel
-    if (c->class_n[3] > 0) {
+    const int kl = kNumClasses - 1;
+    if (c->class_n[kl] > 0) {
         CK(cudaMemsetAsync(c->counters.p + 6, 0, sizeof(unsigned long long), c->stream));
-        launch_span_max(c->class_n[3], c->class_rays[3].p, c->ray_z.p, c->counters.p + 6, c->stream);
+        launch_span_max(c->class_n[kl], c->class_rays[kl].p, c->ray_z.p, c->counters.p + 6, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, 1);
         long long span = 0;
         if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
-        const long long tile = 256;
+        const long long tile = 512;
         c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
-        c->n_warps_long = (int)std::min<long long>(c->class_n[3], 148LL * 16);
+        c->n_warps_long = (int)std::min<long long>(c->class_n[kl], 148LL * 16);
         CK(c->long_scratch.ensure((size_t)(c->long_scratch_per_warp * c->n_warps_long), 0, c->stream));
     }
     c->dirty = false;
@@ -273,9 +331,14 @@ mrf_status prepare(mrf_ctx* c) {
 // K6 over the current messages into `out` (zeroed first).
 mrf_status voxel_sums(mrf_ctx* c, long long* out) {
     ProfScope ps(c, MRF_K_VOXEL_SUM);
-    CK(cudaMemsetAsync(out, 0, sizeof(long long) * c->V, c->stream));
-    launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
-    CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
+    CK(cudaMemsetAsync(out, 0, sizeof(long long) * c->VI, c->stream));
+    if (c->k6_voxel) {
+        launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
+        CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
+    } else {
+        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->vid.p, c->lam.p, out, c->stream);
+        CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
+    }
     return MRF_OK;
 }
 
@@ -293,7 +356,7 @@ mrf_status ray_messages(mrf_ctx* c) {
 
 mrf_status allreduce_T(mrf_ctx* c) {
     ProfScope ps(c, MRF_K_ALLREDUCE);
-    NCK(ncclAllReduce(c->T_part.p, c->T.p, (size_t)c->V, ncclInt64, ncclSum, c->comm, c->stream));
+    NCK(ncclAllReduce(c->T_part.p, c->T.p, (size_t)c->VI, ncclInt64, ncclSum, c->comm, c->stream));
     c->prof_launch[MRF_K_ALLREDUCE] += 1;
     return MRF_OK;
 }
@@ -333,6 +396,13 @@ mrf_status host_layout(mrf_ctx* c, HostLayout& h) {
     return MRF_OK;
 }
 
+// belief slot (tile-major) -> external voxel id x + nx (y + ny z)
+long long slot_to_voxel(const GridDesc& g, long long s) {
+    int x, y, z;
+    slot_xyz(g, s, x, y, z);
+    return x + (long long)g.nx * (y + (long long)g.ny * z);
+}
+
 // padded -> canonical copy (to_canon) or back, element size `es`
 void relayout(const HostLayout& h, const void* src, void* dst, size_t es, bool to_canon) {
     const char* s = static_cast<const char*>(src);
@@ -365,6 +435,8 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         if (dims[k] <= 0 || dims[k] > 8192) return reject("dims must be in [1, 8192]");
     const long long V = (long long)dims[0] * dims[1] * dims[2];
     if (V >= (1LL << 31)) return reject("nx*ny*nz must be < 2^31");
+    if ((long long)((dims[0] + 31) / 32) * ((dims[1] + 31) / 32) * ((dims[2] + 15) / 16) * 16384 >= (1LL << 31))
+        return reject("tile-padded grid (32x32x16 tiles) must have < 2^31 voxels");
     if (!std::isfinite(resolution_m) || !(resolution_m > 0)) return reject("resolution must be finite and > 0");
     if (!finite_all(origin_m, 3)) return reject("origin must be finite");
     if (!(prior > 0.f && prior < 1.f)) return reject("prior must be in (0, 1)");
@@ -390,7 +462,11 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
 
     mrf_ctx* c = new mrf_ctx();
     cudaGetDevice(&c->device);
-    c->grid = {dims[0], dims[1], dims[2], resolution_m, origin_m[0], origin_m[1], origin_m[2]};
+    c->grid = {dims[0], dims[1], dims[2], (dims[0] + 31) / 32, (dims[1] + 31) / 32, (dims[2] + 15) / 16,
+               resolution_m, origin_m[0], origin_m[1], origin_m[2]};
+    c->NT = (long long)c->grid.ntx * c->grid.nty * c->grid.ntz;
+    c->VI = c->NT * kTileSlots;
+    if (const char* k6 = getenv("MRF_K6")) c->k6_voxel = strcmp(k6, "voxel") == 0;
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
                 noise->sigma_c[0], noise->sigma_c[1], noise->sigma_c[2], noise->n_z, noise->n_off};
     c->V = V;
@@ -412,17 +488,23 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     c->stream = c->own_stream;
     mrf_status st = MRF_OK;
     auto alloc = [&]() -> mrf_status {
-        CK(c->T.ensure((size_t)V, 0, c->stream));
-        if (world > 1) CK(c->T_part.ensure((size_t)V, 0, c->stream));
-        CK(c->vox_count.ensure((size_t)V, 0, c->stream));
-        CK(c->cursor.ensure((size_t)V, 0, c->stream));
-        CK(c->n_items.ensure((size_t)V, 0, c->stream));
-        CK(c->col_ptr.ensure((size_t)V + 1, 0, c->stream));
-        CK(c->item_ptr.ensure((size_t)V + 1, 0, c->stream));
+        const long long VI = c->VI, NT = c->NT;
+        CK(c->T.ensure((size_t)VI, 0, c->stream));
+        if (world > 1) CK(c->T_part.ensure((size_t)VI, 0, c->stream));
+        CK(c->vox_count.ensure((size_t)VI, 0, c->stream));
+        CK(c->cursor.ensure((size_t)VI, 0, c->stream));
+        CK(c->n_items.ensure((size_t)VI, 0, c->stream));
+        CK(c->col_ptr.ensure((size_t)VI + 1, 0, c->stream));
+        CK(c->item_ptr.ensure((size_t)VI + 1, 0, c->stream));
+        CK(c->tile_runs.ensure((size_t)NT, 0, c->stream));
+        CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
+        CK(c->tile_nitems.ensure((size_t)NT, 0, c->stream));
+        CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
+        CK(c->bitem_ptr.ensure((size_t)NT + 1, 0, c->stream));
         CK(c->counters.ensure(8, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
-        CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * V, c->stream));
-        CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * V, c->stream));
+        CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
+        CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * VI, c->stream));
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
         CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 8, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
@@ -485,6 +567,8 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
     c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
+    c->tile_runs.release(); c->tile_cursor.release(); c->tile_nitems.release(); c->tile_ptr.release();
+    c->bitem_ptr.release(); c->runs.release(); c->bitems.release();
     for (auto& b : c->class_rays) b.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -511,8 +595,8 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences) {
     CK(c->status.ensure((size_t)n_rays, (size_t)c->R, c->stream));
     CK(c->ray_z.ensure((size_t)n_rays, (size_t)c->R, c->stream));
     CK(c->row_ptr.ensure((size_t)n_rays + 1, (size_t)c->R + 1, c->stream));
-    CK(c->flags.ensure((size_t)std::max<long long>(n_rays, c->V) + 1, 0, c->stream));
-    CK(c->pos.ensure((size_t)std::max<long long>(n_rays, c->V) + 1, 0, c->stream));
+    CK(c->flags.ensure((size_t)std::max<long long>(n_rays, c->VI) + 1, 0, c->stream));
+    CK(c->pos.ensure((size_t)std::max<long long>(n_rays, c->VI) + 1, 0, c->stream));
     const size_t ne = (size_t)n_incidences + kPadElems;
     CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
     CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
@@ -526,8 +610,8 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->R = c->E = c->E_real = 0;
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
-    CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * c->V, c->stream));
-    CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * c->V, c->stream));
+    CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * c->VI, c->stream));
+    CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * c->VI, c->stream));
     CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
     c->dirty = true;
     return MRF_OK;
@@ -655,7 +739,7 @@ mrf_status mrf_bp_partial(mrf_ctx* ctx, int32_t iterate, int64_t* partial_out_de
 mrf_status mrf_bp_finish(mrf_ctx* ctx, const int64_t* total_device) {
     ENTER(ctx);
     if (!total_device) return set_err(c, MRF_ERR_INVALID_ARG, "NULL input");
-    CK(cudaMemcpyAsync(c->T.p, total_device, sizeof(long long) * c->V, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->T.p, total_device, sizeof(long long) * c->VI, cudaMemcpyDeviceToDevice, c->stream));
     return MRF_OK;
 }
 
@@ -669,7 +753,7 @@ mrf_status mrf_marginals(mrf_ctx* ctx, float* out, int32_t out_is_device) {
     }
     {
         ProfScope ps(c, MRF_K_MARGINALS);
-        launch_marginals(c->V, c->T.p, c->L0, dst, c->stream);
+        launch_marginals(c->grid, c->T.p, c->L0, dst, c->stream);
         CK_LAUNCH(MRF_K_MARGINALS, 1);
     }
     if (!out_is_device)
@@ -686,14 +770,14 @@ mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences,
     if (n_invalid) *n_invalid = c->n_invalid;
     if (n_dropped) *n_dropped = c->n_dropped;
     if (n_active_vox) {
-        CK(c->flags.ensure((size_t)c->V + 1, 0, c->stream));
-        CK(c->pos.ensure((size_t)c->V + 1, 0, c->stream));
-        launch_active_flags(c->V, c->vox_count.p, c->flags.p, c->stream);
+        CK(c->flags.ensure((size_t)c->VI + 1, 0, c->stream));
+        CK(c->pos.ensure((size_t)c->VI + 1, 0, c->stream));
+        launch_active_flags(c->VI, c->vox_count.p, c->flags.p, c->stream);
         CK_LAUNCH(MRF_K_SCAN, 1);
         mrf_status st;
-        if ((st = scan(c, c->flags.p, c->pos.p, c->V, 0)) != MRF_OK) return st;
+        if ((st = scan(c, c->flags.p, c->pos.p, c->VI, 0)) != MRF_OK) return st;
         long long a = 0;
-        if ((st = read_ll(c, c->pos.p + c->V, &a)) != MRF_OK) return st;
+        if ((st = read_ll(c, c->pos.p + c->VI, &a)) != MRF_OK) return st;
         *n_active_vox = a;
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -725,6 +809,7 @@ mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, 
         CK(cudaMemcpyAsync(tmp.data(), c->vid.p, sizeof(int32_t) * c->E, cudaMemcpyDeviceToHost, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         relayout(h, tmp.data(), vid, sizeof(int32_t), true);
+        for (long long e = 0; e < c->E_real; ++e) vid[e] = (int32_t)slot_to_voxel(c->grid, vid[e]);
     }
     if (off_q && c->E) {
         std::vector<int16_t> tmp((size_t)c->E);
@@ -739,20 +824,35 @@ mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr) {
     ENTER(ctx);
     mrf_status st;
     if ((st = prepare(c)) != MRF_OK) return st;
-    if (col_ptr) CK(cudaMemcpyAsync(col_ptr, c->col_ptr.p, sizeof(long long) * (c->V + 1), cudaMemcpyDeviceToHost, c->stream));
-    if (tr && c->E_real) {
-        HostLayout h;
-        if ((st = host_layout(c, h)) != MRF_OK) return st;
-        std::vector<int32_t> tmp((size_t)c->E_real);
+    if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
+    std::vector<long long> cp((size_t)c->VI + 1);
+    CK(cudaMemcpyAsync(cp.data(), c->col_ptr.p, sizeof(long long) * (c->VI + 1), cudaMemcpyDeviceToHost, c->stream));
+    std::vector<int32_t> tmp((size_t)std::max(1LL, c->E_real));
+    if (c->E_real)
         CK(cudaMemcpyAsync(tmp.data(), c->tr.p, sizeof(int32_t) * c->E_real, cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        // padded slot -> canonical index
-        std::vector<long long> map((size_t)c->E, -1);
-        for (size_t r = 0; r < h.info.size(); ++r)
-            for (int j = 0; j < h.info[r].n; ++j) map[(size_t)h.row_ptr[r] + j] = h.canon[r] + j;
-        for (long long k = 0; k < c->E_real; ++k) tr[k] = (int32_t)map[(size_t)tmp[k]];
-    }
     CK(cudaStreamSynchronize(c->stream));
+    HostLayout h;
+    if ((st = host_layout(c, h)) != MRF_OK) return st;
+    // padded slot -> canonical incidence index
+    std::vector<long long> map((size_t)std::max(1LL, c->E), -1);
+    for (size_t r = 0; r < h.info.size(); ++r)
+        for (int j = 0; j < h.info[r].n; ++j) map[(size_t)h.row_ptr[r] + j] = h.canon[r] + j;
+    // external voxel order
+    std::vector<long long> slot_of((size_t)c->V);
+    for (long long s = 0; s < c->VI; ++s) {
+        const GridDesc& g = c->grid;
+        int x, y, z;
+        slot_xyz(g, s, x, y, z);
+        if (x < g.nx && y < g.ny && z < g.nz) slot_of[(size_t)(x + (long long)g.nx * (y + (long long)g.ny * z))] = s;
+    }
+    long long k = 0;
+    for (long long v = 0; v < c->V; ++v) {
+        const long long s = slot_of[(size_t)v];
+        if (col_ptr) col_ptr[v] = k;
+        for (long long i = cp[(size_t)s]; i < cp[(size_t)s + 1]; ++i, ++k)
+            if (tr) tr[k] = (int32_t)map[(size_t)tmp[(size_t)i]];
+    }
+    if (col_ptr) col_ptr[c->V] = k;
     return MRF_OK;
 }
 
@@ -795,8 +895,14 @@ mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda) {
 mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T) {
     ENTER(ctx);
     if (!T) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
-    CK(cudaMemcpyAsync(T, c->T.p, sizeof(long long) * c->V, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<long long> tmp((size_t)c->VI);
+    CK(cudaMemcpyAsync(tmp.data(), c->T.p, sizeof(long long) * c->VI, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    const GridDesc& g = c->grid;
+    for (long long v = 0; v < c->V; ++v) {
+        const int x = (int)(v % g.nx), y = (int)((v / g.nx) % g.ny), z = (int)(v / ((long long)g.nx * g.ny));
+        T[v] = tmp[(size_t)voxel_slot(g, x, y, z)];
+    }
     return MRF_OK;
 }
 
@@ -835,5 +941,7 @@ mrf_status mrf_profile_read(mrf_ctx* ctx, int64_t* launches, double* total_ms) {
 }
 
 int64_t mrf_launch_count(const mrf_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int64_t mrf_belief_slots(const mrf_ctx* ctx) { return ctx ? ctx->VI : 0; }
 
 }  // extern "C"

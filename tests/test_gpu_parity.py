@@ -286,7 +286,7 @@ def test_virtual_ranks_bit_identical_beliefs(frame1):
         marg1 = m.marginals()
     for world in (2, 3):
         maps = [_gpu_map(w, rank=r, world=world, comm=pkg.MRF_COMM_EXTERNAL) for r in range(world)]
-        parts = [torch.empty(w.n_voxels, dtype=torch.int64, device="cuda") for _ in range(world)]
+        parts = [torch.empty(maps[0].belief_slots(), dtype=torch.int64, device="cuda") for _ in range(world)]
         for _ in range(3):
             for m, part in zip(maps, parts):
                 m.bp_partial(part, iterate=True)
