@@ -118,7 +118,9 @@ const char* mrf_last_error(const mrf_ctx* ctx);
 
 /* ------------------------------------------------------------------ runtime / introspection */
 
-/* Use cuda_stream (a cudaStream_t, or NULL for the ctx's own stream) for all later work. */
+/* Use cuda_stream (a cudaStream_t; NULL = the CUDA default stream) for all later work.  Until
+ * this is called the ctx uses a private non-blocking stream.  Device buffers passed to the ABI
+ * are read/written in stream order on this stream. */
 mrf_status mrf_set_stream(mrf_ctx* ctx, void* cuda_stream);
 
 /* Drop every frame, ray, incidence and message (buffers are kept for reuse); T = 0. */

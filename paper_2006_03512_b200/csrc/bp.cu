@@ -14,8 +14,9 @@
 // Eq.13/14; dividing both messages by V_i leaves the log-odds unchanged and keeps every
 // quantity O(1) in the log domain.  Both recurrences are affine maps x -> 2^a x + 2^b, so a warp
 // composes per-lane chunks and runs two 5-level shuffle scans (prefix for Q, suffix for R).
-// Everything is evaluated in base-2 logs: ex2.approx on the MUFU, log2(1+y) as a polynomial on
-// the FMA pipe (relative accuracy, see log1p2), and lambda without cancellation (lambda2).
+// Everything is evaluated in natural logs (the units of the input table): e^x as ex2.approx on the
+// MUFU, ln(1+y) as a polynomial on the FMA pipe (relative accuracy, see log1pn), and lambda
+// without cancellation (lambda_n).
 //
 // Layout: warp per ray; lane l owns the K consecutive incidences [e0 + l*K, e0 + l*K + K) of
 // the ray; ray segments start at multiples of 4 (RayInfo), so vid/lambda are read as 16-byte
@@ -46,43 +47,37 @@ __device__ __forceinline__ float lg2(float x) {
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
-// log2(1 + y) for y in [0, 1] with RELATIVE accuracy (~2e-7), on the FMA pipe:
-// y * P(y), P a degree-8 fit of log2(1+y)/y (lg2.approx(1+y) is only absolutely accurate
-// near 1, which biased the tiny messages of occluded voxels).
-__device__ __forceinline__ float log1p2(float y) {
-    float r = 0.00754914153367281f;
-    r = fmaf(r, y, -0.04256688803434372f);
-    r = fmaf(r, y, 0.11285588890314102f);
-    r = fmaf(r, y, -0.19711868464946747f);
-    r = fmaf(r, y, 0.2756412625312805f);
-    r = fmaf(r, y, -0.3584084212779999f);
-    r = fmaf(r, y, 0.48069295287132263f);
-    r = fmaf(r, y, -0.7213401794433594f);
-    r = fmaf(r, y, 1.4426950216293335f);
+// ln(1 + y) for y in [0, 1] with RELATIVE accuracy (~2e-7), on the FMA pipe: y * P(y), P a
+// degree-8 fit of ln(1+y)/y.  (lg2.approx(1+y) is only absolutely accurate near 1, which biased
+// the tiny messages of occluded voxels.)
+__device__ __forceinline__ float log1pn(float y) {
+    float r = 0.00523269456f;
+    r = fmaf(r, y, -0.0295052417f);
+    r = fmaf(r, y, 0.0782259554f);
+    r = fmaf(r, y, -0.136632457f);
+    r = fmaf(r, y, 0.191060066f);
+    r = fmaf(r, y, -0.24842982f);
+    r = fmaf(r, y, 0.333190978f);
+    r = fmaf(r, y, -0.499994934f);
+    r = fmaf(r, y, 0.99999994f);
     return r * y;
 }
-// log2(2^a + 2^b), relative-accurate remainder (used where results are differenced)
-__device__ __forceinline__ float lse2(float a, float b) {
-    return fmaxf(a, b) + log1p2(ex2(-fabsf(a - b)));
-}
-// log2(2^a + 2^b) on the MUFU (lg2.approx: ~2^-22 absolute in log2, i.e. ~1.7e-7 relative in
-// the linear quantity).  Used for the Q/R recurrences, the cavity softplus and the scans, whose
-// results are only ever used through differences that are O(1) or through lambda2.
-__device__ __forceinline__ float lse2f(float a, float b) {
-#if MRF_ACCURATE_RECURRENCES
-    return lse2(a, b);
-#else
-    return fmaxf(a, b) + lg2(1.0f + ex2(-fabsf(a - b)));
-#endif
+// e^x on the MUFU (ex2.approx, relative error ~2^-22)
+__device__ __forceinline__ float expn(float x) { return ex2(x * kLog2e); }
+// ln(e^a + e^b), relative-accurate remainder.  Every log-domain quantity is kept in nats, the
+// units of the input table, so no large value is ever rescaled (a nats->bits conversion of a
+// value near the table floor, ~-100, would round at ~1e-5).
+__device__ __forceinline__ float lse(float a, float b) {
+    return fmaxf(a, b) + log1pn(expn(-fabsf(a - b)));
 }
 
-// Affine map x -> 2^a x + 2^b in log2 form.
+// Affine map x -> e^a x + e^b in log form (nats).
 struct Aff {
     float a, b;
 };
 // outer o inner (inner applied first)
 __device__ __forceinline__ Aff compose(Aff outer, Aff inner) {
-    return {outer.a + inner.a, lse2f(outer.a + inner.b, outer.b)};
+    return {outer.a + inner.a, lse(outer.a + inner.b, outer.b)};
 }
 template <int G>
 __device__ __forceinline__ Aff shfl_up(Aff v, int d) {
@@ -98,7 +93,7 @@ __device__ __forceinline__ Aff shfl_idx(Aff v, int l) {
 }
 
 // ---------------------------------------------------------------- per-lane element loads
-// For the K elements [s, s+K) of this lane (log2 units):
+// For the K elements [s, s+K) of this lane (nats):
 //   la = log mu(o=0) = -softplus(c),  w = log mu(o=1) + log nu,  l = log nu.
 // la and log mu(o=1) share one ex2 and are both computed directly, never as a difference of
 // two large numbers.  Masked elements get the identity maps (la = 0, w = NEG).
@@ -134,7 +129,7 @@ __device__ __forceinline__ void load_elems(long long s, long long e0, long long 
     for (int j = 0; j < K; ++j) {
         if (s + j < e1) {
             // cavity (Eq.6): prior + every other incoming message, exact in fixed point
-            const float c2 = fmaf(__ll2float_rn(t[j] - (long long)q[j]), kQInv * kLog2e, mp.L0_2);
+            const float c = fmaf(__ll2float_rn(t[j] - (long long)q[j]), kQInv, mp.L0);
             float fo = fmaf((float)o[j], mp.s_off, mp.b_off);
             fo = fminf(fmaxf(fo, 0.f), mp.fo_max);
             const int io = min((int)fo, mp.n_offm1 - 1);
@@ -143,17 +138,17 @@ __device__ __forceinline__ void load_elems(long long s, long long e0, long long 
             const float ra = fmaf(wo, ta.y - ta.x, ta.x);
             const float rb = fmaf(wo, tb.y - tb.x, tb.x);
             const float lnu = fmaf(wz, rb - ra, ra);
-            const float L1 = lse2f(0.f, -fabsf(c2));  // log2(1 + 2^-|c|)
-            la[j] = -(fmaxf(c2, 0.f) + L1);
-            w[j] = lnu - (fmaxf(-c2, 0.f) + L1);
+            const float L1 = log1pn(expn(-fabsf(c)));  // ln(1 + e^-|c|)
+            la[j] = -(fmaxf(c, 0.f) + L1);
+            w[j] = lnu - (fmaxf(-c, 0.f) + L1);
             l[j] = lnu;
         }
     }
 }
 
-// Lane composite of the suffix maps R -> 2^{la} R + 2^{w} over the chunk (first applied last):
-// aB = sum la, bB = log2 sum_j 2^{w_j + sum_{k<j} la_k}.  The prefix maps
-// Q -> 2^{-la} (Q + 2^{w}) compose to (-aB, bB - aB).
+// Lane composite of the suffix maps R -> e^{la} R + e^{w} over the chunk (first applied last):
+// aB = sum la, bB = ln sum_j e^{w_j + sum_{k<j} la_k}.  The prefix maps
+// Q -> e^{-la} (Q + e^{w}) compose to (-aB, bB - aB).
 template <int K>
 __device__ __forceinline__ void lane_composite(const float (&la)[K], const float (&w)[K], float& aB, float& bB) {
     float acc = 0.f, m = kNeg, t[K];
@@ -165,9 +160,9 @@ __device__ __forceinline__ void lane_composite(const float (&la)[K], const float
     }
     float sum = 0.f;
 #pragma unroll
-    for (int j = 0; j < K; ++j) sum += ex2(t[j] - m);
+    for (int j = 0; j < K; ++j) sum += expn(t[j] - m);
     aB = acc;
-    bB = m + lg2(sum);
+    bB = m + lg2(sum) * kLn2;
 }
 
 // Both lane scans of a ray's G lanes at once (two independent shuffle chains per level):
@@ -176,8 +171,8 @@ __device__ __forceinline__ void lane_composite(const float (&la)[K], const float
 template <int G>
 __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc, float Qc, float& Rin, float& Qin,
                                            float* Rc_out, float* Qc_out) {
-    Aff H = {aB, bB};          // suffix maps R -> 2^{la} R + 2^{w}
-    Aff P = {-aB, bB - aB};    // prefix maps Q -> 2^{-la} (Q + 2^{w})
+    Aff H = {aB, bB};          // suffix maps R -> e^{la} R + e^{w}
+    Aff P = {-aB, bB - aB};    // prefix maps Q -> e^{-la} (Q + e^{w})
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
         const Aff oh = shfl_down<G>(H, d);
@@ -192,16 +187,16 @@ __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc,
     if (Rc_out) {
         const Aff H0 = shfl_idx<G>(H, 0);
         const Aff Pl = shfl_idx<G>(P, G - 1);
-        *Rc_out = lse2f(H0.a + Rc, H0.b);
-        *Qc_out = lse2f(Pl.a + Qc, Pl.b);
+        *Rc_out = lse(H0.a + Rc, H0.b);
+        *Qc_out = lse(Pl.a + Qc, Pl.b);
     }
-    Rin = lse2f(Hx.a + Rc, Hx.b);
-    Qin = lse2f(Px.a + Qc, Px.b);
+    Rin = lse(Hx.a + Rc, Hx.b);
+    Qin = lse(Px.a + Qc, Px.b);
 }
 
 // The two per-lane recurrences, interleaved (independent chains):
-//   lR[j] = log2 R_j (suffix strictly after j),  R_{j-1} = mu(o_j=0) R_j + mu(o_j=1) nu_j
-//   lQ[j] = log2 Q_j (prefix strictly before j), Q_{j+1} = (Q_j + mu(o_j=1) nu_j) / mu(o_j=0)
+//   lR[j] = ln R_j (suffix strictly after j),  R_{j-1} = mu(o_j=0) R_j + mu(o_j=1) nu_j
+//   lQ[j] = ln Q_j (prefix strictly before j), Q_{j+1} = (Q_j + mu(o_j=1) nu_j) / mu(o_j=0)
 template <int K>
 __device__ __forceinline__ void lane_recurrences(const float (&la)[K], const float (&w)[K], float Rin, float Qin,
                                                  float (&lR)[K], float (&lQ)[K]) {
@@ -211,21 +206,19 @@ __device__ __forceinline__ void lane_recurrences(const float (&la)[K], const flo
         const int jb = K - 1 - i;
         lR[jb] = R;
         lQ[i] = Q;
-        R = lse2f(la[jb] + R, w[jb]);
-        Q = lse2f(Q, w[i]) - la[i];
+        R = lse(la[jb] + R, w[jb]);
+        Q = lse(Q, w[i]) - la[i];
     }
 }
 
-// lambda2 = log2(2^Q + 2^l) - log2(2^Q + 2^R) without cancellation: the max parts subtract
-// exactly (both are Q when Q dominates) and the remainders are small, relative-accurate log1p
-// terms.
-__device__ __forceinline__ float lambda2(float Q, float l, float R) {
+// lambda = ln(e^Q + e^l) - ln(e^Q + e^R) without cancellation: the max parts subtract exactly
+// (both are Q when Q dominates) and the remainders are small, relative-accurate log1p terms.
+__device__ __forceinline__ float lambda_n(float Q, float l, float R) {
     const float m1 = fmaxf(Q, l), m2 = fmaxf(Q, R);
-    return (m1 - m2) + (log1p2(ex2(-fabsf(Q - l))) - log1p2(ex2(-fabsf(Q - R))));
+    return (m1 - m2) + (log1pn(expn(-fabsf(Q - l))) - log1pn(expn(-fabsf(Q - R))));
 }
 
-__device__ __forceinline__ int32_t quantise(float lam2) {
-    float lam = lam2 * kLn2;
+__device__ __forceinline__ int32_t quantise(float lam) {
     lam = fminf(fmaxf(lam, -kLambdaClip), kLambdaClip);
     return __float2int_rn(lam * kQScale);  // saturates at +2^31-1 for +256
 }
@@ -236,7 +229,7 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
                                          long long e1, int32_t* lam) {
     int32_t out[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) out[j] = quantise(lambda2(lQ[j], l[j], lR[j]));
+    for (int j = 0; j < K; ++j) out[j] = quantise(lambda_n(lQ[j], l[j], lR[j]));
     if (s + K <= e1) {
 #pragma unroll
         for (int j = 0; j < K; j += 4)

@@ -80,13 +80,13 @@ struct RayInfo {
     int unused;
 };
 
-// K5 parameters (log2 units).
+// K5 parameters (natural logs).
 struct MsgParams {
-    const float2* lutp;       // pair table [n_z][n_off-1] of (L[i][j], L[i][j+1]) * log2(e)
+    const float2* lutp;       // pair table [n_z][n_off-1] of (L[i][j], L[i][j+1]): the input log nu, exactly
     int n_offm1;              // n_off - 1
     float s_off, b_off;       // fo = off_q * s_off + b_off
     float fo_max;             // n_off - 1
-    float L0_2;               // prior log-odds * log2(e)
+    float L0;                 // prior log-odds ln(gamma / (1 - gamma))
 };
 
 // ---- launchers (all asynchronous on `s`)

@@ -508,20 +508,13 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
         CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 8, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
-        // LUT as (L[i][j], L[i][j+1]) pairs in log2 units: one 8-byte load per LUT row in K5.
-        // Each row is shifted by its maximum: a ray's lookups interpolate two rows with one
-        // weight, so the shift is a per-ray constant factor on nu, which leaves every message
-        // unchanged (nu-scale invariance, R2) while keeping the values near the
-        // surface close to 0, where fp32 has its finest absolute resolution.
+        // LUT as (L[i][j], L[i][j+1]) pairs: one 8-byte load per LUT row in K5.  The values are
+        // the input table's floats, unscaled and unshifted.
         const int nz = noise->n_z, no = noise->n_off;
         std::vector<float2> h((size_t)nz * (no - 1));
         for (int i = 0; i < nz; ++i) {
             const float* row = noise->log_nu + (size_t)i * no;
-            double mx = row[0];
-            for (int j = 1; j < no; ++j) mx = std::max(mx, (double)row[j]);
-            for (int j = 0; j < no - 1; ++j)
-                h[(size_t)i * (no - 1) + j] = make_float2((float)(((double)row[j] - mx) * (double)kLog2e),
-                                                          (float)(((double)row[j + 1] - mx) * (double)kLog2e));
+            for (int j = 0; j < no - 1; ++j) h[(size_t)i * (no - 1) + j] = make_float2(row[j], row[j + 1]);
         }
         CK(c->lutp.ensure(h.size(), 0, c->stream));
         CK(cudaMemcpyAsync(c->lutp.p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
@@ -532,7 +525,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         c->mp.s_off = (float)((double)no / (32768.0 * span));
         c->mp.b_off = (float)(-noise->off_lo * (double)no / span - 0.5);
         c->mp.fo_max = (float)(no - 1);
-        c->mp.L0_2 = (float)(c->L0 * (double)kLog2e);
+        c->mp.L0 = (float)c->L0;
         return MRF_OK;
     };
     if ((st = alloc()) != MRF_OK) return fail(st);
@@ -584,7 +577,7 @@ const char* mrf_last_error(const mrf_ctx* ctx) {
 mrf_status mrf_set_stream(mrf_ctx* ctx, void* cuda_stream) {
     ENTER(ctx);
     CK(cudaStreamSynchronize(c->stream));
-    c->stream = cuda_stream ? (cudaStream_t)cuda_stream : c->own_stream;
+    c->stream = (cudaStream_t)cuda_stream;  // NULL = the CUDA default stream
     return MRF_OK;
 }
 
