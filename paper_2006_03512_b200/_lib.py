@@ -58,9 +58,10 @@ def load(build: bool = True):
         if _lib is None:
             if build:
                 _build.build()
-            if not os.path.exists(_build.LIB):
-                raise MrfError(-1, f"{_build.LIB} missing: run paper_2006_03512_b200._build")
-            L = ctypes.CDLL(_build.LIB)
+            path = os.environ.get("MRF_LIB") or _build.LIB  # MRF_LIB: an in-tree build variant (kernel experiments)
+            if not os.path.exists(path):
+                raise MrfError(-1, f"{path} missing: run paper_2006_03512_b200._build")
+            L = ctypes.CDLL(path)
             P = ctypes.POINTER
             vp, i32, i64, f32, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_double
             st = ctypes.c_int

@@ -12,30 +12,44 @@
 //     lambda_i = log mu_{psi->o_i}(1) - log mu_{psi->o_i}(0) = log(Q_i + nu_i) - log(Q_i + R_i)
 // where P_i = sum_{j<i} mu(o_j=1) nu_j V_j and V_i = prod_{k<i} mu(o_k=0) are the terms of
 // Eq.13/14; dividing both messages by V_i leaves the log-odds unchanged and keeps every
-// quantity O(1) in the log domain.  Both recurrences are affine maps x -> 2^a x + 2^b, so a warp
-// composes per-lane chunks and runs two 5-level shuffle scans (prefix for Q, suffix for R).
-// Everything is evaluated in natural logs (the units of the input table): e^x as ex2.approx on the
-// MUFU, ln(1+y) as a polynomial on the FMA pipe (relative accuracy, see log1pn), and lambda
-// without cancellation (lambda_n).
+// quantity O(1) in the log domain.  Both recurrences are affine maps x -> e^a x + e^b, so
+// 8-element chunks compose in closed form and the chunks of a ray are combined by scans (prefix
+// for Q, suffix for R).  Everything is in natural logs (the units of the input table): e^x as
+// ex2.approx on the MUFU; ln(1+y) either as a relative-accurate polynomial on the FMA pipe
+// (log1pn) or, where only absolute accuracy matters, as lg2.approx on the MUFU (MATH levels
+// below); lambda without cancellation (lambda_n).
 //
-// Layout: warp per ray; lane l owns the K consecutive incidences [e0 + l*K, e0 + l*K + K) of
-// the ray; ray segments start at multiples of 4 (RayInfo), so vid/lambda are read as 16-byte
-// vectors and the partition -- hence every rounding -- is independent of where the ray is
-// stored (bit-identical results for any rank count).  Elements past e1 are masked to the
-// identity map.  Rays are
-// bucketed by span into K = 4 / 8 / 16 (single tile of 32K in registers); longer rays run a
-// tiled two-pass variant with the suffix values staged in a per-warp global scratch.
+// log nu_i is interpolated from the LUT once per frame by the DDA fill (graph.cu, lut_log_nu)
+// and read as one fp32 per incidence.
+//
+// Chunking: a chunk is 8 consecutive incidences of ONE ray, counted from the ray's start (ray
+// segments start at multiples of 8 slots), and the chunk scans are Hillis-Steele on the
+// ray-relative chunk index -- so every rounding depends only on the ray, never on where (or on
+// which rank) it is stored: beliefs are bit-identical for any rank count.  Masked elements are
+// identity maps.  Two layouts of the same arithmetic:
+//   * staged (default): stages of consecutive short rays are bulk-copied (TMA) into shared
+//     memory; thread = chunk; scans in shared memory (ray_msg_staged_kernel);
+//   * classes (MRF_K5=class): G lanes per ray by length class, scans by warp shuffles
+//     (ray_msg_kernel).
+// Rays longer than kShortMax run the tiled warp kernel (ray_msg_long_kernel) in both.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace mrf {
 namespace {
 
-#ifndef MRF_ACCURATE_RECURRENCES
-#define MRF_ACCURATE_RECURRENCES 1
-#endif
-
 constexpr unsigned kFull = 0xffffffffu;
-constexpr float kNeg = -1e30f;  // log2(0); finite so that NEG - NEG = 0 stays NaN-free
+constexpr float kNeg = -1e30f;  // log(0); finite so that NEG - NEG = 0 stays NaN-free
+
+// MATH levels (template parameter M):
+//   0  every ln(1+y) by the relative-accurate polynomial;
+//   1  the recurrences and chunk scans by lg2.approx (they carry max(a, b), so absolute accuracy
+//      ~1e-7 nats is all they need), the cavity softplus and lambda by the polynomial (default);
+//   2  also the softplus by lg2.approx.
+#ifndef MRF_K5_MATH
+#define MRF_K5_MATH 1
+#endif
 
 __device__ __forceinline__ float ex2(float x) {
     float y;
@@ -62,13 +76,15 @@ __device__ __forceinline__ float log1pn(float y) {
     r = fmaf(r, y, 0.99999994f);
     return r * y;
 }
+// ln(1 + y), y in [0, 1], absolutely accurate (~1e-7) on the MUFU
+__device__ __forceinline__ float log1pf_abs(float y) { return kLn2 * lg2(1.f + y); }
 // e^x on the MUFU (ex2.approx, relative error ~2^-22)
 __device__ __forceinline__ float expn(float x) { return ex2(x * kLog2e); }
-// ln(e^a + e^b), relative-accurate remainder.  Every log-domain quantity is kept in nats, the
-// units of the input table, so no large value is ever rescaled (a nats->bits conversion of a
-// value near the table floor, ~-100, would round at ~1e-5).
+// ln(e^a + e^b) = max + ln(1 + e^-|a-b|)
+template <bool ABS>
 __device__ __forceinline__ float lse(float a, float b) {
-    return fmaxf(a, b) + log1pn(expn(-fabsf(a - b)));
+    const float y = expn(-fabsf(a - b));
+    return fmaxf(a, b) + (ABS ? log1pf_abs(y) : log1pn(y));
 }
 
 // Affine map x -> e^a x + e^b in log form (nats).
@@ -76,8 +92,9 @@ struct Aff {
     float a, b;
 };
 // outer o inner (inner applied first)
+template <int M>
 __device__ __forceinline__ Aff compose(Aff outer, Aff inner) {
-    return {outer.a + inner.a, lse(outer.a + inner.b, outer.b)};
+    return {outer.a + inner.a, lse<(M >= 1)>(outer.a + inner.b, outer.b)};
 }
 template <int G>
 __device__ __forceinline__ Aff shfl_up(Aff v, int d) {
@@ -92,63 +109,26 @@ __device__ __forceinline__ Aff shfl_idx(Aff v, int l) {
     return {__shfl_sync(kFull, v.a, l, G), __shfl_sync(kFull, v.b, l, G)};
 }
 
-// ---------------------------------------------------------------- per-lane element loads
-// For the K elements [s, s+K) of this lane (nats):
-//   la = log mu(o=0) = -softplus(c),  w = log mu(o=1) + log nu,  l = log nu.
-// la and log mu(o=1) share one ex2 and are both computed directly, never as a difference of
-// two large numbers.  Masked elements get the identity maps (la = 0, w = NEG).
-template <int K>
-__device__ __forceinline__ void load_elems(long long s, long long e0, long long e1, const float2* __restrict__ rowA,
-                                           const float2* __restrict__ rowB, float wz, const MsgParams& mp,
-                                           const int32_t* __restrict__ vid, const int16_t* __restrict__ off_q,
-                                           const int32_t* __restrict__ lam, const long long* __restrict__ T,
-                                           float (&la)[K], float (&w)[K], float (&l)[K]) {
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        la[j] = 0.f;
-        w[j] = kNeg;
-        l[j] = kNeg;
-    }
-    if (s >= e1) return;
-    int v[K], q[K];
-    short o[K];
-#pragma unroll
-    for (int j = 0; j < K; j += 4) {
-        const int4 a = __ldg(reinterpret_cast<const int4*>(vid + s + j));
-        const int4 b = __ldg(reinterpret_cast<const int4*>(lam + s + j));
-        const uint2 c = __ldg(reinterpret_cast<const uint2*>(off_q + s + j));
-        v[j] = a.x; v[j + 1] = a.y; v[j + 2] = a.z; v[j + 3] = a.w;
-        q[j] = b.x; q[j + 1] = b.y; q[j + 2] = b.z; q[j + 3] = b.w;
-        o[j] = (short)(c.x & 0xffff); o[j + 1] = (short)(c.x >> 16);
-        o[j + 2] = (short)(c.y & 0xffff); o[j + 3] = (short)(c.y >> 16);
-    }
-    long long t[K];
-#pragma unroll
-    for (int j = 0; j < K; ++j) t[j] = (s + j < e1) ? __ldg(T + v[j]) : 0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        if (s + j < e1) {
-            // cavity (Eq.6): prior + every other incoming message, exact in fixed point
-            const float c = fmaf(__ll2float_rn(t[j] - (long long)q[j]), kQInv, mp.L0);
-            float fo = fmaf((float)o[j], mp.s_off, mp.b_off);
-            fo = fminf(fmaxf(fo, 0.f), mp.fo_max);
-            const int io = min((int)fo, mp.n_offm1 - 1);
-            const float wo = fo - (float)io;
-            const float2 ta = __ldg(rowA + io), tb = __ldg(rowB + io);
-            const float ra = fmaf(wo, ta.y - ta.x, ta.x);
-            const float rb = fmaf(wo, tb.y - tb.x, tb.x);
-            const float lnu = fmaf(wz, rb - ra, ra);
-            const float L1 = log1pn(expn(-fabsf(c)));  // ln(1 + e^-|c|)
-            la[j] = -(fmaxf(c, 0.f) + L1);
-            w[j] = lnu - (fmaxf(-c, 0.f) + L1);
-            l[j] = lnu;
-        }
-    }
+// ---------------------------------------------------------------- per-element terms
+// From the gathered belief sum t = sum of q over the voxel, this incidence's own q and its
+// log nu (nats):  la = log mu(o=0) = -softplus(c),  w = log mu(o=1) + log nu,  l = log nu, with
+// the cavity c = L0 + (t - q) 2^-23 (Eq.6) formed exactly in integers.  la and log mu(o=1)
+// share one ex2 and are both computed directly, never as a difference of two large numbers.
+// Masked elements (ok = false) are identity maps: la = 0, w = l = NEG.
+template <int M>
+__device__ __forceinline__ void elem_terms(long long t, int q, float lnu, float L0, bool ok, float& la, float& w,
+                                           float& l) {
+    const float c = fmaf(__ll2float_rn(t - (long long)q), kQInv, L0);
+    const float y = expn(-fabsf(c));
+    const float L1 = M >= 2 ? log1pf_abs(y) : log1pn(y);  // ln(1 + e^-|c|)
+    la = ok ? -(fmaxf(c, 0.f) + L1) : 0.f;
+    w = ok ? lnu - (fmaxf(-c, 0.f) + L1) : kNeg;
+    l = ok ? lnu : kNeg;
 }
 
-// Lane composite of the suffix maps R -> e^{la} R + e^{w} over the chunk (first applied last):
-// aB = sum la, bB = ln sum_j e^{w_j + sum_{k<j} la_k}.  The prefix maps
-// Q -> e^{-la} (Q + e^{w}) compose to (-aB, bB - aB).
+// Chunk composite of the suffix maps R -> e^{la} R + e^{w} (first applied last):
+// aB = sum la, bB = ln sum_j e^{w_j + sum_{k<j} la_k}.  The prefix maps Q -> e^{-la} (Q + e^{w})
+// compose to (-aB, bB - aB).
 template <int K>
 __device__ __forceinline__ void lane_composite(const float (&la)[K], const float (&w)[K], float& aB, float& bB) {
     float acc = 0.f, m = kNeg, t[K];
@@ -167,18 +147,18 @@ __device__ __forceinline__ void lane_composite(const float (&la)[K], const float
 
 // Both lane scans of a ray's G lanes at once (two independent shuffle chains per level):
 // returns R entering this lane from the right and Q entering it from the left, given the tile
-// carries Rc (log2 R after the tile) and Qc (log2 Q before it); optional carries out.
-template <int G>
+// carries Rc (R after the tile) and Qc (Q before it); optional carries out.
+template <int G, int M>
 __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc, float Qc, float& Rin, float& Qin,
                                            float* Rc_out, float* Qc_out) {
-    Aff H = {aB, bB};          // suffix maps R -> e^{la} R + e^{w}
-    Aff P = {-aB, bB - aB};    // prefix maps Q -> e^{-la} (Q + e^{w})
+    Aff H = {aB, bB};        // suffix maps R -> e^{la} R + e^{w}
+    Aff P = {-aB, bB - aB};  // prefix maps Q -> e^{-la} (Q + e^{w})
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
         const Aff oh = shfl_down<G>(H, d);
         const Aff op = shfl_up<G>(P, d);
-        if (sl + d < G) H = compose(H, oh);
-        if (sl >= d) P = compose(P, op);
+        if (sl + d < G) H = compose<M>(H, oh);
+        if (sl >= d) P = compose<M>(P, op);
     }
     Aff Hx = shfl_down<G>(H, 1);
     Aff Px = shfl_up<G>(P, 1);
@@ -187,17 +167,17 @@ __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc,
     if (Rc_out) {
         const Aff H0 = shfl_idx<G>(H, 0);
         const Aff Pl = shfl_idx<G>(P, G - 1);
-        *Rc_out = lse(H0.a + Rc, H0.b);
-        *Qc_out = lse(Pl.a + Qc, Pl.b);
+        *Rc_out = lse<(M >= 1)>(H0.a + Rc, H0.b);
+        *Qc_out = lse<(M >= 1)>(Pl.a + Qc, Pl.b);
     }
-    Rin = lse(Hx.a + Rc, Hx.b);
-    Qin = lse(Px.a + Qc, Px.b);
+    Rin = lse<(M >= 1)>(Hx.a + Rc, Hx.b);
+    Qin = lse<(M >= 1)>(Px.a + Qc, Px.b);
 }
 
-// The two per-lane recurrences, interleaved (independent chains):
+// The two per-chunk recurrences, interleaved (independent chains):
 //   lR[j] = ln R_j (suffix strictly after j),  R_{j-1} = mu(o_j=0) R_j + mu(o_j=1) nu_j
 //   lQ[j] = ln Q_j (prefix strictly before j), Q_{j+1} = (Q_j + mu(o_j=1) nu_j) / mu(o_j=0)
-template <int K>
+template <int K, int M>
 __device__ __forceinline__ void lane_recurrences(const float (&la)[K], const float (&w)[K], float Rin, float Qin,
                                                  float (&lR)[K], float (&lQ)[K]) {
     float R = Rin, Q = Qin;
@@ -206,8 +186,8 @@ __device__ __forceinline__ void lane_recurrences(const float (&la)[K], const flo
         const int jb = K - 1 - i;
         lR[jb] = R;
         lQ[i] = Q;
-        R = lse(la[jb] + R, w[jb]);
-        Q = lse(Q, w[i]) - la[i];
+        R = lse<(M >= 1)>(la[jb] + R, w[jb]);
+        Q = lse<(M >= 1)>(Q, w[i]) - la[i];
     }
 }
 
@@ -223,70 +203,95 @@ __device__ __forceinline__ int32_t quantise(float lam) {
     return __float2int_rn(lam * kQScale);  // saturates at +2^31-1 for +256
 }
 
+// ---------------------------------------------------------------- K5: class kernels
+// Loads of one lane's chunk [s, s+K) (s < e1; the chunk lies inside the ray's padded segment):
+// vid, q, log nu as 16-byte vectors, then the belief gathers.
+template <int K, int M>
+__device__ __forceinline__ void load_chunk(long long s, long long e1, float L0, const int32_t* __restrict__ vid,
+                                           const float* __restrict__ lnu, const int32_t* __restrict__ lam,
+                                           const long long* __restrict__ T, float (&la)[K], float (&w)[K],
+                                           float (&l)[K]) {
+    int v[K], q[K];
+    float ln[K];
+#pragma unroll
+    for (int j = 0; j < K; j += 4) {
+        const int4 a = __ldg(reinterpret_cast<const int4*>(vid + s + j));
+        const int4 b = __ldg(reinterpret_cast<const int4*>(lam + s + j));
+        const float4 c = __ldg(reinterpret_cast<const float4*>(lnu + s + j));
+        v[j] = a.x; v[j + 1] = a.y; v[j + 2] = a.z; v[j + 3] = a.w;
+        q[j] = b.x; q[j + 1] = b.y; q[j + 2] = b.z; q[j + 3] = b.w;
+        ln[j] = c.x; ln[j + 1] = c.y; ln[j + 2] = c.z; ln[j + 3] = c.w;
+    }
+    long long t[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) t[j] = (s + j < e1) ? __ldg(T + v[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], ln[j], L0, s + j < e1, la[j], w[j], l[j]);
+}
+template <int K>
+__device__ __forceinline__ void identity_chunk(float (&la)[K], float (&w)[K], float (&l)[K]) {
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        la[j] = 0.f;
+        w[j] = kNeg;
+        l[j] = kNeg;
+    }
+}
+
 // lambda_j = log(Q_j + nu_j) - log(Q_j + R_j)   (Eq.13 / Eq.14, both divided by V_j)
 template <int K>
 __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[K], const float (&lQ)[K], long long s,
                                          long long e1, int32_t* lam) {
     int32_t out[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) out[j] = quantise(lambda_n(lQ[j], l[j], lR[j]));
-    if (s + K <= e1) {
+    for (int j = 0; j < K; ++j) out[j] = s + j < e1 ? quantise(lambda_n(lQ[j], l[j], lR[j])) : 0;
 #pragma unroll
-        for (int j = 0; j < K; j += 4)
-            *reinterpret_cast<int4*>(lam + s + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < K; ++j)
-            if (s + j < e1) lam[s + j] = out[j];
-    }
+    for (int j = 0; j < K; j += 4)
+        *reinterpret_cast<int4*>(lam + s + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
 }
 
-// ---------------------------------------------------------------- K5: single-tile classes
 // G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.
-#ifndef MRF_K5_MIN_BLOCKS
-#define MRF_K5_MIN_BLOCKS 3
-#endif
-template <int G, int K>
-__global__ void __launch_bounds__(256, MRF_K5_MIN_BLOCKS) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
-                                                      const long long* __restrict__ row_ptr,
-                                                      const RayInfo* __restrict__ ray_z,
-                                                      const int32_t* __restrict__ vid,
-                                                      const int16_t* __restrict__ off_q, int32_t* lam,
-                                                      const long long* __restrict__ T, MsgParams mp) {
+template <int G, int K, int M>
+__global__ void __launch_bounds__(256, 3) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
+                                                         const long long* __restrict__ row_ptr,
+                                                         const RayInfo* __restrict__ ray_z,
+                                                         const int32_t* __restrict__ vid,
+                                                         const float* __restrict__ lnu, int32_t* lam,
+                                                         const long long* __restrict__ T, MsgParams mp) {
     constexpr int RPW = 32 / G;
     const long long wi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wi * RPW >= n) return;  // warp-uniform
     const int lane = threadIdx.x & 31, sl = lane & (G - 1);
     const long long ri = wi * RPW + lane / G;
-    RayInfo rz{0, 0.f, 0, 0};
+    int nr = 0;
     long long e0 = 0;
     if (ri < n) {
         const int r = __ldg(rays + ri);
-        rz = ray_z[r];
+        nr = ray_z[r].n;
         e0 = __ldg(row_ptr + r);
     }
-    const long long e1 = e0 + rz.n;
-    const float2* rowA = mp.lutp + (long long)rz.iz * mp.n_offm1;
-    const float2* rowB = rowA + mp.n_offm1;
+    const long long e1 = e0 + nr;
     const long long s = e0 + (long long)sl * K;
     float la[K], w[K], l[K], lR[K], lQ[K];
-    load_elems<K>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
+    identity_chunk<K>(la, w, l);
+    if (s < e1) load_chunk<K, M>(s, e1, mp.L0, vid, lnu, lam, T, la, w, l);
     float aB, bB, Rin, Qin;
     lane_composite<K>(la, w, aB, bB);
-    lane_scans<G>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
-    lane_recurrences<K>(la, w, Rin, Qin, lR, lQ);
+    lane_scans<G, M>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
+    lane_recurrences<K, M>(la, w, Rin, Qin, lR, lQ);
     if (s < e1) lane_out<K>(l, lR, lQ, s, e1, lam);
 }
 
 // ---------------------------------------------------------------- K5: long rays (tiled)
-constexpr int kLongK = 16;
+constexpr int kLongK = 8;
 constexpr int kLongTile = 32 * kLongK;
 
+template <int M>
 __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const int32_t* __restrict__ rays,
                                                            const long long* __restrict__ row_ptr,
                                                            const RayInfo* __restrict__ ray_z,
                                                            const int32_t* __restrict__ vid,
-                                                           const int16_t* __restrict__ off_q, int32_t* lam,
+                                                           const float* __restrict__ lnu, int32_t* lam,
                                                            const long long* __restrict__ T, MsgParams mp,
                                                            float* scratch, long long scratch_per_warp) {
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -295,10 +300,7 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
     float* my_scratch = scratch + gw * scratch_per_warp;
     for (long long wi = gw; wi < n; wi += n_warps) {
         const int r = __ldg(rays + wi);
-        const RayInfo rz = ray_z[r];
-        const long long e0 = __ldg(row_ptr + r), e1 = e0 + rz.n;
-        const float2* rowA = mp.lutp + (long long)rz.iz * mp.n_offm1;
-        const float2* rowB = rowA + mp.n_offm1;
+        const long long e0 = __ldg(row_ptr + r), e1 = e0 + ray_z[r].n;
         const int n_tiles = (int)((e1 - e0 + kLongTile - 1) / kLongTile);
         float la[kLongK], w[kLongK], l[kLongK], lR[kLongK], lQ[kLongK];
         float aB, bB, Rin, Qin, Rc_out, Qc_out;
@@ -306,11 +308,12 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         float Rc = kNeg;
         for (int t = n_tiles - 1; t >= 0; --t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
-            load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
+            identity_chunk<kLongK>(la, w, l);
+            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
-            lane_scans<32>(aB, bB, lane, Rc, kNeg, Rin, Qin, &Rc_out, &Qc_out);
+            lane_scans<32, M>(aB, bB, lane, Rc, kNeg, Rin, Qin, &Rc_out, &Qc_out);
             Rc = Rc_out;
-            lane_recurrences<kLongK>(la, w, Rin, kNeg, lR, lQ);
+            lane_recurrences<kLongK, M>(la, w, Rin, kNeg, lR, lQ);
             float* dst = my_scratch + (long long)t * kLongTile + lane * kLongK;
 #pragma unroll
             for (int j = 0; j < kLongK; j += 4)
@@ -320,11 +323,12 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         float Qc = kNeg;
         for (int t = 0; t < n_tiles; ++t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
-            load_elems<kLongK>(s, e0, e1, rowA, rowB, rz.wz, mp, vid, off_q, lam, T, la, w, l);
+            identity_chunk<kLongK>(la, w, l);
+            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
-            lane_scans<32>(aB, bB, lane, kNeg, Qc, Rin, Qin, &Rc_out, &Qc_out);
+            lane_scans<32, M>(aB, bB, lane, kNeg, Qc, Rin, Qin, &Rc_out, &Qc_out);
             Qc = Qc_out;
-            lane_recurrences<kLongK>(la, w, kNeg, Qin, lR, lQ);
+            lane_recurrences<kLongK, M>(la, w, kNeg, Qin, lR, lQ);
             const float* src = my_scratch + (long long)t * kLongTile + lane * kLongK;
 #pragma unroll
             for (int j = 0; j < kLongK; j += 4) {
@@ -333,6 +337,192 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
             }
             if (s < e1) lane_out<kLongK>(l, lR, lQ, s, e1, lam);
         }
+    }
+}
+
+// ---------------------------------------------------------------- K5: staged (TMA bulk copies)
+// A persistent CTA (kStageThreads threads) walks its stages; thread 0 bulk-copies the NEXT
+// stage's vid / lambda / log-nu slots, its row_ptr entries and its RayInfo records into the
+// other shared-memory buffer (cp.async.bulk, completion on an mbarrier) while the CTA computes
+// the current one, so the incidence stream reaches HBM as a few large asynchronous copies per
+// stage instead of per-warp dependent loads.  Thread t owns the 8 slots [s0 + 8t, s0 + 8t + 8) =
+// chunk c of one ray.  Per chunk: the 8 elements' maps in closed form (lane_composite); then,
+// per ray, inclusive scans over its chunks in shared memory, Hillis-Steele on the RAY-RELATIVE
+// chunk index (chunk c combines with c - d iff c >= d) -- the same association tree as the class
+// kernels' lane scans, so both layouts give bit-identical messages; then the two recurrences
+// and lambda.
+constexpr int kStSlots = kStageCap + kShortMax;                   // >= span of any stage (8-aligned)
+constexpr int kStChunks = kStSlots / kSegAlign;                   // = kStageThreads
+constexpr int kStRp = kStageMaxRays + 2;                          // row_ptr entries [r0&~1, (r1+2)&~1)
+constexpr int kOffVid = 0;
+constexpr int kOffLam = kOffVid + 4 * kStSlots;
+constexpr int kOffLnu = kOffLam + 4 * kStSlots;
+constexpr int kOffRp = kOffLnu + 4 * kStSlots;
+constexpr int kOffRi = kOffRp + 8 * kStRp;
+constexpr int kOffCm = kOffRi + 16 * kStageMaxRays;               // chunk -> ray (uint16)
+constexpr int kBufBytes = (kOffCm + 2 * kStChunks + 127) & ~127;
+constexpr int kOffScan = 2 * kBufBytes;                           // [2 ping-pong][kStChunks] x (P, H) float4
+constexpr int kOffBar = kOffScan + 2 * kStChunks * 16;
+constexpr int kStageSmem = kOffBar + 128;
+static_assert(kStChunks == kStageThreads, "one 8-slot chunk per thread");
+static_assert(kOffRp % 16 == 0 && kOffRi % 16 == 0 && kOffLam % 16 == 0 && kOffLnu % 16 == 0, "16-byte aligned");
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MRF_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra MRF_WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+
+// Thread 0: start the copies of stage `st` into `buf`, completion on `bar`.  All sources and
+// sizes are 16-byte multiples (segments 8-aligned, row_ptr read from an even index).
+__device__ __forceinline__ void stage_issue(const Stage& st, char* buf, unsigned long long* bar,
+                                            const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                                            const float* lnu, const int32_t* lam) {
+    const unsigned ns = (unsigned)(st.s1 - st.s0);
+    const int a0 = st.r0 & ~1, a1 = (st.r1 + 2) & ~1;
+    const unsigned nrp = (unsigned)(a1 - a0), nri = (unsigned)(st.r1 - st.r0);
+    // generic-proxy reads of this buffer (previous stage) are ordered before the async writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar, ns * 12u + nrp * 8u + nri * 16u);
+    if (ns) {
+        bulk_g2s(buf + kOffVid, vid + st.s0, ns * 4u, bar);
+        bulk_g2s(buf + kOffLam, lam + st.s0, ns * 4u, bar);
+        bulk_g2s(buf + kOffLnu, lnu + st.s0, ns * 4u, bar);
+    }
+    bulk_g2s(buf + kOffRp, row_ptr + a0, nrp * 8u, bar);
+    bulk_g2s(buf + kOffRi, info + st.r0, nri * 16u, bar);
+}
+
+template <int M>
+__global__ void __launch_bounds__(kStageThreads, kStageCtas)
+    ray_msg_staged_kernel(long long n_stages, const Stage* __restrict__ stages, const long long* __restrict__ row_ptr,
+                          const RayInfo* __restrict__ info, const int32_t* __restrict__ vid,
+                          const float* __restrict__ lnu, int32_t* lam, const long long* __restrict__ T,
+                          MsgParams mp) {
+    extern __shared__ __align__(128) char st_smem[];
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(st_smem + kOffBar);
+    Stage* sd = reinterpret_cast<Stage*>(st_smem + kOffBar + 16);   // descriptors of the two buffers
+    int* s_maxc = reinterpret_cast<int*>(st_smem + kOffBar + 80);  // per buffer: longest ray, in chunks
+    float4* scan = reinterpret_cast<float4*>(st_smem + kOffScan);  // [2][kStChunks]: (P.a, P.b, H.a, H.b)
+    const int t = threadIdx.x;
+    long long k = blockIdx.x;
+    if (k >= n_stages) return;
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        sd[0] = stages[k];
+        s_maxc[0] = 1;
+        stage_issue(sd[0], st_smem, &bars[0], row_ptr, info, vid, lnu, lam);
+    }
+    Stage nxt{};
+    if (t == 0 && k + gridDim.x < n_stages) nxt = stages[k + gridDim.x];
+    __syncthreads();
+    for (int i = 0; k < n_stages; ++i, k += gridDim.x) {
+        const int b = i & 1;
+        char* buf = st_smem + b * kBufBytes;
+        if (t == 0) {
+            const long long k1 = k + gridDim.x, k2 = k1 + gridDim.x;
+            if (k1 < n_stages) {
+                sd[b ^ 1] = nxt;
+                s_maxc[b ^ 1] = 1;
+                stage_issue(nxt, st_smem + (b ^ 1) * kBufBytes, &bars[b ^ 1], row_ptr, info, vid, lnu, lam);
+            }
+            if (k2 < n_stages) nxt = stages[k2];
+        }
+        mbar_wait(&bars[b], (unsigned)(i >> 1) & 1u);
+        const Stage st = sd[b];
+        const int32_t* svid = reinterpret_cast<const int32_t*>(buf + kOffVid);
+        const int32_t* slam = reinterpret_cast<const int32_t*>(buf + kOffLam);
+        const float* slnu = reinterpret_cast<const float*>(buf + kOffLnu);
+        const long long* srp = reinterpret_cast<const long long*>(buf + kOffRp) + (st.r0 & 1);
+        const RayInfo* sri = reinterpret_cast<const RayInfo*>(buf + kOffRi);
+        uint16_t* cmap = reinterpret_cast<uint16_t*>(buf + kOffCm);
+        const int span = (int)(st.s1 - st.s0), nr = st.r1 - st.r0;
+        // chunk -> ray map, and the longest ray (in chunks) of the stage
+        for (int j = t; j < nr; j += kStageThreads) {
+            const int c0 = (int)(srp[j] - st.s0) >> 3, c1 = (int)(srp[j + 1] - st.s0) >> 3;
+            for (int c = c0; c < c1; ++c) cmap[c] = (uint16_t)j;
+            if (c1 - c0 > 1) atomicMax(&s_maxc[b], c1 - c0);
+        }
+        __syncthreads();
+        const int rel = 8 * t;
+        const bool act = rel < span;
+        int c = 0, nch = 1, nv = 0;
+        if (act) {
+            const int j = cmap[t];
+            const int st_j = (int)(srp[j] - st.s0);
+            c = (rel - st_j) >> 3;
+            nch = (int)(srp[j + 1] - srp[j]) >> 3;
+            nv = min(8, st_j + sri[j].n - rel);
+        }
+        float la[8], w[8], l[8];
+        identity_chunk<8>(la, w, l);
+        if (act) {
+            const int4 v0 = *reinterpret_cast<const int4*>(svid + rel);
+            const int4 v1 = *reinterpret_cast<const int4*>(svid + rel + 4);
+            const int4 q0 = *reinterpret_cast<const int4*>(slam + rel);
+            const int4 q1 = *reinterpret_cast<const int4*>(slam + rel + 4);
+            const float4 n0 = *reinterpret_cast<const float4*>(slnu + rel);
+            const float4 n1 = *reinterpret_cast<const float4*>(slnu + rel + 4);
+            const int v[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+            const int q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+            const float ln[8] = {n0.x, n0.y, n0.z, n0.w, n1.x, n1.y, n1.z, n1.w};
+            long long tv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) tv[e] = e < nv ? __ldg(T + v[e]) : 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) elem_terms<M>(tv[e], q[e], ln[e], mp.L0, e < nv, la[e], w[e], l[e]);
+        }
+        float aB, bB;
+        lane_composite<8>(la, w, aB, bB);
+        Aff P = {-aB, bB - aB}, H = {aB, bB};
+        // ray-relative inclusive scans over chunks: P over chunks 0..c, H over chunks c..nch-1
+        const int maxc = s_maxc[b];
+        int pp = 0;
+        for (int d = 1; d < maxc; d <<= 1, pp ^= 1) {
+            scan[pp * kStChunks + t] = make_float4(P.a, P.b, H.a, H.b);
+            __syncthreads();
+            if (act && c >= d) {
+                const float4 x = scan[pp * kStChunks + t - d];
+                P = compose<M>(P, Aff{x.x, x.y});
+            }
+            if (act && c + d < nch) {
+                const float4 x = scan[pp * kStChunks + t + d];
+                H = compose<M>(H, Aff{x.z, x.w});
+            }
+        }
+        scan[pp * kStChunks + t] = make_float4(P.a, P.b, H.a, H.b);
+        __syncthreads();
+        // Q entering the chunk (chunk c-1's inclusive prefix applied to Q_1 = 0), R entering it
+        // from the right (chunk c+1's inclusive suffix applied to R_N = 0)
+        float Qin = kNeg, Rin = kNeg;
+        if (act && c > 0) Qin = scan[pp * kStChunks + t - 1].y;
+        if (act && c + 1 < nch) Rin = scan[pp * kStChunks + t + 1].w;
+        float lR[8], lQ[8];
+        lane_recurrences<8, M>(la, w, Rin, Qin, lR, lQ);
+        if (act) lane_out<8>(l, lR, lQ, st.s0 + rel, st.s0 + rel + nv, lam);
+        __syncthreads();  // buffer b and the scan scratch are free again
     }
 }
 
@@ -448,27 +638,72 @@ __global__ void lambda_to_float_kernel(long long n, const int32_t* __restrict__ 
 
 inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
+template <int M>
+void launch_ray_messages_m(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+                           const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
+                           const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
+                           int n_warps_long, cudaStream_t s) {
+    auto grid = [&](int G) { return blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256); };
+    constexpr int G0 = kMinGroup, K = kLaneK;
+#define MRF_K5_ARGS n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp
+    switch (cls) {
+        case 0: ray_msg_kernel<G0, K, M><<<grid(G0), 256, 0, s>>>(MRF_K5_ARGS); break;
+        case 1: ray_msg_kernel<2 * G0, K, M><<<grid(2 * G0), 256, 0, s>>>(MRF_K5_ARGS); break;
+        case 2: ray_msg_kernel<4 * G0, K, M><<<grid(4 * G0), 256, 0, s>>>(MRF_K5_ARGS); break;
+        case 3: ray_msg_kernel<8 * G0, K, M><<<grid(8 * G0), 256, 0, s>>>(MRF_K5_ARGS); break;
+        default: {
+            const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
+            ray_msg_long_kernel<M><<<g, 256, 0, s>>>(MRF_K5_ARGS, scratch, scratch_per_warp);
+        }
+    }
+#undef MRF_K5_ARGS
+}
+
+template <int M>
+void launch_staged_m(long long n_stages, const Stage* stages, const long long* row_ptr, const RayInfo* info,
+                     const int32_t* vid, const float* lnu, int32_t* lam, const long long* T, const MsgParams& mp,
+                     cudaStream_t s) {
+    static bool configured = false;
+    static int sms = 148;
+    if (!configured) {
+        cudaFuncSetAttribute(ray_msg_staged_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        configured = true;
+    }
+    const long long grid = std::min<long long>(n_stages, (long long)kStageCtas * sms);
+    ray_msg_staged_kernel<M><<<(unsigned)grid, kStageThreads, kStageSmem, s>>>(n_stages, stages, row_ptr, info, vid,
+                                                                              lnu, lam, T, mp);
+}
+
 }  // namespace
 
 int class_capacity(int cls) { return cls < kNumClasses - 1 ? kLaneK * (kMinGroup << cls) : 0x7fffffff; }
 
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
-                         const RayInfo* ray_z, const int32_t* vid, const int16_t* off_q, int32_t* lam,
+                         const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
-                         int n_warps_long, cudaStream_t s) {
+                         int n_warps_long, int math, cudaStream_t s) {
     if (n_rays == 0) return;
-    auto grid = [&](int G) { return blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256); };
-    constexpr int G0 = kMinGroup, K = kLaneK;
-    switch (cls) {
-        case 0: ray_msg_kernel<G0, K><<<grid(G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
-        case 1: ray_msg_kernel<2 * G0, K><<<grid(2 * G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
-        case 2: ray_msg_kernel<4 * G0, K><<<grid(4 * G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
-        case 3: ray_msg_kernel<8 * G0, K><<<grid(8 * G0), 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp); break;
-        default: {
-            const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
-            ray_msg_long_kernel<<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, off_q, lam, T, mp, scratch,
-                                                  scratch_per_warp);
-        }
+    switch (math) {
+        case 0: launch_ray_messages_m<0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                         scratch_per_warp, n_warps_long, s); break;
+        case 2: launch_ray_messages_m<2>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                         scratch_per_warp, n_warps_long, s); break;
+        default: launch_ray_messages_m<1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                          scratch_per_warp, n_warps_long, s);
+    }
+}
+
+void launch_ray_messages_staged(long long n_stages, const Stage* stages, const long long* row_ptr,
+                                const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
+                                const long long* T, const MsgParams& mp, int math, cudaStream_t s) {
+    if (n_stages == 0) return;
+    switch (math) {
+        case 0: launch_staged_m<0>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s); break;
+        case 2: launch_staged_m<2>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s); break;
+        default: launch_staged_m<1>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s);
     }
 }
 

@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
             rz.wz = (float)(fz - (double)iz);
         }
         rz.n = count;
-        n_r[f.ray_base + i] = (count + 3) & ~3;  // segments start at multiples of 4
+        n_r[f.ray_base + i] = (count + kSegAlign - 1) & ~(kSegAlign - 1);  // segments start at multiples of 8
         status[f.ray_base + i] = (int8_t)st;
         ray_z[f.ray_base + i] = rz;
         ne = count;
@@ -187,10 +187,11 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
 // ---------------------------------------------------------------- K3
 // B3: off_q = clamp(rint((0.5 (t_in + t_out) L - Z) * 32768), +-32767), the span midpoint
 // relative to the measured range (reading R6).
-__global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
+__global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n, MsgParams mp,
                                                        const float* __restrict__ depth,
-                                                       const long long* __restrict__ row_ptr, int32_t* vid,
-                                                       int16_t* off_q, int32_t* vox_count) {
+                                                       const long long* __restrict__ row_ptr,
+                                                       const RayInfo* __restrict__ ray_z, int32_t* vid,
+                                                       int16_t* off_q, float* lnu, int32_t* vox_count) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n_pix = (long long)f.rows_owned * f.W;
     const int lane = threadIdx.x & 31;
@@ -198,6 +199,8 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
     Segment sg;
     Walker w;
     long long e = 0;
+    int iz = 0;
+    float wz = 0.f;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
@@ -205,6 +208,9 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             w.start(sg);
             alive = w.inside(g);
             e = row_ptr[f.ray_base + i];
+            const RayInfo ri = ray_z[f.ray_base + i];
+            iz = ri.iz;
+            wz = ri.wz;
         }
     }
     for (;;) {
@@ -220,6 +226,7 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
             vid[e] = vx;
             off_q[e] = (int16_t)q;
+            lnu[e] = lut_log_nu(mp, iz, wz, (int)q);
             ++e;
             const unsigned peers = __match_any_sync(am, vx);
             if (lane == __ffs(peers) - 1) atomicAdd(&vox_count[vx], __popc(peers));
@@ -395,9 +402,55 @@ __global__ void span_max_kernel(long long n, const int32_t* __restrict__ rays, c
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+// Staged-K5 stage list.  Ray r is "short" when 0 <= n <= kShortMax.  A short ray opens a stage
+// when the previous ray is long, or starts in another kStageCap-slot window, or lies in another
+// kStageMaxRays block of ray indices.  flags[r] = opens a stage.
+__device__ __forceinline__ bool ray_short(const RayInfo* info, long long r) { return info[r].n <= kShortMax; }
+__device__ __forceinline__ bool opens_stage(long long r, const long long* row_ptr, const RayInfo* info) {
+    if (!ray_short(info, r)) return false;
+    if (r == 0) return true;
+    return !ray_short(info, r - 1) || (row_ptr[r] / kStageCap) != (row_ptr[r - 1] / kStageCap) ||
+           (r / kStageMaxRays) != ((r - 1) / kStageMaxRays);
+}
+
+__global__ void stage_flags_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                   const RayInfo* __restrict__ info, int32_t* flags) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n_rays) flags[r] = opens_stage(r, row_ptr, info) ? 1 : 0;
+}
+
+// pos = exclusive scan of flags (n_rays + 1 entries).  Stage of short ray r = pos[r + 1] - 1.
+__global__ void stage_fill_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                  const RayInfo* __restrict__ info, const int32_t* __restrict__ flags,
+                                  const long long* __restrict__ pos, Stage* stages) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays || !ray_short(info, r)) return;
+    const long long sid = pos[r + 1] - 1;
+    if (flags[r]) {
+        stages[sid].r0 = (int)r;
+        stages[sid].s0 = row_ptr[r];
+    }
+    if (r + 1 == n_rays || flags[r + 1] || !ray_short(info, r + 1)) {
+        stages[sid].r1 = (int)(r + 1);
+        stages[sid].s1 = row_ptr[r + 1];
+    }
+}
+
 inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
 }  // namespace
+
+void launch_stage_flags(long long n_rays, const long long* row_ptr, const RayInfo* info, int32_t* flags,
+                        cudaStream_t s) {
+    if (n_rays == 0) return;
+    stage_flags_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, flags);
+}
+
+void launch_stage_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* flags,
+                       const long long* pos, Stage* stages, cudaStream_t s) {
+    if (n_rays == 0) return;
+    stage_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, flags, pos, stages);
+}
 
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
                          int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
@@ -407,12 +460,13 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
     raygen_count_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, n_r, status, ray_z, counters);
 }
 
-void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
-                     const long long* row_ptr, int32_t* vid, int16_t* off_q, int32_t* vox_count,
-                     cudaStream_t s) {
+void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
+                     const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
+                     int16_t* off_q, float* lnu, int32_t* vox_count, cudaStream_t s) {
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
-    dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q, vox_count);
+    dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, mp, depth, row_ptr, ray_z, vid, off_q, lnu,
+                                                           vox_count);
 }
 
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,

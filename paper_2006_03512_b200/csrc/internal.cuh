@@ -19,6 +19,7 @@ constexpr float kQInv = 1.0f / 8388608.0f;
 constexpr double kQInvD = 1.0 / 8388608.0;
 constexpr float kLambdaClip = 256.0f;         // reading R9
 constexpr int kPadElems = 64;                 // slack after incidence arrays (aligned over-reads)
+constexpr int kSegAlign = 8;                  // ray segments start at multiples of 8 slots (row_ptr += pad8(n))
 constexpr int kVoxelChunk = 4096;             // per-voxel K6 work item: <= 4096 transpose entries
 // Internal voxel layout: 32 x 32 x 16 tiles (16384 slots), tile-major.  K6 accumulates one tile
 // at a time in shared memory, so a tile's slots must fit one CTA (2 x int32 x 16384 = 128 KB).
@@ -70,8 +71,8 @@ struct FrameDesc {
 };
 
 // Per-ray record: LUT row iz (<= n_z-2) and weight wz in [0,1] of the measured range, and the
-// number of incidences n.  Ray segments start at multiples of 4 in the incidence arrays
-// (row_ptr advances by pad4(n)), so per-lane chunks are relative to the ray start, 16-byte
+// number of incidences n.  Ray segments start at multiples of 8 in the incidence arrays
+// (row_ptr advances by pad8(n)), so per-lane chunks are relative to the ray start, 16-byte
 // aligned, and a ray's arithmetic never depends on where (or on which rank) it is stored.
 struct RayInfo {
     int iz;
@@ -89,16 +90,31 @@ struct MsgParams {
     float L0;                 // prior log-odds ln(gamma / (1 - gamma))
 };
 
+// log nu at (measured range row iz + wz, quantised offset off_q): bilinear interpolation of the
+// input table in fp32, bin-centre coordinates clamped to the edge centres.
+// Evaluated once per incidence by the DDA fill; K5 reads the result.
+__device__ __forceinline__ float lut_log_nu(const MsgParams& mp, int iz, float wz, int off) {
+    float fo = fmaf((float)off, mp.s_off, mp.b_off);
+    fo = fminf(fmaxf(fo, 0.f), mp.fo_max);
+    const int io = min((int)fo, mp.n_offm1 - 1);
+    const float wo = fo - (float)io;
+    const float2* rowA = mp.lutp + (long long)iz * mp.n_offm1;
+    const float2 ta = __ldg(rowA + io), tb = __ldg(rowA + mp.n_offm1 + io);
+    const float ra = fmaf(wo, ta.y - ta.x, ta.x);
+    const float rb = fmaf(wo, tb.y - tb.x, tb.x);
+    return fmaf(wz, rb - ra, ra);
+}
+
 // ---- launchers (all asynchronous on `s`)
-// K1: per owned pixel -> status, pad4(length) (scan input), RayInfo; counters[0] += invalid,
+// K1: per owned pixel -> status, pad8(length) (scan input), RayInfo; counters[0] += invalid,
 // counters[1] += dropped, counters[2] += incidences
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
                          int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s);
-// K3: walk again, write vid/off_q at row_ptr offsets, histogram voxel degrees
-void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
-                     const long long* row_ptr, int32_t* vid, int16_t* off_q, int32_t* vox_count,
-                     cudaStream_t s);
+// K3: walk again, write vid / off_q / log nu at row_ptr offsets, histogram voxel degrees
+void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
+                     const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
+                     int16_t* off_q, float* lnu, int32_t* vox_count, cudaStream_t s);
 // K2: out[i] = offset + sum_{j<i} in[j] for i in [0, n]; out has n+1 entries.
 void launch_exclusive_scan(const int32_t* in, long long* out, long long n, long long offset,
                            long long* scratch, cudaStream_t s);
@@ -123,6 +139,42 @@ void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, 
 void launch_span_max(long long n, const int32_t* rays, const RayInfo* info, unsigned long long* out,
                      cudaStream_t s);
 
+// ---- staged K5 (bp.cu ray_msg_staged_kernel): stages of consecutive short rays, bulk-copied
+// (TMA, cp.async.bulk) into shared memory and processed by one CTA; thread t owns the 8-slot
+// chunk t of the stage, which (segments being 8-aligned) is chunk c of exactly one ray, and the
+// per-ray scans run over ray-relative chunk indices, so a ray's rounding never depends on
+// where (or on which rank) it is stored.
+// A stage is a maximal run of consecutive rays with n <= kShortMax whose first slot lies in one
+// kStageCap-slot window and whose index lies in one kStageMaxRays block; longer rays go to the
+// tiled long-ray kernel.  Span of a stage < kStageCap + kShortMax.
+#ifndef MRF_STAGE_CAP
+#define MRF_STAGE_CAP 2048
+#endif
+#ifndef MRF_STAGE_RAYS
+#define MRF_STAGE_RAYS 512
+#endif
+#ifndef MRF_STAGE_CTAS
+#define MRF_STAGE_CTAS 2
+#endif
+constexpr int kStageCap = MRF_STAGE_CAP;
+constexpr int kShortMax = 256;
+constexpr int kStageMaxRays = MRF_STAGE_RAYS;
+constexpr int kStageThreads = (kStageCap + kShortMax) / 8;  // one 8-slot chunk per thread >= max span
+constexpr int kStageCtas = MRF_STAGE_CTAS;                   // resident CTAs per SM
+struct Stage {
+    int r0, r1;                      // rays [r0, r1)
+    int pad0, pad1;
+    long long s0, s1;                // slots [s0, s1) = [row_ptr[r0], row_ptr[r1])
+};
+// stage list: flags over rays (scan input), then fill (stage count known after the scan)
+void launch_stage_flags(long long n_rays, const long long* row_ptr, const RayInfo* info, int32_t* flags,
+                        cudaStream_t s);
+void launch_stage_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* flags,
+                       const long long* pos, Stage* stages, cudaStream_t s);
+void launch_ray_messages_staged(long long n_stages, const Stage* stages, const long long* row_ptr,
+                                const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
+                                const long long* T, const MsgParams& mp, int math, cudaStream_t s);
+
 // ---- BP kernels (bp.cu)
 #ifndef MRF_LANE_K
 #define MRF_LANE_K 8
@@ -132,9 +184,9 @@ constexpr int kMinGroup = 32 / MRF_LANE_K;      // classes: G = kMinGroup << k l
 constexpr int kNumClasses = 5;      // 4 group widths (capacity kLaneK * G) + class 4 = long rays (tiled)
 int class_capacity(int cls);        // max span handled by class cls (class 3: unbounded)
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
-                         const RayInfo* info, const int32_t* vid, const int16_t* off_q, int32_t* lam,
+                         const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
-                         int n_warps_long, cudaStream_t s);
+                         int n_warps_long, int math, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,

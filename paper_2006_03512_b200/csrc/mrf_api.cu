@@ -79,6 +79,8 @@ struct mrf_ctx {
     long long VI = 0;  // internal belief slots: tiles * 16384 (tile-major, DESIGN.md §Data layout)
     long long NT = 0;  // tiles
     bool k6_voxel = false;  // ablation: per-voxel transpose K6 instead of the tile-run K6 (MRF_K6=voxel)
+    int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1|2)
+    bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
     float prior = 0.5f;
     double L0 = 0.0;
@@ -98,6 +100,7 @@ struct mrf_ctx {
     DBuf<long long> row_ptr;
     DBuf<int32_t> vid;
     DBuf<int16_t> off_q;
+    DBuf<float> lnu;      // log nu per incidence (interpolated at fill time; read by K5)
     DBuf<int32_t> lam;
     DBuf<int32_t> tr;
     DBuf<int32_t> vox_count, cursor, n_items, flags;
@@ -115,6 +118,8 @@ struct mrf_ctx {
     DBuf<long long> scan_scratch;
     DBuf<unsigned long long> counters;
     DBuf<int32_t> class_rays[kNumClasses];
+    DBuf<Stage> stages;
+    long long n_stages = 0;
     long long class_n[kNumClasses] = {};
     DBuf<float> long_scratch;
     long long long_scratch_per_warp = 0;
@@ -302,7 +307,18 @@ mrf_status prepare(mrf_ctx* c) {
     // K5 classes by ray length (stable compaction keeps pixel order inside a class)
     CK(c->flags.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
     CK(c->pos.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
-    for (int k = 0; k < kNumClasses; ++k) {
+    if (c->k5_staged) {
+        // stage list over the short rays (the bulk copies read row_ptr up to index R + 1)
+        CK(c->row_ptr.ensure((size_t)c->R + 2, (size_t)c->R + 1, c->stream));
+        launch_stage_flags(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        if ((st = scan(c, c->flags.p, c->pos.p, c->R, 0)) != MRF_OK) return st;
+        if ((st = read_ll(c, c->pos.p + c->R, &c->n_stages)) != MRF_OK) return st;
+        CK(c->stages.ensure((size_t)std::max(1LL, c->n_stages), 0, c->stream));
+        launch_stage_fill(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->pos.p, c->stages.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    }
+    for (int k = c->k5_staged ? kNumClasses - 1 : 0; k < kNumClasses; ++k) {
         launch_class_flags(c->R, c->ray_z.p, k, c->flags.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
         if ((st = scan(c, c->flags.p, c->pos.p, c->R, 0)) != MRF_OK) return st;
@@ -342,13 +358,20 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
     return MRF_OK;
 }
 
+// K5: the staged kernel over the short rays (or the class kernels), the tiled kernel over the long
 mrf_status ray_messages(mrf_ctx* c) {
     ProfScope ps(c, MRF_K_RAY_MSG);
-    for (int k = 0; k < kNumClasses; ++k) {
+    const bool staged = c->k5_staged;
+    if (staged && c->n_stages > 0) {
+        launch_ray_messages_staged(c->n_stages, c->stages.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lnu.p, c->lam.p,
+                                   c->T.p, c->mp, c->k5_math, c->stream);
+        CK_LAUNCH(MRF_K_RAY_MSG, 1);
+    }
+    for (int k = staged ? kNumClasses - 1 : 0; k < kNumClasses; ++k) {
         if (c->class_n[k] == 0) continue;
-        launch_ray_messages(k, c->class_n[k], c->class_rays[k].p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
+        launch_ray_messages(k, c->class_n[k], c->class_rays[k].p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lnu.p,
                             c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long,
-                            c->stream);
+                            c->k5_math, c->stream);
         CK_LAUNCH(MRF_K_RAY_MSG, 1);
     }
     return MRF_OK;
@@ -467,6 +490,9 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     c->NT = (long long)c->grid.ntx * c->grid.nty * c->grid.ntz;
     c->VI = c->NT * kTileSlots;
     if (const char* k6 = getenv("MRF_K6")) c->k6_voxel = strcmp(k6, "voxel") == 0;
+    if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
+    if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
+    if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
                 noise->sigma_c[0], noise->sigma_c[1], noise->sigma_c[2], noise->n_z, noise->n_off};
     c->V = V;
@@ -555,13 +581,13 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
         cudaEventDestroy(e.b);
     }
     c->n_r.release(); c->status.release(); c->ray_z.release(); c->row_ptr.release();
-    c->vid.release(); c->off_q.release(); c->lam.release(); c->tr.release();
+    c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
     c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_nitems.release(); c->tile_ptr.release();
-    c->bitem_ptr.release(); c->runs.release(); c->bitems.release();
+    c->bitem_ptr.release(); c->runs.release(); c->bitems.release(); c->stages.release();
     for (auto& b : c->class_rays) b.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -593,6 +619,7 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences) {
     const size_t ne = (size_t)n_incidences + kPadElems;
     CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
     CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->lnu.ensure(ne, (size_t)c->E, c->stream));
     CK(c->lam.ensure(ne, (size_t)c->E, c->stream));
     CK(c->tr.ensure(ne, 0, c->stream));
     return MRF_OK;
@@ -681,11 +708,13 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     const size_t ne = (size_t)E_new + kPadElems;
     CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
     CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->lnu.ensure(ne, (size_t)c->E, c->stream));
     CK(c->lam.ensure(ne, (size_t)c->E, c->stream));
     CK(cudaMemsetAsync(c->lam.p + c->E, 0, sizeof(int32_t) * (size_t)(E_new - c->E), c->stream));
     {
         ProfScope ps(c, MRF_K_DDA_FILL);
-        launch_dda_fill(f, c->grid, c->noise, d_depth, c->row_ptr.p, c->vid.p, c->off_q.p, c->vox_count.p, c->stream);
+        launch_dda_fill(f, c->grid, c->noise, c->mp, d_depth, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p, c->lnu.p,
+                        c->vox_count.p, c->stream);
         CK_LAUNCH(MRF_K_DDA_FILL, Rf > 0 ? 1 : 0);
     }
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
