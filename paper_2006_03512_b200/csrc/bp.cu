@@ -252,7 +252,10 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
 
 // G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.
 template <int G, int K, int M>
-__global__ void __launch_bounds__(256, 3) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
+#ifndef MRF_K5_MIN_BLOCKS
+#define MRF_K5_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(256, MRF_K5_MIN_BLOCKS) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ ray_z,
                                                          const int32_t* __restrict__ vid,
@@ -560,23 +563,47 @@ __global__ void __launch_bounds__(256) voxel_reduce_kernel(long long n_items, co
 
 // ---------------------------------------------------------------- K6 (tile-run transpose)
 // Same sums, over the tile->ray-run transpose: a CTA (1024 threads) takes a work item (tile t,
-// <= kRunsPerItem of its runs).  Groups of 8 lanes read one run's vid/q contiguously and add q
-// into the tile's 16384 slots in shared memory, split into 16-bit halves held in two int32
-// arrays (native 32-bit shared atomics; a slot gets at most one contribution per run, so the
-// halves cannot overflow within an item).  The slots then go to T with one int64 atomic each
-// (a tile spans several items).  Integer sums: exact, independent of order and scheduling.
+// <= kRunsPerItem of its runs).  A group of 8 lanes takes one run, 4 consecutive incidences per
+// lane: q read contiguously, the in-tile slot decoded from the run's step masks (no vid read).
+// q is added into the tile's 16384 slots in shared memory, split into 16-bit halves held in two
+// int32 arrays (native 32-bit shared atomics; a slot gets at most one contribution per run, so
+// the halves cannot overflow within an item); slot s lives at the bank-swizzled index
+// swz(s) = s with its low 5 bits rotated by y + 5z, so that runs stepping along y or z (slot
+// strides 32, 1024) spread over the banks.  The slots then go to T with one int64 atomic each
+// (a tile spans several items).  Integer sums: exact, independent of order.  Each group loads
+// the next run (descriptor and q) before adding the current one.
 constexpr int kK6Threads = 1024;
+
+__device__ __forceinline__ int swz(int s) { return (s & ~31) | ((s + (s >> 5) + 5 * (s >> 10)) & 31); }
+__device__ __forceinline__ int unswz(int i) { return (i & ~31) | ((i - (i >> 5) - 5 * (i >> 10)) & 31); }
+
+struct K6Run {
+    Run r;
+    int q[4];
+};
+__device__ __forceinline__ void k6_load(const Run* __restrict__ runs, const int32_t* __restrict__ lam, long long ri,
+                                        bool ok, int k0, K6Run& x) {
+    x.r = Run{0u, 0u, 0u, 0u};
+    x.q[0] = x.q[1] = x.q[2] = x.q[3] = 0;
+    if (!ok) return;
+    const uint4 rr = __ldg(reinterpret_cast<const uint4*>(runs + ri));
+    x.r = Run{rr.x, rr.y, rr.z, rr.w};
+    const int n = (int)((rr.y >> 14) & 63u) + 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (k0 + j < n) x.q[j] = __ldg(lam + rr.x + k0 + j);
+}
 
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
                                                                    const long long* __restrict__ tile_ptr,
                                                                    const Run* __restrict__ runs,
-                                                                   const int32_t* __restrict__ vid,
                                                                    const int32_t* __restrict__ lam, long long* T) {
     extern __shared__ int smem[];
-    int* acc_lo = smem;                 // sum of (q & 0xffff)
+    int* acc_lo = smem;                 // sum of (q & 0xffff), at swz(slot)
     int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane >> 3, sl = lane & 7;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane >> 3, k0 = 4 * (lane & 7);
     constexpr int kWarps = kK6Threads / 32;
+    constexpr int kStride = 4 * kWarps;
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int2 item = __ldg(items + it);
         for (int i = threadIdx.x; i < 2 * kTileSlots; i += kK6Threads) smem[i] = 0;
@@ -584,36 +611,38 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
         const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * kRunsPerItem;
         long long r1 = __ldg(tile_ptr + item.x + 1);
         if (r1 > r0 + kRunsPerItem) r1 = r0 + kRunsPerItem;
-        for (long long rb = r0 + 4 * wid; rb < r1; rb += 4 * kWarps) {
-            Run run{0u, 0u};
-            if (rb + sub < r1) {
-                const uint2 rr = __ldg(reinterpret_cast<const uint2*>(runs + rb + sub));
-                run = Run{rr.x, rr.y};
-            }
-            for (int k = sl; k < (int)run.n; k += 32) {
-                int v[4], q[4];
+        long long rb = r0 + 4 * wid + sub;
+        K6Run cur, nxt;
+        k6_load(runs, lam, rb, rb < r1, k0, cur);
+        for (; rb < r1; rb += kStride) {
+            k6_load(runs, lam, rb + kStride, rb + kStride < r1, k0, nxt);
+            const unsigned meta = cur.r.meta;
+            const int n = (int)((meta >> 14) & 63u) + 1;
+            if (k0 < n) {
+                const int sx = (meta >> 20) & 1 ? -1 : 1, sy = (meta >> 21) & 1 ? -32 : 32;
+                const int sz = (meta >> 22) & 1 ? -1024 : 1024;
+                const unsigned below = (1u << k0) - 1u;
+                int cx = __popc(cur.r.mx & below), cy = __popc(cur.r.my & below);
+                const int base = (int)(meta & (kTileSlots - 1));
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const bool ok = k + 8 * u < (int)run.n;
-                    const long long e = (long long)run.e + k + 8 * u;
-                    v[u] = ok ? __ldg(vid + e) : -1;
-                    q[u] = ok ? __ldg(lam + e) : 0;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    if (v[u] >= 0) {
-                        const int slot = v[u] & (kTileSlots - 1);
-                        atomicAdd(acc_lo + slot, q[u] & 0xffff);
-                        atomicAdd(acc_hi + slot, q[u] >> 16);
+                for (int j = 0; j < 4; ++j) {
+                    const int k = k0 + j;
+                    if (k < n) {
+                        const int slot = swz(base + sx * cx + sy * cy + sz * (k - cx - cy));
+                        atomicAdd(acc_lo + slot, cur.q[j] & 0xffff);
+                        atomicAdd(acc_hi + slot, cur.q[j] >> 16);
                     }
+                    cx += (cur.r.mx >> k) & 1u;
+                    cy += (cur.r.my >> k) & 1u;
                 }
             }
+            cur = nxt;
         }
         __syncthreads();
         long long* Tt = T + ((long long)item.x << kTileShift);
         for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
             const long long sum = (long long)acc_hi[i] * 65536 + (long long)acc_lo[i];
-            if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
+            if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + unswz(i)), (unsigned long long)sum);
         }
         __syncthreads();
     }
@@ -715,7 +744,7 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
 }
 
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* vid, const int32_t* lam, long long* T, cudaStream_t s) {
+                        const int32_t* lam, long long* T, cudaStream_t s) {
     if (n_items == 0) return;
     static bool configured = false;
     if (!configured) {
@@ -725,7 +754,7 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
     }
     const long long grid = n_items < 148LL ? n_items : 148LL;
     tile_reduce_kernel<<<(unsigned)grid, kK6Threads, 2 * kTileSlots * sizeof(int), s>>>(n_items, items, tile_ptr, runs,
-                                                                                     vid, lam, T);
+                                                                                     lam, T);
 }
 
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s) {

@@ -184,23 +184,56 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
     }
 }
 
+// Tile-run builder (K4b): a run ends where the tile changes (a ray crosses a convex tile once),
+// after kRunMax incidences, or before a step that is not a single-axis unit step (an exact DDA
+// tie).  Used by the DDA fill (runs per tile) and by run_fill (the runs themselves).
+struct RunBuilder {
+    int tile = -1, n = 0, prev = 0;  // current run: tile, length, in-tile slot of its last element
+    long long start = 0;
+    unsigned mx = 0, my = 0, neg = 0, slot0 = 0;
+    // Does incidence (tile b, in-tile slot l) extend the current run?  Records the step if so.
+    __device__ __forceinline__ bool extend(int b, int l) {
+        if (b != tile || n >= kRunMax) return false;
+        const int dx = (l & 31) - (prev & 31), dy = ((l >> 5) & 31) - ((prev >> 5) & 31), dz = (l >> 10) - (prev >> 10);
+        if ((dx != 0) + (dy != 0) + (dz != 0) != 1) return false;
+        const int d = dx + dy + dz;
+        if (d != 1 && d != -1) return false;
+        const int ax = dx ? 0 : (dy ? 1 : 2);
+        if (ax == 0) mx |= 1u << (n - 1);
+        if (ax == 1) my |= 1u << (n - 1);
+        if (d < 0) neg |= 1u << ax;
+        ++n;
+        prev = l;
+        return true;
+    }
+    __device__ __forceinline__ void begin(int b, int l, long long e) {
+        tile = b;
+        n = 1;
+        prev = l;
+        start = e;
+        mx = my = neg = 0;
+        slot0 = (unsigned)l;
+    }
+    __device__ __forceinline__ Run make() const {
+        return Run{(unsigned)start, slot0 | ((unsigned)(n - 1) << 14) | (neg << 20), mx, my};
+    }
+};
+
 // ---------------------------------------------------------------- K3
 // B3: off_q = clamp(rint((0.5 (t_in + t_out) L - Z) * 32768), +-32767), the span midpoint
 // relative to the measured range (reading R6).
-__global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n, MsgParams mp,
+__global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
                                                        const float* __restrict__ depth,
-                                                       const long long* __restrict__ row_ptr,
-                                                       const RayInfo* __restrict__ ray_z, int32_t* vid,
-                                                       int16_t* off_q, float* lnu, int32_t* vox_count) {
+                                                       const long long* __restrict__ row_ptr, int32_t* vid,
+                                                       int16_t* off_q, int32_t* tile_runs) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n_pix = (long long)f.rows_owned * f.W;
     const int lane = threadIdx.x & 31;
     bool alive = false;
     Segment sg;
     Walker w;
+    RunBuilder rb;
     long long e = 0;
-    int iz = 0;
-    float wz = 0.f;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
@@ -208,9 +241,6 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             w.start(sg);
             alive = w.inside(g);
             e = row_ptr[f.ray_base + i];
-            const RayInfo ri = ray_z[f.ray_base + i];
-            iz = ri.iz;
-            wz = ri.wz;
         }
     }
     for (;;) {
@@ -226,10 +256,16 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
             vid[e] = vx;
             off_q[e] = (int16_t)q;
-            lnu[e] = lut_log_nu(mp, iz, wz, (int)q);
             ++e;
-            const unsigned peers = __match_any_sync(am, vx);
-            if (lane == __ffs(peers) - 1) atomicAdd(&vox_count[vx], __popc(peers));
+            // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
+            const int b = vx >> kTileShift, l = vx & (kTileSlots - 1);
+            const bool start = !rb.extend(b, l);
+            if (start) rb.begin(b, l, 0);
+            const unsigned sm = __ballot_sync(am, start);
+            if (start) {
+                const unsigned peers = __match_any_sync(sm, b);
+                if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[b], __popc(peers));
+            }
             if (last) {
                 alive = false;
             } else {
@@ -238,6 +274,31 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
                 alive = w.inside(g);
             }
         }
+    }
+}
+
+// log nu per incidence (B3): thread per ray of the frame, one 8-slot chunk per step (a 16-byte
+// off_q read, a 32-byte log-nu write); the table rows of the ray stay in L1.
+__global__ void __launch_bounds__(256) lnu_fill_kernel(long long r0, long long n_rays, MsgParams mp,
+                                                       const long long* __restrict__ row_ptr,
+                                                       const RayInfo* __restrict__ ray_z,
+                                                       const int16_t* __restrict__ off_q, float* lnu) {
+    const long long r = r0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= r0 + n_rays) return;
+    const RayInfo ri = ray_z[r];
+    const long long e0 = row_ptr[r];
+    for (int c = 0; c < ri.n; c += 8) {
+        const uint4 o = __ldg(reinterpret_cast<const uint4*>(off_q + e0 + c));
+        const unsigned ow[4] = {o.x, o.y, o.z, o.w};
+        float out[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int q = (int)(short)((ow[k >> 1] >> (16 * (k & 1))) & 0xffffu);
+            out[k] = c + k < ri.n ? lut_finish(lut_fetch(mp, ri.iz, q), ri.wz) : 0.f;
+        }
+        float4* dst = reinterpret_cast<float4*>(lnu + e0 + c);
+        dst[0] = make_float4(out[0], out[1], out[2], out[3]);
+        dst[1] = make_float4(out[4], out[5], out[6], out[7]);
     }
 }
 
@@ -279,11 +340,14 @@ __global__ void item_counts_kernel(long long V, const int32_t* __restrict__ cnt,
     if (v < V) n_items[v] = (cnt[v] + chunk - 1) / chunk;
 }
 
-// K4b: tile-run transpose.  Thread per ray; a run starts at the ray's first incidence and
-// wherever the tile changes (a ray crosses a convex tile once, so (ray, tile) -> one run).
-__global__ void __launch_bounds__(256) run_count_kernel(long long n_rays, const long long* __restrict__ row_ptr,
-                                                        const RayInfo* __restrict__ info,
-                                                        const int32_t* __restrict__ vid, int32_t* tile_runs) {
+// K4b: tile-run transpose.  Thread per ray walking its incidences; a run ends where the tile
+// changes (a ray crosses a convex tile once), after kRunMax incidences, or before a step that is
+// not a single-axis unit step (an exact DDA tie).  run_count counts runs per tile, run_fill
+// writes them (order inside a tile is irrelevant: K6 sums integers).
+// Voxel degrees (per belief slot), only for the per-voxel transpose and the active-voxel count.
+__global__ void __launch_bounds__(256) vox_hist_kernel(long long n_rays, const long long* __restrict__ row_ptr,
+                                                       const RayInfo* __restrict__ info,
+                                                       const int32_t* __restrict__ vid, int32_t* vox_count) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     long long e = 0, e1 = 0;
@@ -291,20 +355,14 @@ __global__ void __launch_bounds__(256) run_count_kernel(long long n_rays, const 
         e = row_ptr[r];
         e1 = e + info[r].n;
     }
-    int prev = -1;
     for (;;) {
         const bool alive = e < e1;
         const unsigned am = __ballot_sync(kFull, alive);
         if (am == 0) break;
         if (alive) {
-            const int b = vid[e] >> kTileShift;
-            const bool start = b != prev;
-            prev = b;
-            const unsigned sm = __ballot_sync(am, start);
-            if (start) {
-                const unsigned peers = __match_any_sync(sm, b);
-                if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[b], __popc(peers));
-            }
+            const int vx = vid[e];
+            const unsigned peers = __match_any_sync(am, vx);
+            if (lane == __ffs(peers) - 1) atomicAdd(&vox_count[vx], __popc(peers));
             ++e;
         }
     }
@@ -317,36 +375,45 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
                                                        Run* runs) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    long long e = 0, e1 = 0, start = 0;
+    long long e = 0, e1 = 0;
     if (r < n_rays) {
         e = row_ptr[r];
         e1 = e + info[r].n;
     }
     bool alive = e < e1;
-    int cur = -1;
+    RunBuilder rb;
     for (;;) {
         const unsigned am = __ballot_sync(kFull, alive);
         if (am == 0) break;
         if (alive) {
             const bool at_end = e == e1;
-            const int b = at_end ? -1 : (vid[e] >> kTileShift);
-            const bool emit = cur >= 0 && b != cur;  // the run in tile `cur` ends before e
+            int b = -1, l = 0;
+            if (!at_end) {
+                const int v = vid[e];
+                b = v >> kTileShift;
+                l = v & (kTileSlots - 1);
+            }
+            RunBuilder nb = rb;
+            const bool ext = !at_end && nb.extend(b, l);
+            const bool emit = rb.tile >= 0 && !ext;  // the current run ends before e
             const unsigned em = __ballot_sync(am, emit);
             if (emit) {
+                const int cur = rb.tile;
                 const unsigned peers = __match_any_sync(em, cur);
                 const int leader = __ffs(peers) - 1;
                 int base = 0;
                 if (lane == leader) base = atomicAdd(&cursor[cur], __popc(peers));
                 base = __shfl_sync(peers, base, leader);
                 const int rank = __popc(peers & ((1u << lane) - 1u));
-                runs[tile_ptr[cur] + base + rank] = Run{(unsigned)start, (unsigned)(e - start)};
+                runs[tile_ptr[cur] + base + rank] = rb.make();
             }
             if (at_end) {
                 alive = false;
             } else {
-                if (b != cur) {
-                    cur = b;
-                    start = e;
+                if (ext) {
+                    rb = nb;
+                } else {
+                    rb.begin(b, l, e);
                 }
                 ++e;
             }
@@ -462,11 +529,11 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
 
 void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
-                     int16_t* off_q, float* lnu, int32_t* vox_count, cudaStream_t s) {
+                     int16_t* off_q, float* lnu, int32_t* tile_runs, cudaStream_t s) {
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
-    dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, mp, depth, row_ptr, ray_z, vid, off_q, lnu,
-                                                           vox_count);
+    dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q, tile_runs);
+    lnu_fill_kernel<<<blocks_for(n_pix, 256), 256, 0, s>>>(f.ray_base, n_pix, mp, row_ptr, ray_z, off_q, lnu);
 }
 
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
@@ -479,10 +546,10 @@ void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items,
     item_counts_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, n_items, chunk);
 }
 
-void launch_run_count(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
-                      int32_t* tile_runs, cudaStream_t s) {
+void launch_vox_hist(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                     int32_t* vox_count, cudaStream_t s) {
     if (n_rays == 0) return;
-    run_count_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, tile_runs);
+    vox_hist_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, vox_count);
 }
 
 void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,

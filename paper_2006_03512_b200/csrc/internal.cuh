@@ -50,10 +50,17 @@ __host__ __device__ __forceinline__ void slot_xyz(const GridDesc& g, long long s
     z = (int)(t / ((long long)g.ntx * g.nty)) * 16 + (l >> 10);
 }
 
-// A run: the contiguous incidences [e, e + n) of one ray inside one tile.
+// A run: up to kRunMax contiguous incidences [e, e + n) of one ray inside one tile, stored with
+// the DDA steps between them so that K6 never reads vid.  Step i (from element i to i+1) is a
+// unit step along x (bit i of mx), y (bit i of my) or z (neither); element k then sits at the
+// in-tile slot  slot0 + sx cx + 32 sy cy + 1024 sz (k - cx - cy),  cx = popc(mx & (2^k - 1)),
+// cy likewise.  A step along several axes at once (an exact DDA tie) starts a new run.
+// meta: slot0 (bits 0-13) | (n-1) << 14 | negative-direction flags of x, y, z << 20.
+constexpr int kRunMax = 32;
 struct Run {
-    unsigned e;
-    unsigned n;
+    unsigned e;                 // first incidence slot (this rank holds < 2^31 slots)
+    unsigned meta;
+    unsigned mx, my;
 };
 
 struct NoiseDesc {
@@ -93,15 +100,21 @@ struct MsgParams {
 // log nu at (measured range row iz + wz, quantised offset off_q): bilinear interpolation of the
 // input table in fp32, bin-centre coordinates clamped to the edge centres.
 // Evaluated once per incidence by the DDA fill; K5 reads the result.
-__device__ __forceinline__ float lut_log_nu(const MsgParams& mp, int iz, float wz, int off) {
+// Split in two so that a caller can issue the table loads one step before it needs them.
+struct LutFetch {
+    float wo;
+    float2 ta, tb;
+};
+__device__ __forceinline__ LutFetch lut_fetch(const MsgParams& mp, int iz, int off) {
     float fo = fmaf((float)off, mp.s_off, mp.b_off);
     fo = fminf(fmaxf(fo, 0.f), mp.fo_max);
     const int io = min((int)fo, mp.n_offm1 - 1);
-    const float wo = fo - (float)io;
     const float2* rowA = mp.lutp + (long long)iz * mp.n_offm1;
-    const float2 ta = __ldg(rowA + io), tb = __ldg(rowA + mp.n_offm1 + io);
-    const float ra = fmaf(wo, ta.y - ta.x, ta.x);
-    const float rb = fmaf(wo, tb.y - tb.x, tb.x);
+    return LutFetch{fo - (float)io, __ldg(rowA + io), __ldg(rowA + mp.n_offm1 + io)};
+}
+__device__ __forceinline__ float lut_finish(const LutFetch& f, float wz) {
+    const float ra = fmaf(f.wo, f.ta.y - f.ta.x, f.ta.x);
+    const float rb = fmaf(f.wo, f.tb.y - f.tb.x, f.tb.x);
     return fmaf(wz, rb - ra, ra);
 }
 
@@ -111,10 +124,14 @@ __device__ __forceinline__ float lut_log_nu(const MsgParams& mp, int iz, float w
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
                          int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s);
-// K3: walk again, write vid / off_q / log nu at row_ptr offsets, histogram voxel degrees
+// K3: walk again, write vid / off_q at row_ptr offsets and count the tile runs (K4b) per tile;
+// then log nu per incidence
 void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
-                     int16_t* off_q, float* lnu, int32_t* vox_count, cudaStream_t s);
+                     int16_t* off_q, float* lnu, int32_t* tile_runs, cudaStream_t s);
+// voxel degrees (per-voxel transpose, active count): vox_count zeroed by the caller
+void launch_vox_hist(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
+                     int32_t* vox_count, cudaStream_t s);
 // K2: out[i] = offset + sum_{j<i} in[j] for i in [0, n]; out has n+1 entries.
 void launch_exclusive_scan(const int32_t* in, long long* out, long long n, long long offset,
                            long long* scratch, cudaStream_t s);
@@ -123,8 +140,6 @@ long long scan_scratch_elems(long long n);
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                            const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s);
 // tile-run transpose (K4b): runs per tile, then the run list grouped by tile
-void launch_run_count(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
-                      int32_t* tile_runs, cudaStream_t s);
 void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                      const long long* tile_ptr, int32_t* cursor, Run* runs, cudaStream_t s);
 // K6 work list: n_items[i] = ceil(count[i] / chunk); items (i, j) from item_ptr
@@ -190,7 +205,7 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                         const int32_t* vid, const int32_t* lam, long long* T, cudaStream_t s);
+                        const int32_t* lam, long long* T, cudaStream_t s);
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s);
 void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s);
 

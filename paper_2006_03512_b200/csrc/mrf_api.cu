@@ -82,6 +82,7 @@ struct mrf_ctx {
     int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1|2)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
+    bool hist_valid = false; // vox_count (voxel degrees) computed for the current graph
     float prior = 0.5f;
     double L0 = 0.0;
     MsgParams mp{};
@@ -235,10 +236,24 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
 
 // Per-voxel transpose (col_ptr over belief slots, tr) + its K6 work list.  Built by prepare()
 // only for the per-voxel K6 ablation, and lazily for mrf_export_transpose.
+// Voxel degrees on demand (not needed by the BP iteration).
+mrf_status voxel_histogram(mrf_ctx* c) {
+    if (c->hist_valid) return MRF_OK;
+    CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * c->VI, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_vox_hist(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->vox_count.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    }
+    c->hist_valid = true;
+    return MRF_OK;
+}
+
 mrf_status build_voxel_transpose(mrf_ctx* c) {
     if (c->vtr_valid) return MRF_OK;
     const long long VI = c->VI;
     mrf_status st;
+    if ((st = voxel_histogram(c)) != MRF_OK) return st;
     if ((st = scan(c, c->vox_count.p, c->col_ptr.p, VI, 0)) != MRF_OK) return st;
     CK(c->tr.ensure((size_t)c->E + kPadElems, 0, c->stream));
     CK(cudaMemsetAsync(c->cursor.p, 0, sizeof(int32_t) * VI, c->stream));
@@ -261,16 +276,11 @@ mrf_status build_voxel_transpose(mrf_ctx* c) {
     return MRF_OK;
 }
 
-// Tile-run transpose (runs grouped by tile) + its K6 work list.
+// Tile-run transpose (runs grouped by tile) + its K6 work list.  The runs per tile were counted
+// by the DDA fills.
 mrf_status build_tile_runs(mrf_ctx* c) {
     const long long NT = c->NT;
     mrf_status st;
-    CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
-    {
-        ProfScope ps(c, MRF_K_TRANSPOSE);
-        launch_run_count(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_runs.p, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
-    }
     if ((st = scan(c, c->tile_runs.p, c->tile_ptr.p, NT, 0)) != MRF_OK) return st;
     if ((st = read_ll(c, c->tile_ptr.p + NT, &c->n_runs)) != MRF_OK) return st;
     CK(c->runs.ensure((size_t)std::max(1LL, c->n_runs), 0, c->stream));
@@ -326,6 +336,7 @@ mrf_status prepare(mrf_ctx* c) {
         CK(c->class_rays[k].ensure((size_t)std::max(1LL, c->class_n[k]), 0, c->stream));
         launch_compact(c->R, c->flags.p, c->pos.p, c->class_rays[k].p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+
     }
     // scratch for the tiled long-ray kernel
     const int kl = kNumClasses - 1;
@@ -352,7 +363,7 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
     } else {
-        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->vid.p, c->lam.p, out, c->stream);
+        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -530,7 +541,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(c->counters.ensure(8, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
         CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
-        CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * VI, c->stream));
+        CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
         CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 8, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
@@ -630,10 +641,11 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->R = c->E = c->E_real = 0;
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
-    CK(cudaMemsetAsync(c->vox_count.p, 0, sizeof(int32_t) * c->VI, c->stream));
+    CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * c->NT, c->stream));
     CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * c->VI, c->stream));
     CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
     c->dirty = true;
+    c->hist_valid = false;
     return MRF_OK;
 }
 
@@ -714,8 +726,8 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     {
         ProfScope ps(c, MRF_K_DDA_FILL);
         launch_dda_fill(f, c->grid, c->noise, c->mp, d_depth, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p, c->lnu.p,
-                        c->vox_count.p, c->stream);
-        CK_LAUNCH(MRF_K_DDA_FILL, Rf > 0 ? 1 : 0);
+                        c->tile_runs.p, c->stream);
+        CK_LAUNCH(MRF_K_DDA_FILL, Rf > 0 ? 2 : 0);  // DDA fill + log-nu fill
     }
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
     c->frames.push_back({width, height, rows_owned, c->R, Rf});
@@ -726,6 +738,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     c->n_dropped += drp;
     c->n_kept += Rf - inv - drp;
     c->dirty = true;
+    c->hist_valid = false;
     if (!on_device) CK(cudaStreamSynchronize(c->stream));  // staging buffer reused by the next frame
     return MRF_OK;
 }
@@ -794,6 +807,8 @@ mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences,
     if (n_active_vox) {
         CK(c->flags.ensure((size_t)c->VI + 1, 0, c->stream));
         CK(c->pos.ensure((size_t)c->VI + 1, 0, c->stream));
+        mrf_status sh;
+        if ((sh = voxel_histogram(c)) != MRF_OK) return sh;
         launch_active_flags(c->VI, c->vox_count.p, c->flags.p, c->stream);
         CK_LAUNCH(MRF_K_SCAN, 1);
         mrf_status st;
