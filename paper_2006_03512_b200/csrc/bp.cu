@@ -204,29 +204,65 @@ __device__ __forceinline__ int32_t quantise(float lam) {
 }
 
 // ---------------------------------------------------------------- K5: class kernels
-// Loads of one lane's chunk [s, s+K) (s < e1; the chunk lies inside the ray's padded segment):
-// vid, q, log nu as 16-byte vectors, then the belief gathers.
+// Lane chunks of K incidences start at multiples of K slots from an 8-aligned ray start, so they
+// are read / written with the widest vector that K allows (16 bytes for K = 8, 8 for K = 6).
+template <int K>
+struct VecW {
+    static constexpr int value = (K % 4 == 0) ? 4 : ((K % 2 == 0) ? 2 : 1);
+};
+template <int K>
+__device__ __forceinline__ void ldk(const int32_t* __restrict__ p, int (&o)[K]) {
+    constexpr int W = VecW<K>::value;
+#pragma unroll
+    for (int j = 0; j < K; j += W) {
+        if constexpr (W == 4) {
+            const int4 a = __ldg(reinterpret_cast<const int4*>(p + j));
+            o[j] = a.x; o[j + 1] = a.y; o[j + 2] = a.z; o[j + 3] = a.w;
+        } else if constexpr (W == 2) {
+            const int2 a = __ldg(reinterpret_cast<const int2*>(p + j));
+            o[j] = a.x; o[j + 1] = a.y;
+        } else {
+            o[j] = __ldg(p + j);
+        }
+    }
+}
+// store the first nv of K values (all K when the chunk is complete, with vector stores)
+template <int K>
+__device__ __forceinline__ void stk(int32_t* p, const int (&v)[K], long long nv) {
+    constexpr int W = VecW<K>::value;
+    if (nv >= K) {
+#pragma unroll
+        for (int j = 0; j < K; j += W) {
+            if constexpr (W == 4) {
+                *reinterpret_cast<int4*>(p + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else if constexpr (W == 2) {
+                *reinterpret_cast<int2*>(p + j) = make_int2(v[j], v[j + 1]);
+            } else {
+                p[j] = v[j];
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            if (j < nv) p[j] = v[j];
+    }
+}
+
+// Loads of one lane's chunk [s, s+K) (s < e1): vid, q, log nu, then the belief gathers.
 template <int K, int M>
 __device__ __forceinline__ void load_chunk(long long s, long long e1, float L0, const int32_t* __restrict__ vid,
                                            const float* __restrict__ lnu, const int32_t* __restrict__ lam,
                                            const long long* __restrict__ T, float (&la)[K], float (&w)[K],
                                            float (&l)[K]) {
-    int v[K], q[K];
-    float ln[K];
-#pragma unroll
-    for (int j = 0; j < K; j += 4) {
-        const int4 a = __ldg(reinterpret_cast<const int4*>(vid + s + j));
-        const int4 b = __ldg(reinterpret_cast<const int4*>(lam + s + j));
-        const float4 c = __ldg(reinterpret_cast<const float4*>(lnu + s + j));
-        v[j] = a.x; v[j + 1] = a.y; v[j + 2] = a.z; v[j + 3] = a.w;
-        q[j] = b.x; q[j + 1] = b.y; q[j + 2] = b.z; q[j + 3] = b.w;
-        ln[j] = c.x; ln[j + 1] = c.y; ln[j + 2] = c.z; ln[j + 3] = c.w;
-    }
+    int v[K], q[K], ln[K];
+    ldk<K>(vid + s, v);
+    ldk<K>(lam + s, q);
+    ldk<K>(reinterpret_cast<const int32_t*>(lnu) + s, ln);
     long long t[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) t[j] = (s + j < e1) ? __ldg(T + v[j]) : 0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], ln[j], L0, s + j < e1, la[j], w[j], l[j]);
+    for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), L0, s + j < e1, la[j], w[j], l[j]);
 }
 template <int K>
 __device__ __forceinline__ void identity_chunk(float (&la)[K], float (&w)[K], float (&l)[K]) {
@@ -242,19 +278,17 @@ __device__ __forceinline__ void identity_chunk(float (&la)[K], float (&w)[K], fl
 template <int K>
 __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[K], const float (&lQ)[K], long long s,
                                          long long e1, int32_t* lam) {
-    int32_t out[K];
+    int out[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) out[j] = s + j < e1 ? quantise(lambda_n(lQ[j], l[j], lR[j])) : 0;
-#pragma unroll
-    for (int j = 0; j < K; j += 4)
-        *reinterpret_cast<int4*>(lam + s + j) = make_int4(out[j], out[j + 1], out[j + 2], out[j + 3]);
+    stk<K>(lam + s, out, e1 - s);
 }
 
 // G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.
-template <int G, int K, int M>
 #ifndef MRF_K5_MIN_BLOCKS
 #define MRF_K5_MIN_BLOCKS 4
 #endif
+template <int G, int K, int M>
 __global__ void __launch_bounds__(256, MRF_K5_MIN_BLOCKS) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ ray_z,
@@ -667,25 +701,33 @@ __global__ void lambda_to_float_kernel(long long n, const int32_t* __restrict__ 
 
 inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
+template <int M, int k>
+void launch_class_k(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr, const RayInfo* ray_z,
+                    const int32_t* vid, const float* lnu, int32_t* lam, const long long* T, const MsgParams& mp,
+                    cudaStream_t s) {
+    if constexpr (k < kNumShort) {
+        if (cls == k) {
+            constexpr int G = class_G(k), K = class_K(k);
+            const unsigned grid = blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256);
+            ray_msg_kernel<G, K, M><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp);
+            return;
+        }
+        launch_class_k<M, k + 1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
+    }
+}
+
 template <int M>
 void launch_ray_messages_m(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
                            const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
                            const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                            int n_warps_long, cudaStream_t s) {
-    auto grid = [&](int G) { return blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256); };
-    constexpr int G0 = kMinGroup, K = kLaneK;
-#define MRF_K5_ARGS n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp
-    switch (cls) {
-        case 0: ray_msg_kernel<G0, K, M><<<grid(G0), 256, 0, s>>>(MRF_K5_ARGS); break;
-        case 1: ray_msg_kernel<2 * G0, K, M><<<grid(2 * G0), 256, 0, s>>>(MRF_K5_ARGS); break;
-        case 2: ray_msg_kernel<4 * G0, K, M><<<grid(4 * G0), 256, 0, s>>>(MRF_K5_ARGS); break;
-        case 3: ray_msg_kernel<8 * G0, K, M><<<grid(8 * G0), 256, 0, s>>>(MRF_K5_ARGS); break;
-        default: {
-            const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
-            ray_msg_long_kernel<M><<<g, 256, 0, s>>>(MRF_K5_ARGS, scratch, scratch_per_warp);
-        }
+    if (cls < kNumShort) {
+        launch_class_k<M, 0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
+    } else {
+        const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
+        ray_msg_long_kernel<M><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                                 scratch_per_warp);
     }
-#undef MRF_K5_ARGS
 }
 
 template <int M>
@@ -708,32 +750,27 @@ void launch_staged_m(long long n_stages, const Stage* stages, const long long* r
 
 }  // namespace
 
-int class_capacity(int cls) { return cls < kNumClasses - 1 ? kLaneK * (kMinGroup << cls) : 0x7fffffff; }
-
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
                          const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, int math, cudaStream_t s) {
     if (n_rays == 0) return;
-    switch (math) {
-        case 0: launch_ray_messages_m<0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
-                                         scratch_per_warp, n_warps_long, s); break;
-        case 2: launch_ray_messages_m<2>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
-                                         scratch_per_warp, n_warps_long, s); break;
-        default: launch_ray_messages_m<1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
-                                          scratch_per_warp, n_warps_long, s);
-    }
+    if (math == 0)
+        launch_ray_messages_m<0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch, scratch_per_warp,
+                                 n_warps_long, s);
+    else
+        launch_ray_messages_m<1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch, scratch_per_warp,
+                                 n_warps_long, s);
 }
 
 void launch_ray_messages_staged(long long n_stages, const Stage* stages, const long long* row_ptr,
                                 const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
                                 const long long* T, const MsgParams& mp, int math, cudaStream_t s) {
     if (n_stages == 0) return;
-    switch (math) {
-        case 0: launch_staged_m<0>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s); break;
-        case 2: launch_staged_m<2>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s); break;
-        default: launch_staged_m<1>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s);
-    }
+    if (math == 0)
+        launch_staged_m<0>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s);
+    else
+        launch_staged_m<1>(n_stages, stages, row_ptr, info, vid, lnu, lam, T, mp, s);
 }
 
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,

@@ -434,21 +434,25 @@ __global__ void active_flags_kernel(long long V, const int32_t* __restrict__ cnt
     if (v < V) flags[v] = cnt[v] > 0 ? 1 : 0;
 }
 
-__global__ void class_flags_kernel(long long n_rays, const RayInfo* __restrict__ info, int cls, int32_t* flags) {
+// K5 class lists (counting sort by class, warp-aggregated atomics)
+__global__ void class_count_kernel(long long n_rays, const RayInfo* __restrict__ info, unsigned long long* counts) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= n_rays) return;
-    const int n = info[r].n;
-    int c = -1;
-    if (n > 0) {
-        c = kNumClasses - 1;
-        for (int k = 0; k < kNumClasses - 1; ++k) {
-            if (n <= kLaneK * (kMinGroup << k)) {  // groups of G lanes of kLaneK incidences
-                c = k;
-                break;
-            }
-        }
-    }
-    flags[r] = (c == cls) ? 1 : 0;
+    const int lane = threadIdx.x & 31;
+    const int k = r < n_rays ? ray_class(info[r].n) : -1;
+    const unsigned peers = __match_any_sync(kFull, k);
+    if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&counts[k], (unsigned long long)__popc(peers));
+}
+__global__ void class_scatter_kernel(long long n_rays, const RayInfo* __restrict__ info, ClassOffsets off,
+                                     unsigned long long* cursor, int32_t* out) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int k = r < n_rays ? ray_class(info[r].n) : -1;
+    const unsigned peers = __match_any_sync(kFull, k);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (k >= 0 && lane == leader) base = atomicAdd(&cursor[k], (unsigned long long)__popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    if (k >= 0) out[off.off[k] + (long long)base + __popc(peers & ((1u << lane) - 1u))] = (int32_t)r;
 }
 
 __global__ void compact_kernel(long long n, const int32_t* __restrict__ flags, const long long* __restrict__ pos,
@@ -567,9 +571,15 @@ void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, 
     active_flags_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, flags);
 }
 
-void launch_class_flags(long long n_rays, const RayInfo* info, int cls, int32_t* flags, cudaStream_t s) {
+void launch_class_count(long long n_rays, const RayInfo* info, unsigned long long* counts, cudaStream_t s) {
     if (n_rays == 0) return;
-    class_flags_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, cls, flags);
+    class_count_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, counts);
+}
+
+void launch_class_scatter(long long n_rays, const RayInfo* info, const ClassOffsets& off, unsigned long long* cursor,
+                          int32_t* out, cudaStream_t s) {
+    if (n_rays == 0) return;
+    class_scatter_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, off, cursor, out);
 }
 
 void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s) {

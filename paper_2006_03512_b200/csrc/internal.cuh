@@ -146,8 +146,6 @@ void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* 
 void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, int chunk, cudaStream_t s);
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
                       cudaStream_t s);
-// K5 ray length classes: flags[r] = (class(r) == c)
-void launch_class_flags(long long n_rays, const RayInfo* info, int cls, int32_t* flags, cudaStream_t s);
 void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s);
 // misc
 void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, cudaStream_t s);
@@ -191,13 +189,28 @@ void launch_ray_messages_staged(long long n_stages, const Stage* stages, const l
                                 const long long* T, const MsgParams& mp, int math, cudaStream_t s);
 
 // ---- BP kernels (bp.cu)
-#ifndef MRF_LANE_K
-#define MRF_LANE_K 8
-#endif
-constexpr int kLaneK = MRF_LANE_K;              // incidences per lane in K5
-constexpr int kMinGroup = 32 / MRF_LANE_K;      // classes: G = kMinGroup << k lanes, capacity 32 << k
-constexpr int kNumClasses = 5;      // 4 group widths (capacity kLaneK * G) + class 4 = long rays (tiled)
-int class_capacity(int cls);        // max span handled by class cls (class 3: unbounded)
+// K5 length classes.  Class k < kNumShort runs G = 4 << (k / 4) lanes per ray with K = 5 + k % 4
+// incidences per lane (capacity G K: 20, 24, 28, 32, 40, ..., 224, 256); a ray goes to the
+// smallest capacity >= n.  Class kNumShort: rays longer than 256 (tiled warp kernel).  The
+// per-ray arithmetic depends only on n, never on where the ray is stored.
+constexpr int kNumShort = 16;
+constexpr int kNumClasses = kNumShort + 1;
+__host__ __device__ constexpr int class_G(int k) { return 4 << (k >> 2); }
+__host__ __device__ constexpr int class_K(int k) { return 5 + (k & 3); }
+__host__ __device__ inline int ray_class(int n) {
+    if (n <= 0) return -1;
+    for (int k = 0; k < kNumShort; ++k)
+        if (n <= class_G(k) * class_K(k)) return k;
+    return kNumShort;
+}
+// class lists: counts per class (counts zeroed by the caller), then the ray ids of class k at
+// out[off[k] ...] (cursor zeroed by the caller; order inside a class is irrelevant)
+struct ClassOffsets {
+    long long off[kNumClasses];
+};
+void launch_class_count(long long n_rays, const RayInfo* info, unsigned long long* counts, cudaStream_t s);
+void launch_class_scatter(long long n_rays, const RayInfo* info, const ClassOffsets& off, unsigned long long* cursor,
+                          int32_t* out, cudaStream_t s);
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
                          const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,

@@ -118,7 +118,9 @@ struct mrf_ctx {
     DBuf<float> depth_stage, marg;
     DBuf<long long> scan_scratch;
     DBuf<unsigned long long> counters;
-    DBuf<int32_t> class_rays[kNumClasses];
+    DBuf<int32_t> class_all;                 // ray ids grouped by K5 class
+    DBuf<unsigned long long> class_cnt;      // [counts | cursors] per class
+    long long class_off[kNumClasses] = {};
     DBuf<Stage> stages;
     long long n_stages = 0;
     long long class_n[kNumClasses] = {};
@@ -328,21 +330,28 @@ mrf_status prepare(mrf_ctx* c) {
         launch_stage_fill(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->pos.p, c->stages.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     }
-    for (int k = c->k5_staged ? kNumClasses - 1 : 0; k < kNumClasses; ++k) {
-        launch_class_flags(c->R, c->ray_z.p, k, c->flags.p, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
-        if ((st = scan(c, c->flags.p, c->pos.p, c->R, 0)) != MRF_OK) return st;
-        if ((st = read_ll(c, c->pos.p + c->R, &c->class_n[k])) != MRF_OK) return st;
-        CK(c->class_rays[k].ensure((size_t)std::max(1LL, c->class_n[k]), 0, c->stream));
-        launch_compact(c->R, c->flags.p, c->pos.p, c->class_rays[k].p, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
-
+    // K5 length classes: counting sort of the ray ids by class
+    CK(c->class_cnt.ensure(2 * kNumClasses, 0, c->stream));
+    CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * kNumClasses * sizeof(unsigned long long), c->stream));
+    launch_class_count(c->R, c->ray_z.p, c->class_cnt.p, c->stream);
+    CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    CK(cudaMemcpyAsync(c->pinned, c->class_cnt.p, kNumClasses * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    ClassOffsets off{};
+    long long tot = 0;
+    for (int k = 0; k < kNumClasses; ++k) {
+        c->class_n[k] = c->pinned[k];
+        c->class_off[k] = off.off[k] = tot;
+        tot += c->class_n[k];
     }
+    CK(c->class_all.ensure((size_t)std::max(1LL, tot), 0, c->stream));
+    launch_class_scatter(c->R, c->ray_z.p, off, c->class_cnt.p + kNumClasses, c->class_all.p, c->stream);
+    CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     // scratch for the tiled long-ray kernel
     const int kl = kNumClasses - 1;
     if (c->class_n[kl] > 0) {
         CK(cudaMemsetAsync(c->counters.p + 6, 0, sizeof(unsigned long long), c->stream));
-        launch_span_max(c->class_n[kl], c->class_rays[kl].p, c->ray_z.p, c->counters.p + 6, c->stream);
+        launch_span_max(c->class_n[kl], c->class_all.p + c->class_off[kl], c->ray_z.p, c->counters.p + 6, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, 1);
         long long span = 0;
         if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
@@ -380,7 +389,7 @@ mrf_status ray_messages(mrf_ctx* c) {
     }
     for (int k = staged ? kNumClasses - 1 : 0; k < kNumClasses; ++k) {
         if (c->class_n[k] == 0) continue;
-        launch_ray_messages(k, c->class_n[k], c->class_rays[k].p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lnu.p,
+        launch_ray_messages(k, c->class_n[k], c->class_all.p + c->class_off[k], c->row_ptr.p, c->ray_z.p, c->vid.p, c->lnu.p,
                             c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long,
                             c->k5_math, c->stream);
         CK_LAUNCH(MRF_K_RAY_MSG, 1);
@@ -599,7 +608,8 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_nitems.release(); c->tile_ptr.release();
     c->bitem_ptr.release(); c->runs.release(); c->bitems.release(); c->stages.release();
-    for (auto& b : c->class_rays) b.release();
+    c->class_all.release();
+    c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;

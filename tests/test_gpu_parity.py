@@ -126,24 +126,29 @@ def test_frame1_graph_and_bp_parity(frame1):
 def test_frame1_full_trajectory_within_conditioning_envelope(frame1):
     """End-to-end after all 8 iterations.  This loopy graph amplifies perturbations ~1e4x by
     iteration 8 (tests/test_oracle_conditioning.py), so the bar is the oracle's own spread
-    under fp32-sized noise: the fp64 oracle re-run with 1e-7 relative noise on every message
-    of every iteration.  GPU deviation <= max(1e-4, 10 x that spread)."""
+    under fp32-sized noise (reading R16): the fp64 oracle re-run with noise of the
+    size the one-step GPU comparison measures on every message of every iteration -- rms
+    2e-7 absolute + 6e-8 relative (`python -m tests.parity_report onestep frame1 2`: rms
+    1.3e-7..2.3e-7 absolute for |lambda| < 10, 1.5e-6 for |lambda| in [10, 300)) -- max over
+    two noise seeds.  GPU deviation <= max(1e-4, 5 x that spread)."""
     w = frame1
     p = oracle.Params.from_workload(w)
     g = oracle.build_graph(p, w.frames)
     _, T_ref = oracle.bp(p, g, w.n_iter)
     m_ref = oracle.marginals(p, T_ref)
-    rng = np.random.default_rng(1)
-    lam = np.zeros(g.E)
-    for _ in range(w.n_iter):
-        lam, _ = oracle.bp(p, g, 1, lam=lam)
-        lam = lam * (1.0 + 1e-7 * rng.standard_normal(g.E))
-    spread = np.max(np.abs(oracle.marginals(p, oracle.accumulate(p, g, lam)) - m_ref))
+    spread = 0.0
+    for seed in (1, 2):
+        rng = np.random.default_rng(seed)
+        lam = np.zeros(g.E)
+        for _ in range(w.n_iter):
+            lam, _ = oracle.bp(p, g, 1, lam=lam)
+            lam = lam + (2e-7 + 6e-8 * np.abs(lam)) * rng.standard_normal(g.E)
+        spread = max(spread, np.max(np.abs(oracle.marginals(p, oracle.accumulate(p, g, lam)) - m_ref)))
     with _gpu_map(w) as m:
         m.bp_iterate(w.n_iter)
         dev = np.max(np.abs(m.marginals() - m_ref))
     print(f"frame1 n={w.n_iter}: gpu max|dp| {dev:.3e}, oracle fp32-noise spread {spread:.3e}")
-    assert dev <= max(MARG_TOL, 10 * spread)
+    assert dev <= max(MARG_TOL, 5 * spread)
 
 
 def test_determinism(frame1):
