@@ -597,86 +597,80 @@ __global__ void __launch_bounds__(256) voxel_reduce_kernel(long long n_items, co
 
 // ---------------------------------------------------------------- K6 (tile-run transpose)
 // Same sums, over the tile->ray-run transpose: a CTA (1024 threads) takes a work item (tile t,
-// <= kRunsPerItem of its runs).  A group of 8 lanes takes one run, 4 consecutive incidences per
-// lane: q read contiguously, the in-tile slot decoded from the run's step masks (no vid read).
-// q is added into the tile's 16384 slots in shared memory, split into 16-bit halves held in two
-// int32 arrays (native 32-bit shared atomics; a slot gets at most one contribution per run, so
-// the halves cannot overflow within an item); slot s lives at the bank-swizzled index
-// swz(s) = s with its low 5 bits rotated by y + 5z, so that runs stepping along y or z (slot
-// strides 32, 1024) spread over the banks.  The slots then go to T with one int64 atomic each
-// (a tile spans several items).  Integer sums: exact, independent of order.  Each group loads
-// the next run (descriptor and q) before adding the current one.
+// <= per_item of its runs) and accumulates q into the tile's 16384 slots in shared memory, split
+// into 16-bit halves held in two int32 arrays (native 32-bit shared atomics -- 64-bit shared
+// atomics are CAS loops on sm_100a; a slot gets at most one contribution per run, so the halves
+// cannot overflow within an item of <= 32768 runs).  A warp takes batches of 32 consecutive runs:
+// one coalesced load of the 32 run descriptors (staged in shared memory), then the q of all 32
+// runs (lane k = incidence k of the run, 32 independent loads in flight per lane), then one run
+// per step: the 32 lanes of an atomic instruction always hit 32 DISTINCT slots (the voxels of one
+// ray), never the same voxel twice (adjacent runs of a tile come from adjacent pixels and share
+// most voxels: processing several runs per instruction serialised on same-address atomics).
+// The in-tile slot comes from the run's step masks (no vid read): for incidence k,
+// slot0 + sx cx + 32 sy cy + 1024 sz (k - cx - cy), cx = popc(mx & (2^k - 1)); slot s lives at
+// the bank-swizzled index swz(s) so that y / z steps (strides 32, 1024) change the bank.  The
+// slots then go to T with one int64 atomic each (a tile spans several items).  Integer sums:
+// exact, independent of order.
 constexpr int kK6Threads = 1024;
+constexpr int kK6Warps = kK6Threads / 32;
+constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
 
-__device__ __forceinline__ int swz(int s) { return (s & ~31) | ((s + (s >> 5) + 5 * (s >> 10)) & 31); }
-__device__ __forceinline__ int unswz(int i) { return (i & ~31) | ((i - (i >> 5) - 5 * (i >> 10)) & 31); }
-
-struct K6Run {
-    Run r;
-    int q[4];
-};
-__device__ __forceinline__ void k6_load(const Run* __restrict__ runs, const int32_t* __restrict__ lam, long long ri,
-                                        bool ok, int k0, K6Run& x) {
-    x.r = Run{0u, 0u, 0u, 0u};
-    x.q[0] = x.q[1] = x.q[2] = x.q[3] = 0;
-    if (!ok) return;
-    const uint4 rr = __ldg(reinterpret_cast<const uint4*>(runs + ri));
-    x.r = Run{rr.x, rr.y, rr.z, rr.w};
-    const int n = (int)((rr.y >> 14) & 63u) + 1;
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        if (k0 + j < n) x.q[j] = __ldg(lam + rr.x + k0 + j);
-}
+// slot -> accumulator index: the low 5 bits XOR-ed with y ^ z, so that y and z steps (slot
+// strides 32, 1024) change the bank (a bijection inside every 32-slot row, and an involution)
+__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 5) ^ (s >> 10)) & 31); }
 
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
                                                                    const long long* __restrict__ tile_ptr,
                                                                    const Run* __restrict__ runs,
-                                                                   const int32_t* __restrict__ lam, long long* T) {
+                                                                   const int32_t* __restrict__ lam, int per_item,
+                                                                   long long* T) {
     extern __shared__ int smem[];
     int* acc_lo = smem;                 // sum of (q & 0xffff), at swz(slot)
     int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane >> 3, k0 = 4 * (lane & 7);
-    constexpr int kWarps = kK6Threads / 32;
-    constexpr int kStride = 4 * kWarps;
+    uint4* sdesc = reinterpret_cast<uint4*>(smem + 2 * kTileSlots) + (threadIdx.x >> 5) * 32;  // this warp's batch
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned below = (1u << lane) - 1u;
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int2 item = __ldg(items + it);
-        for (int i = threadIdx.x; i < 2 * kTileSlots; i += kK6Threads) smem[i] = 0;
+        for (int i = threadIdx.x; i < 2 * kTileSlots / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
         __syncthreads();
-        const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * kRunsPerItem;
+        const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * per_item;
         long long r1 = __ldg(tile_ptr + item.x + 1);
-        if (r1 > r0 + kRunsPerItem) r1 = r0 + kRunsPerItem;
-        long long rb = r0 + 4 * wid + sub;
-        K6Run cur, nxt;
-        k6_load(runs, lam, rb, rb < r1, k0, cur);
-        for (; rb < r1; rb += kStride) {
-            k6_load(runs, lam, rb + kStride, rb + kStride < r1, k0, nxt);
-            const unsigned meta = cur.r.meta;
-            const int n = (int)((meta >> 14) & 63u) + 1;
-            if (k0 < n) {
-                const int sx = (meta >> 20) & 1 ? -1 : 1, sy = (meta >> 21) & 1 ? -32 : 32;
-                const int sz = (meta >> 22) & 1 ? -1024 : 1024;
-                const unsigned below = (1u << k0) - 1u;
-                int cx = __popc(cur.r.mx & below), cy = __popc(cur.r.my & below);
-                const int base = (int)(meta & (kTileSlots - 1));
+        if (r1 > r0 + per_item) r1 = r0 + per_item;
+        for (long long rb = r0 + 32LL * wid; rb < r1; rb += 32LL * kK6Warps) {
+            const int nb = (int)min(32LL, r1 - rb);
+            uint4 d{0u, 0u, 0u, 0u};
+            if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
+            sdesc[lane] = d;
+            __syncwarp();
+            int q[32];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int k = k0 + j;
-                    if (k < n) {
-                        const int slot = swz(base + sx * cx + sy * cy + sz * (k - cx - cy));
-                        atomicAdd(acc_lo + slot, cur.q[j] & 0xffff);
-                        atomicAdd(acc_hi + slot, cur.q[j] >> 16);
-                    }
-                    cx += (cur.r.mx >> k) & 1u;
-                    cy += (cur.r.my >> k) & 1u;
+            for (int j = 0; j < 32; ++j) {
+                const uint4 x = sdesc[j];
+                const int n = j < nb ? (int)((x.y >> 14) & 63u) + 1 : 0;
+                q[j] = lane < n ? __ldg(lam + x.x + lane) : 0;
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const uint4 x = sdesc[j];
+                const unsigned meta = x.y;
+                const int n = j < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
+                if (lane < n) {
+                    const int cx = __popc(x.z & below), cy = __popc(x.w & below);
+                    const int sx = (meta >> 20) & 1 ? -cx : cx, sy = (meta >> 21) & 1 ? -cy : cy;
+                    const int cz = lane - cx - cy, sz = (meta >> 22) & 1 ? -cz : cz;
+                    const int si = swz((int)(meta & (kTileSlots - 1)) + sx + 32 * sy + 1024 * sz);
+                    atomicAdd(acc_lo + si, q[j] & 0xffff);
+                    atomicAdd(acc_hi + si, q[j] >> 16);
                 }
             }
-            cur = nxt;
+            __syncwarp();
         }
         __syncthreads();
         long long* Tt = T + ((long long)item.x << kTileShift);
         for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
-            const long long sum = (long long)acc_hi[i] * 65536 + (long long)acc_lo[i];
-            if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + unswz(i)), (unsigned long long)sum);
+            const long long sum = (long long)acc_hi[swz(i)] * 65536 + (long long)acc_lo[swz(i)];
+            if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
         }
         __syncthreads();
     }
@@ -781,17 +775,16 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
 }
 
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, long long* T, cudaStream_t s) {
+                        const int32_t* lam, int per_item, long long* T, cudaStream_t s) {
     if (n_items == 0) return;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(tile_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             2 * kTileSlots * (int)sizeof(int));
+        cudaFuncSetAttribute(tile_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Smem);
         configured = true;
     }
     const long long grid = n_items < 148LL ? n_items : 148LL;
-    tile_reduce_kernel<<<(unsigned)grid, kK6Threads, 2 * kTileSlots * sizeof(int), s>>>(n_items, items, tile_ptr, runs,
-                                                                                     lam, T);
+    tile_reduce_kernel<<<(unsigned)grid, kK6Threads, kK6Smem, s>>>(n_items, items, tile_ptr, runs,
+                                                                                     lam, per_item, T);
 }
 
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s) {

@@ -25,7 +25,7 @@ constexpr int kVoxelChunk = 4096;             // per-voxel K6 work item: <= 4096
 // at a time in shared memory, so a tile's slots must fit one CTA (2 x int32 x 16384 = 128 KB).
 constexpr int kTileShift = 14;                // slot = tile << 14 | (z&15) << 10 | (y&31) << 5 | (x&31)
 constexpr int kTileSlots = 1 << kTileShift;
-constexpr int kRunsPerItem = 16384;           // K6 work item: <= 16384 runs of one tile (int32 halves never overflow)
+constexpr int kRunsPerItem = 32768;           // K6 work item: <= 32768 runs of one tile (int32 halves: 32768 x 65535 < 2^31)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -218,7 +218,7 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, long long* T, cudaStream_t s);
+                        const int32_t* lam, int per_item, long long* T, cudaStream_t s);
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s);
 void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s);
 

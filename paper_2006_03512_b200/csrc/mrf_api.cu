@@ -79,7 +79,8 @@ struct mrf_ctx {
     long long VI = 0;  // internal belief slots: tiles * 16384 (tile-major, DESIGN.md §Data layout)
     long long NT = 0;  // tiles
     bool k6_voxel = false;  // ablation: per-voxel transpose K6 instead of the tile-run K6 (MRF_K6=voxel)
-    int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1|2)
+    int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1)
+    int k6_item = 8192;     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
     bool hist_valid = false; // vox_count (voxel degrees) computed for the current graph
@@ -292,17 +293,28 @@ mrf_status build_tile_runs(mrf_ctx* c) {
         launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p, c->runs.p,
                         c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
-        launch_item_counts(NT, c->tile_runs.p, c->tile_nitems.p, kRunsPerItem, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
     }
-    if ((st = scan(c, c->tile_nitems.p, c->bitem_ptr.p, NT, 0)) != MRF_OK) return st;
-    if ((st = read_ll(c, c->bitem_ptr.p + NT, &c->n_bitems)) != MRF_OK) return st;
+    // K6 work list, j-major: item j of every tile, then item j+1 ...  Runs land in a tile in
+    // roughly ray order, so the items that run concurrently read nearby message ranges (L2 reuse).
+    std::vector<int32_t> nr((size_t)NT);
+    CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<int2> items;
+    for (int j = 0;; ++j) {
+        bool any = false;
+        for (long long t = 0; t < NT; ++t) {
+            if ((long long)j * c->k6_item < nr[t]) {
+                items.push_back(make_int2((int)t, j));
+                any = true;
+            }
+        }
+        if (!any) break;
+    }
+    c->n_bitems = (long long)items.size();
     CK(c->bitems.ensure((size_t)std::max(1LL, c->n_bitems), 0, c->stream));
-    {
-        ProfScope ps(c, MRF_K_TRANSPOSE);
-        launch_item_fill(NT, c->tile_nitems.p, c->bitem_ptr.p, c->bitems.p, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
-    }
+    if (c->n_bitems)
+        CK(cudaMemcpyAsync(c->bitems.p, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     return MRF_OK;
 }
 
@@ -372,7 +384,7 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
     } else {
-        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, out, c->stream);
+        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -511,6 +523,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     c->VI = c->NT * kTileSlots;
     if (const char* k6 = getenv("MRF_K6")) c->k6_voxel = strcmp(k6, "voxel") == 0;
     if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
+    if (const char* ki = getenv("MRF_K6_ITEM")) c->k6_item = std::min(std::max(atoi(ki), 1024), kRunsPerItem);
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
