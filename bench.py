@@ -227,18 +227,25 @@ def run_ours(args, rank, world, local_rank):
     h2d = sum(fr.depth.nbytes for fr in w.frames)
     d2h = w.n_voxels * 4
 
-    # ---- roofline of the dominant kernel (K5 = ray messages, one launch group per iteration)
+    # ---- roofline of the dominant kernel (one launch group = one BP iteration over all classes)
+    # Algorithmic bytes of THIS design per iteration:
+    #   K5: vid 4 + log nu 4 + lambda read 4 + lambda write 4 per incidence, + T gather 8 per voxel
+    #   K6: lambda 4 per incidence + 16 per tile run (step-coded descriptor), + T write 8 per voxel
+    # and, for comparison, SURVEY §8(d)'s canonical model (22 B per incidence + 16 per voxel).
     peak, peak_kind = _peaks()
     V = w.n_voxels
+    lay = m.layout_sizes()
+    n_runs = lay["n_runs"]
     n_k5, ms_k5 = prof["ray_messages"]
     n_k6, ms_k6 = prof["voxel_sum"]
     per_iter_k5 = ms_k5 / max(1, args.steps * n_iter)
     per_iter_k6 = ms_k6 / max(1, args.steps * n_iter)
-    bytes_k5 = 14 * E_local + 8 * V      # vid 4 + off_q 2 + lambda r/w 8 per incidence; T gather per voxel
-    bytes_k6 = 8 * E_local + 8 * V       # tr 4 + lambda 4 per incidence; T write per voxel
-    ach_k5 = bytes_k5 / (per_iter_k5 / 1e3) / 1e9 if per_iter_k5 > 0 else 0.0
-    ach_k6 = bytes_k6 / (per_iter_k6 / 1e3) / 1e9 if per_iter_k6 > 0 else 0.0
-    ach_bp = (bytes_k5 + bytes_k6) / ((per_iter_k5 + per_iter_k6) / 1e3) / 1e9 if per_iter_k5 > 0 else 0.0
+    bytes_k5 = 16 * E_local + 8 * V
+    bytes_k6 = 4 * E_local + 16 * n_runs + 8 * V
+    gbs = lambda b, t: b / (t / 1e3) / 1e9 if t > 0 else 0.0
+    ach_k5, ach_k6 = gbs(bytes_k5, per_iter_k5), gbs(bytes_k6, per_iter_k6)
+    ach_bp = gbs(bytes_k5 + bytes_k6, per_iter_k5 + per_iter_k6)
+    ach_22 = gbs(22 * E_local + 16 * V, per_iter_k5 + per_iter_k6)
     dominant = "ray_messages" if ms_k5 >= ms_k6 else "voxel_sum"
     ach = ach_k5 if dominant == "ray_messages" else ach_k6
     traffic = None
@@ -268,7 +275,9 @@ def run_ours(args, rank, world, local_rank):
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": bytes_k5 if dominant == "ray_messages" else bytes_k6,
-                         "bp_iteration_frac": ach_bp / peak, "k5_frac": ach_k5 / peak, "k6_frac": ach_k6 / peak},
+                         "k5_frac": ach_k5 / peak, "k6_frac": ach_k6 / peak,
+                         "bp_iteration_frac": ach_bp / peak, "bp_iteration_frac_survey22B": ach_22 / peak,
+                         "ms_k5": per_iter_k5, "ms_k6": per_iter_k6, "tile_runs": n_runs},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -62,7 +62,9 @@ typedef struct {
     double off_lo, off_hi; /* metres, -1 <= off_lo < off_hi <= 1 (span of the int16 offset code) */
     double margin_min;     /* metres, >= 0 */
     double margin_k;       /* >= 0 */
-    double sigma_c[3];     /* c0, c1, c2 */
+    double sigma_c[3];     /* c0, c1, c2.  Bounded margin: with D the grid diagonal (metres),
+                              margin_min <= D and margin_k (|c0| + |c1| D + |c2| D^2) <= D, so a
+                              traversal segment never exceeds 2 D (the DDA's 32-bit exact products) */
 } mrf_noise_desc;
 
 /* Data-parallel sharding: rank keeps the rays of pixel rows v % world == rank.
@@ -133,6 +135,12 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences);
  * invalid pixels and dropped rays.  Any pointer may be NULL.  Synchronises. */
 mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences, int64_t* n_active_vox,
                            int64_t* n_invalid, int64_t* n_dropped);
+
+/* Sizes of this rank's device layout, for the roofline byte counts: n_slots =
+ * incidence slots incl. the padding of every ray segment to a multiple of 8; n_runs = tile runs
+ * of the K6 transpose; n_belief_slots = tile-major belief slots (32x32x16 tiles).  Builds the
+ * transpose if the graph changed.  Any pointer may be NULL.  Synchronises. */
+mrf_status mrf_layout_sizes(mrf_ctx* ctx, int64_t* n_slots, int64_t* n_runs, int64_t* n_belief_slots);
 
 /* Copy this rank's graph to host buffers in canonical order: ray_pixel[n_rays] = frame*2^32 +
  * (v*W + u) of each kept ray, row_ptr[n_rays+1], vid[E], off_q[E] (metres * 32768).  Any pointer

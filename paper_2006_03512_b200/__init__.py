@@ -147,6 +147,12 @@ class MRFMap:
         return dict(n_rays=v[0].value, E=v[1].value, n_active=v[2].value if active else None,
                     n_invalid=v[3].value, n_dropped=v[4].value)
 
+    def layout_sizes(self) -> dict:
+        """mrf_layout_sizes: padded incidence slots, K6 tile runs, belief slots."""
+        v = [ctypes.c_int64() for _ in range(3)]
+        self._chk(self._L.mrf_layout_sizes(self._h, *(ctypes.byref(x) for x in v)))
+        return dict(n_slots=v[0].value, n_runs=v[1].value, n_belief_slots=v[2].value)
+
     def export_graph(self):
         s = self.graph_sizes(active=False)
         ray_pixel = np.empty(s["n_rays"], np.int64)

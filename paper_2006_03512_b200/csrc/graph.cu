@@ -57,73 +57,75 @@ __device__ __forceinline__ int pixel_segment(const FrameDesc& f, const GridDesc&
 
 // ---------------------------------------------------------------- B2: integer 3D-DDA
 // State of the walk: current cell, per-axis step direction, and the exact crossing parameter
-// of the next boundary on each axis as the rational num/den (den = |dG| > 0).
+// of the next boundary on each axis as the rational num/den (den = |dG| > 0).  Held in scalar
+// registers (no runtime-indexed arrays, which would live in local memory), 32-bit: mrf_create
+// bounds the segment length (margin(D) <= D for the grid diagonal D, dims <= 8192), so
+// den < 2^31 and num <= den + 2^16 fit in uint32 and the exact products in one IMAD.WIDE.U32.
 struct Walker {
-    long long num[3], den[3];
-    int cell[3], dir[3];
+    unsigned n0, n1, n2, d0, d1, d2;  // d = 0: the axis never crosses
+    int c0, c1, c2, s0, s1, s2;       // cell, step direction
     double t_in;
 
-    __device__ __forceinline__ void start(const Segment& sg) {
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const long long d = sg.g1[k] - sg.g0[k];
-            long long c = sg.g0[k] >> kFixShift;  // arithmetic shift == floor
-            const bool on_face = (sg.g0[k] & (kFixOne - 1)) == 0;
-            if (d < 0 && on_face) c -= 1;         // cell that contains t = 0+
-            cell[k] = (int)c;
-            if (d > 0) {
-                dir[k] = 1;
-                num[k] = ((c + 1) << kFixShift) - sg.g0[k];
-                den[k] = d;
-            } else if (d < 0) {
-                dir[k] = -1;
-                num[k] = sg.g0[k] - (c << kFixShift);
-                den[k] = -d;
-            } else {
-                dir[k] = 0;
-                num[k] = 1;
-                den[k] = 0;
-            }
+    __device__ __forceinline__ static void axis_start(long long g0, long long g1, int& c, int& s, unsigned& n,
+                                                      unsigned& d) {
+        const long long dg = g1 - g0;
+        long long cc = g0 >> kFixShift;  // arithmetic shift == floor
+        const bool on_face = (g0 & (kFixOne - 1)) == 0;
+        if (dg < 0 && on_face) cc -= 1;  // cell that contains t = 0+
+        c = (int)cc;
+        if (dg > 0) {
+            s = 1;
+            n = (unsigned)(((cc + 1) << kFixShift) - g0);
+            d = (unsigned)dg;
+        } else if (dg < 0) {
+            s = -1;
+            n = (unsigned)(g0 - (cc << kFixShift));
+            d = (unsigned)(-dg);
+        } else {
+            s = 0;
+            n = 1;
+            d = 0;
         }
+    }
+    __device__ __forceinline__ void start(const Segment& sg) {
+        axis_start(sg.g0[0], sg.g1[0], c0, s0, n0, d0);
+        axis_start(sg.g0[1], sg.g1[1], c1, s1, n1, d1);
+        axis_start(sg.g0[2], sg.g1[2], c2, s2, n2, d2);
         t_in = 0.0;
     }
     __device__ __forceinline__ bool inside(const GridDesc& g) const {
-        return (unsigned)cell[0] < (unsigned)g.nx && (unsigned)cell[1] < (unsigned)g.ny &&
-               (unsigned)cell[2] < (unsigned)g.nz;
+        return (unsigned)c0 < (unsigned)g.nx && (unsigned)c1 < (unsigned)g.ny && (unsigned)c2 < (unsigned)g.nz;
     }
-    // Axis of the earliest next crossing (-1 if none); exact comparison of num/den.
-    __device__ __forceinline__ int earliest() const {
+    // n_a / d_a < n_b / d_b, exactly
+    __device__ __forceinline__ static bool before(unsigned na, unsigned da, unsigned nb, unsigned db) {
+        return (unsigned long long)na * db < (unsigned long long)nb * da;
+    }
+    // The earliest next crossing as (num, den) and its axis (-1 if no axis crosses).
+    __device__ __forceinline__ int earliest(unsigned& na, unsigned& da) const {
         int a = -1;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (dir[k] == 0) continue;
-            if (a < 0) {
-                a = k;
-            } else if (num[k] * den[a] < num[a] * den[k]) {
-                a = k;
-            }
-        }
+        na = 1;
+        da = 0;
+        if (d0) { a = 0; na = n0; da = d0; }
+        if (d1 && (a < 0 || before(n1, d1, na, da))) { a = 1; na = n1; da = d1; }
+        if (d2 && (a < 0 || before(n2, d2, na, da))) { a = 2; na = n2; da = d2; }
         return a;
     }
-    // Advance every axis whose crossing ties with axis a (simultaneous steps on corners/edges).
-    __device__ __forceinline__ void advance(int a) {
-        const long long na = num[a], da = den[a];
-        bool tie[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) tie[k] = dir[k] != 0 && num[k] * da == na * den[k];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (tie[k]) {
-                cell[k] += dir[k];
-                num[k] += kFixOne;
-            }
-        }
+    // Advance every axis whose crossing ties with (na, da) (simultaneous steps on corners/edges).
+    __device__ __forceinline__ void advance(unsigned na, unsigned da) {
+        const unsigned long long r = (unsigned long long)na;
+        const bool t0 = d0 && (unsigned long long)n0 * da == r * d0;
+        const bool t1 = d1 && (unsigned long long)n1 * da == r * d1;
+        const bool t2 = d2 && (unsigned long long)n2 * da == r * d2;
+        if (t0) { c0 += s0; n0 += (unsigned)kFixOne; }
+        if (t1) { c1 += s1; n1 += (unsigned)kFixOne; }
+        if (t2) { c2 += s2; n2 += (unsigned)kFixOne; }
     }
 };
 
-__device__ __forceinline__ double crossing_t(const Walker& w, int a, bool& last) {
-    last = (a < 0) || (w.num[a] >= w.den[a]);
-    return last ? 1.0 : __ddiv_rn((double)w.num[a], (double)w.den[a]);
+// t of the next crossing (num/den, correctly rounded) or 1 when the walk ends in this cell.
+__device__ __forceinline__ double crossing_t(int a, unsigned na, unsigned da, bool& last) {
+    last = (a < 0) || (na >= da);
+    return last ? 1.0 : __ddiv_rn((double)na, (double)da);
 }
 
 __device__ __forceinline__ void owned_pixel(const FrameDesc& f, long long i, int& u, int& v) {
@@ -153,9 +155,10 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
             w.start(sg);
             while (w.inside(g)) {
                 ++count;
-                const int a = w.earliest();
-                if (a < 0 || w.num[a] >= w.den[a]) break;  // end point inside this cell
-                w.advance(a);
+                unsigned na, da;
+                const int a = w.earliest(na, da);
+                if (a < 0 || na >= da) break;  // end point inside this cell
+                w.advance(na, da);
             }
             // LUT row of the measured range (bin centres, clamped to the edge centres)
             double fz = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(sg.Z, n.z_lo), __dsub_rn(n.z_hi, n.z_lo)),
@@ -248,9 +251,10 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
         if (am == 0) break;
         if (alive) {
             bool last;
-            const int a = w.earliest();
-            const double t_out = crossing_t(w, a, last);
-            const int vx = voxel_slot(g, w.cell[0], w.cell[1], w.cell[2]);
+            unsigned na, da;
+            const int a = w.earliest(na, da);
+            const double t_out = crossing_t(a, na, da, last);
+            const int vx = voxel_slot(g, w.c0, w.c1, w.c2);
             const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
             long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
             q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
@@ -269,7 +273,7 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             if (last) {
                 alive = false;
             } else {
-                w.advance(a);
+                w.advance(na, da);
                 w.t_in = t_out;
                 alive = w.inside(g);
             }

@@ -503,6 +503,14 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (!(noise->off_hi > noise->off_lo) || noise->off_lo < -1.0 || noise->off_hi > 1.0)
         return reject("offset axis must satisfy -1 <= off_lo < off_hi <= 1");
     if (noise->margin_min < 0 || noise->margin_k < 0) return reject("margin parameters must be >= 0");
+    {
+        const double D = resolution_m * std::sqrt((double)dims[0] * dims[0] + (double)dims[1] * dims[1] +
+                                                  (double)dims[2] * dims[2]);
+        const double sig = std::fabs(noise->sigma_c[0]) + std::fabs(noise->sigma_c[1]) * D +
+                           std::fabs(noise->sigma_c[2]) * D * D;
+        if (noise->margin_min > D || noise->margin_k * sig > D)
+            return reject("traversal margin must stay below the grid diagonal (margin bound)");
+    }
     const long long nlut = (long long)noise->n_z * noise->n_off;
     for (long long i = 0; i < nlut; ++i)
         if (!std::isfinite(noise->log_nu[i])) return reject("noise table has non-finite entries");
@@ -817,6 +825,16 @@ mrf_status mrf_marginals(mrf_ctx* ctx, float* out, int32_t out_is_device) {
     if (!out_is_device)
         CK(cudaMemcpyAsync(out, dst, sizeof(float) * c->V, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_layout_sizes(mrf_ctx* ctx, int64_t* n_slots, int64_t* n_runs, int64_t* n_belief_slots) {
+    ENTER(ctx);
+    mrf_status st;
+    if ((st = prepare(c)) != MRF_OK) return st;
+    if (n_slots) *n_slots = c->E;
+    if (n_runs) *n_runs = c->n_runs;
+    if (n_belief_slots) *n_belief_slots = c->VI;
     return MRF_OK;
 }
 

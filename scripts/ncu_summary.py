@@ -67,7 +67,7 @@ def to_bytes(v, unit):
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1.0)
 
 
-def full(rep, config, E):
+def full(rep, config, E, quiet=False):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     hdr, units = rows[0], rows[1]
@@ -75,25 +75,31 @@ def full(rep, config, E):
     summary = {}
     for r in rows[2:]:
         name = short(r[hdr.index("Kernel Name")])
-        print(f"## {name}\n\n| metric | value |\n|---|---|")
         rec = {}
         for key, label in METRICS:
             if key in hdr:
                 i = hdr.index(key)
-                print(f"| {label} | {r[i]} {units[i]} |")
                 rec[key] = (r[i], units[i])
+        if not quiet:
+            print(f"## {name}\n\n| metric | value |\n|---|---|")
+            for key, label in METRICS:
+                if key in rec:
+                    print(f"| {label} | {rec[key][0]} {rec[key][1]} |")
         rd = to_bytes(float(rec["dram__bytes_read.sum"][0].replace(",", "")), rec["dram__bytes_read.sum"][1])
         wr = to_bytes(float(rec["dram__bytes_write.sum"][0].replace(",", "")), rec["dram__bytes_write.sum"][1])
-        print(f"| DRAM read+write per launch | {(rd + wr)/1e9:.3f} GB |\n")
+        if not quiet:
+            print(f"| DRAM read+write per launch | {(rd + wr)/1e9:.3f} GB |\n")
         kind = "ray_messages" if "ray_msg" in name else ("voxel_sum" if "reduce" in name else name)
         summary.setdefault(kind, {"config": config, "E": E, "dram_bytes_per_launch": 0.0, "launches": []})
         summary[kind]["launches"].append({"kernel": name, "dram_bytes": rd + wr})
-    # one K5 "launch" in bench.py = all length classes of one iteration: sum one of each class
+    # one K5 "launch" in bench.py = all length classes of one iteration: sum the LAST launch of
+    # each class kernel (the capture spans whole iterations)
     for kind, s in summary.items():
         per = {}
         for l in s["launches"]:
-            per.setdefault(l["kernel"], l["dram_bytes"])
+            per[l["kernel"]] = l["dram_bytes"]
         s["dram_bytes_per_launch"] = sum(per.values())
+        s["launches"] = [{"kernel": k, "dram_bytes": v} for k, v in per.items()]
     json.dump({"kernels": summary}, open(os.path.join(ROOT, "profiles", "ncu_summary.json"), "w"), indent=1)
 
 
@@ -103,5 +109,6 @@ if __name__ == "__main__":
     ap.add_argument("path")
     ap.add_argument("--config", default="frames30")
     ap.add_argument("--E", type=int, default=0)
+    ap.add_argument("--quiet", action="store_true", help="only write profiles/ncu_summary.json")
     a = ap.parse_args()
-    launches(a.path) if a.mode == "launches" else full(a.path, a.config, a.E)
+    launches(a.path) if a.mode == "launches" else full(a.path, a.config, a.E, a.quiet)

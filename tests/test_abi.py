@@ -51,6 +51,8 @@ def _noise(n_z=4, n_off=4):
     (dict(noise=dict(z_hi=0.0)), "z_hi"),
     (dict(noise=dict(off_lo=-2.0)), "offset"),
     (dict(noise=dict(log_nu=np.full((4, 4), np.inf, np.float32))), "non-finite"),
+    (dict(noise=dict(margin_min=1.0)), "margin bound"),
+    (dict(noise=dict(sigma_c=(0.0, 0.0, 50.0))), "margin bound"),
 ])
 def test_create_rejects_bad_arguments(kw, msg):
     args = dict(dims=(4, 4, 4), res=0.05, origin=(0, 0, 0), prior=0.5)
