@@ -224,11 +224,35 @@ struct RunBuilder {
 
 // ---------------------------------------------------------------- K3
 // B3: off_q = clamp(rint((0.5 (t_in + t_out) L - Z) * 32768), +-32767), the span midpoint
-// relative to the measured range (reading R6).
-__global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
+// relative to the measured range (reading R6).  Each thread stages its ray's outputs in a private
+// 8-slot chunk of shared memory and writes a whole chunk at once (two 16-byte vid stores, one
+// 16-byte off_q store; segments are 8-aligned, padding slots get 0): one scattered 4-byte and
+// one 2-byte store per step had the walk waiting on the store queue.
+constexpr int kFillThreads = 128;
+__device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long long e_chunk, int nvalid,
+                                            const int* sv, const short* so) {
+    int v[8];
+    short o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        v[k] = k < nvalid ? sv[k] : 0;
+        o[k] = k < nvalid ? so[k] : (short)0;
+    }
+    int4* dv = reinterpret_cast<int4*>(vid + e_chunk);
+    dv[0] = make_int4(v[0], v[1], v[2], v[3]);
+    dv[1] = make_int4(v[4], v[5], v[6], v[7]);
+    auto pk = [](short a, short b) { return (unsigned)(unsigned short)a | ((unsigned)(unsigned short)b << 16); };
+    *reinterpret_cast<uint4*>(off_q + e_chunk) = make_uint4(pk(o[0], o[1]), pk(o[2], o[3]), pk(o[4], o[5]), pk(o[6], o[7]));
+}
+
+__global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
                                                        const float* __restrict__ depth,
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
                                                        int16_t* off_q, int32_t* tile_runs) {
+    __shared__ int s_vid[kFillThreads][8];
+    __shared__ short s_off[kFillThreads][8];
+    int* sv = s_vid[threadIdx.x];
+    short* so = s_off[threadIdx.x];
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n_pix = (long long)f.rows_owned * f.W;
     const int lane = threadIdx.x & 31;
@@ -258,8 +282,9 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
             const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
             long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
             q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
-            vid[e] = vx;
-            off_q[e] = (int16_t)q;
+            sv[e & 7] = vx;
+            so[e & 7] = (short)q;
+            if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so);
             ++e;
             // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
             const int b = vx >> kTileShift, l = vx & (kTileSlots - 1);
@@ -277,6 +302,7 @@ __global__ void __launch_bounds__(128) dda_fill_kernel(FrameDesc f, GridDesc g, 
                 w.t_in = t_out;
                 alive = w.inside(g);
             }
+            if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so);  // partial tail
         }
     }
 }
@@ -540,7 +566,8 @@ void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, 
                      int16_t* off_q, float* lnu, int32_t* tile_runs, cudaStream_t s) {
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
-    dda_fill_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q, tile_runs);
+    dda_fill_kernel<<<blocks_for(n_pix, kFillThreads), kFillThreads, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q,
+                                                                              tile_runs);
     lnu_fill_kernel<<<blocks_for(n_pix, 256), 256, 0, s>>>(f.ray_base, n_pix, mp, row_ptr, ray_z, off_q, lnu);
 }
 
