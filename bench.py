@@ -150,9 +150,19 @@ def run_ours(args, rank, world, local_rank):
         ids = [pkg.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(ids, src=0)
         kw = dict(rank=rank, world=world, comm=pkg.MRF_COMM_NCCL, nccl_id=ids[0])
-    m = pkg.MRFMap.from_workload(w, **kw)
     stream = torch.cuda.current_stream(dev)
-    m.set_stream(stream.cuda_stream)
+    # The 0.02 m configs exceed one ctx's 2^31 incidence slots on a single GPU: there the GPU
+    # holds several emulated ranks (dist.EmulatedRanks) whose per-iteration int64 partials are
+    # summed on the device.
+    emulate = args.emulate_ranks if args.emulate_ranks is not None else (
+        4 if (world == 1 and args.config in ("frames100", "sweep300")) else 1)
+    if emulate > 1:
+        assert world == 1, "--emulate-ranks is a single-GPU mode"
+        from paper_2006_03512_b200.dist import EmulatedRanks
+        m = EmulatedRanks(w, emulate, stream.cuda_stream)
+    else:
+        m = pkg.MRFMap.from_workload(w, **kw)
+        m.set_stream(stream.cuda_stream)
 
     depth_dev = [torch.from_numpy(fr.depth).to(dev) for fr in w.frames]
     depth_host = [torch.from_numpy(fr.depth).pin_memory() for fr in w.frames]
@@ -300,6 +310,8 @@ def main():
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--emulate-ranks", type=int, default=None,
+                    help="ranks emulated on the one GPU (default: 4 for the 0.02 m configs, else 1)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -147,6 +147,15 @@ mrf_status mrf_layout_sizes(mrf_ctx* ctx, int64_t* n_slots, int64_t* n_runs, int
  * may be NULL.  Synchronises. */
 mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, int32_t* vid, int16_t* off_q);
 
+/* Selected rays of this rank, without copying the whole graph (tests at full size): for k < n,
+ * ray k is pixel pixel[k] = v*W + u of frame frame[k] (frame add order); row v must be owned by
+ * this rank (v % world == rank), else MRF_ERR_INVALID_ARG.  Outputs, host buffers, any may be
+ * NULL: row_ptr[n+1] (offsets into the concatenated lists; 0-length for invalid or dropped
+ * pixels), and up to cap entries each of vid (voxel index x + nx (y + ny z)), off_q, lambda
+ * (nats).  MRF_ERR_CAPACITY if the lists exceed cap.  Synchronises. */
+mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const int64_t* pixel, int64_t cap,
+                           int64_t* row_ptr, int32_t* vid, int16_t* off_q, float* lambda);
+
 /* Voxel->ray transpose: col_ptr[V+1] and, per voxel, the incidence indices tr[E] (order inside a
  * voxel is unspecified).  Builds the transpose if needed.  Synchronises. */
 mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr);

@@ -153,6 +153,21 @@ class MRFMap:
         self._chk(self._L.mrf_layout_sizes(self._h, *(ctypes.byref(x) for x in v)))
         return dict(n_slots=v[0].value, n_runs=v[1].value, n_belief_slots=v[2].value)
 
+    def export_rays(self, frame, pixel):
+        """mrf_export_rays: incidence lists of the selected (frame, pixel) rays of this rank."""
+        frame = np.ascontiguousarray(frame, dtype=np.int32)
+        pixel = np.ascontiguousarray(pixel, dtype=np.int64)
+        n = len(frame)
+        row_ptr = np.zeros(n + 1, np.int64)
+        self._chk(self._L.mrf_export_rays(self._h, n, _ptr(frame), _ptr(pixel), 0, _ptr(row_ptr), None, None, None))
+        cap = int(row_ptr[-1])
+        vid = np.zeros(max(cap, 1), np.int32)
+        off_q = np.zeros(max(cap, 1), np.int16)
+        lam = np.zeros(max(cap, 1), np.float32)
+        self._chk(self._L.mrf_export_rays(self._h, n, _ptr(frame), _ptr(pixel), cap, _ptr(row_ptr), _ptr(vid),
+                                          _ptr(off_q), _ptr(lam)))
+        return dict(row_ptr=row_ptr, vid=vid[:cap], off_q=off_q[:cap], lam=lam[:cap])
+
     def export_graph(self):
         s = self.graph_sizes(active=False)
         ray_pixel = np.empty(s["n_rays"], np.int64)

@@ -27,7 +27,7 @@ MRF_K_COUNT = len(KERNEL_NAMES)
 
 # every symbol include/mrf.h declares
 EXPORTS = ["mrf_create", "mrf_add_frame", "mrf_bp_iterate", "mrf_marginals", "mrf_destroy", "mrf_last_error",
-           "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph",
+           "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph", "mrf_export_rays",
            "mrf_export_transpose", "mrf_export_messages", "mrf_import_messages", "mrf_export_beliefs",
            "mrf_bp_partial", "mrf_bp_finish", "mrf_belief_slots", "mrf_nccl_unique_id", "mrf_set_profiling",
            "mrf_profile_read", "mrf_launch_count"]
@@ -77,6 +77,7 @@ def load(build: bool = True):
                 "mrf_reserve": (st, [vp, i64, i64]),
                 "mrf_graph_sizes": (st, [vp, P(i64), P(i64), P(i64), P(i64), P(i64)]),
                 "mrf_layout_sizes": (st, [vp, P(i64), P(i64), P(i64)]),
+                "mrf_export_rays": (st, [vp, i64, vp, vp, i64, vp, vp, vp, vp]),
                 "mrf_export_graph": (st, [vp, vp, vp, vp, vp]),
                 "mrf_export_transpose": (st, [vp, vp, vp]),
                 "mrf_export_messages": (st, [vp, vp]),

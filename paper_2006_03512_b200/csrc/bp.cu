@@ -289,7 +289,7 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
 #define MRF_K5_MIN_BLOCKS 4
 #endif
 template <int G, int K, int M>
-__global__ void __launch_bounds__(256, MRF_K5_MIN_BLOCKS) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ ray_z,
                                                          const int32_t* __restrict__ vid,

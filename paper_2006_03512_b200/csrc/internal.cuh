@@ -189,14 +189,15 @@ void launch_ray_messages_staged(long long n_stages, const Stage* stages, const l
                                 const long long* T, const MsgParams& mp, int math, cudaStream_t s);
 
 // ---- BP kernels (bp.cu)
-// K5 length classes.  Class k < kNumShort runs G = 4 << (k / 4) lanes per ray with K = 5 + k % 4
-// incidences per lane (capacity G K: 20, 24, 28, 32, 40, ..., 224, 256); a ray goes to the
-// smallest capacity >= n.  Class kNumShort: rays longer than 256 (tiled warp kernel).  The
-// per-ray arithmetic depends only on n, never on where the ray is stored.
-constexpr int kNumShort = 16;
+// K5 length classes.  Class k < 16 runs G = 4 << (k / 4) lanes per ray with K = 5 + k % 4
+// incidences per lane (capacity G K: 20, 24, 28, 32, 40, ..., 224, 256); classes 16..19 run
+// G = 32 lanes with K = 10, 12, 14, 16 (capacity 320 ... 512: the 0.02 m configs' rays); a ray
+// goes to the smallest capacity >= n.  Class kNumShort: rays longer than 512 (tiled warp
+// kernel).  The per-ray arithmetic depends only on n, never on where the ray is stored.
+constexpr int kNumShort = 20;
 constexpr int kNumClasses = kNumShort + 1;
-__host__ __device__ constexpr int class_G(int k) { return 4 << (k >> 2); }
-__host__ __device__ constexpr int class_K(int k) { return 5 + (k & 3); }
+__host__ __device__ constexpr int class_G(int k) { return k < 16 ? 4 << (k >> 2) : 32; }
+__host__ __device__ constexpr int class_K(int k) { return k < 16 ? 5 + (k & 3) : 10 + 2 * (k - 16); }
 __host__ __device__ inline int ray_class(int n) {
     if (n <= 0) return -1;
     for (int k = 0; k < kNumShort; ++k)

@@ -27,10 +27,11 @@ template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t cap = 0;
-    // Grow to at least n elements (x1.5 geometric); copies the first `used` elements.
+    // Grow to at least n elements (x1.125 geometric: the 0.02 m configs fill most of the 180 GB);
+    // copies the first `used` elements.
     cudaError_t ensure(size_t n, size_t used, cudaStream_t s) {
         if (n <= cap) return cudaSuccess;
-        size_t nc = std::max(n, cap + cap / 2);
+        size_t nc = std::max(n, cap + cap / 8);
         T* q = nullptr;
         cudaError_t e = cudaMalloc(&q, nc * sizeof(T));
         if (e != cudaSuccess) {
@@ -399,8 +400,9 @@ mrf_status ray_messages(mrf_ctx* c) {
                                    c->T.p, c->mp, c->k5_math, c->stream);
         CK_LAUNCH(MRF_K_RAY_MSG, 1);
     }
-    for (int k = staged ? kNumClasses - 1 : 0; k < kNumClasses; ++k) {
+    for (int k = 0; k < kNumClasses; ++k) {
         if (c->class_n[k] == 0) continue;
+        if (staged && k < kNumShort && class_G(k) * class_K(k) <= kShortMax) continue;  // done by the stages
         launch_ray_messages(k, c->class_n[k], c->class_all.p + c->class_off[k], c->row_ptr.p, c->ray_z.p, c->vid.p, c->lnu.p,
                             c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long,
                             c->k5_math, c->stream);
@@ -895,6 +897,56 @@ mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, 
         CK(cudaStreamSynchronize(c->stream));
         relayout(h, tmp.data(), off_q, sizeof(int16_t), true);
     }
+    return MRF_OK;
+}
+
+mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const int64_t* pixel, int64_t cap,
+                           int64_t* row_ptr, int32_t* vid, int16_t* off_q, float* lambda) {
+    ENTER(ctx);
+    if (n < 0 || (n > 0 && (!frame || !pixel)) || cap < 0) return set_err(c, MRF_ERR_INVALID_ARG, "bad ray selection");
+    std::vector<long long> rid((size_t)n);
+    for (long long k = 0; k < n; ++k) {
+        if (frame[k] < 0 || frame[k] >= (int)c->frames.size()) return set_err(c, MRF_ERR_INVALID_ARG, "bad frame id");
+        const FrameRec& fr = c->frames[(size_t)frame[k]];
+        const long long v = pixel[k] / fr.W, u = pixel[k] % fr.W;
+        if (pixel[k] < 0 || v >= fr.H || v % c->world != c->rank)
+            return set_err(c, MRF_ERR_INVALID_ARG, "pixel not owned by this rank");
+        rid[(size_t)k] = fr.ray_base + (v / c->world) * fr.W + u;
+    }
+    // per selected ray: padded start and length
+    std::vector<long long> e0((size_t)n);
+    std::vector<RayInfo> info((size_t)n);
+    for (long long k = 0; k < n; ++k) {
+        CK(cudaMemcpyAsync(&e0[(size_t)k], c->row_ptr.p + rid[(size_t)k], sizeof(long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaMemcpyAsync(&info[(size_t)k], c->ray_z.p + rid[(size_t)k], sizeof(RayInfo), cudaMemcpyDeviceToHost,
+                           c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    std::vector<long long> off((size_t)n + 1, 0);
+    for (long long k = 0; k < n; ++k) off[(size_t)k + 1] = off[(size_t)k] + info[(size_t)k].n;
+    if (row_ptr) std::copy(off.begin(), off.end(), row_ptr);
+    if (off[(size_t)n] > cap && (vid || off_q || lambda)) return set_err(c, MRF_ERR_CAPACITY, "rays exceed cap");
+    for (long long k = 0; k < n; ++k) {
+        const int len = info[(size_t)k].n;
+        if (!len) continue;
+        const long long a = e0[(size_t)k], o = off[(size_t)k];
+        if (vid) CK(cudaMemcpyAsync(vid + o, c->vid.p + a, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, c->stream));
+        if (off_q)
+            CK(cudaMemcpyAsync(off_q + o, c->off_q.p + a, sizeof(int16_t) * len, cudaMemcpyDeviceToHost, c->stream));
+        if (lambda)  // raw int32 q first, converted below
+            CK(cudaMemcpyAsync(lambda + o, c->lam.p + a, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    const long long tot = off[(size_t)n];
+    if (vid)
+        for (long long e = 0; e < tot; ++e) vid[e] = (int32_t)slot_to_voxel(c->grid, vid[e]);
+    if (lambda)
+        for (long long e = 0; e < tot; ++e) {
+            int32_t q;
+            memcpy(&q, lambda + e, sizeof q);
+            lambda[e] = (float)((double)q * kQInvD);
+        }
     return MRF_OK;
 }
 

@@ -369,3 +369,61 @@ def test_frames30_sampled_graph_and_one_step(f30):
     seen[gg["vid"]] = True
     assert np.all(marg[~seen] == np.float32(w.prior))
     assert s["E"] == len(gg["vid"]) and s["n_active"] == int(seen.sum())
+
+
+# ------------------------------------------------------------------ 0.02 m config (BASELINE configs[3])
+
+def test_frames100_emulated_ranks_sampled_rays():
+    """frames100 (400x400x150 @ 0.02 m, 100 frames, ~7 G incidences: more than one ctx's 2^31
+    slots) as 4 emulated ranks on one GPU (dist.EmulatedRanks).  2000 sampled pixels: kept /
+    invalid / dropped status, vid and off_q bit-exact against the oracle's one-by-one trace;
+    one BP step on those rays from the GPU state after 2 iterations within the message bar."""
+    from paper_2006_03512_b200.dist import EmulatedRanks
+    w = synth.frames100()
+    p = oracle.Params.from_workload(w)
+    world = 4
+    er = EmulatedRanks(w, world)
+    for fr in w.frames:
+        er.add_frame(torch.from_numpy(fr.depth).cuda(), fr.K, fr.T_wc)
+    sizes = er.graph_sizes()
+    er.bp_iterate(2)
+    H, W = w.frames[0].depth.shape
+    rng = np.random.default_rng(3)
+    key = np.unique(rng.integers(0, len(w.frames) * H * W, 2000))
+    fsel = (key // (H * W)).astype(np.int32)
+    psel = (key % (H * W)).astype(np.int64)
+    rank_of = (psel // W) % world
+    before = [er.maps[r].export_rays(fsel[rank_of == r], psel[rank_of == r]) for r in range(world)]
+    T = er.maps[0].export_beliefs().astype(np.float64) / 2.0 ** 23
+    er.bp_iterate(1)
+    after = [er.maps[r].export_rays(fsel[rank_of == r], psel[rank_of == r]) for r in range(world)]
+    marg = er.marginals()
+    er.close()
+    assert sizes["E"] > 2 ** 31  # the reason for the emulated ranks
+    n_kept = 0
+    for r in range(world):
+        fr_r, px_r = fsel[rank_of == r], psel[rank_of == r]
+        b, a = before[r], after[r]
+        for fi in np.unique(fr_r):
+            idx = np.nonzero(fr_r == fi)[0]
+            sub = oracle.trace_pixels(p, w.frames[fi], px_r[idx], int(fi))
+            lens = np.diff(b["row_ptr"])[idx]
+            assert np.array_equal(np.sort(px_r[idx][lens > 0]), np.sort(sub.pixel))
+            kept = idx[lens > 0]
+            order = {int(px): k for k, px in enumerate(sub.pixel)}
+            lam_sub = np.zeros(sub.E)
+            got = np.zeros(sub.E)
+            for i in kept:
+                k = order[int(px_r[i])]
+                s0, s1 = b["row_ptr"][i], b["row_ptr"][i + 1]
+                o0, o1 = sub.row_ptr[k], sub.row_ptr[k + 1]
+                assert np.array_equal(b["vid"][s0:s1], sub.vid[o0:o1])
+                assert np.array_equal(b["off_q"][s0:s1], sub.off_q[o0:o1])
+                lam_sub[o0:o1] = b["lam"][s0:s1]
+                got[o0:o1] = a["lam"][s0:s1]
+            if sub.E:
+                oracle.ray_pass(p, sub, T, lam_sub)
+                _assert_msgs_close(got, lam_sub)
+            n_kept += len(kept)
+    assert n_kept > 1000
+    assert np.all((marg >= 0) & (marg <= 1))
