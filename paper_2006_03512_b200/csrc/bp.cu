@@ -607,17 +607,21 @@ __global__ void __launch_bounds__(256) voxel_reduce_kernel(long long n_items, co
 // ray), never the same voxel twice (adjacent runs of a tile come from adjacent pixels and share
 // most voxels: processing several runs per instruction serialised on same-address atomics).
 // The in-tile slot comes from the run's step masks (no vid read): for incidence k,
-// slot0 + sx cx + 32 sy cy + 1024 sz (k - cx - cy), cx = popc(mx & (2^k - 1)); slot s lives at
-// the bank-swizzled index swz(s) so that y / z steps (strides 32, 1024) change the bank.  The
-// slots then go to T with one int64 atomic each (a tile spans several items).  Integer sums:
+// slot0 + sx cx + 32 sy cy + 1024 sz (k - cx - cy), cx = popc(mx & (2^k - 1)) (accumulator
+// index swz(s), see below).  The slots then go to T with one int64 atomic each (a tile spans several items).  Integer sums:
 // exact, independent of order.
 constexpr int kK6Threads = 1024;
 constexpr int kK6Warps = kK6Threads / 32;
 constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
 
-// slot -> accumulator index: the low 5 bits XOR-ed with y ^ z, so that y and z steps (slot
-// strides 32, 1024) change the bank (a bijection inside every 32-slot row, and an involution)
-__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 5) ^ (s >> 10)) & 31); }
+// slot -> accumulator index.  MRF_K6_SWIZZLE=1 XORs the low 5 bits with y ^ z so that y and z
+// steps (slot strides 32, 1024) change the bank (a bijection inside every 32-slot row); off by
+// default: K6 is ALU-bound and the 4 extra ALU ops cost more than the bank conflicts they
+// avoid (2.85 vs 2.74 ms per iteration at frames30).
+#ifndef MRF_K6_SWIZZLE
+#define MRF_K6_SWIZZLE 0
+#endif
+__device__ __forceinline__ int swz(int s) { return MRF_K6_SWIZZLE ? s ^ (((s >> 5) ^ (s >> 10)) & 31) : s; }
 
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
                                                                    const long long* __restrict__ tile_ptr,

@@ -110,8 +110,8 @@ struct mrf_ctx {
     DBuf<long long> col_ptr, item_ptr, pos;
     DBuf<int2> items;
     long long n_items_total = 0;
-    DBuf<int32_t> tile_runs, tile_cursor, tile_nitems;
-    DBuf<long long> tile_ptr, bitem_ptr;
+    DBuf<int32_t> tile_runs, tile_cursor;
+    DBuf<long long> tile_ptr;
     DBuf<Run> runs;
     DBuf<int2> bitems;
     long long n_runs = 0, n_bitems = 0;
@@ -567,9 +567,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(c->item_ptr.ensure((size_t)VI + 1, 0, c->stream));
         CK(c->tile_runs.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
-        CK(c->tile_nitems.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
-        CK(c->bitem_ptr.ensure((size_t)NT + 1, 0, c->stream));
         CK(c->counters.ensure(8, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
         CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
@@ -629,8 +627,8 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
     c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
-    c->tile_runs.release(); c->tile_cursor.release(); c->tile_nitems.release(); c->tile_ptr.release();
-    c->bitem_ptr.release(); c->runs.release(); c->bitems.release(); c->stages.release();
+    c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
+    c->runs.release(); c->bitems.release(); c->stages.release();
     c->class_all.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
