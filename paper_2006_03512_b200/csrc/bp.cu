@@ -284,7 +284,9 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
     stk<K>(lam + s, out, e1 - s);
 }
 
-// G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.
+// G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.  Incidence indices
+// are 32-bit (a ctx holds < 2^31 slots), and the per-element masks are selects on the lane's
+// valid count nv, so the only divergence is a lane without a chunk skipping its loads.
 #ifndef MRF_K5_MIN_BLOCKS
 #define MRF_K5_MIN_BLOCKS 4
 #endif
@@ -300,23 +302,40 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     if (wi * RPW >= n) return;  // warp-uniform
     const int lane = threadIdx.x & 31, sl = lane & (G - 1);
     const long long ri = wi * RPW + lane / G;
-    int nr = 0;
-    long long e0 = 0;
+    int nr = 0, e0 = 0;
     if (ri < n) {
         const int r = __ldg(rays + ri);
         nr = ray_z[r].n;
-        e0 = __ldg(row_ptr + r);
+        e0 = (int)__ldg(row_ptr + r);
     }
-    const long long e1 = e0 + nr;
-    const long long s = e0 + (long long)sl * K;
+    const int s = e0 + sl * K;
+    const int nv = min(max(nr - sl * K, 0), K);  // valid incidences of this lane's chunk
     float la[K], w[K], l[K], lR[K], lQ[K];
     identity_chunk<K>(la, w, l);
-    if (s < e1) load_chunk<K, M>(s, e1, mp.L0, vid, lnu, lam, T, la, w, l);
+    if (nv > 0) {
+        int v[K], q[K], ln[K];
+        ldk<K>(vid + s, v);
+        ldk<K>(lam + s, q);
+        ldk<K>(reinterpret_cast<const int32_t*>(lnu) + s, ln);
+        long long t[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) t[j] = j < nv ? __ldg(T + v[j]) : 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
+    }
     float aB, bB, Rin, Qin;
     lane_composite<K>(la, w, aB, bB);
     lane_scans<G, M>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
     lane_recurrences<K, M>(la, w, Rin, Qin, lR, lQ);
-    if (s < e1) lane_out<K>(l, lR, lQ, s, e1, lam);
+    if (nv > 0) {
+        int out[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int x = quantise(lambda_n(lQ[j], l[j], lR[j]));
+            out[j] = j < nv ? x : 0;
+        }
+        stk<K>(lam + s, out, nv);
+    }
 }
 
 // ---------------------------------------------------------------- K5: long rays (tiled)
