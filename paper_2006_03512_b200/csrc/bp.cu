@@ -155,10 +155,14 @@ __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc,
     Aff P = {-aB, bB - aB};  // prefix maps Q -> e^{-la} (Q + e^{w})
 #pragma unroll
     for (int d = 1; d < G; d <<= 1) {
-        const Aff oh = shfl_down<G>(H, d);
-        const Aff op = shfl_up<G>(P, d);
-        if (sl + d < G) H = compose<M>(H, oh);
-        if (sl >= d) P = compose<M>(P, op);
+        // partners outside the ray's lanes are identity maps (0, NEG): composing with them is
+        // exact (the remainder e^-huge vanishes), so no branch is needed
+        Aff oh = shfl_down<G>(H, d);
+        Aff op = shfl_up<G>(P, d);
+        if (sl + d >= G) oh = Aff{0.f, kNeg};
+        if (sl < d) op = Aff{0.f, kNeg};
+        H = compose<M>(H, oh);
+        P = compose<M>(P, op);
     }
     Aff Hx = shfl_down<G>(H, 1);
     Aff Px = shfl_up<G>(P, 1);
