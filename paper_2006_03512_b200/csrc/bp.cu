@@ -314,13 +314,14 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     }
     const int s = e0 + sl * K;
     const int nv = min(max(nr - sl * K, 0), K);  // valid incidences of this lane's chunk
+    // lanes past the ray's end re-read the ray's first chunk (in bounds) and mask everything
+    const int sr = nv > 0 ? s : e0;
     float la[K], w[K], l[K], lR[K], lQ[K];
-    identity_chunk<K>(la, w, l);
-    if (nv > 0) {
+    {
         int v[K], q[K], ln[K];
-        ldk<K>(vid + s, v);
-        ldk<K>(lam + s, q);
-        ldk<K>(reinterpret_cast<const int32_t*>(lnu) + s, ln);
+        ldk<K>(vid + sr, v);
+        ldk<K>(lam + sr, q);
+        ldk<K>(reinterpret_cast<const int32_t*>(lnu) + sr, ln);
         long long t[K];
 #pragma unroll
         for (int j = 0; j < K; ++j) t[j] = j < nv ? __ldg(T + v[j]) : 0;
@@ -331,15 +332,13 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     lane_composite<K>(la, w, aB, bB);
     lane_scans<G, M>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
     lane_recurrences<K, M>(la, w, Rin, Qin, lR, lQ);
-    if (nv > 0) {
-        int out[K];
+    int out[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-            const int x = quantise(lambda_n(lQ[j], l[j], lR[j]));
-            out[j] = j < nv ? x : 0;
-        }
-        stk<K>(lam + s, out, nv);
+    for (int j = 0; j < K; ++j) {
+        const int x = quantise(lambda_n(lQ[j], l[j], lR[j]));
+        out[j] = j < nv ? x : 0;
     }
+    stk<K>(lam + s, out, nv);
 }
 
 // ---------------------------------------------------------------- K5: long rays (tiled)
