@@ -115,15 +115,22 @@ __device__ __forceinline__ Aff shfl_idx(Aff v, int l) {
 // the cavity c = L0 + (t - q) 2^-23 (Eq.6) formed exactly in integers.  la and log mu(o=1)
 // share one ex2 and are both computed directly, never as a difference of two large numbers.
 // Masked elements (ok = false) are identity maps: la = 0, w = l = NEG.
+// select without a branch (ptxas otherwise turns "ok ? expensive : constant" into a divergent
+// branch around the whole softplus, which also serialises the elements' instruction streams)
+__device__ __forceinline__ float selp(bool p, float a, float b) {
+    float r;
+    asm("{\n.reg .pred q;\nsetp.ne.u32 q, %3, 0;\nselp.f32 %0, %1, %2, q;\n}" : "=f"(r) : "f"(a), "f"(b), "r"((unsigned)p));
+    return r;
+}
 template <int M>
 __device__ __forceinline__ void elem_terms(long long t, int q, float lnu, float L0, bool ok, float& la, float& w,
                                            float& l) {
     const float c = fmaf(__ll2float_rn(t - (long long)q), kQInv, L0);
     const float y = expn(-fabsf(c));
     const float L1 = M >= 2 ? log1pf_abs(y) : log1pn(y);  // ln(1 + e^-|c|)
-    la = ok ? -(fmaxf(c, 0.f) + L1) : 0.f;
-    w = ok ? lnu - (fmaxf(-c, 0.f) + L1) : kNeg;
-    l = ok ? lnu : kNeg;
+    la = selp(ok, -(fmaxf(c, 0.f) + L1), 0.f);
+    w = selp(ok, lnu - (fmaxf(-c, 0.f) + L1), kNeg);
+    l = selp(ok, lnu, kNeg);
 }
 
 // Chunk composite of the suffix maps R -> e^{la} R + e^{w} (first applied last):
@@ -322,9 +329,12 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
         ldk<K>(vid + sr, v);
         ldk<K>(lam + sr, q);
         ldk<K>(reinterpret_cast<const int32_t*>(lnu) + sr, ln);
+        // every slot of a chunk holds a valid voxel id (padding slots hold 0), so the gathers
+        // and the element terms run unpredicated (straight-line code, full ILP) and are masked
+        // by select afterwards
         long long t[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) t[j] = j < nv ? __ldg(T + v[j]) : 0;
+        for (int j = 0; j < K; ++j) t[j] = __ldg(T + v[j]);
 #pragma unroll
         for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
     }
