@@ -665,7 +665,6 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
     uint4* sdesc = reinterpret_cast<uint4*>(smem + 2 * kTileSlots) + (threadIdx.x >> 5) * 32;  // this warp's batch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned below = (1u << lane) - 1u;
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int2 item = __ldg(items + it);
         for (int i = threadIdx.x; i < 2 * kTileSlots / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
@@ -679,25 +678,37 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
             sdesc[lane] = d;
             __syncwarp();
+            // Half-warp pairs: in round 0 lanes 0-15 take incidences 0-15 of run j and lanes 16-31
+            // those of run j + 16 (16 pixels away: rarely the same voxel at the same time); round 1
+            // takes incidences 16-31 of the same pairs.
+            const int hw = lane >> 4, hl = lane & 15;
             int q[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint4 x = sdesc[j];
-                const int n = j < nb ? (int)((x.y >> 14) & 63u) + 1 : 0;
-                q[j] = lane < n ? __ldg(lam + x.x + lane) : 0;
+            for (int j = 0; j < 16; ++j) {
+                const uint4 x = sdesc[j + 16 * hw];
+                const int n = j + 16 * hw < nb ? (int)((x.y >> 14) & 63u) + 1 : 0;
+                q[j] = hl < n ? __ldg(lam + x.x + hl) : 0;
+                q[16 + j] = hl + 16 < n ? __ldg(lam + x.x + hl + 16) : 0;  // predicated off for short runs
             }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const uint4 x = sdesc[j];
-                const unsigned meta = x.y;
-                const int n = j < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
-                if (lane < n) {
-                    const int cx = __popc(x.z & below), cy = __popc(x.w & below);
-                    const int sx = (meta >> 20) & 1 ? -cx : cx, sy = (meta >> 21) & 1 ? -cy : cy;
-                    const int cz = lane - cx - cy, sz = (meta >> 22) & 1 ? -cz : cz;
-                    const int si = swz((int)(meta & (kTileSlots - 1)) + sx + 32 * sy + 1024 * sz);
-                    atomicAdd(acc_lo + si, q[j] & 0xffff);
-                    atomicAdd(acc_hi + si, q[j] >> 16);
+            for (int rnd = 0; rnd < 2; ++rnd) {
+                const int k = hl + 16 * rnd;
+                const unsigned below_k = (1u << k) - 1u;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const uint4 x = sdesc[j + 16 * hw];
+                    const unsigned meta = x.y;
+                    const int n = j + 16 * hw < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
+                    if (rnd == 1 && !__any_sync(kFull, k < n)) continue;  // both runs <= 16 long
+                    if (k < n) {
+                        const int cx = __popc(x.z & below_k), cy = __popc(x.w & below_k);
+                        const int sx = (meta >> 20) & 1 ? -cx : cx, sy = (meta >> 21) & 1 ? -cy : cy;
+                        const int cz = k - cx - cy, sz = (meta >> 22) & 1 ? -cz : cz;
+                        const int si = swz((int)(meta & (kTileSlots - 1)) + sx + 32 * sy + 1024 * sz);
+                        const int qv = q[16 * rnd + j];
+                        atomicAdd(acc_lo + si, qv & 0xffff);
+                        atomicAdd(acc_hi + si, qv >> 16);
+                    }
                 }
             }
             __syncwarp();
