@@ -644,6 +644,10 @@ __global__ void __launch_bounds__(256) voxel_reduce_kernel(long long n_items, co
 // exact, independent of order.
 constexpr int kK6Threads = 1024;
 constexpr int kK6Warps = kK6Threads / 32;
+#ifndef MRF_K6_W
+#define MRF_K6_W 16
+#endif
+constexpr int kK6W = MRF_K6_W;  // lanes per run in the add loop
 constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
 
 // slot -> accumulator index.  MRF_K6_SWIZZLE=1 XORs the low 5 bits with y ^ z so that y and z
@@ -678,34 +682,39 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
             sdesc[lane] = d;
             __syncwarp();
-            // Half-warp pairs: in round 0 lanes 0-15 take incidences 0-15 of run j and lanes 16-31
-            // those of run j + 16 (16 pixels away: rarely the same voxel at the same time); round 1
-            // takes incidences 16-31 of the same pairs.
-            const int hw = lane >> 4, hl = lane & 15;
-            int q[32];
+            // Lane groups of kK6W lanes (32 / kK6W runs per instruction): in round r, group g takes
+            // incidences r*kK6W .. r*kK6W+kK6W-1 of run j + g*kK6W (runs kK6W apart in the batch:
+            // pixels far enough apart to rarely hit the same voxel at the same time); rounds past
+            // every run's end are skipped.
+            constexpr int NJ = kK6W, NR = 32 / kK6W;
+            const int hw = lane / kK6W, hl = lane % kK6W;
+            int q[NR][NJ];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint4 x = sdesc[j + 16 * hw];
-                const int n = j + 16 * hw < nb ? (int)((x.y >> 14) & 63u) + 1 : 0;
-                q[j] = hl < n ? __ldg(lam + x.x + hl) : 0;
-                q[16 + j] = hl + 16 < n ? __ldg(lam + x.x + hl + 16) : 0;  // predicated off for short runs
+            for (int j = 0; j < NJ; ++j) {
+                const uint4 x = sdesc[j + NJ * hw];
+                const int n = j + NJ * hw < nb ? (int)((x.y >> 14) & 63u) + 1 : 0;
+#pragma unroll
+                for (int rnd = 0; rnd < NR; ++rnd) {
+                    const int k = hl + kK6W * rnd;
+                    q[rnd][j] = k < n ? __ldg(lam + x.x + k) : 0;
+                }
             }
 #pragma unroll
-            for (int rnd = 0; rnd < 2; ++rnd) {
-                const int k = hl + 16 * rnd;
+            for (int rnd = 0; rnd < NR; ++rnd) {
+                const int k = hl + kK6W * rnd;
                 const unsigned below_k = (1u << k) - 1u;
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const uint4 x = sdesc[j + 16 * hw];
+                for (int j = 0; j < NJ; ++j) {
+                    const uint4 x = sdesc[j + NJ * hw];
                     const unsigned meta = x.y;
-                    const int n = j + 16 * hw < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
-                    if (rnd == 1 && !__any_sync(kFull, k < n)) continue;  // both runs <= 16 long
+                    const int n = j + NJ * hw < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
+                    if (rnd > 0 && !__any_sync(kFull, k < n)) continue;  // every run of the column ended
                     if (k < n) {
                         const int cx = __popc(x.z & below_k), cy = __popc(x.w & below_k);
                         const int sx = (meta >> 20) & 1 ? -cx : cx, sy = (meta >> 21) & 1 ? -cy : cy;
                         const int cz = k - cx - cy, sz = (meta >> 22) & 1 ? -cz : cz;
                         const int si = swz((int)(meta & (kTileSlots - 1)) + sx + 32 * sy + 1024 * sz);
-                        const int qv = q[16 * rnd + j];
+                        const int qv = q[rnd][j];
                         atomicAdd(acc_lo + si, qv & 0xffff);
                         atomicAdd(acc_hi + si, qv >> 16);
                     }
