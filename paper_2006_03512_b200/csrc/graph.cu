@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
     }
     bool alive = e < e1;
     RunBuilder rb;
+    int4 buf{0, 0, 0, 0};  // vid[e & ~3 .. +4): 16-byte loads (segments are 8-aligned)
     for (;;) {
         const unsigned am = __ballot_sync(kFull, alive);
         if (am == 0) break;
@@ -419,7 +420,9 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
             const bool at_end = e == e1;
             int b = -1, l = 0;
             if (!at_end) {
-                const int v = vid[e];
+                if ((e & 3) == 0) buf = __ldg(reinterpret_cast<const int4*>(vid + e));
+                const int k = (int)(e & 3);
+                const int v = k == 0 ? buf.x : (k == 1 ? buf.y : (k == 2 ? buf.z : buf.w));
                 b = v >> kTileShift;
                 l = v & (kTileSlots - 1);
             }
