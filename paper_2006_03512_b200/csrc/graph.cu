@@ -321,10 +321,12 @@ __global__ void __launch_bounds__(256) lnu_fill_kernel(long long r0, long long n
         const uint4 o = __ldg(reinterpret_cast<const uint4*>(off_q + e0 + c));
         const unsigned ow[4] = {o.x, o.y, o.z, o.w};
         float out[8];
+        // every slot holds a valid code (padding: 0), so all 16 table loads issue back to back;
+        // padding slots are zeroed by multiplication afterwards (no branch around the loads)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int q = (int)(short)((ow[k >> 1] >> (16 * (k & 1))) & 0xffffu);
-            out[k] = c + k < ri.n ? lut_finish(lut_fetch(mp, ri.iz, q), ri.wz) : 0.f;
+            out[k] = lut_finish(lut_fetch(mp, ri.iz, q), ri.wz) * (float)(c + k < ri.n);
         }
         float4* dst = reinterpret_cast<float4*>(lnu + e0 + c);
         dst[0] = make_float4(out[0], out[1], out[2], out[3]);
