@@ -215,7 +215,22 @@ def test_long_rays_tiled_class():
         assert np.max(np.abs(m.marginals() - oracle.marginals(p, T_ref))) <= MARG_TOL
 
 
-@pytest.mark.parametrize("wall_vox", [130.4, 250.7, 400.2])
+def test_max_dim_corridor():
+    """dims = 8192 (the largest accepted): 8100-cell rays along the grid, DDA crossing
+    numerators / denominators near 2^29 (the 32-bit exact products of the walker)."""
+    w = _corridor(n_vox=8192, wall_vox=8100.3)
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    assert np.diff(g.row_ptr).max() > 8000
+    lam_ref, T_ref = oracle.bp(p, g, w.n_iter)
+    with _gpu_map(w) as m:
+        _assert_graph_equal(m.export_graph(), g)
+        m.bp_iterate(w.n_iter)
+        _assert_msgs_close(m.export_messages(), lam_ref)
+        assert np.max(np.abs(m.marginals() - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+@pytest.mark.parametrize("wall_vox", [130.4, 250.7, 320.9, 400.2, 470.6])
 def test_medium_rays_k8_k16_classes(wall_vox):
     w = _corridor(n_vox=480, wall_vox=wall_vox)
     p = oracle.Params.from_workload(w)
