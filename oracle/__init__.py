@@ -10,7 +10,7 @@ numpy arrays to it and assembles the per-frame CSR in canonical order
 Every function cites the SURVEY §8(c) step (B1..B7) / PAPER.md lines it follows;
 the pins that tie it to the paper are in tests/test_oracle_*.py.  Parity status:
   B1 ray setup, B2 DDA, B3 offsets/LUT, B5 single-ray messages, B5+B6 on tree
-  graphs: pinned.  B5+B6 on loopy graphs (several overlapping rays): parity
+  graphs, §III.D evaluation metric (vis_profile / eval_pixel): pinned.  B5+B6 on loopy graphs (several overlapping rays): parity
   unpinned beyond the invariants (loopy BP has no closed form).
 """
 
@@ -76,6 +76,12 @@ def lib():
             L.orc_frame_count.restype = None
             L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p]
             L.orc_frame_fill.restype = None
+            L.orc_vis_profile.argtypes = [i64, dp, dp, d, dp, dp]
+            L.orc_vis_profile.restype = i64
+            L.orc_eval_pixel.argtypes = [i32p, dp, dp, dp, dp, i32, i32, ctypes.c_float, dp, d, d, dp]
+            L.orc_eval_pixel.restype = ctypes.c_int
+            L.orc_eval_frame.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, dp, d, d, i32, i32, i8p, i64p, i64p]
+            L.orc_eval_frame.restype = None
             _lib = L
     return _lib
 
@@ -299,3 +305,50 @@ def run(workload, n_iter=None, rank=0, world=1):
     g = build_graph(p, workload.frames, rank, world)
     lam, T = bp(p, g, workload.n_iter if n_iter is None else n_iter)
     return p, g, lam, T, marginals(p, T)
+
+
+# --------------------------------------------------------------------------- §III.D metric
+
+def vis_profile(x, ell, res):
+    """Visibility / generating-surface density along one ray (Eq.15-18):
+    per step occupancy log-odds x_i and traversed length ell_i -> (ln vis[0..n], ln omega[0..n-1],
+    argmax_i ln omega_i or -1)."""
+    x = _c(x, np.float64)
+    ell = _c(ell, np.float64)
+    n = len(x)
+    lvis = np.zeros(n + 1)
+    lom = np.zeros(max(n, 1))
+    best = lib().orc_vis_profile(n, _ptr(x, ctypes.c_double), _ptr(ell, ctypes.c_double), float(res),
+                                 _ptr(lvis, ctypes.c_double), _ptr(lom, ctypes.c_double))
+    return lvis, lom[:n], int(best)
+
+
+def eval_pixel(p: Params, frame, u, v, xmap, k_sigma=1.5, vis_thr=0.5):
+    """One pixel against the map xmap[V] (occupancy log-odds): (class, Z, s*, s_inf, vis_inf)."""
+    out = np.zeros(4)
+    K = _c(frame.K, np.float64)
+    T = _c(frame.T_wc, np.float64)
+    xm = _c(xmap, np.float64)
+    r = lib().orc_eval_pixel(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
+                             _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), int(u), int(v),
+                             float(frame.depth[v, u]), _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr),
+                             _ptr(out, ctypes.c_double))
+    return (int(r),) + tuple(float(a) for a in out)
+
+
+def eval_frame(p: Params, frame, xmap, k_sigma=1.5, vis_thr=0.5, rank=0, world=1):
+    """§V per-image accuracy: per-pixel class (-1 invalid, 0 / 1, -2 other rank), n_valid,
+    n_accurate."""
+    H, W = frame.depth.shape
+    cls = np.zeros(H * W, np.int8)
+    nv = ctypes.c_int64()
+    na = ctypes.c_int64()
+    depth = _c(frame.depth, np.float32)
+    K = _c(frame.K, np.float64)
+    T = _c(frame.T_wc, np.float64)
+    xm = _c(xmap, np.float64)
+    lib().orc_eval_frame(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
+                         _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
+                         _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr), rank, world,
+                         _ptr(cls, ctypes.c_int8), ctypes.byref(nv), ctypes.byref(na))
+    return cls.reshape(H, W), nv.value, na.value

@@ -317,3 +317,119 @@ void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par
         }
     }
 }
+
+/* ------------------------------------------------------------------ §III.D evaluation metric
+ * Generating-surface accuracy of a probabilistic map (applied per pixel in §V
+ * P:240).  Readings (R18-R21):
+ *   R18 occlusion density of voxel i with occupancy p_i: alpha_i = -ln(1 - p_i) / res, so a
+ *       full-side crossing multiplies the visibility by (1 - p_i);
+ *   R19 the evaluation ray runs from the camera to the map boundary (s_inf): the segment
+ *       C -> C + 1.5 D d (D = grid diagonal, d the unit ray), walked by the same B2 DDA;
+ *   R20 omega(s) = alpha(s) vis(s) decreases inside a constant-alpha step, so its maximum over
+ *       a step is at the step entry and s* = entry of argmax_i alpha_i vis_i (first on ties);
+ *   R21 classification: vis_inf > thr (0.5, "not reduced sufficiently") -> accurate iff
+ *       Z > s_inf; else accurate iff |Z - s*| <= k sigma(Z) (k = 1.5), sigma the map's
+ *       noise model sigma(Z) = c0 + c1 Z + c2 Z^2.
+ *
+ * Per step i with occupancy log-odds x_i (p_i = sigma(x_i)) and length ell_i (m):
+ *   ln vis_0 = 0,  ln vis_{i+1} = ln vis_i + (ell_i / res) ln(1 - p_i) = ln vis_i - (ell_i/res) softplus(x_i)
+ *   ln omega_i = ln(alpha_i) + ln vis_i = ln(softplus(x_i) / res) + ln vis_i      (Eq.17-18)
+ *   Omega_i = vis_i - vis_{i+1}                                                   (Eq.16)
+ * orc_vis_profile writes ln vis[0..n] and ln omega[0..n-1] and returns argmax_i ln omega_i
+ * (-1 if every p_i = 0). */
+int64_t orc_vis_profile(int64_t n, const double* x, const double* ell, double res, double* lvis,
+                        double* lomega) {
+    lvis[0] = 0.0;
+    int64_t best = -1;
+    double bw = -INFINITY;
+    for (int64_t i = 0; i < n; ++i) {
+        const double sp = softplus(x[i]); /* -ln(1 - p_i) */
+        lomega[i] = (sp > 0.0 ? log(sp / res) : -INFINITY) + lvis[i];
+        if (lomega[i] > bw) {
+            bw = lomega[i];
+            best = i;
+        }
+        lvis[i + 1] = lvis[i] - (ell[i] / res) * sp;
+    }
+    return best;
+}
+
+/* Evaluate one pixel against the map given by its occupancy log-odds xmap[V] (x = L0 + T_v).
+ * Returns -1 for an invalid pixel (z not finite or <= 0), else 1 accurate / 0 inaccurate;
+ * out[0..3] = {Z, s*, s_inf, vis_inf} (s* = -1 if no step occludes). */
+int orc_eval_pixel(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+                   const double Twc[12], int32_t u, int32_t v, float zf, const double* xmap, double k_sigma,
+                   double vis_thr, double out[4]) {
+    const double z = (double)zf;
+    if (!isfinite(z) || !(z > 0.0)) return -1;
+    const double res = geo[0];
+    const double xc = ((double)u - K[2]) / K[0];
+    const double yc = ((double)v - K[3]) / K[1];
+    const double rho = sqrt((xc * xc + yc * yc) + 1.0);
+    const double Z = z * rho;
+    const double D = res * sqrt((double)dims[0] * dims[0] + (double)dims[1] * dims[1] + (double)dims[2] * dims[2]);
+    const double Lev = 1.5 * D; /* R19: beyond the map boundary from any camera inside it */
+    int64_t G0[3], G1[3];
+    for (int k = 0; k < 3; ++k) {
+        const double Ck = Twc[4 * k + 3];
+        const double Dk = (Twc[4 * k + 0] * xc + Twc[4 * k + 1] * yc) + Twc[4 * k + 2];
+        const double Ek = Ck + (Lev / rho) * Dk;
+        G0[k] = llrint(((Ck - geo[1 + k]) / res) * 65536.0);
+        G1[k] = llrint(((Ek - geo[1 + k]) / res) * 65536.0);
+    }
+    const int64_t n = orc_dda(dims, G0, G1, 0.0, 1.0, NULL, NULL, NULL, NULL, 0);
+    int32_t* vid = (int32_t*)malloc(sizeof(int32_t) * (n > 0 ? n : 1));
+    double* tin = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    double* tout = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    double* x = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    double* ell = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    double* lvis = (double*)malloc(sizeof(double) * (n + 1));
+    double* lom = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+    orc_dda(dims, G0, G1, 0.0, 1.0, vid, NULL, tin, tout, n);
+    for (int64_t i = 0; i < n; ++i) {
+        x[i] = xmap[vid[i]];
+        ell[i] = (tout[i] - tin[i]) * Lev;
+    }
+    const int64_t best = orc_vis_profile(n, x, ell, res, lvis, lom);
+    const double s_inf = n > 0 ? tout[n - 1] * Lev : 0.0;
+    const double vis_inf = exp(lvis[n]);
+    const double s_star = best >= 0 ? tin[best] * Lev : -1.0;
+    const double sigma = (par[6] + par[7] * Z) + (par[8] * Z) * Z;
+    int acc;
+    if (vis_inf > vis_thr)
+        acc = Z > s_inf;
+    else
+        acc = fabs(Z - s_star) <= k_sigma * sigma;
+    out[0] = Z;
+    out[1] = s_star;
+    out[2] = s_inf;
+    out[3] = vis_inf;
+    free(vid); free(tin); free(tout); free(x); free(ell); free(lvis); free(lom);
+    return acc;
+}
+
+/* All pixels of one frame (rows v % world == rank; others -2).  cls[H*W]; returns
+ * n_valid, n_accurate through the pointers. */
+void orc_eval_frame(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+                    const double Twc[12], int32_t W, int32_t H, const float* depth, const double* xmap,
+                    double k_sigma, double vis_thr, int32_t rank, int32_t world, int8_t* cls,
+                    int64_t* n_valid, int64_t* n_acc) {
+    int64_t nv = 0, na = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(+ : nv, na)
+    for (int64_t i = 0; i < (int64_t)W * H; ++i) {
+        const int32_t v = (int32_t)(i / W), u = (int32_t)(i % W);
+        if (v % world != rank) {
+            cls[i] = -2;
+            continue;
+        }
+        double out[4];
+        const int r = orc_eval_pixel(dims, geo, par, K, Twc, u, v, depth[i], xmap, k_sigma, vis_thr, out);
+        cls[i] = (int8_t)r;
+        if (r >= 0) {
+            nv += 1;
+            na += r;
+        }
+    }
+    *n_valid = nv;
+    *n_acc = na;
+}
