@@ -136,6 +136,22 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences);
 mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences, int64_t* n_active_vox,
                            int64_t* n_invalid, int64_t* n_dropped);
 
+/* Generating-surface accuracy of one posed depth image against the CURRENT beliefs (PAPER.md
+ * §III.D P:168-196 -- visibility Eq.15, occlusion probability Eq.16, generating-surface density
+ * Eq.17-18 -- and the per-image score of §V; readings R18-R21 in DESIGN.md).  For every
+ * valid pixel of the rows this rank owns, the ray from the camera to the map boundary is walked
+ * by the same fixed-point DDA: alpha = -ln(1 - p_v)/res, vis and omega = alpha vis along it,
+ * s* = entry of the most likely generating voxel.  Accurate iff vis_inf > vis_threshold ? Z >
+ * s_inf : (mode MRF_EVAL_SIGMA_BAND, §V) |Z - s*| <= k_sigma sigma(Z) (sigma: the ctx's noise
+ * model) or (mode MRF_EVAL_VOXEL_BOUNDS, §III.D) Z inside the argmax voxel.  depth/K/T_wc as in
+ * mrf_add_frame (camera inside the grid).  cls (nullable, host, W*H): -2 row of another rank,
+ * -1 invalid pixel, 0 inaccurate, 1 accurate.  n_valid / n_accurate: this rank's counts
+ * (sum over ranks for the image score).  k_sigma > 0, 0 < vis_threshold < 1.  Synchronises. */
+enum { MRF_EVAL_SIGMA_BAND = 0, MRF_EVAL_VOXEL_BOUNDS = 1 };
+mrf_status mrf_evaluate(mrf_ctx* ctx, const float* depth, int32_t width, int32_t height, const double K[4],
+                        const double T_wc[12], int32_t mode, double k_sigma, double vis_threshold, int8_t* cls,
+                        int64_t* n_valid, int64_t* n_accurate);
+
 /* Sizes of this rank's device layout, for the roofline byte counts: n_slots =
  * incidence slots incl. the padding of every ray segment to a multiple of 8; n_runs = tile runs
  * of the K6 transpose; n_belief_slots = tile-major belief slots (32x32x16 tiles).  Builds the

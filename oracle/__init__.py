@@ -78,9 +78,9 @@ def lib():
             L.orc_frame_fill.restype = None
             L.orc_vis_profile.argtypes = [i64, dp, dp, d, dp, dp]
             L.orc_vis_profile.restype = i64
-            L.orc_eval_pixel.argtypes = [i32p, dp, dp, dp, dp, i32, i32, ctypes.c_float, dp, d, d, dp]
+            L.orc_eval_pixel.argtypes = [i32p, dp, dp, dp, dp, i32, i32, ctypes.c_float, dp, d, d, i32, dp]
             L.orc_eval_pixel.restype = ctypes.c_int
-            L.orc_eval_frame.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, dp, d, d, i32, i32, i8p, i64p, i64p]
+            L.orc_eval_frame.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, dp, d, d, i32, i32, i32, i8p, i64p, i64p]
             L.orc_eval_frame.restype = None
             _lib = L
     return _lib
@@ -323,8 +323,9 @@ def vis_profile(x, ell, res):
     return lvis, lom[:n], int(best)
 
 
-def eval_pixel(p: Params, frame, u, v, xmap, k_sigma=1.5, vis_thr=0.5):
-    """One pixel against the map xmap[V] (occupancy log-odds): (class, Z, s*, s_inf, vis_inf)."""
+def eval_pixel(p: Params, frame, u, v, xmap, k_sigma=1.5, vis_thr=0.5, mode=0):
+    """One pixel against the map xmap[V] (occupancy log-odds): (class, Z, s*, s_inf, vis_inf).
+    mode 0: 1.5-sigma band around s* (§V); mode 1: Z inside the argmax voxel (§III.D)."""
     out = np.zeros(4)
     K = _c(frame.K, np.float64)
     T = _c(frame.T_wc, np.float64)
@@ -332,11 +333,11 @@ def eval_pixel(p: Params, frame, u, v, xmap, k_sigma=1.5, vis_thr=0.5):
     r = lib().orc_eval_pixel(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                              _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), int(u), int(v),
                              float(frame.depth[v, u]), _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr),
-                             _ptr(out, ctypes.c_double))
+                             int(mode), _ptr(out, ctypes.c_double))
     return (int(r),) + tuple(float(a) for a in out)
 
 
-def eval_frame(p: Params, frame, xmap, k_sigma=1.5, vis_thr=0.5, rank=0, world=1):
+def eval_frame(p: Params, frame, xmap, k_sigma=1.5, vis_thr=0.5, rank=0, world=1, mode=0):
     """§V per-image accuracy: per-pixel class (-1 invalid, 0 / 1, -2 other rank), n_valid,
     n_accurate."""
     H, W = frame.depth.shape
@@ -349,6 +350,6 @@ def eval_frame(p: Params, frame, xmap, k_sigma=1.5, vis_thr=0.5, rank=0, world=1
     xm = _c(xmap, np.float64)
     lib().orc_eval_frame(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                          _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
-                         _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr), rank, world,
+                         _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr), int(mode), rank, world,
                          _ptr(cls, ctypes.c_int8), ctypes.byref(nv), ctypes.byref(na))
     return cls.reshape(H, W), nv.value, na.value

@@ -328,8 +328,9 @@ void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par
  *   R20 omega(s) = alpha(s) vis(s) decreases inside a constant-alpha step, so its maximum over
  *       a step is at the step entry and s* = entry of argmax_i alpha_i vis_i (first on ties);
  *   R21 classification: vis_inf > thr (0.5, "not reduced sufficiently") -> accurate iff
- *       Z > s_inf; else accurate iff |Z - s*| <= k sigma(Z) (k = 1.5), sigma the map's
- *       noise model sigma(Z) = c0 + c1 Z + c2 Z^2.
+ *       Z > s_inf; else, mode 0 (sigma band, §V): accurate iff |Z - s*| <= k sigma(Z)
+ *       (k = 1.5), sigma the map's noise model sigma(Z) = c0 + c1 Z + c2 Z^2; mode 1 (voxel
+ *       bounds, §III.D): accurate iff Z lies in [entry, exit] of the argmax voxel.
  *
  * Per step i with occupancy log-odds x_i (p_i = sigma(x_i)) and length ell_i (m):
  *   ln vis_0 = 0,  ln vis_{i+1} = ln vis_i + (ell_i / res) ln(1 - p_i) = ln vis_i - (ell_i/res) softplus(x_i)
@@ -359,7 +360,7 @@ int64_t orc_vis_profile(int64_t n, const double* x, const double* ell, double re
  * out[0..3] = {Z, s*, s_inf, vis_inf} (s* = -1 if no step occludes). */
 int orc_eval_pixel(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
                    const double Twc[12], int32_t u, int32_t v, float zf, const double* xmap, double k_sigma,
-                   double vis_thr, double out[4]) {
+                   double vis_thr, int32_t mode, double out[4]) {
     const double z = (double)zf;
     if (!isfinite(z) || !(z > 0.0)) return -1;
     const double res = geo[0];
@@ -394,12 +395,15 @@ int orc_eval_pixel(const int32_t dims[3], const double geo[4], const double par[
     const double s_inf = n > 0 ? tout[n - 1] * Lev : 0.0;
     const double vis_inf = exp(lvis[n]);
     const double s_star = best >= 0 ? tin[best] * Lev : -1.0;
+    const double s_star_out = best >= 0 ? tout[best] * Lev : -1.0;
     const double sigma = (par[6] + par[7] * Z) + (par[8] * Z) * Z;
     int acc;
     if (vis_inf > vis_thr)
         acc = Z > s_inf;
-    else
+    else if (mode == 0)
         acc = fabs(Z - s_star) <= k_sigma * sigma;
+    else
+        acc = Z >= s_star && Z <= s_star_out;
     out[0] = Z;
     out[1] = s_star;
     out[2] = s_inf;
@@ -412,7 +416,7 @@ int orc_eval_pixel(const int32_t dims[3], const double geo[4], const double par[
  * n_valid, n_accurate through the pointers. */
 void orc_eval_frame(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
                     const double Twc[12], int32_t W, int32_t H, const float* depth, const double* xmap,
-                    double k_sigma, double vis_thr, int32_t rank, int32_t world, int8_t* cls,
+                    double k_sigma, double vis_thr, int32_t mode, int32_t rank, int32_t world, int8_t* cls,
                     int64_t* n_valid, int64_t* n_acc) {
     int64_t nv = 0, na = 0;
 #pragma omp parallel for schedule(dynamic, 64) reduction(+ : nv, na)
@@ -423,7 +427,7 @@ void orc_eval_frame(const int32_t dims[3], const double geo[4], const double par
             continue;
         }
         double out[4];
-        const int r = orc_eval_pixel(dims, geo, par, K, Twc, u, v, depth[i], xmap, k_sigma, vis_thr, out);
+        const int r = orc_eval_pixel(dims, geo, par, K, Twc, u, v, depth[i], xmap, k_sigma, vis_thr, mode, out);
         cls[i] = (int8_t)r;
         if (r >= 0) {
             nv += 1;

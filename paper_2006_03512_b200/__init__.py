@@ -153,6 +153,23 @@ class MRFMap:
         self._chk(self._L.mrf_layout_sizes(self._h, *(ctypes.byref(x) for x in v)))
         return dict(n_slots=v[0].value, n_runs=v[1].value, n_belief_slots=v[2].value)
 
+    def evaluate(self, depth, K, T_wc, k_sigma=1.5, vis_threshold=0.5, mode=0):
+        """mrf_evaluate: §III.D generating-surface accuracy of one posed depth image against the
+        current beliefs -> (cls[H, W] int8, n_valid, n_accurate) for this rank's rows.
+        mode 0: k_sigma band around s* (§V); mode 1: Z inside the argmax voxel (§III.D)."""
+        is_dev = _is_device(depth)
+        H, W = (depth.shape if hasattr(depth, "shape") else np.shape(depth))
+        if not is_dev:
+            depth = np.ascontiguousarray(depth, dtype=np.float32)
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        T_wc = np.ascontiguousarray(T_wc, dtype=np.float64).reshape(-1)
+        cls = np.zeros((H, W), np.int8)
+        nv, na = ctypes.c_int64(), ctypes.c_int64()
+        self._chk(self._L.mrf_evaluate(self._h, _ptr(depth), W, H, K.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                       T_wc.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(mode), float(k_sigma),
+                                       float(vis_threshold), _ptr(cls), ctypes.byref(nv), ctypes.byref(na)))
+        return cls, nv.value, na.value
+
     def export_rays(self, frame, pixel):
         """mrf_export_rays: incidence lists of the selected (frame, pixel) rays of this rank."""
         frame = np.ascontiguousarray(frame, dtype=np.int32)

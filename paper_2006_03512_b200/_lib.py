@@ -21,13 +21,14 @@ MRF_OK, MRF_ERR_INVALID_ARG, MRF_ERR_OUT_OF_MEMORY, MRF_ERR_CAPACITY, MRF_ERR_CU
 STATUS_NAMES = {0: "MRF_OK", 1: "MRF_ERR_INVALID_ARG", 2: "MRF_ERR_OUT_OF_MEMORY", 3: "MRF_ERR_CAPACITY",
                 4: "MRF_ERR_CUDA", 5: "MRF_ERR_NCCL", 6: "MRF_ERR_STATE"}
 MRF_COMM_NCCL, MRF_COMM_EXTERNAL = 0, 1
+MRF_EVAL_SIGMA_BAND, MRF_EVAL_VOXEL_BOUNDS = 0, 1
 KERNEL_NAMES = ["raygen_count", "dda_fill", "scan", "transpose", "ray_messages", "voxel_sum", "allreduce",
                 "marginals"]
 MRF_K_COUNT = len(KERNEL_NAMES)
 
 # every symbol include/mrf.h declares
 EXPORTS = ["mrf_create", "mrf_add_frame", "mrf_bp_iterate", "mrf_marginals", "mrf_destroy", "mrf_last_error",
-           "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph", "mrf_export_rays",
+           "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph", "mrf_export_rays", "mrf_evaluate",
            "mrf_export_transpose", "mrf_export_messages", "mrf_import_messages", "mrf_export_beliefs",
            "mrf_bp_partial", "mrf_bp_finish", "mrf_belief_slots", "mrf_nccl_unique_id", "mrf_set_profiling",
            "mrf_profile_read", "mrf_launch_count"]
@@ -78,6 +79,7 @@ def load(build: bool = True):
                 "mrf_graph_sizes": (st, [vp, P(i64), P(i64), P(i64), P(i64), P(i64)]),
                 "mrf_layout_sizes": (st, [vp, P(i64), P(i64), P(i64)]),
                 "mrf_export_rays": (st, [vp, i64, vp, vp, i64, vp, vp, vp, vp]),
+                "mrf_evaluate": (st, [vp, vp, i32, i32, P(f64), P(f64), i32, f64, f64, vp, P(i64), P(i64)]),
                 "mrf_export_graph": (st, [vp, vp, vp, vp, vp]),
                 "mrf_export_transpose": (st, [vp, vp, vp]),
                 "mrf_export_messages": (st, [vp, vp]),

@@ -334,6 +334,85 @@ __global__ void __launch_bounds__(256) lnu_fill_kernel(long long r0, long long n
     }
 }
 
+// ---------------------------------------------------------------- K9: §III.D evaluation
+// Generating-surface accuracy of one posed depth image against the current beliefs (
+// §V; readings R18-R21 in DESIGN.md).  Thread per owned pixel, fp64 (an evaluation kernel,
+// not on the BP hot path; decisions taken in the oracle's precision): the ray from the camera
+// to 1.5 x the grid diagonal is walked by the same fixed-point DDA until it leaves the grid;
+// per cell x = L0 + T 2^-23, softplus(x) = -ln(1 - p), alpha = softplus / res,
+// ln omega = ln(alpha) + ln vis at the cell entry, ln vis -= (ell / res) softplus; s* = entry of
+// the first maximal omega; vis_inf, s_inf at the exit.  Accurate: vis_inf > thr ? Z > s_inf :
+// mode 0: |Z - s*| <= k sigma(Z) (§V), mode 1: Z inside the argmax voxel (§III.D).  cls: -1
+// invalid pixel, 0 / 1.
+__device__ __forceinline__ double softplus_d(double x) { return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
+
+__global__ void __launch_bounds__(128) eval_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const float* __restrict__ depth,
+                                                   const long long* __restrict__ T, double L0, double k_sigma,
+                                                   double vis_thr, int mode, double L_eval, int8_t* cls,
+                                                   unsigned long long* counts) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long n_pix = (long long)f.rows_owned * f.W;
+    int r = -2;
+    if (i < n_pix) {
+        int u, v;
+        owned_pixel(f, i, u, v);
+        const double z = (double)depth[(long long)v * f.W + u];
+        r = -1;
+        if (z > 0.0 && !isinf(z)) {
+            const double xc = __ddiv_rn(__dsub_rn((double)u, f.cx), f.fx);
+            const double yc = __ddiv_rn(__dsub_rn((double)v, f.cy), f.fy);
+            const double rho = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xc, xc), __dmul_rn(yc, yc)), 1.0));
+            const double Z = __dmul_rn(z, rho);
+            const double l_over_rho = __ddiv_rn(L_eval, rho);
+            const double org[3] = {g.ox, g.oy, g.oz};
+            Segment sg;
+            for (int k = 0; k < 3; ++k) {
+                const double d = __dadd_rn(__dadd_rn(__dmul_rn(f.R[3 * k], xc), __dmul_rn(f.R[3 * k + 1], yc)), f.R[3 * k + 2]);
+                const double end = __dadd_rn(f.C[k], __dmul_rn(l_over_rho, d));
+                sg.g0[k] = __double2ll_rn(__dmul_rn(__ddiv_rn(__dsub_rn(f.C[k], org[k]), g.res), 65536.0));
+                sg.g1[k] = __double2ll_rn(__dmul_rn(__ddiv_rn(__dsub_rn(end, org[k]), g.res), 65536.0));
+            }
+            Walker w;
+            w.start(sg);
+            double lvis = 0.0, best = -INFINITY, s_star = -1.0, s_star_out = -1.0, s_inf = 0.0;
+            while (w.inside(g)) {
+                unsigned na, da;
+                bool last;
+                const int a = w.earliest(na, da);
+                const double t_out = crossing_t(a, na, da, last);
+                const double x = L0 + (double)__ldg(T + voxel_slot(g, w.c0, w.c1, w.c2)) * kQInvD;
+                const double sp = softplus_d(x);
+                const double lom = __dadd_rn(sp > 0.0 ? log(__ddiv_rn(sp, g.res)) : -INFINITY, lvis);
+                if (lom > best) {
+                    best = lom;
+                    s_star = w.t_in * L_eval;
+                    s_star_out = t_out * L_eval;
+                }
+                // explicit roundings (no FMA contraction): the oracle's op order, R18
+                lvis = __dsub_rn(lvis, __dmul_rn(__ddiv_rn(__dmul_rn(__dsub_rn(t_out, w.t_in), L_eval), g.res), sp));
+                s_inf = t_out * L_eval;
+                if (last) break;
+                w.advance(na, da);
+                w.t_in = t_out;
+            }
+            const double vis_inf = exp(lvis);
+            const double sig = __dadd_rn(__dadd_rn(n.c0, __dmul_rn(n.c1, Z)), __dmul_rn(__dmul_rn(n.c2, Z), Z));
+            if (vis_inf > vis_thr)
+                r = Z > s_inf;
+            else if (mode == 0)
+                r = fabs(__dsub_rn(Z, s_star)) <= __dmul_rn(k_sigma, sig);
+            else
+                r = Z >= s_star && Z <= s_star_out;
+        }
+        cls[(long long)v * f.W + u] = (int8_t)r;
+    }
+    const unsigned valid = __ballot_sync(0xffffffffu, r >= 0), acc = __ballot_sync(0xffffffffu, r == 1);
+    if ((threadIdx.x & 31) == 0) {
+        if (valid) atomicAdd(&counts[0], (unsigned long long)__popc(valid));
+        if (acc) atomicAdd(&counts[1], (unsigned long long)__popc(acc));
+    }
+}
+
 // ---------------------------------------------------------------- K4
 // Thread per ray walking its incidences in lock step with its warp neighbours; incidences
 // that land in the same voxel at the same step share one cursor atomic.
@@ -584,6 +663,15 @@ void launch_transpose_fill(long long n_rays, const long long* row_ptr, const Ray
 
 void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, int chunk, cudaStream_t s) {
     item_counts_kernel<<<blocks_for(V, 256), 256, 0, s>>>(V, vox_count, n_items, chunk);
+}
+
+void launch_eval(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, const long long* T,
+                 double L0, double k_sigma, double vis_thr, int mode, double L_eval, int8_t* cls,
+                 unsigned long long* counts, cudaStream_t s) {
+    const long long n_pix = (long long)f.rows_owned * f.W;
+    if (n_pix == 0) return;
+    eval_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, T, L0, k_sigma, vis_thr, mode, L_eval, cls,
+                                                       counts);
 }
 
 void launch_vox_hist(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,

@@ -129,6 +129,11 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
 void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, cudaStream_t s);
+// K9 §III.D evaluation of one frame against T: cls per pixel (-1 invalid, 0/1), counts[0..1] +=
+// (valid, accurate) (zeroed by the caller)
+void launch_eval(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, const long long* T,
+                 double L0, double k_sigma, double vis_thr, int mode, double L_eval, int8_t* cls,
+                 unsigned long long* counts, cudaStream_t s);
 // voxel degrees (per-voxel transpose, active count): vox_count zeroed by the caller
 void launch_vox_hist(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                      int32_t* vox_count, cudaStream_t s);

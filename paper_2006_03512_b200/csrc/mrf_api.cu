@@ -118,6 +118,7 @@ struct mrf_ctx {
     DBuf<long long> T, T_part;
     DBuf<float2> lutp;
     DBuf<float> depth_stage, marg;
+    DBuf<int8_t> eval_cls;
     DBuf<long long> scan_scratch;
     DBuf<unsigned long long> counters;
     DBuf<int32_t> class_all;                 // ray ids grouped by K5 class
@@ -568,12 +569,12 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(c->tile_runs.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
-        CK(c->counters.ensure(8, 0, c->stream));
+        CK(c->counters.ensure(10, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
         CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
         CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
-        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 8, c->stream));
+        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 10, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
         // LUT as (L[i][j], L[i][j+1]) pairs: one 8-byte load per LUT row in K5.  The values are
         // the input table's floats, unscaled and unshifted.
@@ -625,7 +626,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
-    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release(); c->eval_cls.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
@@ -825,6 +826,60 @@ mrf_status mrf_marginals(mrf_ctx* ctx, float* out, int32_t out_is_device) {
     if (!out_is_device)
         CK(cudaMemcpyAsync(out, dst, sizeof(float) * c->V, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
+mrf_status mrf_evaluate(mrf_ctx* ctx, const float* depth, int32_t width, int32_t height, const double K[4],
+                        const double T_wc[12], int32_t mode, double k_sigma, double vis_threshold, int8_t* cls,
+                        int64_t* n_valid, int64_t* n_accurate) {
+    ENTER(ctx);
+    if (!depth || !K || !T_wc) return set_err(c, MRF_ERR_INVALID_ARG, "NULL argument");
+    if (width <= 0 || height <= 0) return set_err(c, MRF_ERR_INVALID_ARG, "width/height must be > 0");
+    if (!(k_sigma > 0) || !(vis_threshold > 0 && vis_threshold < 1) || (mode != MRF_EVAL_SIGMA_BAND && mode != MRF_EVAL_VOXEL_BOUNDS))
+        return set_err(c, MRF_ERR_INVALID_ARG, "need k_sigma > 0, 0 < vis_threshold < 1 and a known mode");
+    if (!finite_all(K, 4) || !(K[0] > 0) || !(K[1] > 0)) return set_err(c, MRF_ERR_INVALID_ARG, "bad K");
+    if (!finite_all(T_wc, 12)) return set_err(c, MRF_ERR_INVALID_ARG, "T_wc must be finite");
+    const double org[3] = {c->grid.ox, c->grid.oy, c->grid.oz};
+    const int dims[3] = {c->grid.nx, c->grid.ny, c->grid.nz};
+    for (int k = 0; k < 3; ++k) {
+        const double g = (T_wc[4 * k + 3] - org[k]) / c->grid.res;
+        if (!(g >= 0.0 && g < (double)dims[k]))
+            return set_err(c, MRF_ERR_INVALID_ARG, "camera centre lies outside the grid");
+    }
+    const size_t npix = (size_t)width * height;
+    const float* d_depth = depth;
+    cudaPointerAttributes attr;
+    cudaError_t pe = cudaPointerGetAttributes(&attr, depth);
+    if (pe != cudaSuccess) cudaGetLastError();
+    if (!(pe == cudaSuccess && (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged))) {
+        CK(c->depth_stage.ensure(npix, 0, c->stream));
+        CK(cudaMemcpyAsync(c->depth_stage.p, depth, npix * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+        d_depth = c->depth_stage.p;
+    }
+    CK(c->eval_cls.ensure(npix, 0, c->stream));
+    CK(cudaMemsetAsync(c->eval_cls.p, -2, npix, c->stream));
+    CK(cudaMemsetAsync(c->counters.p + 8, 0, 2 * sizeof(unsigned long long), c->stream));
+    FrameDesc f{};
+    f.fx = K[0]; f.fy = K[1]; f.cx = K[2]; f.cy = K[3];
+    for (int k = 0; k < 3; ++k) {
+        for (int j = 0; j < 3; ++j) f.R[3 * k + j] = T_wc[4 * k + j];
+        f.C[k] = T_wc[4 * k + 3];
+    }
+    f.W = width; f.H = height; f.rank = c->rank; f.world = c->world;
+    f.rows_owned = height > c->rank ? (height - c->rank + c->world - 1) / c->world : 0;
+    f.ray_base = 0;
+    // R19: the evaluation ray runs to 1.5 x the grid diagonal (past the boundary from any camera
+    // inside the grid); same expression as the oracle's
+    const double D = c->grid.res * std::sqrt((double)dims[0] * dims[0] + (double)dims[1] * dims[1] +
+                                             (double)dims[2] * dims[2]);
+    launch_eval(f, c->grid, c->noise, d_depth, c->T.p, c->L0, k_sigma, vis_threshold, mode, 1.5 * D, c->eval_cls.p,
+                c->counters.p + 8, c->stream);
+    CK_LAUNCH(MRF_K_MARGINALS, 1);
+    CK(cudaMemcpyAsync(c->pinned, c->counters.p + 8, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    if (cls) CK(cudaMemcpyAsync(cls, c->eval_cls.p, npix, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (n_valid) *n_valid = c->pinned[0];
+    if (n_accurate) *n_accurate = c->pinned[1];
     return MRF_OK;
 }
 

@@ -442,3 +442,27 @@ def test_frames100_emulated_ranks_sampled_rays():
             n_kept += len(kept)
     assert n_kept > 1000
     assert np.all((marg >= 0) & (marg <= 1))
+
+
+# ------------------------------------------------------------------ §III.D evaluation metric (NEXT #2)
+
+@pytest.mark.parametrize("name,n_iter", [("tiny", 10), ("frame1", 3)])
+def test_evaluate_matches_oracle(name, n_iter, tiny, frame1):
+    """mrf_evaluate (K9) against the oracle's eval_frame on the same map (the GPU's own beliefs
+    after n_iter iterations): every pixel's class identical, counts identical."""
+    w = tiny if name == "tiny" else frame1
+    p = oracle.Params.from_workload(w)
+    fr = w.frames[0]
+    with _gpu_map(w) as m:
+        m.bp_iterate(n_iter)
+        xmap = p.L0 + m.export_beliefs().astype(np.float64) / 2.0 ** 23
+        cls, nv, na = m.evaluate(fr.depth, fr.K, fr.T_wc)
+        cls_d, nv_d, na_d = m.evaluate(torch.from_numpy(fr.depth).cuda(), fr.K, fr.T_wc, k_sigma=3.0, vis_threshold=0.3)
+        cls_v, nv_v, na_v = m.evaluate(fr.depth, fr.K, fr.T_wc, mode=1)
+    rcls, rnv, rna = oracle.eval_frame(p, fr, xmap)
+    assert np.array_equal(cls, rcls) and (nv, na) == (rnv, rna)
+    rcls3, rnv3, rna3 = oracle.eval_frame(p, fr, xmap, k_sigma=3.0, vis_thr=0.3)
+    assert np.array_equal(cls_d, rcls3) and (nv_d, na_d) == (rnv3, rna3)
+    rclsv, rnvv, rnav = oracle.eval_frame(p, fr, xmap, mode=1)
+    assert np.array_equal(cls_v, rclsv) and (nv_v, na_v) == (rnvv, rnav)
+    assert nv == int(np.sum(fr.depth > 0)) and 0 < na <= nv

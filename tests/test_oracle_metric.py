@@ -140,6 +140,10 @@ def test_eval_pixel_rules_and_brute_force():
         assert vis_inf < 0.5 and abs(s_star - 0.2) < 1e-6  # the slab face 0.2 m ahead (16-bit fixed point)
         sig = p.par[6] + p.par[7] * Z + p.par[8] * Z * Z
         assert cls == (abs(Z - s_star) <= 1.5 * sig) == expect
+    # voxel-bounds mode (§III.D): accurate iff Z lies inside the argmax voxel [0.2, 0.25) m
+    for Zm, expect in [(0.21, 1), (0.249, 1), (0.26, 0), (0.19, 0)]:
+        depth[v, u] = np.float32(Zm)
+        assert oracle.eval_pixel(p, Frame(depth, fr.K, fr.T_wc), u, v, xmap, mode=1)[0] == expect
     # empty map: accurate iff the measurement lies beyond the map boundary
     empty = np.full(p.V, -800.0)
     for Zm, expect in [(5.0, 1), (0.5, 0)]:
