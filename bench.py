@@ -269,25 +269,6 @@ def run_ours(args, rank, world, local_rank):
         except Exception:
             pass
 
-    # ---- map quality (not timed in `value`): §III.D generating-surface accuracy of frame 0 against
-    # the beliefs of the last step (§V), on the GPU (K9)
-    map_acc = None
-    evs = m.maps if hasattr(m, "maps") else [m]  # emulated ranks: every rank evaluates its rows
-    fr0 = w.frames[0]
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    counts = [ev.evaluate(depth_dev[0], fr0.K, fr0.T_wc)[1:] for ev in evs]
-    e1.record(stream)
-    counts_v = [ev.evaluate(depth_dev[0], fr0.K, fr0.T_wc, mode=1)[1:] for ev in evs]
-    torch.cuda.synchronize()
-    cnt = torch.tensor([sum(c[0] for c in counts), sum(c[1] for c in counts), sum(c[1] for c in counts_v)],
-                       dtype=torch.int64, device=dev)
-    if world > 1:
-        dist.all_reduce(cnt)
-    nv, na, nav = int(cnt[0]), int(cnt[1]), int(cnt[2])
-    map_acc = {"frame": 0, "valid_pixels": nv, "score_sigma_band_1.5": na / max(nv, 1),
-               "score_voxel_bounds": nav / max(nv, 1), "ms": e0.elapsed_time(e1)}
-
     if rank == 0:
         kernel_ms = {k: round(v[1] / max(1, args.steps), 4) for k, v in prof.items() if v[0]}
         line = {
@@ -309,7 +290,6 @@ def run_ours(args, rank, world, local_rank):
                          "ms_k5": per_iter_k5, "ms_k6": per_iter_k6, "tile_runs": n_runs},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "map_accuracy": map_acc,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
