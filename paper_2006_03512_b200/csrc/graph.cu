@@ -154,23 +154,22 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long n_pix = (long long)f.rows_owned * f.W;
     int st = 3;
-    int ne = 0;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
         Segment sg;
         st = pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg);
-        int count = 0;
+        int bound = 0;
         RayInfo rz{0, 0.f, 0, 0};
         if (st == 0) {
+            // Upper bound of the walk's length without walking: every DDA step moves at least one
+            // axis one cell towards the cell of the end point, so n <= 1 + sum_k |c_end,k - c_0,k|
+            // (0 if the start cell is outside the grid).  The fill writes the exact n.
             Walker w;
             w.start(sg);
-            while (w.inside(g)) {
-                ++count;
-                unsigned na, da;
-                const int a = w.earliest(na, da);
-                if (a < 0 || na >= da) break;  // end point inside this cell
-                w.advance(na, da);
+            if (w.inside(g)) {
+                bound = 1 + abs((int)(sg.g1[0] >> kFixShift) - w.c0) + abs((int)(sg.g1[1] >> kFixShift) - w.c1) +
+                        abs((int)(sg.g1[2] >> kFixShift) - w.c2);
             }
             // LUT row of the measured range (bin centres, clamped to the edge centres)
             double fz = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(sg.Z, n.z_lo), __dsub_rn(n.z_hi, n.z_lo)),
@@ -182,20 +181,16 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
             rz.iz = iz;
             rz.wz = (float)(fz - (double)iz);
         }
-        rz.n = count;
-        n_r[f.ray_base + i] = (count + kSegAlign - 1) & ~(kSegAlign - 1);  // segments start at multiples of 8
+        rz.n = 0;  // set by the fill
+        n_r[f.ray_base + i] = (bound + kSegAlign - 1) & ~(kSegAlign - 1);  // segments start at multiples of 8
         status[f.ray_base + i] = (int8_t)st;
         ray_z[f.ray_base + i] = rz;
-        ne = count;
     }
     const unsigned inv = __ballot_sync(kFull, st == 1);
     const unsigned drp = __ballot_sync(kFull, st == 2);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(kFull, ne, o);
     if ((threadIdx.x & 31) == 0) {
         if (inv) atomicAdd(&counters[0], (unsigned long long)__popc(inv));
         if (drp) atomicAdd(&counters[1], (unsigned long long)__popc(drp));
-        if (ne) atomicAdd(&counters[2], (unsigned long long)ne);
     }
 }
 
@@ -260,7 +255,8 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long l
 __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
                                                        const float* __restrict__ depth,
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
-                                                       int16_t* off_q, int32_t* tile_runs) {
+                                                       int16_t* off_q, int32_t* tile_runs, RayInfo* ray_z,
+                                                       unsigned long long* counters) {
     __shared__ int s_vid[kFillThreads][8];
     __shared__ short s_off[kFillThreads][8];
     int* sv = s_vid[threadIdx.x];
@@ -272,16 +268,19 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(FrameDesc f, Gri
     Segment sg;
     Walker w;
     RunBuilder rb;
-    long long e = 0;
+    long long e = 0, e_cap = 0;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
+        e = row_ptr[f.ray_base + i];
         if (pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg) == 0) {
             w.start(sg);
             alive = w.inside(g);
-            e = row_ptr[f.ray_base + i];
+            e_cap = row_ptr[f.ray_base + i + 1];  // the segment K1 sized from its bound
         }
     }
+    const long long e_ray = e;
+    bool overflow = false;
     for (;;) {
         const unsigned am = __ballot_sync(kFull, alive);
         if (am == 0) break;
@@ -313,9 +312,25 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(FrameDesc f, Gri
                 w.advance(na, da);
                 w.t_in = t_out;
                 alive = w.inside(g);
+                if (alive && e >= e_cap) {  // cannot happen (K1's bound); never write past the segment
+                    alive = false;
+                    overflow = true;
+                }
             }
             if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so);  // partial tail
         }
+    }
+    int ne = 0;
+    if (i < n_pix) {
+        ne = (int)(e - e_ray);
+        ray_z[f.ray_base + i].n = ne;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(kFull, ne, o);
+    const unsigned ovf = __ballot_sync(kFull, overflow);
+    if (lane == 0) {
+        if (ne) atomicAdd(&counters[0], (unsigned long long)ne);
+        if (ovf) atomicAdd(&counters[1], (unsigned long long)__popc(ovf));
     }
 }
 
@@ -658,12 +673,12 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
 }
 
 void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
-                     const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
-                     int16_t* off_q, float* lnu, int32_t* tile_runs, cudaStream_t s) {
+                     const float* depth, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
+                     int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s) {
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
     dda_fill_kernel<<<blocks_for(n_pix, kFillThreads), kFillThreads, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q,
-                                                                              tile_runs);
+                                                                              tile_runs, ray_z, counters);
     lnu_fill_kernel<<<blocks_for(n_pix, 256), 256, 0, s>>>(f.ray_base, n_pix, mp, row_ptr, ray_z, off_q, lnu);
 }
 

@@ -119,16 +119,17 @@ __device__ __forceinline__ float lut_finish(const LutFetch& f, float wz) {
 }
 
 // ---- launchers (all asynchronous on `s`)
-// K1: per owned pixel -> status, pad8(length) (scan input), RayInfo; counters[0] += invalid,
-// counters[1] += dropped, counters[2] += incidences
+// K1: per owned pixel -> status, pad8(upper bound of the walk's length) (scan input), RayInfo
+// (n = 0); counters[0] += invalid, counters[1] += dropped
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
                          int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s);
 // K3: walk again, write vid / off_q at row_ptr offsets and count the tile runs (K4b) per tile;
 // then log nu per incidence
+// (RayInfo.n = the walk's length; counters[0] += incidences, counters[1] += bound overflows = 0)
 void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
-                     const float* depth, const long long* row_ptr, const RayInfo* ray_z, int32_t* vid,
-                     int16_t* off_q, float* lnu, int32_t* tile_runs, cudaStream_t s);
+                     const float* depth, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
+                     int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s);
 // K9 §III.D evaluation of one frame against T: cls per pixel (-1 invalid, 0/1), counts[0..1] +=
 // (valid, accurate) (zeroed by the caller)
 void launch_eval(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, const long long* T,

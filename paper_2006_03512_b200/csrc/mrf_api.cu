@@ -95,7 +95,8 @@ struct mrf_ctx {
     mrf_status sticky = MRF_OK;
 
     long long R = 0, E = 0;  // rays (owned pixels) and incidence slots (ray segments padded to 4)
-    long long E_real = 0;    // incidences
+    long long E_real = 0;    // incidences (counted by the fills on the device; see sync_fill)
+    bool fill_pending = false;
     long long n_invalid = 0, n_dropped = 0, n_kept = 0;
     DBuf<int32_t> n_r;
     DBuf<int8_t> status;
@@ -239,6 +240,22 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
     return MRF_OK;
 }
 
+// The DDA fills count their incidences (and any bound overflow, which K1's bound excludes) on
+// the device, counters[10..11]; read them once when something needs E_real.
+mrf_status sync_fill(mrf_ctx* c) {
+    if (!c->fill_pending) return MRF_OK;
+    CK(cudaMemcpyAsync(c->pinned, c->counters.p + 10, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->fill_pending = false;
+    c->E_real = c->pinned[0];
+    if (c->pinned[1]) {
+        c->sticky = MRF_ERR_STATE;
+        c->err = "internal: a DDA walk exceeded its precomputed bound";
+        return MRF_ERR_STATE;
+    }
+    return MRF_OK;
+}
+
 // Per-voxel transpose (col_ptr over belief slots, tr) + its K6 work list.  Built by prepare()
 // only for the per-voxel K6 ablation, and lazily for mrf_export_transpose.
 // Voxel degrees on demand (not needed by the BP iteration).
@@ -324,6 +341,7 @@ mrf_status build_tile_runs(mrf_ctx* c) {
 mrf_status prepare(mrf_ctx* c) {
     if (!c->dirty) return MRF_OK;
     mrf_status st;
+    if ((st = sync_fill(c)) != MRF_OK) return st;
     c->vtr_valid = false;
     if (c->k6_voxel) {
         if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
@@ -439,6 +457,10 @@ struct HostLayout {
 };
 
 mrf_status host_layout(mrf_ctx* c, HostLayout& h) {
+    {
+        mrf_status sf = sync_fill(c);
+        if (sf != MRF_OK) return sf;
+    }
     h.row_ptr.resize((size_t)c->R + 1);
     h.info.resize((size_t)c->R);
     h.status.resize((size_t)c->R);
@@ -569,12 +591,12 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(c->tile_runs.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
-        CK(c->counters.ensure(10, 0, c->stream));
+        CK(c->counters.ensure(16, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
         CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
         CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
-        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 10, c->stream));
+        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 16, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
         // LUT as (L[i][j], L[i][j+1]) pairs: one 8-byte load per LUT row in K5.  The values are
         // the input table's floats, unscaled and unshifted.
@@ -671,6 +693,8 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences) {
 mrf_status mrf_reset(mrf_ctx* ctx) {
     ENTER(ctx);
     c->R = c->E = c->E_real = 0;
+    c->fill_pending = false;
+    CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
     CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * c->NT, c->stream));
@@ -735,7 +759,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     f.rows_owned = rows_owned;
     f.ray_base = c->R;
     mrf_status st;
-    CK(cudaMemsetAsync(c->counters.p + 2, 0, 3 * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
     {
         ProfScope ps(c, MRF_K_RAYGEN_COUNT);
         launch_raygen_count(f, c->grid, c->noise, d_depth, c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2,
@@ -744,9 +768,9 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     }
     if ((st = scan(c, c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->E)) != MRF_OK) return st;
     CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R + Rf, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2], n_inc = c->pinned[3];
+    const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2];
     if (E_new >= (1LL << 31) - kPadElems)
         return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
     const size_t ne = (size_t)E_new + kPadElems;
@@ -758,14 +782,14 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     {
         ProfScope ps(c, MRF_K_DDA_FILL);
         launch_dda_fill(f, c->grid, c->noise, c->mp, d_depth, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p, c->lnu.p,
-                        c->tile_runs.p, c->stream);
+                        c->tile_runs.p, c->counters.p + 10, c->stream);
         CK_LAUNCH(MRF_K_DDA_FILL, Rf > 0 ? 2 : 0);  // DDA fill + log-nu fill
     }
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
     c->frames.push_back({width, height, rows_owned, c->R, Rf});
     c->R += Rf;
     c->E = E_new;
-    c->E_real += n_inc;
+    c->fill_pending = true;
     c->n_invalid += inv;
     c->n_dropped += drp;
     c->n_kept += Rf - inv - drp;
@@ -896,6 +920,10 @@ mrf_status mrf_layout_sizes(mrf_ctx* ctx, int64_t* n_slots, int64_t* n_runs, int
 mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences, int64_t* n_active_vox,
                            int64_t* n_invalid, int64_t* n_dropped) {
     ENTER(ctx);
+    {
+        mrf_status sf = sync_fill(c);
+        if (sf != MRF_OK) return sf;
+    }
     if (n_rays) *n_rays = c->n_kept;
     if (n_incidences) *n_incidences = c->E_real;
     if (n_invalid) *n_invalid = c->n_invalid;
@@ -1057,6 +1085,10 @@ mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda) {
 mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda) {
     ENTER(ctx);
     if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL input");
+    {
+        mrf_status sf = sync_fill(c);
+        if (sf != MRF_OK) return sf;
+    }
     std::vector<int32_t> qc((size_t)c->E_real), q((size_t)c->E, 0);
     for (long long e = 0; e < c->E_real; ++e) {
         double x = lambda[e];
