@@ -1,4 +1,5 @@
-"""Diagnostic: messages into the worst one-step marginal voxel (run by hand on a GPU box)."""
+"""Diagnostic (test infrastructure: compares with the oracle): messages into the worst one-step
+marginal voxel (run by hand on a GPU box: python -m tests.debug_voxel)."""
 import numpy as np
 
 import oracle
