@@ -235,7 +235,6 @@ struct RunBuilder {
 // 8-slot chunk of shared memory and writes a whole chunk at once (two 16-byte vid stores, one
 // 16-byte off_q store; segments are 8-aligned, padding slots get 0): one scattered 4-byte and
 // one 2-byte store per step had the walk waiting on the store queue.
-constexpr int kFillThreads = 128;
 __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long long e_chunk, int nvalid,
                                             const int* sv, const short* so) {
     int v[8];
@@ -252,16 +251,32 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long l
     *reinterpret_cast<uint4*>(off_q + e_chunk) = make_uint4(pk(o[0], o[1]), pk(o[2], o[3]), pk(o[4], o[5]), pk(o[6], o[7]));
 }
 
-__global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
-                                                       const float* __restrict__ depth,
+// One launch fills every frame added since the last fill (frames[k] owns the CTAs
+// [cta0[k], cta0[k+1])): one wave-quantisation tail per batch instead of per frame.
+__global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc* __restrict__ frames,
+                                                       const int* __restrict__ cta0, int n_frames, GridDesc g,
+                                                       NoiseDesc n, const float* __restrict__ depth_all,
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
                                                        int16_t* off_q, int32_t* tile_runs, RayInfo* ray_z,
                                                        unsigned long long* counters) {
     __shared__ int s_vid[kFillThreads][8];
     __shared__ short s_off[kFillThreads][8];
+    __shared__ FrameDesc f;
+    __shared__ int s_fi;
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = n_frames - 1;  // last k with cta0[k] <= blockIdx.x
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(cta0 + mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+        }
+        s_fi = lo;
+        f = frames[lo];
+    }
+    __syncthreads();
     int* sv = s_vid[threadIdx.x];
     short* so = s_off[threadIdx.x];
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long i = (long long)((int)blockIdx.x - __ldg(cta0 + s_fi)) * kFillThreads + threadIdx.x;
+    const float* __restrict__ depth = depth_all + f.depth_off;
     const long long n_pix = (long long)f.rows_owned * f.W;
     const int lane = threadIdx.x & 31;
     bool alive = false;
@@ -672,14 +687,14 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
     raygen_count_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, n_r, status, ray_z, counters);
 }
 
-void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
-                     const float* depth, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
+void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, long long r0,
+                     long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
+                     const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s) {
-    const long long n_pix = (long long)f.rows_owned * f.W;
-    if (n_pix == 0) return;
-    dda_fill_kernel<<<blocks_for(n_pix, kFillThreads), kFillThreads, 0, s>>>(f, g, n, depth, row_ptr, vid, off_q,
-                                                                              tile_runs, ray_z, counters);
-    lnu_fill_kernel<<<blocks_for(n_pix, 256), 256, 0, s>>>(f.ray_base, n_pix, mp, row_ptr, ray_z, off_q, lnu);
+    if (n_ctas > 0)
+        dda_fill_kernel<<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, off_q,
+                                                        tile_runs, ray_z, counters);
+    if (n_rays > 0) lnu_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(r0, n_rays, mp, row_ptr, ray_z, off_q, lnu);
 }
 
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,

@@ -75,6 +75,7 @@ struct FrameDesc {
     int W, H, rank, world;
     int rows_owned;           // number of pixel rows v with v % world == rank
     long long ray_base;       // index of this frame's first ray
+    long long depth_off;      // offset of the frame's depth image in the pending-depth buffer
 };
 
 // Per-ray record: LUT row iz (<= n_z-2) and weight wz in [0,1] of the measured range, and the
@@ -124,11 +125,14 @@ __device__ __forceinline__ float lut_finish(const LutFetch& f, float wz) {
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
                          int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s);
-// K3: walk again, write vid / off_q at row_ptr offsets and count the tile runs (K4b) per tile;
-// then log nu per incidence
+// K3: the walk of every pending frame (device FrameDesc array, frame k owning the CTAs
+// [cta0[k], cta0[k+1]) of kFillThreads pixels), writing vid / off_q at row_ptr offsets and
+// counting the tile runs (K4b) per tile; then log nu per incidence of the rays [r0, r0 + n_rays)
 // (RayInfo.n = the walk's length; counters[0] += incidences, counters[1] += bound overflows = 0)
-void launch_dda_fill(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
-                     const float* depth, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
+constexpr int kFillThreads = 128;
+void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, long long r0,
+                     long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
+                     const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s);
 // K9 §III.D evaluation of one frame against T: cls per pixel (-1 invalid, 0/1), counts[0..1] +=
 // (valid, accurate) (zeroed by the caller)

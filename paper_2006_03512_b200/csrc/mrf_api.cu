@@ -119,6 +119,14 @@ struct mrf_ctx {
     DBuf<long long> T, T_part;
     DBuf<float2> lutp;
     DBuf<float> depth_stage, marg;
+    // frames added since the last fill: the walk (K3) of all of them runs as one launch when
+    // the graph is next needed (sync_fill)
+    DBuf<float> depth_all;       // their depth images
+    long long depth_used = 0;
+    std::vector<FrameDesc> pend;
+    DBuf<FrameDesc> d_frames;
+    DBuf<int> d_cta0;
+    long long E_filled = 0, R_filled = 0;  // incidences / rays already walked
     DBuf<int8_t> eval_cls;
     DBuf<long long> scan_scratch;
     DBuf<unsigned long long> counters;
@@ -244,6 +252,35 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
 // the device, counters[10..11]; read them once when something needs E_real.
 mrf_status sync_fill(mrf_ctx* c) {
     if (!c->fill_pending) return MRF_OK;
+    if (!c->pend.empty()) {
+        const size_t ne = (size_t)c->E + kPadElems;
+        CK(c->vid.ensure(ne, (size_t)c->E_filled, c->stream));
+        CK(c->off_q.ensure(ne, (size_t)c->E_filled, c->stream));
+        CK(c->lnu.ensure(ne, (size_t)c->E_filled, c->stream));
+        CK(c->lam.ensure(ne, (size_t)c->E_filled, c->stream));
+        CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
+        const int nf = (int)c->pend.size();
+        std::vector<int> cta0((size_t)nf + 1, 0);
+        for (int k = 0; k < nf; ++k) {
+            const long long n_pix = (long long)c->pend[k].rows_owned * c->pend[k].W;
+            cta0[k + 1] = cta0[k] + (int)((n_pix + kFillThreads - 1) / kFillThreads);
+        }
+        CK(c->d_frames.ensure((size_t)nf, 0, c->stream));
+        CK(c->d_cta0.ensure((size_t)nf + 1, 0, c->stream));
+        CK(cudaMemcpyAsync(c->d_frames.p, c->pend.data(), sizeof(FrameDesc) * nf, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->d_cta0.p, cta0.data(), sizeof(int) * (nf + 1), cudaMemcpyHostToDevice, c->stream));
+        {
+            ProfScope ps(c, MRF_K_DDA_FILL);
+            launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
+                            c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
+                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, c->stream);
+            CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (c->R > c->R_filled ? 1 : 0));
+        }
+        c->pend.clear();
+        c->depth_used = 0;
+        c->E_filled = c->E;
+        c->R_filled = c->R;
+    }
     CK(cudaMemcpyAsync(c->pinned, c->counters.p + 10, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->fill_pending = false;
@@ -648,7 +685,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
-    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->marg.release(); c->eval_cls.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->marg.release(); c->eval_cls.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
@@ -682,10 +719,10 @@ mrf_status mrf_reserve(mrf_ctx* ctx, int64_t n_rays, int64_t n_incidences) {
     CK(c->flags.ensure((size_t)std::max<long long>(n_rays, c->VI) + 1, 0, c->stream));
     CK(c->pos.ensure((size_t)std::max<long long>(n_rays, c->VI) + 1, 0, c->stream));
     const size_t ne = (size_t)n_incidences + kPadElems;
-    CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
-    CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
-    CK(c->lnu.ensure(ne, (size_t)c->E, c->stream));
-    CK(c->lam.ensure(ne, (size_t)c->E, c->stream));
+    CK(c->vid.ensure(ne, (size_t)c->E_filled, c->stream));
+    CK(c->off_q.ensure(ne, (size_t)c->E_filled, c->stream));
+    CK(c->lnu.ensure(ne, (size_t)c->E_filled, c->stream));
+    CK(c->lam.ensure(ne, (size_t)c->E_filled, c->stream));
     CK(c->tr.ensure(ne, 0, c->stream));
     return MRF_OK;
 }
@@ -694,6 +731,9 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     ENTER(ctx);
     c->R = c->E = c->E_real = 0;
     c->fill_pending = false;
+    c->pend.clear();
+    c->depth_used = 0;
+    c->E_filled = c->R_filled = 0;
     CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
@@ -732,18 +772,16 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     const long long Rf = (long long)rows_owned * width;
     if (c->R + Rf >= (1LL << 31)) return set_err(c, MRF_ERR_CAPACITY, "ray count would exceed 2^31");
 
-    // depth: device pointer used in place, host memory staged
-    const float* d_depth = depth;
+    // depth (host or device memory) copied into the pending-depth buffer: the walk runs later
     cudaPointerAttributes attr;
     cudaError_t pe = cudaPointerGetAttributes(&attr, depth);
     if (pe != cudaSuccess) cudaGetLastError();
     const bool on_device = pe == cudaSuccess && (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged);
     const size_t npix = (size_t)width * height;
-    if (!on_device) {
-        CK(c->depth_stage.ensure(npix, 0, c->stream));
-        CK(cudaMemcpyAsync(c->depth_stage.p, depth, npix * sizeof(float), cudaMemcpyHostToDevice, c->stream));
-        d_depth = c->depth_stage.p;
-    }
+    CK(c->depth_all.ensure((size_t)c->depth_used + npix, (size_t)c->depth_used, c->stream));
+    const float* d_depth = c->depth_all.p + c->depth_used;
+    CK(cudaMemcpyAsync(c->depth_all.p + c->depth_used, depth, npix * sizeof(float),
+                       on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, c->stream));
     CK(c->n_r.ensure((size_t)(c->R + Rf), (size_t)c->R, c->stream));
     CK(c->status.ensure((size_t)(c->R + Rf), (size_t)c->R, c->stream));
     CK(c->ray_z.ensure((size_t)(c->R + Rf), (size_t)c->R, c->stream));
@@ -773,18 +811,9 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2];
     if (E_new >= (1LL << 31) - kPadElems)
         return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
-    const size_t ne = (size_t)E_new + kPadElems;
-    CK(c->vid.ensure(ne, (size_t)c->E, c->stream));
-    CK(c->off_q.ensure(ne, (size_t)c->E, c->stream));
-    CK(c->lnu.ensure(ne, (size_t)c->E, c->stream));
-    CK(c->lam.ensure(ne, (size_t)c->E, c->stream));
-    CK(cudaMemsetAsync(c->lam.p + c->E, 0, sizeof(int32_t) * (size_t)(E_new - c->E), c->stream));
-    {
-        ProfScope ps(c, MRF_K_DDA_FILL);
-        launch_dda_fill(f, c->grid, c->noise, c->mp, d_depth, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p, c->lnu.p,
-                        c->tile_runs.p, c->counters.p + 10, c->stream);
-        CK_LAUNCH(MRF_K_DDA_FILL, Rf > 0 ? 2 : 0);  // DDA fill + log-nu fill
-    }
+    f.depth_off = c->depth_used;
+    c->depth_used += (long long)npix;
+    if (Rf > 0) c->pend.push_back(f);
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
     c->frames.push_back({width, height, rows_owned, c->R, Rf});
     c->R += Rf;
@@ -795,7 +824,6 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     c->n_kept += Rf - inv - drp;
     c->dirty = true;
     c->hist_valid = false;
-    if (!on_device) CK(cudaStreamSynchronize(c->stream));  // staging buffer reused by the next frame
     return MRF_OK;
 }
 
@@ -985,6 +1013,10 @@ mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const 
                            int64_t* row_ptr, int32_t* vid, int16_t* off_q, float* lambda) {
     ENTER(ctx);
     if (n < 0 || (n > 0 && (!frame || !pixel)) || cap < 0) return set_err(c, MRF_ERR_INVALID_ARG, "bad ray selection");
+    {
+        mrf_status sf = sync_fill(c);
+        if (sf != MRF_OK) return sf;
+    }
     std::vector<long long> rid((size_t)n);
     for (long long k = 0; k < n; ++k) {
         if (frame[k] < 0 || frame[k] >= (int)c->frames.size()) return set_err(c, MRF_ERR_INVALID_ARG, "bad frame id");
