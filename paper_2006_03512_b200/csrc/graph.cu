@@ -194,9 +194,20 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
     }
 }
 
-// Tile-run builder (K4b): a run ends where the tile changes (a ray crosses a convex tile once),
-// after kRunMax incidences, or before a step that is not a single-axis unit step (an exact DDA
-// tie).  Used by the DDA fill (runs per tile) and by run_fill (the runs themselves).
+// Tile runs (K4b): a run ends where the tile changes (a ray crosses a convex tile once), after
+// kRunMax incidences, or before a step that is not a single-axis unit step (an exact DDA tie).
+// Split rule (shared by the count in K3 and the transpose fill K4b, which must agree):
+// incidence (tile b, in-tile slot l) extends the current run (tile, length n, last slot prev)
+// iff it lies in the same tile, the run holds fewer than kRunMax incidences and the step is a
+// single-axis unit step.  Consecutive cells of a DDA walk differ by at most one per axis, so
+// the slot difference d = dx + 32 dy + 1024 dz (balanced base-32 digits) is a single-axis unit
+// step iff |d| is 1, 32 or 1024.
+__device__ __forceinline__ bool run_extends(int b, int l, int tile, int n, int prev) {
+    const int ad = abs(l - prev);
+    return b == tile && n < kRunMax && (ad == 1 || ad == 32 || ad == 1024);
+}
+
+// Run builder of the transpose fill (K4b)
 struct RunBuilder {
     int tile = -1, n = 0, prev = 0;  // current run: tile, length, in-tile slot of its last element
     long long start = 0;
@@ -207,7 +218,7 @@ struct RunBuilder {
         const int dx = (l & 31) - (prev & 31), dy = ((l >> 5) & 31) - ((prev >> 5) & 31), dz = (l >> 10) - (prev >> 10);
         if ((dx != 0) + (dy != 0) + (dz != 0) != 1) return false;
         const int d = dx + dy + dz;
-        if (d != 1 && d != -1) return false;
+        if (d != 1 && d != -1) return false;  // same rule as run_extends
         const int ax = dx ? 0 : (dy ? 1 : 2);
         if (ax == 0) mx |= 1u << (n - 1);
         if (ax == 1) my |= 1u << (n - 1);
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
     bool alive = false;
     Segment sg;
     Walker w;
-    RunBuilder rb;
+    int run_tile = -1, run_n = 0, run_prev = 0;  // current tile run (K4b count)
     long long e = 0, e_cap = 0;
     if (i < n_pix) {
         int u, v;
@@ -314,8 +325,10 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             ++e;
             // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
             const int b = vx >> kTileShift, l = vx & (kTileSlots - 1);
-            const bool start = !rb.extend(b, l);
-            if (start) rb.begin(b, l, 0);
+            const bool start = !run_extends(b, l, run_tile, run_n, run_prev);
+            run_n = start ? 1 : run_n + 1;
+            run_tile = b;
+            run_prev = l;
             const unsigned sm = __ballot_sync(am, start);
             if (start) {
                 const unsigned peers = __match_any_sync(sm, b);
