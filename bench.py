@@ -258,16 +258,24 @@ def run_ours(args, rank, world, local_rank):
     ach_22 = gbs(22 * E_local + 16 * V, per_iter_k5 + per_iter_k6)
     dominant = "ray_messages" if ms_k5 >= ms_k6 else "voxel_sum"
     ach = ach_k5 if dominant == "ray_messages" else ach_k6
-    traffic = None
+    # ncu DRAM bytes per launch (one --set full capture of this workload, profiles/ncu_summary.json)
+    # over the live kernel times: SURVEY §8(d)'s reporting rule 1 (achieved DRAM GB/s / peak)
+    traffic_of = {}
     prof_json = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_json):
         try:
             d = json.load(open(prof_json))
-            k = d.get("kernels", {}).get(dominant)
-            if k and k.get("config") == args.config and k.get("E") == E_local:
-                traffic = k.get("dram_bytes_per_launch")
+            for name, k in d.get("kernels", {}).items():
+                if k.get("config") == args.config and k.get("E") == E_local:
+                    traffic_of[name] = k.get("dram_bytes_per_launch")
         except Exception:
             pass
+    traffic = traffic_of.get(dominant)
+    dram = {}
+    if "ray_messages" in traffic_of and "voxel_sum" in traffic_of:
+        t5, t6 = traffic_of["ray_messages"], traffic_of["voxel_sum"]
+        dram = {"k5_dram_frac": gbs(t5, per_iter_k5) / peak, "k6_dram_frac": gbs(t6, per_iter_k6) / peak,
+                "bp_iteration_dram_frac": gbs(t5 + t6, per_iter_k5 + per_iter_k6) / peak}
 
     if rank == 0:
         kernel_ms = {k: round(v[1] / max(1, args.steps), 4) for k, v in prof.items() if v[0]}
@@ -287,7 +295,7 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_bytes_per_launch": bytes_k5 if dominant == "ray_messages" else bytes_k6,
                          "k5_frac": ach_k5 / peak, "k6_frac": ach_k6 / peak,
                          "bp_iteration_frac": ach_bp / peak, "bp_iteration_frac_survey22B": ach_22 / peak,
-                         "ms_k5": per_iter_k5, "ms_k6": per_iter_k6, "tile_runs": n_runs},
+                         "ms_k5": per_iter_k5, "ms_k6": per_iter_k6, "tile_runs": n_runs, **dram},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),
