@@ -10,7 +10,8 @@ numpy arrays to it and assembles the per-frame CSR in canonical order
 Every function cites the SURVEY §8(c) step (B1..B7) / PAPER.md lines it follows;
 the pins that tie it to the paper are in tests/test_oracle_*.py.  Parity status:
   B1 ray setup, B2 DDA, B3 offsets/LUT, B5 single-ray messages, B5+B6 on tree
-  graphs, §III.D evaluation metric (vis_profile / eval_pixel): pinned.  B5+B6 on loopy graphs (several overlapping rays): parity
+  graphs, §III.D evaluation metric (vis_profile / eval_pixel), NEXT #3 keyframe averages
+  (kf_*: SPEC's worked examples, and equal to B5 when each keyframe has one ray per voxel): pinned.  B5+B6 on loopy graphs (several overlapping rays): parity
   unpinned beyond the invariants (loopy BP has no closed form).
 """
 
@@ -72,6 +73,14 @@ def lib():
             L.orc_bp.restype = None
             L.orc_marginals.argtypes = [i64, d, dp, dp]
             L.orc_marginals.restype = None
+            L.orc_kf_beliefs.argtypes = [i64, i64, dp, dp]
+            L.orc_kf_beliefs.restype = None
+            L.orc_kf_average.argtypes = [i64, i64p, i32p, i32p, dp, i64, i64, dp]
+            L.orc_kf_average.restype = None
+            L.orc_kf_pass.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, dp, dp]
+            L.orc_kf_pass.restype = None
+            L.orc_kf_bp.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, i32, dp, dp, dp]
+            L.orc_kf_bp.restype = None
             L.orc_frame_count.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32, i8p, i64p, dp, dp]
             L.orc_frame_count.restype = None
             L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p]
@@ -297,6 +306,54 @@ def marginals(p: Params, T):
     out = np.zeros(len(T))
     lib().orc_marginals(len(T), p.L0, _ptr(T, ctypes.c_double), _ptr(out, ctypes.c_double))
     return out
+
+
+# --------------------------------------------------------------------------- NEXT #3
+
+def kf_average(g: Graph, lam, F: int, V: int):
+    """Keyframe averages (SPEC accumulate_outgoing): lbar[f, v] = log(mean sigma(lam) /
+    mean sigma(-lam)) over keyframe f's incidences of v, 0 where f has none."""
+    lbar = np.zeros(F * V)
+    lib().orc_kf_average(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
+                         _ptr(_c(g.frame, np.int32), ctypes.c_int32), _ptr(_c(lam, np.float64), ctypes.c_double),
+                         F, V, _ptr(lbar, ctypes.c_double))
+    return lbar.reshape(F, V)
+
+
+def kf_beliefs(lbar):
+    """T_v = sum_f lbar[f, v] (one message per keyframe)."""
+    lbar = _c(lbar, np.float64)
+    F, V = lbar.shape
+    T = np.zeros(V)
+    lib().orc_kf_beliefs(F, V, _ptr(lbar, ctypes.c_double), _ptr(T, ctypes.c_double))
+    return T
+
+
+def kf_pass(p: Params, g: Graph, lbar):
+    """One flooding pass of the keyframe-average variant from the snapshot lbar[F, V] ->
+    per-incidence messages (cavity excludes the ray's whole keyframe)."""
+    lbar = _c(lbar, np.float64)
+    F, V = lbar.shape
+    lam = np.zeros(g.E)
+    lib().orc_kf_pass(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
+                      _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
+                      _ptr(_c(g.frame, np.int32), ctypes.c_int32), _ptr(p.lut, ctypes.c_float), p.lut.shape[0],
+                      p.lut.shape[1], _ptr(p.par, ctypes.c_double), p.L0, F, V, _ptr(lbar, ctypes.c_double),
+                      _ptr(lam, ctypes.c_double))
+    return lam
+
+
+def kf_bp(p: Params, g: Graph, n_iter: int, F: int, lbar=None):
+    """n iterations of the keyframe-average variant -> (lam, lbar[F, V], T)."""
+    lbar = np.zeros((F, p.V)) if lbar is None else _c(lbar, np.float64).copy()
+    lam = np.zeros(g.E)
+    T = np.zeros(p.V)
+    lib().orc_kf_bp(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
+                    _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
+                    _ptr(_c(g.frame, np.int32), ctypes.c_int32), _ptr(p.lut, ctypes.c_float), p.lut.shape[0],
+                    p.lut.shape[1], _ptr(p.par, ctypes.c_double), p.L0, F, p.V, int(n_iter),
+                    _ptr(lam, ctypes.c_double), _ptr(lbar, ctypes.c_double), _ptr(T, ctypes.c_double))
+    return lam, lbar, T
 
 
 def run(workload, n_iter=None, rank=0, world=1):

@@ -18,6 +18,8 @@
  *   orc_ray_messages B5 single-ray messages (Eq.13/14)     pinned: 2^N enumeration of Eq.12
  *   orc_ray_pass + orc_accumulate  B5 flooding iteration   pinned: exact marginals on trees
  *   orc_marginals   B6 (Eq.8)                              pinned: unseen voxel = prior
+ *   orc_kf_*        NEXT #3 keyframe-average variant       pinned: SPEC worked examples, one ray
+ *                                                          per (keyframe, voxel) = B5 iteration
  */
 #include <math.h>
 #include <stdint.h>
@@ -270,6 +272,95 @@ void orc_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const in
 /* B6: p_v = sigma(L0 + T_v) (Eq.8); an unobserved voxel (T_v = 0) gives gamma. */
 void orc_marginals(int64_t V, double L0, const double* T, double* p) {
     for (int64_t v = 0; v < V; ++v) p[v] = 1.0 / (1.0 + exp(-(L0 + T[v])));
+}
+
+/* ------------------------------------------------------------------ NEXT #3: keyframe averages
+ * The paper's memory-saving variant: "we make an assumption that all rays going through
+ * a voxel from a single keyframe send the same average message.  Thus, for each new keyframe
+ * image we create an auxiliary buffer that stores the average outgoing message."  Restated with
+ * SPEC's KeyframeBuffer / accumulate_outgoing / incoming_product (reading R22 in DESIGN.md):
+ *   lbar[f][v]  log-odds of keyframe f's average message into voxel v; 0 (the uniform pair) when
+ *               no ray of f reaches v ("zero accumulations -> uniform");
+ *   T_v         = sum_f lbar[f][v]  (Eq.6 / Eq.8 with one message per keyframe);
+ *   pass        every ray r of keyframe f from the same snapshot (flooding, reading R4):
+ *               c_i = L0 + T[v_i] - lbar[f][v_i]  (incoming_product excluding the ray's whole
+ *               keyframe), messages by B5, lambda_e = clip(lpos - lneg, +-256);
+ *   average     mu1 = mean of sigma(lambda_e), mu0 = mean of sigma(-lambda_e) over the keyframe's
+ *               incidences of v (arithmetic mean of the normalised pairs), and
+ *               lbar[f][v] = clip(log(mu1 / mu0), +-256). */
+static double sigmoid(double x) { return x >= 0.0 ? 1.0 / (1.0 + exp(-x)) : exp(x) / (1.0 + exp(x)); }
+
+/* T_v = sum over keyframes of lbar[f][v] (F*V, keyframe-major) */
+void orc_kf_beliefs(int64_t F, int64_t V, const double* lbar, double* T) {
+    memset(T, 0, sizeof(double) * (size_t)V);
+    for (int64_t f = 0; f < F; ++f)
+        for (int64_t v = 0; v < V; ++v) T[v] += lbar[f * V + v];
+}
+
+/* accumulate_outgoing + average: lbar[f][v] from the per-incidence messages of every ray;
+ * frame[r] is the keyframe of ray r.  Pairs without a ray keep lbar = 0. */
+void orc_kf_average(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int32_t* frame,
+                    const double* lambda, int64_t F, int64_t V, double* lbar) {
+    double* s1 = (double*)calloc((size_t)(F * V), sizeof(double));
+    double* s0 = (double*)calloc((size_t)(F * V), sizeof(double));
+    for (int64_t r = 0; r < n_rays; ++r)
+        for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+            const int64_t k = (int64_t)frame[r] * V + vid[e];
+            s1[k] += sigmoid(lambda[e]);  /* mu_{psi->o}(1) of the normalised pair */
+            s0[k] += sigmoid(-lambda[e]); /* mu_{psi->o}(0) */
+        }
+    for (int64_t k = 0; k < F * V; ++k) lbar[k] = (s1[k] + s0[k] > 0.0) ? clip256(log(s1[k] / s0[k])) : 0.0;
+    free(s1);
+    free(s0);
+}
+
+/* One flooding pass of the variant: lambda (per incidence, out) from the snapshot lbar. */
+void orc_kf_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
+                 const double* Z_ray, const int32_t* frame, const float* lut, int32_t n_z, int32_t n_off,
+                 const double par[9], double L0, int64_t F, int64_t V, const double* lbar, double* lambda) {
+    double* T = (double*)malloc(sizeof(double) * (size_t)V);
+    orc_kf_beliefs(F, V, lbar, T);
+#pragma omp parallel
+    {
+        int64_t cap = 0;
+        double* buf = NULL;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t r = 0; r < n_rays; ++r) {
+            const int64_t e0 = row_ptr[r], N = row_ptr[r + 1] - e0;
+            if (N <= 0) continue;
+            if (N > cap) {
+                free(buf);
+                cap = N * 2;
+                buf = (double*)malloc(sizeof(double) * 9 * cap);
+            }
+            double* c = buf;
+            double* lnu = buf + N;
+            double* lpos = buf + 2 * N;
+            double* lneg = buf + 3 * N;
+            double* work = buf + 4 * N;
+            const double* lb = lbar + (int64_t)frame[r] * V;
+            for (int64_t i = 0; i < N; ++i) {
+                c[i] = L0 + T[vid[e0 + i]] - lb[vid[e0 + i]];
+                lnu[i] = orc_log_nu(lut, n_z, n_off, par, Z_ray[r], off_q[e0 + i]);
+            }
+            orc_ray_messages(N, c, lnu, lpos, lneg, work);
+            for (int64_t i = 0; i < N; ++i) lambda[e0 + i] = clip256(lpos[i] - lneg[i]);
+        }
+        free(buf);
+    }
+    free(T);
+}
+
+/* n iterations of the variant from lbar (in/out; zeros = B4); lambda out; T = sum_f lbar. */
+void orc_kf_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
+               const double* Z_ray, const int32_t* frame, const float* lut, int32_t n_z, int32_t n_off,
+               const double par[9], double L0, int64_t F, int64_t V, int32_t n_iter, double* lambda,
+               double* lbar, double* T) {
+    for (int32_t it = 0; it < n_iter; ++it) {
+        orc_kf_pass(n_rays, row_ptr, vid, off_q, Z_ray, frame, lut, n_z, n_off, par, L0, F, V, lbar, lambda);
+        orc_kf_average(n_rays, row_ptr, vid, frame, lambda, F, V, lbar);
+    }
+    orc_kf_beliefs(F, V, lbar, T);
 }
 
 /* ------------------------------------------------------------------ frames -> CSR */
