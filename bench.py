@@ -95,14 +95,17 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- reference arm
 
-def _oracle_sample(w, max_frames=1):
+def _oracle_sample(w, max_frames=1, messages="per-ray"):
     """The oracle as it stands on a bounded sample: the first `max_frames` frames of the
     workload, graph build + n iterations.  Returns (updates, seconds, E)."""
     import oracle
     p = oracle.Params.from_workload(w)
     t0 = time.perf_counter()
     g = oracle.build_graph(p, w.frames[:max_frames])
-    oracle.bp(p, g, w.n_iter)
+    if messages == "keyframe-avg":
+        oracle.kf_bp(p, g, w.n_iter, F=max_frames)
+    else:
+        oracle.bp(p, g, w.n_iter)
     dt = time.perf_counter() - t0
     return g.E * w.n_iter, dt, g.E
 
@@ -113,10 +116,10 @@ def run_reference(args, rank, world):
         return
     w = synth.make_workload(args.config)
     for _ in range(args.warmup):
-        _oracle_sample(w, 1)
+        _oracle_sample(w, 1, args.messages)
     tot_u = tot_t = 0.0
     for _ in range(args.steps):
-        u, dt, E = _oracle_sample(w, 1)
+        u, dt, E = _oracle_sample(w, 1, args.messages)
         tot_u += u
         tot_t += dt
     v = tot_u / tot_t
@@ -156,6 +159,8 @@ def run_ours(args, rank, world, local_rank):
     # summed on the device.
     emulate = args.emulate_ranks if args.emulate_ranks is not None else (
         4 if (world == 1 and args.config in ("frames100", "sweep300")) else 1)
+    if args.messages == "keyframe-avg":
+        assert world == 1 and emulate == 1, "keyframe averages are single-rank (one ctx, < 2^31 incidences)"
     if emulate > 1:
         assert world == 1, "--emulate-ranks is a single-GPU mode"
         from paper_2006_03512_b200.dist import EmulatedRanks
@@ -163,6 +168,8 @@ def run_ours(args, rank, world, local_rank):
     else:
         m = pkg.MRFMap.from_workload(w, **kw)
         m.set_stream(stream.cuda_stream)
+        if args.messages == "keyframe-avg":  # NEXT #3: the paper's per-keyframe average messages
+            m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
 
     depth_dev = [torch.from_numpy(fr.depth).to(dev) for fr in w.frames]
     depth_host = [torch.from_numpy(fr.depth).pin_memory() for fr in w.frames]
@@ -266,7 +273,7 @@ def run_ours(args, rank, world, local_rank):
         try:
             d = json.load(open(prof_json))
             for name, k in d.get("kernels", {}).items():
-                if k.get("config") == args.config and k.get("E") == E_local:
+                if k.get("config") == args.config and k.get("E") == E_local and args.messages == "per-ray":
                     traffic_of[name] = k.get("dram_bytes_per_launch")
         except Exception:
             pass
@@ -285,6 +292,7 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": args.config, "frames": len(w.frames), "bp_iterations": n_iter,
+                       "messages": args.messages,
                        "incidences": E_all, "rays": R_all, "voxels": V, "grid": list(w.dims), "res_m": w.res,
                        "parallelism": f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else "1 GPU",
                        "l2": f"inputs larger than L2: messages {4 * E_all / 1e9:.2f} GB, graph {10 * E_all / 1e9:.2f} GB"},
@@ -301,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            u, dt, Es = _oracle_sample(w, 1)
+            u, dt, Es = _oracle_sample(w, 1, args.messages)
             line["cpu_baseline"] = {"value": u / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
                                     "sample": f"first frame of {args.config} (E={Es}), graph build + "
                                               f"{w.n_iter} BP iterations, fp64"}
@@ -318,6 +326,8 @@ def main():
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--messages", default="per-ray", choices=["per-ray", "keyframe-avg"],
+                    help="message model: exact per-ray messages (north_star) or per-keyframe averages (P:200)")
     ap.add_argument("--emulate-ranks", type=int, default=None,
                     help="ranks emulated on the one GPU (default: 4 for the 0.02 m configs, else 1)")
     args = ap.parse_args()

@@ -190,7 +190,7 @@ mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T);
 
 /* MRF_COMM_EXTERNAL mode, one iteration split in two: mrf_bp_partial (iterate = 1) computes
  * this rank's messages from the current T and writes its partial sums to partial_out (device
- * pointer, mrf_belief_slots() int64 in the library's internal brick-major slot order); the
+ * pointer, mrf_belief_slots() int64 in the library's internal tile-major slot order); the
  * caller sums the partials of all ranks element-wise and hands the total back with
  * mrf_bp_finish (device pointer, same size), which becomes T.  iterate = 0 only sums the
  * current messages (e.g. after mrf_import_messages, which in this mode leaves T alone).
@@ -198,9 +198,29 @@ mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T);
 mrf_status mrf_bp_partial(mrf_ctx* ctx, int32_t iterate, int64_t* partial_out_device);
 mrf_status mrf_bp_finish(mrf_ctx* ctx, const int64_t* total_device);
 
-/* Number of int64 belief slots (nx, ny, nz rounded up to multiples of 8, times each other):
- * voxels are stored brick-major in 8^3 bricks internally (cf. the paper's GVDB bricks). */
+/* Number of int64 belief slots (nx, ny rounded up to multiples of 32 and nz to a multiple of 16,
+ * times each other): voxels are stored tile-major in 32 x 32 x 16 tiles internally (the unit of
+ * the shared-memory voxel reduction; cf. the paper's GVDB 8^3 bricks). */
 int64_t mrf_belief_slots(const mrf_ctx* ctx);
+
+/* Message model (reading R22).
+ *   MRF_MSG_PER_RAY (default): every incidence keeps its own factor->voxel message (Eq.6: the
+ *     cavity of a ray excludes only its own message).
+ *   MRF_MSG_KEYFRAME_AVG: the paper's memory-saving assumption ("all rays going through a
+ *     voxel from a single keyframe send the same average message"): per (frame, voxel) the
+ *     average of the normalised messages of the frame's rays, lbar = ln(mean mu(1) / mean mu(0))
+ *     (uniform when the frame has no ray through the voxel); T_v = sum over frames of lbar; a
+ *     ray of frame f sees the cavity L0 + T_v - lbar[f][v].  mu(1), mu(0) are summed in fp64 (so
+ *     the average does not depend on the summation order beyond fp64 rounding, far below the
+ *     2^-23 quantisation of lbar); messages are still computed and stored per incidence.  Costs
+ *     20 bytes per (frame, belief slot) of device memory.
+ * Set before the first frame (MRF_ERR_STATE otherwise); single rank only (MRF_ERR_INVALID_ARG
+ * with world > 1).  Frame ids are the mrf_add_frame order (frame_id_out). */
+enum { MRF_MSG_PER_RAY = 0, MRF_MSG_KEYFRAME_AVG = 1 };
+mrf_status mrf_set_message_mode(mrf_ctx* ctx, int32_t mode);
+/* Keyframe-average mode: frame's current average log-odds lbar (nats) into a host buffer of V
+ * floats, x fastest.  MRF_ERR_STATE in per-ray mode, MRF_ERR_INVALID_ARG for a bad frame id. */
+mrf_status mrf_export_keyframe_average(mrf_ctx* ctx, int64_t frame, float* out);
 
 /* 128-byte ncclUniqueId for MRF_COMM_NCCL (call on rank 0, broadcast to the others). */
 mrf_status mrf_nccl_unique_id(unsigned char out[128]);

@@ -18,6 +18,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import MrfError, KERNEL_NAMES, MRF_COMM_NCCL, MRF_COMM_EXTERNAL  # noqa: F401
+from ._lib import MRF_MSG_PER_RAY, MRF_MSG_KEYFRAME_AVG  # noqa: F401
 
 __all__ = ["MRFMap", "MrfError", "nccl_unique_id", "load"]
 
@@ -211,6 +212,18 @@ class MRFMap:
     def import_messages(self, lam):
         lam = np.ascontiguousarray(lam, dtype=np.float32)
         self._chk(self._L.mrf_import_messages(self._h, _ptr(lam)))
+
+    def set_message_mode(self, mode):
+        """mrf_set_message_mode: MRF_MSG_PER_RAY (default) or MRF_MSG_KEYFRAME_AVG (the paper's
+        per-keyframe average message; before the first frame, single rank)."""
+        self._chk(self._L.mrf_set_message_mode(self._h, int(mode)))
+
+    def export_keyframe_average(self, frame):
+        """mrf_export_keyframe_average: the frame's average log-odds per voxel (float32[V],
+        x fastest) in keyframe-average mode."""
+        out = np.empty(self.V, np.float32)
+        self._chk(self._L.mrf_export_keyframe_average(self._h, int(frame), _ptr(out)))
+        return out
 
     def export_beliefs(self):
         T = np.empty(self.V, np.int64)

@@ -22,6 +22,7 @@ STATUS_NAMES = {0: "MRF_OK", 1: "MRF_ERR_INVALID_ARG", 2: "MRF_ERR_OUT_OF_MEMORY
                 4: "MRF_ERR_CUDA", 5: "MRF_ERR_NCCL", 6: "MRF_ERR_STATE"}
 MRF_COMM_NCCL, MRF_COMM_EXTERNAL = 0, 1
 MRF_EVAL_SIGMA_BAND, MRF_EVAL_VOXEL_BOUNDS = 0, 1
+MRF_MSG_PER_RAY, MRF_MSG_KEYFRAME_AVG = 0, 1
 KERNEL_NAMES = ["raygen_count", "dda_fill", "scan", "transpose", "ray_messages", "voxel_sum", "allreduce",
                 "marginals"]
 MRF_K_COUNT = len(KERNEL_NAMES)
@@ -31,7 +32,7 @@ EXPORTS = ["mrf_create", "mrf_add_frame", "mrf_bp_iterate", "mrf_marginals", "mr
            "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph", "mrf_export_rays", "mrf_evaluate",
            "mrf_export_transpose", "mrf_export_messages", "mrf_import_messages", "mrf_export_beliefs",
            "mrf_bp_partial", "mrf_bp_finish", "mrf_belief_slots", "mrf_nccl_unique_id", "mrf_set_profiling",
-           "mrf_profile_read", "mrf_launch_count"]
+           "mrf_profile_read", "mrf_launch_count", "mrf_set_message_mode", "mrf_export_keyframe_average"]
 
 
 class MrfError(RuntimeError):
@@ -80,6 +81,8 @@ def load(build: bool = True):
                 "mrf_layout_sizes": (st, [vp, P(i64), P(i64), P(i64)]),
                 "mrf_export_rays": (st, [vp, i64, vp, vp, i64, vp, vp, vp, vp]),
                 "mrf_evaluate": (st, [vp, vp, i32, i32, P(f64), P(f64), i32, f64, f64, vp, P(i64), P(i64)]),
+                "mrf_set_message_mode": (st, [vp, i32]),
+                "mrf_export_keyframe_average": (st, [vp, i64, vp]),
                 "mrf_export_graph": (st, [vp, vp, vp, vp, vp]),
                 "mrf_export_transpose": (st, [vp, vp, vp]),
                 "mrf_export_messages": (st, [vp, vp]),

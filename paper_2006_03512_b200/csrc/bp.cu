@@ -273,11 +273,16 @@ __device__ __forceinline__ void stk(int32_t* p, const int (&v)[K], long long nv)
 template <int K, int M>
 __device__ __forceinline__ void load_chunk(long long s, long long e1, float L0, const int32_t* __restrict__ vid,
                                            const float* __restrict__ lnu, const int32_t* __restrict__ lam,
-                                           const long long* __restrict__ T, float (&la)[K], float (&w)[K],
-                                           float (&l)[K]) {
+                                           const long long* __restrict__ T, const int32_t* __restrict__ qrow,
+                                           float (&la)[K], float (&w)[K], float (&l)[K]) {
     int v[K], q[K], ln[K];
     ldk<K>(vid + s, v);
-    ldk<K>(lam + s, q);
+    if (qrow) {  // keyframe-average mode: the ray's keyframe average replaces its own message
+#pragma unroll
+        for (int j = 0; j < K; ++j) q[j] = __ldg(qrow + v[j]);
+    } else {
+        ldk<K>(lam + s, q);
+    }
     ldk<K>(reinterpret_cast<const int32_t*>(lnu) + s, ln);
     long long t[K];
 #pragma unroll
@@ -311,7 +316,7 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
 #ifndef MRF_K5_MIN_BLOCKS
 #define MRF_K5_MIN_BLOCKS 4
 #endif
-template <int G, int K, int M>
+template <int G, int K, int M, bool AVG>
 __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ ray_z,
@@ -323,11 +328,12 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     if (wi * RPW >= n) return;  // warp-uniform
     const int lane = threadIdx.x & 31, sl = lane & (G - 1);
     const long long ri = wi * RPW + lane / G;
-    int nr = 0, e0 = 0;
+    int nr = 0, e0 = 0, fr = 0;
     if (ri < n) {
         const int r = __ldg(rays + ri);
         nr = ray_z[r].n;
         e0 = (int)__ldg(row_ptr + r);
+        if constexpr (AVG) fr = ray_z[r].frame;
     }
     const int s = e0 + sl * K;
     const int nv = min(max(nr - sl * K, 0), K);  // valid incidences of this lane's chunk
@@ -337,7 +343,13 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     {
         int v[K], q[K], ln[K];
         ldk<K>(vid + sr, v);
-        ldk<K>(lam + sr, q);
+        if constexpr (AVG) {  // keyframe-average mode: the cavity excludes the ray's keyframe average
+            const int32_t* qrow = mp.qbar + (long long)fr * mp.qbar_vi;
+#pragma unroll
+            for (int j = 0; j < K; ++j) q[j] = __ldg(qrow + v[j]);
+        } else {
+            ldk<K>(lam + sr, q);
+        }
         ldk<K>(reinterpret_cast<const int32_t*>(lnu) + sr, ln);
         // every slot of a chunk holds a valid voxel id (padding slots hold 0), so the gathers
         // and the element terms run unpredicated (straight-line code, full ILP) and are masked
@@ -365,7 +377,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
 constexpr int kLongK = 8;
 constexpr int kLongTile = 32 * kLongK;
 
-template <int M>
+template <int M, bool AVG>
 __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const int32_t* __restrict__ rays,
                                                            const long long* __restrict__ row_ptr,
                                                            const RayInfo* __restrict__ ray_z,
@@ -380,6 +392,7 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
     for (long long wi = gw; wi < n; wi += n_warps) {
         const int r = __ldg(rays + wi);
         const long long e0 = __ldg(row_ptr + r), e1 = e0 + ray_z[r].n;
+        const int32_t* qrow = AVG ? mp.qbar + (long long)ray_z[r].frame * mp.qbar_vi : nullptr;
         const int n_tiles = (int)((e1 - e0 + kLongTile - 1) / kLongTile);
         float la[kLongK], w[kLongK], l[kLongK], lR[kLongK], lQ[kLongK];
         float aB, bB, Rin, Qin, Rc_out, Qc_out;
@@ -388,7 +401,7 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         for (int t = n_tiles - 1; t >= 0; --t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             identity_chunk<kLongK>(la, w, l);
-            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, la, w, l);
+            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, qrow, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
             lane_scans<32, M>(aB, bB, lane, Rc, kNeg, Rin, Qin, &Rc_out, &Qc_out);
             Rc = Rc_out;
@@ -403,7 +416,7 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         for (int t = 0; t < n_tiles; ++t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             identity_chunk<kLongK>(la, w, l);
-            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, la, w, l);
+            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, qrow, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
             lane_scans<32, M>(aB, bB, lane, kNeg, Qc, Rin, Qin, &Rc_out, &Qc_out);
             Qc = Qc_out;
@@ -669,19 +682,44 @@ constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
 #endif
 __device__ __forceinline__ int swz(int s) { return MRF_K6_SWIZZLE ? s ^ (((s >> 5) ^ (s >> 10)) & 31) : s; }
 
+// MODE 0: the beliefs, sum of q (int32 halves, exact).  MODE 1 (keyframe averages, reading R22):
+// per slot the counts of non-negative / negative messages (packed n_pos + 65536 n_neg, native
+// int32 shared atomics) and D = sum over non-negative messages of their small probability
+// s = mu(0) minus the same over negative messages (s = mu(1)), s = e^-|lambda| / (1 + e^-|lambda|)
+// in fp64 (down to e^-256), summed in an fp64 shared accumulator (shared float atomics of either
+// width are CAS loops on sm_100a) and flushed with fp64 global atomics.  Then
+//     sum mu(1) = n_pos - D,   sum mu(0) = n_neg + D,
+// both well conditioned: with n_neg = 0, sum mu(0) = D is a sum of positive terms; with both
+// counts >= 1 each sum is >= 1/2.  The value depends on the summation order only through fp64
+// rounding, far below the 2^-23 quantisation of the average.
+__device__ __forceinline__ double kf_small(int q) {
+    // y = e^-|lambda| = 2^-t, t = n + f: 2^-f by ex2.approx (relative 2^-22), 2^-n exactly in
+    // the fp64 exponent (|lambda| <= 256: n <= 369, far inside the fp64 range)
+    const float t = fabsf((float)q * kQInv) * kLog2e;
+    const float n = floorf(t);
+    const double y = (double)ex2(n - t) * __hiloint2double((1023 - (int)n) << 20, 0);
+    const double s = y * (double)__frcp_rn(1.f + (float)y);  // relative ~2^-22
+    return q >= 0 ? s : -s;
+}
+constexpr int kK6SmemKf = kTileSlots * (int)(sizeof(double) + sizeof(int)) + kK6Warps * 32 * 16;
+
+template <int MODE>
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
                                                                    const long long* __restrict__ tile_ptr,
                                                                    const Run* __restrict__ runs,
                                                                    const int32_t* __restrict__ lam, int per_item,
-                                                                   long long* T) {
+                                                                   void* out, long long n_out) {
     extern __shared__ int smem[];
+    double* accd = reinterpret_cast<double*>(smem);        // MODE 1: D per slot (128 KB)
+    int* accn = smem + 2 * kTileSlots;                     // MODE 1: packed counts (64 KB)
+    constexpr int kAccInts = MODE == 0 ? 2 * kTileSlots : 3 * kTileSlots;
     int* acc_lo = smem;                 // sum of (q & 0xffff), at swz(slot)
     int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
-    uint4* sdesc = reinterpret_cast<uint4*>(smem + 2 * kTileSlots) + (threadIdx.x >> 5) * 32;  // this warp's batch
+    uint4* sdesc = reinterpret_cast<uint4*>(smem + kAccInts) + (threadIdx.x >> 5) * 32;  // this warp's batch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
         const int2 item = __ldg(items + it);
-        for (int i = threadIdx.x; i < 2 * kTileSlots / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
+        for (int i = threadIdx.x; i < kAccInts / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
         __syncthreads();
         const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * per_item;
         long long r1 = __ldg(tile_ptr + item.x + 1);
@@ -725,18 +763,36 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                         const int cz = k - cx - cy, sz = (meta >> 22) & 1 ? -cz : cz;
                         const int si = swz((int)(meta & (kTileSlots - 1)) + sx + 32 * sy + 1024 * sz);
                         const int qv = q[rnd][j];
-                        atomicAdd(acc_lo + si, qv & 0xffff);
-                        atomicAdd(acc_hi + si, qv >> 16);
+                        if constexpr (MODE == 0) {
+                            atomicAdd(acc_lo + si, qv & 0xffff);
+                            atomicAdd(acc_hi + si, qv >> 16);
+                        } else {
+                            atomicAdd(accd + si, kf_small(qv));
+                            atomicAdd(accn + si, qv >= 0 ? 1 : 65536);
+                        }
                     }
                 }
             }
             __syncwarp();
         }
         __syncthreads();
-        long long* Tt = T + ((long long)item.x << kTileShift);
-        for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
-            const long long sum = (long long)acc_hi[swz(i)] * 65536 + (long long)acc_lo[swz(i)];
-            if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
+        if constexpr (MODE == 0) {
+            long long* Tt = static_cast<long long*>(out) + ((long long)item.x << kTileShift);
+            for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
+                const long long sum = (long long)acc_hi[swz(i)] * 65536 + (long long)acc_lo[swz(i)];
+                if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
+            }
+        } else {  // out: D (fp64) then the packed counts (int64: n_pos + 2^32 n_neg), each [bucket][slot]
+            const long long o = (long long)item.x << kTileShift;
+            double* Dt = static_cast<double*>(out) + o;
+            unsigned long long* Nt = reinterpret_cast<unsigned long long*>(static_cast<double*>(out) + n_out) + o;
+            for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
+                const unsigned cn = (unsigned)accn[swz(i)];
+                if (cn) {
+                    atomicAdd(Dt + i, accd[swz(i)]);
+                    atomicAdd(Nt + i, (unsigned long long)(cn & 0xffffu) | ((unsigned long long)(cn >> 16) << 32));
+                }
+            }
         }
         __syncthreads();
     }
@@ -761,7 +817,7 @@ __global__ void lambda_to_float_kernel(long long n, const int32_t* __restrict__ 
 
 inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
-template <int M, int k>
+template <int M, bool AVG, int k>
 void launch_class_k(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr, const RayInfo* ray_z,
                     const int32_t* vid, const float* lnu, int32_t* lam, const long long* T, const MsgParams& mp,
                     cudaStream_t s) {
@@ -769,24 +825,24 @@ void launch_class_k(int cls, long long n_rays, const int32_t* rays, const long l
         if (cls == k) {
             constexpr int G = class_G(k), K = class_K(k);
             const unsigned grid = blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256);
-            ray_msg_kernel<G, K, M><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp);
+            ray_msg_kernel<G, K, M, AVG><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp);
             return;
         }
-        launch_class_k<M, k + 1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
+        launch_class_k<M, AVG, k + 1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
     }
 }
 
-template <int M>
+template <int M, bool AVG>
 void launch_ray_messages_m(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
                            const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
                            const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                            int n_warps_long, cudaStream_t s) {
     if (cls < kNumShort) {
-        launch_class_k<M, 0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
+        launch_class_k<M, AVG, 0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
     } else {
         const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
-        ray_msg_long_kernel<M><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
-                                                 scratch_per_warp);
+        ray_msg_long_kernel<M, AVG><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                                      scratch_per_warp);
     }
 }
 
@@ -815,12 +871,15 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, int math, cudaStream_t s) {
     if (n_rays == 0) return;
-    if (math == 0)
-        launch_ray_messages_m<0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch, scratch_per_warp,
-                                 n_warps_long, s);
+    if (mp.qbar)  // keyframe-average mode (math level 1)
+        launch_ray_messages_m<1, true>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                       scratch_per_warp, n_warps_long, s);
+    else if (math == 0)
+        launch_ray_messages_m<0, false>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                        scratch_per_warp, n_warps_long, s);
     else
-        launch_ray_messages_m<1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch, scratch_per_warp,
-                                 n_warps_long, s);
+        launch_ray_messages_m<1, false>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                        scratch_per_warp, n_warps_long, s);
 }
 
 void launch_ray_messages_staged(long long n_stages, const Stage* stages, const long long* row_ptr,
@@ -845,12 +904,54 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
     if (n_items == 0) return;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(tile_reduce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Smem);
+        cudaFuncSetAttribute(tile_reduce_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Smem);
         configured = true;
     }
     const long long grid = n_items < 148LL ? n_items : 148LL;
-    tile_reduce_kernel<<<(unsigned)grid, kK6Threads, kK6Smem, s>>>(n_items, items, tile_ptr, runs,
-                                                                                     lam, per_item, T);
+    tile_reduce_kernel<0><<<(unsigned)grid, kK6Threads, kK6Smem, s>>>(n_items, items, tile_ptr, runs, lam, per_item, T,
+                                                                       0);
+}
+
+void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
+                    const int32_t* lam, int per_item, double* D, long long n_slots, cudaStream_t s) {
+    if (n_items == 0) return;
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(tile_reduce_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6SmemKf);
+        configured = true;
+    }
+    const long long grid = n_items < 148LL ? n_items : 148LL;
+    tile_reduce_kernel<1><<<(unsigned)grid, kK6Threads, kK6SmemKf, s>>>(n_items, items, bucket_ptr, runs, lam, per_item,
+                                                                         D, n_slots);
+}
+
+// Keyframe averages -> quantised log-odds per (frame, slot) and their sum per slot (thread per
+// slot, frames in order: T is an exact integer sum).
+__global__ void kf_finalize_kernel(long long F, long long VI, const double* __restrict__ D,
+                                   const unsigned long long* __restrict__ N, int32_t* qbar, long long* T) {
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= VI) return;
+    long long t = 0;
+    for (long long f = 0; f < F; ++f) {
+        const long long k = f * VI + v;
+        const unsigned long long cn = N[k];
+        int qb = 0;
+        if (cn) {
+            const double d = D[k];
+            const double s1 = (double)(cn & 0xffffffffull) - d, s0 = (double)(cn >> 32) + d;  // sum mu(1), mu(0)
+            const double lb = fmin(fmax(log(s1) - log(s0), -(double)kLambdaClip), (double)kLambdaClip);
+            qb = lb >= (double)kLambdaClip ? 0x7fffffff : (int)__double2ll_rn(lb * (double)kQScale);
+        }
+        qbar[k] = qb;
+        t += qb;
+    }
+    T[v] = t;
+}
+
+void launch_kf_finalize(long long F, long long VI, const double* D, int32_t* qbar, long long* T, cudaStream_t s) {
+    if (VI == 0) return;
+    kf_finalize_kernel<<<(unsigned)((VI + 255) / 256), 256, 0, s>>>(
+        F, VI, D, reinterpret_cast<const unsigned long long*>(D + F * VI), qbar, T);
 }
 
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s) {

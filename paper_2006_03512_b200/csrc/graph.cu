@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
         Segment sg;
         st = pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg);
         int bound = 0;
-        RayInfo rz{0, 0.f, 0, 0};
+        RayInfo rz{0, 0.f, 0, f.index};
         if (st == 0) {
             // Upper bound of the walk's length without walking: every DDA step moves at least one
             // axis one cell towards the cell of the end point, so n <= 1 + sum_k |c_end,k - c_0,k|
@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
     Segment sg;
     Walker w;
     int run_tile = -1, run_n = 0, run_prev = 0;  // current tile run (K4b count)
+    const int bucket0 = f.index * f.bucket_stride;
     long long e = 0, e_cap = 0;
     if (i < n_pix) {
         int u, v;
@@ -331,8 +332,9 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             run_prev = l;
             const unsigned sm = __ballot_sync(am, start);
             if (start) {
-                const unsigned peers = __match_any_sync(sm, b);
-                if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[b], __popc(peers));
+                const int key = bucket0 + b;  // (frame, tile) bucket; the tile itself in per-ray mode
+                const unsigned peers = __match_any_sync(sm, key);
+                if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[key], __popc(peers));
             }
             if (last) {
                 alive = false;
@@ -538,13 +540,16 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
                                                        const RayInfo* __restrict__ info,
                                                        const int32_t* __restrict__ vid,
                                                        const long long* __restrict__ tile_ptr, int32_t* cursor,
-                                                       Run* runs) {
+                                                       int bucket_stride, Run* runs) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     long long e = 0, e1 = 0;
+    int bucket0 = 0;
     if (r < n_rays) {
         e = row_ptr[r];
-        e1 = e + info[r].n;
+        const RayInfo ri = info[r];
+        e1 = e + ri.n;
+        bucket0 = ri.frame * bucket_stride;
     }
     bool alive = e < e1;
     RunBuilder rb;
@@ -567,7 +572,7 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
             const bool emit = rb.tile >= 0 && !ext;  // the current run ends before e
             const unsigned em = __ballot_sync(am, emit);
             if (emit) {
-                const int cur = rb.tile;
+                const int cur = bucket0 + rb.tile;
                 const unsigned peers = __match_any_sync(em, cur);
                 const int leader = __ffs(peers) - 1;
                 int base = 0;
@@ -736,9 +741,10 @@ void launch_vox_hist(long long n_rays, const long long* row_ptr, const RayInfo* 
 }
 
 void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
-                     const long long* tile_ptr, int32_t* cursor, Run* runs, cudaStream_t s) {
+                     const long long* tile_ptr, int32_t* cursor, int bucket_stride, Run* runs, cudaStream_t s) {
     if (n_rays == 0) return;
-    run_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, tile_ptr, cursor, runs);
+    run_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, row_ptr, info, vid, tile_ptr, cursor,
+                                                            bucket_stride, runs);
 }
 
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,

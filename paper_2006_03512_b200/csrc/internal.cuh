@@ -76,6 +76,8 @@ struct FrameDesc {
     int rows_owned;           // number of pixel rows v with v % world == rank
     long long ray_base;       // index of this frame's first ray
     long long depth_off;      // offset of the frame's depth image in the pending-depth buffer
+    int index;                // frame index in the ctx
+    int bucket_stride;        // tile-run bucket of a run in tile t: index * bucket_stride + t
 };
 
 // Per-ray record: LUT row iz (<= n_z-2) and weight wz in [0,1] of the measured range, and the
@@ -86,7 +88,7 @@ struct RayInfo {
     int iz;
     float wz;
     int n;
-    int unused;
+    int frame;  // index of the ray's frame in the ctx (keyframe-average mode)
 };
 
 // K5 parameters (natural logs).
@@ -96,6 +98,10 @@ struct MsgParams {
     float s_off, b_off;       // fo = off_q * s_off + b_off
     float fo_max;             // n_off - 1
     float L0;                 // prior log-odds ln(gamma / (1 - gamma))
+    // keyframe-average mode (reading R22): the cavity excludes the ray's keyframe average
+    // qbar[frame * qbar_vi + v] instead of the ray's own message; nullptr in per-ray mode
+    const int32_t* qbar;
+    long long qbar_vi;
 };
 
 // log nu at (measured range row iz + wz, quantised offset off_q): bilinear interpolation of the
@@ -151,7 +157,7 @@ void launch_transpose_fill(long long n_rays, const long long* row_ptr, const Ray
                            const long long* col_ptr, int32_t* cursor, int32_t* tr, cudaStream_t s);
 // tile-run transpose (K4b): runs per tile, then the run list grouped by tile
 void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
-                     const long long* tile_ptr, int32_t* cursor, Run* runs, cudaStream_t s);
+                     const long long* tile_ptr, int32_t* cursor, int bucket_stride, Run* runs, cudaStream_t s);
 // K6 work list: n_items[i] = ceil(count[i] / chunk); items (i, j) from item_ptr
 void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, int chunk, cudaStream_t s);
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
@@ -230,6 +236,13 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
                          const int32_t* lam, long long* T, cudaStream_t s);
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                         const int32_t* lam, int per_item, long long* T, cudaStream_t s);
+// keyframe averages (reading R22): per [bucket = frame * NT + tile][slot], D += signed small
+// probability of each message (fp64, D[0 .. n_slots)) and the packed counts n_pos + 2^32 n_neg
+// (int64, at D + n_slots); both zeroed by the caller (bp.cu tile_reduce_kernel<1>)
+void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
+                    const int32_t* lam, int per_item, double* D, long long n_slots, cudaStream_t s);
+// qbar[f][v] = quantised clip(ln(sum mu(1) / sum mu(0)), +-256) (0 without a ray), T[v] = sum_f qbar
+void launch_kf_finalize(long long F, long long VI, const double* D, int32_t* qbar, long long* T, cudaStream_t s);
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s);
 void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s);
 

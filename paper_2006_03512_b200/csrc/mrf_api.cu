@@ -81,7 +81,13 @@ struct mrf_ctx {
     long long NT = 0;  // tiles
     bool k6_voxel = false;  // ablation: per-voxel transpose K6 instead of the tile-run K6 (MRF_K6=voxel)
     int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1)
-    int k6_item = 8192;     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
+    int k6_item = 8192;
+    // keyframe-average mode (NEXT #3, reading R22): one message per (frame, voxel)
+    bool kf_avg = false;
+    DBuf<int32_t> qbar;           // [frame][VI] quantised average log-odds
+    DBuf<double> kf_sums;          // [frame][VI] fp64 D, then [frame][VI] int64 packed counts
+    long long kf_frames_alloc = 0;
+    long long n_bucket_groups() const { return kf_avg ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
     bool hist_valid = false; // vox_count (voxel degrees) computed for the current graph
@@ -338,16 +344,19 @@ mrf_status build_voxel_transpose(mrf_ctx* c) {
 // Tile-run transpose (runs grouped by tile) + its K6 work list.  The runs per tile were counted
 // by the DDA fills.
 mrf_status build_tile_runs(mrf_ctx* c) {
-    const long long NT = c->NT;
+    // buckets: the tiles (per-ray mode), or (frame, tile) pairs frame-major (keyframe averages)
+    const long long NT = c->NT * c->n_bucket_groups();
     mrf_status st;
+    CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
+    CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
     if ((st = scan(c, c->tile_runs.p, c->tile_ptr.p, NT, 0)) != MRF_OK) return st;
     if ((st = read_ll(c, c->tile_ptr.p + NT, &c->n_runs)) != MRF_OK) return st;
     CK(c->runs.ensure((size_t)std::max(1LL, c->n_runs), 0, c->stream));
     CK(cudaMemsetAsync(c->tile_cursor.p, 0, sizeof(int32_t) * NT, c->stream));
     {
         ProfScope ps(c, MRF_K_TRANSPOSE);
-        launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p, c->runs.p,
-                        c->stream);
+        launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p,
+                        c->kf_avg ? (int)c->NT : 0, c->runs.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     }
     // K6 work list, j-major: item j of every tile, then item j+1 ...  Runs land in a tile in
@@ -434,8 +443,31 @@ mrf_status prepare(mrf_ctx* c) {
 }
 
 // K6 over the current messages into `out` (zeroed first).
+// Keyframe-average buffers for every frame (a new frame's averages start uniform: qbar = 0).
+mrf_status ensure_kf(mrf_ctx* c) {
+    const long long F = (long long)c->frames.size();
+    if (!c->kf_avg || F <= c->kf_frames_alloc) return MRF_OK;
+    const size_t n = (size_t)(F * c->VI), used = (size_t)(c->kf_frames_alloc * c->VI);
+    CK(c->qbar.ensure(n, used, c->stream));
+    CK(cudaMemsetAsync(c->qbar.p + used, 0, sizeof(int32_t) * (n - used), c->stream));
+    CK(c->kf_sums.ensure(2 * n, 0, c->stream));
+    c->kf_frames_alloc = F;
+    return MRF_OK;
+}
+
 mrf_status voxel_sums(mrf_ctx* c, long long* out) {
     ProfScope ps(c, MRF_K_VOXEL_SUM);
+    if (c->kf_avg) {  // per-(frame, slot) averages, then T = sum over frames (reading R22)
+        mrf_status st;
+        if ((st = ensure_kf(c)) != MRF_OK) return st;
+        const long long F = (long long)c->frames.size(), n = F * c->VI;
+        CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(double) * (size_t)n, c->stream));
+        launch_kf_sums(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
+                       c->stream);
+        launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, out, c->stream);
+        CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_bitems > 0 ? 1 : 0) + 1);
+        return MRF_OK;
+    }
     CK(cudaMemsetAsync(out, 0, sizeof(long long) * c->VI, c->stream));
     if (c->k6_voxel) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
@@ -449,6 +481,12 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
 
 // K5: the staged kernel over the short rays (or the class kernels), the tiled kernel over the long
 mrf_status ray_messages(mrf_ctx* c) {
+    if (c->kf_avg) {
+        mrf_status st;
+        if ((st = ensure_kf(c)) != MRF_OK) return st;
+    }
+    c->mp.qbar = c->kf_avg ? c->qbar.p : nullptr;
+    c->mp.qbar_vi = c->VI;
     ProfScope ps(c, MRF_K_RAY_MSG);
     const bool staged = c->k5_staged;
     if (staged && c->n_stages > 0) {
@@ -685,7 +723,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
-    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->marg.release(); c->eval_cls.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->marg.release(); c->eval_cls.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
@@ -734,6 +772,7 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->pend.clear();
     c->depth_used = 0;
     c->E_filled = c->R_filled = 0;
+    c->kf_frames_alloc = 0;
     CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
@@ -796,6 +835,13 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     f.W = width; f.H = height; f.rank = c->rank; f.world = c->world;
     f.rows_owned = rows_owned;
     f.ray_base = c->R;
+    f.index = (int)c->frames.size();
+    f.bucket_stride = c->kf_avg ? (int)c->NT : 0;
+    if (c->kf_avg) {  // this frame's (frame, tile) run counters
+        const size_t F = c->frames.size();
+        CK(c->tile_runs.ensure((F + 1) * (size_t)c->NT, F * (size_t)c->NT, c->stream));
+        CK(cudaMemsetAsync(c->tile_runs.p + F * c->NT, 0, sizeof(int32_t) * (size_t)c->NT, c->stream));
+    }
     mrf_status st;
     CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
     {
@@ -1150,6 +1196,41 @@ mrf_status mrf_export_beliefs(mrf_ctx* ctx, int64_t* T) {
         const int x = (int)(v % g.nx), y = (int)((v / g.nx) % g.ny), z = (int)(v / ((long long)g.nx * g.ny));
         T[v] = tmp[(size_t)voxel_slot(g, x, y, z)];
     }
+    return MRF_OK;
+}
+
+mrf_status mrf_set_message_mode(mrf_ctx* ctx, int32_t mode) {
+    ENTER(ctx);
+    if (mode != MRF_MSG_PER_RAY && mode != MRF_MSG_KEYFRAME_AVG) return set_err(c, MRF_ERR_INVALID_ARG, "bad mode");
+    if (!c->frames.empty()) return set_err(c, MRF_ERR_STATE, "the message mode is set before the first frame");
+    if (mode == MRF_MSG_KEYFRAME_AVG && c->world > 1)
+        return set_err(c, MRF_ERR_INVALID_ARG, "keyframe averages are single-rank (a keyframe's rays span ranks)");
+    c->kf_avg = mode == MRF_MSG_KEYFRAME_AVG;
+    if (c->kf_avg) {
+        c->k5_staged = false;  // the class / long-ray K5 kernels carry the keyframe cavity
+        c->k6_voxel = false;   // the averages are tile-run reductions
+    }
+    c->kf_frames_alloc = 0;
+    c->dirty = true;
+    return MRF_OK;
+}
+
+mrf_status mrf_export_keyframe_average(mrf_ctx* ctx, int64_t frame, float* out) {
+    ENTER(ctx);
+    if (!out) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    if (!c->kf_avg) return set_err(c, MRF_ERR_STATE, "not in keyframe-average mode");
+    if (frame < 0 || frame >= (int64_t)c->frames.size()) return set_err(c, MRF_ERR_INVALID_ARG, "bad frame id");
+    mrf_status st;
+    if ((st = ensure_kf(c)) != MRF_OK) return st;
+    std::vector<int32_t> q((size_t)c->VI);
+    CK(cudaMemcpyAsync(q.data(), c->qbar.p + frame * c->VI, sizeof(int32_t) * c->VI, cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    const GridDesc& g = c->grid;
+    long long v = 0;
+    for (int z = 0; z < g.nz; ++z)
+        for (int y = 0; y < g.ny; ++y)
+            for (int x = 0; x < g.nx; ++x, ++v) out[v] = (float)((double)q[(size_t)voxel_slot(g, x, y, z)] * kQInvD);
     return MRF_OK;
 }
 

@@ -15,6 +15,7 @@ from .scenes import (  # noqa: F401
     CONFIG_NAMES,
     make_workload,
     tiny,
+    tiny_frames,
     single_frame,
     frames30,
     frames100,

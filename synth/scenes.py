@@ -234,9 +234,7 @@ def _add_slabs(scene, rng, n, size):
 
 # --------------------------------------------------------------------------- configs
 
-def tiny(seed: int = 0) -> Workload:
-    """BASELINE.json configs[0]: 64x48 frame, 32^3 grid @0.05 m, camera on a voxel corner."""
-    rs = np.random.default_rng(seed)
+def _tiny_scene(rs):
     scene = _Scene()
     # back wall x = 1.45 over the full y-z face
     scene.rects.append((0, 1.45, (0.0, 0.0), (1.6, 1.6)))
@@ -245,6 +243,13 @@ def tiny(seed: int = 0) -> Workload:
         x0 = rs.uniform(0.9, 1.45 - s[0])
         cy, cz = rs.uniform(0.45, 1.15, 2)
         scene.boxes.append(((x0, cy - s[1] / 2, cz - s[2] / 2), (x0 + s[0], cy + s[1] / 2, cz + s[2] / 2)))
+    return scene
+
+
+def tiny(seed: int = 0) -> Workload:
+    """BASELINE.json configs[0]: 64x48 frame, 32^3 grid @0.05 m, camera on a voxel corner."""
+    rs = np.random.default_rng(seed)
+    scene = _tiny_scene(rs)
     K = (60.0, 60.0, 32.0, 24.0)
     R = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
     C = np.array([0.8, 0.8, 0.8])
@@ -254,6 +259,27 @@ def tiny(seed: int = 0) -> Workload:
     lut = build_log_nu_lut(64, 128, 0.0, 2.0, -0.2, 0.2, sigma_c, 0.0)
     return Workload("tiny", (32, 32, 32), 0.05, (0.0, 0.0, 0.0), 0.5, lut, 0.0, 2.0, -0.2, 0.2,
                     0.1, 3.0, sigma_c, 10, [fr], seed)
+
+
+def tiny_frames(seed: int = 0, n_frames: int = 4) -> Workload:
+    """Test workload: the tiny scene seen from n_frames nearby poses (camera moved back along
+    -x by up to 0.3 m and yawed by up to +-8 degrees), so that several keyframes observe the
+    same voxels -- the small multi-keyframe case of the keyframe-average parity tests."""
+    rs = np.random.default_rng(seed)
+    scene = _tiny_scene(rs)
+    K = (60.0, 60.0, 32.0, 24.0)
+    R0 = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
+    sigma_c = (0.0, 0.0, 0.0012)
+    rn, ri = np.random.default_rng(seed + 2), np.random.default_rng(seed + 3)
+    frames = []
+    for i in range(n_frames):
+        a = math.radians(8.0) * math.sin(1.7 * i)
+        Rz = np.array([[math.cos(a), -math.sin(a), 0.0], [math.sin(a), math.cos(a), 0.0], [0.0, 0.0, 1.0]])
+        C = np.array([0.8 - 0.3 * i / max(1, n_frames - 1), 0.8 + 0.05 * math.cos(i), 0.8 + 0.04 * math.sin(2 * i)])
+        frames.append(_render_frame(scene, 64, 48, K, Rz @ R0, C, sigma_c, 0.0, rn, 0.1, ri))
+    lut = build_log_nu_lut(64, 128, 0.0, 2.0, -0.2, 0.2, sigma_c, 0.0)
+    return Workload(f"tiny_frames[{n_frames}]", (32, 32, 32), 0.05, (0.0, 0.0, 0.0), 0.1, lut, 0.0, 2.0, -0.2,
+                    0.2, 0.1, 3.0, sigma_c, 10, frames, seed)
 
 
 def _room_workload(name, size, res, n_frames, n_boxes, n_slabs, outlier_pi, lut_z_hi, lut_off,

@@ -1,0 +1,133 @@
+"""GPU parity of the keyframe-average message variant (PAPER.md P:200,
+DESIGN.md reading R22) against the oracle's kf_* functions, through the C ABI.
+
+Bars: per-incidence messages and keyframe averages |d| <= 1e-3 max(1, |x|), marginals within
+1e-4 -- the per-ray path's bars (the averages are means of the messages)."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2006_03512_b200 as pkg  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MSG_TOL = 1e-3
+MARG_TOL = 1e-4
+LBAR_TOL = 1e-3
+
+
+def _kf_map(w):
+    m = pkg.MRFMap.from_workload(w)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+    for fr in w.frames:
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+    return m
+
+
+def _msg_err(lam, ref):
+    return float(np.max(np.abs(lam.astype(np.float64) - ref) / np.maximum(1.0, np.abs(ref)))) if len(ref) else 0.0
+
+
+def _lbar_err(lbar, ref):
+    return _msg_err(lbar.reshape(-1), ref.reshape(-1))
+
+
+@pytest.fixture(scope="module")
+def tf4():
+    return synth.tiny_frames(n_frames=4)
+
+
+@pytest.mark.parametrize("n_iter", [1, 2, 5, 10])
+def test_kfavg_trajectory(tf4, n_iter):
+    """Full trajectory from zero messages on four overlapping keyframes."""
+    w = tf4
+    F = len(w.frames)
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    lam_ref, lbar_ref, T_ref = oracle.kf_bp(p, g, n_iter, F=F)
+    with _kf_map(w) as m:
+        m.bp_iterate(n_iter)
+        lam = m.export_messages()
+        marg = m.marginals()
+        lbar = np.stack([m.export_keyframe_average(f) for f in range(F)])
+    assert _msg_err(lam, lam_ref) <= MSG_TOL
+    assert _lbar_err(lbar, lbar_ref) <= LBAR_TOL
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+    if n_iter >= 2:  # the variant is really in effect (not the per-ray iteration)
+        lam_ray, _ = oracle.bp(p, g, n_iter)
+        assert np.max(np.abs(lam_ray - lam_ref)) > 1e-2
+
+
+def test_kfavg_one_step_from_gpu_state(tf4):
+    """T3-style: from the GPU's own keyframe averages after 6 iterations, one more iteration on
+    each side (oracle kf_pass + kf_average from the exported averages)."""
+    w = tf4
+    F = len(w.frames)
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    with _kf_map(w) as m:
+        m.bp_iterate(6)
+        lbar0 = np.stack([m.export_keyframe_average(f) for f in range(F)]).astype(np.float64)
+        m.bp_iterate(1)
+        lam = m.export_messages()
+        lbar1 = np.stack([m.export_keyframe_average(f) for f in range(F)])
+        marg = m.marginals()
+    lam_ref = oracle.kf_pass(p, g, lbar0)
+    lbar_ref = oracle.kf_average(g, lam_ref, F, p.V)
+    assert _msg_err(lam, lam_ref) <= MSG_TOL
+    assert _lbar_err(lbar1, lbar_ref) <= LBAR_TOL
+    assert np.max(np.abs(marg - oracle.marginals(p, oracle.kf_beliefs(lbar_ref)))) <= MARG_TOL
+
+
+def test_kfavg_single_keyframe_rays_equal_per_ray_path():
+    """Frames of one valid pixel each: no keyframe has two rays through a voxel, so the variant
+    must give the per-ray path's messages (the oracle pin of the same reduction, on the GPU)."""
+    w = synth.tiny_frames(n_frames=6)
+    frames = []
+    for k, fr in enumerate(w.frames):
+        d = np.zeros_like(fr.depth)
+        v, u = 10 + 5 * k, 12 + 7 * k
+        d[v, u] = fr.depth[v, u] if fr.depth[v, u] > 0 else 1.0
+        frames.append(synth.Frame(d, fr.K, fr.T_wc))
+    w1 = dataclasses.replace(w, frames=frames)
+    with _kf_map(w1) as a:
+        a.bp_iterate(5)
+        lam_a, marg_a = a.export_messages(), a.marginals()
+    m = pkg.MRFMap.from_workload(w1)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    for fr in frames:
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+    with m:
+        m.bp_iterate(5)
+        lam_b, marg_b = m.export_messages(), m.marginals()
+    assert len(lam_a) == len(lam_b) > 0
+    assert np.max(np.abs(lam_a - lam_b)) <= 1e-5 * max(1.0, float(np.max(np.abs(lam_b))))
+    assert np.max(np.abs(marg_a - marg_b)) <= 1e-6
+
+
+def test_kfavg_mode_errors(tf4):
+    w = tf4
+    m = pkg.MRFMap.from_workload(w)
+    with m:
+        m.add_frame(w.frames[0].depth, w.frames[0].K, w.frames[0].T_wc)
+        with pytest.raises(pkg.MrfError) as e:
+            m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)  # frames already added
+        assert e.value.status == 6
+        with pytest.raises(pkg.MrfError):
+            m.export_keyframe_average(0)  # per-ray mode
+        with pytest.raises(pkg.MrfError):
+            m.set_message_mode(7)
+    with _kf_map(w) as m:
+        with pytest.raises(pkg.MrfError):
+            m.export_keyframe_average(len(w.frames))
+        m.bp_iterate(2)
+        m.reset()  # back to no frames: averages start uniform again
+        m.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
+        assert np.all(m.export_keyframe_average(0) == 0.0)
