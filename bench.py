@@ -294,7 +294,9 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": args.config, "frames": len(w.frames), "bp_iterations": n_iter,
                        "messages": args.messages,
                        "incidences": E_all, "rays": R_all, "voxels": V, "grid": list(w.dims), "res_m": w.res,
-                       "parallelism": f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else "1 GPU",
+                       "parallelism": (f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else
+                                       f"1 GPU, {emulate} emulated ranks (device-side int64 reduce)" if emulate > 1
+                                       else "1 GPU"),
                        "l2": f"inputs larger than L2: messages {4 * E_all / 1e9:.2f} GB, graph {10 * E_all / 1e9:.2f} GB"},
             "ms_per_bp_iteration": (ms_k5 + ms_k6 + prof["allreduce"][1]) / max(1, args.steps * n_iter),
             "kernel_ms_per_step": kernel_ms,
