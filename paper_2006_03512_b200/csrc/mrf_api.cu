@@ -97,6 +97,12 @@ struct mrf_ctx {
     int rank = 0, world = 1, comm_mode = MRF_COMM_NCCL;
     ncclComm_t comm = nullptr;
     cudaStream_t own_stream = nullptr, stream = nullptr;
+    // K5 length classes run concurrently on side streams (fork/join with events on `stream`), so
+    // one class kernel's tail overlaps the next class's work
+    static constexpr int kMaxSide = 8;
+    int k5_streams = 8;  // MRF_K5_STREAMS (1 = all classes on `stream`)
+    cudaStream_t side[kMaxSide] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[kMaxSide] = {};
     std::string err;
     mrf_status sticky = MRF_OK;
 
@@ -494,13 +500,37 @@ mrf_status ray_messages(mrf_ctx* c) {
                                    c->T.p, c->mp, c->k5_math, c->stream);
         CK_LAUNCH(MRF_K_RAY_MSG, 1);
     }
+    // the classes, largest estimated work first, each to the least-loaded stream
+    int order[kNumClasses], n_cls = 0;
     for (int k = 0; k < kNumClasses; ++k) {
         if (c->class_n[k] == 0) continue;
         if (staged && k < kNumShort && class_G(k) * class_K(k) <= kShortMax) continue;  // done by the stages
-        launch_ray_messages(k, c->class_n[k], c->class_all.p + c->class_off[k], c->row_ptr.p, c->ray_z.p, c->vid.p, c->lnu.p,
-                            c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long,
-                            c->k5_math, c->stream);
+        order[n_cls++] = k;
+    }
+    auto work = [&](int k) { return (double)c->class_n[k] * (k < kNumShort ? class_G(k) * class_K(k) : 1024); };
+    std::sort(order, order + n_cls, [&](int a, int b) { return work(a) > work(b); });
+    const int ns = std::min(c->k5_streams, std::max(n_cls, 1));
+    if (ns > 1) {
+        CK(cudaEventRecord(c->ev_fork, c->stream));
+        for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(c->side[i], c->ev_fork, 0));
+    }
+    double load[mrf_ctx::kMaxSide] = {};
+    for (int i = 0; i < n_cls; ++i) {
+        const int k = order[i];
+        int si = 0;
+        for (int j = 1; j < ns; ++j)
+            if (load[j] < load[si]) si = j;
+        load[si] += work(k);
+        launch_ray_messages(k, c->class_n[k], c->class_all.p + c->class_off[k], c->row_ptr.p, c->ray_z.p, c->vid.p,
+                            c->lnu.p, c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp,
+                            c->n_warps_long, c->k5_math, ns > 1 ? c->side[si] : c->stream);
         CK_LAUNCH(MRF_K_RAY_MSG, 1);
+    }
+    if (ns > 1) {
+        for (int i = 0; i < ns; ++i) {
+            CK(cudaEventRecord(c->ev_join[i], c->side[i]));
+            CK(cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
+        }
     }
     return MRF_OK;
 }
@@ -653,6 +683,18 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         return fail(MRF_ERR_CUDA);
     }
     c->stream = c->own_stream;
+    if (const char* ks = getenv("MRF_K5_STREAMS")) c->k5_streams = std::min(std::max(atoi(ks), 1), mrf_ctx::kMaxSide);
+    if (c->k5_streams > 1) {
+        bool ok = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; ok && i < c->k5_streams; ++i)
+            ok = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) == cudaSuccess;
+        if (!ok) {
+            c->err = "side stream / event creation failed";
+            cudaGetLastError();
+            return fail(MRF_ERR_CUDA);
+        }
+    }
     mrf_status st = MRF_OK;
     auto alloc = [&]() -> mrf_status {
         const long long VI = c->VI, NT = c->NT;
@@ -731,6 +773,11 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    for (int i = 0; i < mrf_ctx::kMaxSide; ++i) {
+        if (c->side[i]) cudaStreamDestroy(c->side[i]);
+        if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     delete c;
     return MRF_OK;
 }
