@@ -165,7 +165,10 @@ __device__ __forceinline__ void lane_composite(const float (&la)[K], const float
 // Both lane scans of a ray's G lanes at once (two independent shuffle chains per level):
 // returns R entering this lane from the right and Q entering it from the left, given the tile
 // carries Rc (R after the tile) and Qc (Q before it); optional carries out.
-template <int G, int M>
+// CARRY = false (class kernels: no carries, Rc = Qc = log 0): R and Q entering a lane are just
+// the b parts of its neighbours' composites -- lse(a + log 0, b) = b exactly -- which saves two
+// log-sum-exps (4 MUFU ops) and two shuffles per lane.
+template <int G, int M, bool CARRY = true>
 __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc, float Qc, float& Rin, float& Qin,
                                            float* Rc_out, float* Qc_out) {
     Aff H = {aB, bB};        // suffix maps R -> e^{la} R + e^{w}
@@ -180,6 +183,12 @@ __device__ __forceinline__ void lane_scans(float aB, float bB, int sl, float Rc,
         if (sl < d) op = Aff{0.f, kNeg};
         H = compose<M>(H, oh);
         P = compose<M>(P, op);
+    }
+    if constexpr (!CARRY) {
+        const float hb = __shfl_down_sync(kFull, H.b, 1, G), pb = __shfl_up_sync(kFull, P.b, 1, G);
+        Rin = sl == G - 1 ? kNeg : hb;
+        Qin = sl == 0 ? kNeg : pb;
+        return;
     }
     Aff Hx = shfl_down<G>(H, 1);
     Aff Px = shfl_up<G>(P, 1);
@@ -362,7 +371,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     }
     float aB, bB, Rin, Qin;
     lane_composite<K>(la, w, aB, bB);
-    lane_scans<G, M>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
+    lane_scans<G, M, false>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
     lane_recurrences<K, M>(la, w, Rin, Qin, lR, lQ);
     int out[K];
 #pragma unroll
