@@ -131,3 +131,37 @@ def test_kfavg_mode_errors(tf4):
         m.reset()  # back to no frames: averages start uniform again
         m.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
         assert np.all(m.export_keyframe_average(0) == 0.0)
+
+
+def test_kfavg_import_and_warm_start(tf4):
+    """mrf_import_messages in keyframe-average mode rebuilds the averages from the messages
+    (the same K6' + finalize as an iteration); a frame added after iterations starts uniform
+    and the earlier keyframes keep their averages (warm start, as in the per-ray mode)."""
+    w = tf4
+    F = len(w.frames)
+    with _kf_map(w) as m:
+        m.bp_iterate(4)
+        lam = m.export_messages()
+        lbar = np.stack([m.export_keyframe_average(f) for f in range(F)])
+        marg = m.marginals()
+        m.import_messages(lam)
+        lbar2 = np.stack([m.export_keyframe_average(f) for f in range(F)])
+        assert np.array_equal(lbar, lbar2)
+        assert np.array_equal(marg, m.marginals())
+    p = oracle.Params.from_workload(w)
+    with _kf_map(dataclasses.replace(w, frames=w.frames[:3])) as m:
+        m.bp_iterate(3)
+        lbar3 = np.stack([m.export_keyframe_average(f) for f in range(3)])
+        fr = w.frames[3]
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+        assert np.all(m.export_keyframe_average(3) == 0.0)
+        assert np.array_equal(np.stack([m.export_keyframe_average(f) for f in range(3)]), lbar3)
+        m.bp_iterate(2)
+        lam = m.export_messages()
+        marg = m.marginals()
+    g = oracle.build_graph(p, w.frames)
+    lb0 = np.zeros((F, p.V))
+    lb0[:3] = lbar3.astype(np.float64)
+    lam_ref, lbar_ref, T_ref = oracle.kf_bp(p, g, 2, F=F, lbar=lb0)
+    assert _msg_err(lam, lam_ref) <= MSG_TOL
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
