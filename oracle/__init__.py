@@ -81,10 +81,16 @@ def lib():
             L.orc_kf_pass.restype = None
             L.orc_kf_bp.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, i32, dp, dp, dp]
             L.orc_kf_bp.restype = None
-            L.orc_frame_count.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32, i8p, i64p, dp, dp]
+            u8p = _P(ctypes.c_uint8)
+            L.orc_frame_count.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32, i8p, i64p, dp, dp, u8p, i32,
+                                          i32p]
             L.orc_frame_count.restype = None
-            L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p]
+            L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p, u8p, i32, i32p]
             L.orc_frame_fill.restype = None
+            L.orc_alloc_bricks.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32p, u8p]
+            L.orc_alloc_bricks.restype = i64
+            L.orc_dda_sparse.argtypes = [i32p, i64p, i64p, d, d, u8p, i32, i32p, i32p, i16p, dp, dp, i64]
+            L.orc_dda_sparse.restype = i64
             L.orc_vis_profile.argtypes = [i64, dp, dp, d, dp, dp]
             L.orc_vis_profile.restype = i64
             L.orc_eval_pixel.argtypes = [i32p, dp, dp, dp, dp, i32, i32, ctypes.c_float, dp, d, d, i32, dp]
@@ -183,9 +189,59 @@ class Graph:
         return int(self.row_ptr[-1])
 
 
-def build_graph(p: Params, frames, rank: int = 0, world: int = 1) -> Graph:
-    """B1-B3 over every frame; keeps pixels of rows v % world == rank."""
+class Bricks:
+    """Brick allocation mask of a sparse map (NEXT #4, reading R23): mask[bz, by, bx] != 0 for an
+    allocated brick of B^3 cells."""
+
+    def __init__(self, p: Params, B: int = 8):
+        self.B = int(B)
+        self.nb = _c([-(-int(d) // self.B) for d in p.dims], np.int32)  # bricks per axis (x, y, z)
+        self.mask = np.zeros((int(self.nb[2]), int(self.nb[1]), int(self.nb[0])), np.uint8)
+
+    def cell_mask(self, p: Params):
+        """Per-voxel allocation flag, x fastest (V,)."""
+        nx, ny, nz = (int(d) for d in p.dims)
+        z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+        return self.mask[z // self.B, y // self.B, x // self.B].reshape(-1) != 0
+
+
+def alloc_bricks(p: Params, frames, B: int = 8, bricks: Bricks = None) -> Bricks:
+    """SPEC allocate_for_depth_image over the frames, in order -> Bricks (a new mask or the one given)."""
+    bk = Bricks(p, B) if bricks is None else bricks
+    bk.added = []
+    for fr in frames:
+        H, W = fr.depth.shape
+        bk.added.append(int(lib().orc_alloc_bricks(
+            _ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
+            _ptr(_c(fr.K, np.float64), ctypes.c_double), _ptr(_c(fr.T_wc, np.float64), ctypes.c_double), W, H,
+            _ptr(_c(fr.depth, np.float32), ctypes.c_float), bk.B, _ptr(bk.nb, ctypes.c_int32),
+            _ptr(bk.mask, ctypes.c_uint8))))
+    return bk
+
+
+def dda_sparse(dims, G0, G1, bricks: Bricks, Z=0.0, L=1.0):
+    """B2+B3 with empty skip: the cells of allocated bricks only -> (vid, off_q, t_in, t_out)."""
+    dims = _c(dims, np.int32)
+    G0 = _c(G0, np.int64)
+    G1 = _c(G1, np.int64)
     L_ = lib()
+    args = (_ptr(dims, ctypes.c_int32), _ptr(G0, ctypes.c_int64), _ptr(G1, ctypes.c_int64), float(Z), float(L),
+            _ptr(bricks.mask, ctypes.c_uint8), bricks.B, _ptr(bricks.nb, ctypes.c_int32))
+    n = L_.orc_dda_sparse(*args, None, None, None, None, 0)
+    vid = np.zeros(n, np.int32)
+    off = np.zeros(n, np.int16)
+    tin = np.zeros(n, np.float64)
+    tout = np.zeros(n, np.float64)
+    L_.orc_dda_sparse(*args, _ptr(vid, ctypes.c_int32), _ptr(off, ctypes.c_int16), _ptr(tin, ctypes.c_double),
+                      _ptr(tout, ctypes.c_double), n)
+    return vid, off, tin, tout
+
+
+def build_graph(p: Params, frames, rank: int = 0, world: int = 1, bricks: Bricks = None) -> Graph:
+    """B1-B3 over every frame; keeps pixels of rows v % world == rank.  With
+    `bricks`, only cells of allocated bricks become incidences (NEXT #4 empty skip, R23)."""
+    L_ = lib()
+    bm = (_ptr(bricks.mask, ctypes.c_uint8), bricks.B, _ptr(bricks.nb, ctypes.c_int32)) if bricks else (None, 0, None)
     parts = []
     total = 0
     n_inv = n_drop = 0
@@ -201,7 +257,7 @@ def build_graph(p: Params, frames, rank: int = 0, world: int = 1) -> Graph:
         L_.orc_frame_count(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                            _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
                            rank, world, _ptr(status, ctypes.c_int8), _ptr(count, ctypes.c_int64),
-                           _ptr(Z, ctypes.c_double), _ptr(Lr, ctypes.c_double))
+                           _ptr(Z, ctypes.c_double), _ptr(Lr, ctypes.c_double), *bm)
         kept = np.nonzero(status == STATUS_KEPT)[0]
         n_inv += int(np.sum(status == STATUS_INVALID))
         n_drop += int(np.sum(status == STATUS_DROPPED))
@@ -218,7 +274,7 @@ def build_graph(p: Params, frames, rank: int = 0, world: int = 1) -> Graph:
         offs[kept] = starts
         L_.orc_frame_fill(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                           _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
-                          _ptr(offs, ctypes.c_int64), _ptr(vid, ctypes.c_int32), _ptr(off_q, ctypes.c_int16))
+                          _ptr(offs, ctypes.c_int64), _ptr(vid, ctypes.c_int32), _ptr(off_q, ctypes.c_int16), *bm)
         row_ptr.append(base + np.cumsum(cnt).astype(np.int64))
         base += int(cnt.sum())
         Zs.append(Z)
@@ -229,9 +285,10 @@ def build_graph(p: Params, frames, rank: int = 0, world: int = 1) -> Graph:
                  np.concatenate(pix) if pix else np.zeros(0, np.int64), n_inv, n_drop)
 
 
-def trace_pixels(p: Params, frame, pixels, frame_index: int = 0) -> Graph:
+def trace_pixels(p: Params, frame, pixels, frame_index: int = 0, bricks: Bricks = None) -> Graph:
     """B1-B3 for selected pixel ids (v*W+u) of one frame, one by one (sampled parity at full
-    size).  Only kept pixels (status 0) become rays, in the order given."""
+    size).  Only kept pixels (status 0) become rays, in the order given.  With `bricks`, the
+    empty-skip walk (NEXT #4)."""
     H, W = frame.depth.shape
     row_ptr = [0]
     vids, offs, Zs, pix = [], [], [], []
@@ -245,7 +302,7 @@ def trace_pixels(p: Params, frame, pixels, frame_index: int = 0) -> Graph:
         if s == STATUS_DROPPED:
             n_drop += 1
             continue
-        vid, off, _, _ = dda(p.dims, G0, G1, Z, L)
+        vid, off, _, _ = dda(p.dims, G0, G1, Z, L) if bricks is None else dda_sparse(p.dims, G0, G1, bricks, Z, L)
         vids.append(vid)
         offs.append(off)
         row_ptr.append(row_ptr[-1] + len(vid))

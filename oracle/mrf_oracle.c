@@ -20,6 +20,8 @@
  *   orc_marginals   B6 (Eq.8)                              pinned: unseen voxel = prior
  *   orc_kf_*        NEXT #3 keyframe-average variant       pinned: SPEC worked examples, one ray
  *                                                          per (keyframe, voxel) = B5 iteration
+ *   orc_alloc_bricks, orc_dda_sparse  NEXT #4 sparse bricks pinned: SPEC allocation examples, full
+ *                                                          mask = dense walk, skipped cells = empty
  */
 #include <math.h>
 #include <stdint.h>
@@ -75,8 +77,42 @@ static int64_t floor_div(int64_t a, int64_t b) { /* b > 0 */
  * and off_q = clamp(llrint((0.5 (t_in + t_out) L - Z) * 32768), +-32767) (B3, reading R6).
  * Pointers may be NULL (count only).  Returns the number of cells (all of them, even
  * beyond cap; only the first cap are written). */
+/* Brick allocation mask (NEXT #4, reading R23): NULL = dense grid; else a cell is part of the map
+ * iff mask[brick of the cell] != 0, bricks B^3 cells, brick index bx + nb[0] (by + nb[1] bz). */
+typedef struct {
+    const uint8_t* mask;
+    int32_t B;
+    int32_t nb[3];
+} BrickMask;
+
+static int cell_allocated(const BrickMask* bm, const int64_t c[3]) {
+    if (!bm || !bm->mask) return 1;
+    const int64_t b = c[0] / bm->B + (int64_t)bm->nb[0] * (c[1] / bm->B + (int64_t)bm->nb[1] * (c[2] / bm->B));
+    return bm->mask[b] != 0;
+}
+
+static int64_t dda_core(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3], double Z, double L,
+                        const BrickMask* bm, int32_t* vid, int16_t* off_q, double* t_in_out, double* t_out_out,
+                        int64_t cap);
+
 int64_t orc_dda(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3], double Z, double L,
                 int32_t* vid, int16_t* off_q, double* t_in_out, double* t_out_out, int64_t cap) {
+    return dda_core(dims, G0, G1, Z, L, NULL, vid, off_q, t_in_out, t_out_out, cap);
+}
+
+/* The B2 walk with empty skip (SPEC traverse_3dda over a brick-sparse grid, reading R23): cells of
+ * unallocated bricks are walked through but not emitted (they are not part of the map, so they
+ * are not variables of the ray's factor).  Emitted cells keep their own t_in / t_out. */
+int64_t orc_dda_sparse(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3], double Z, double L,
+                       const uint8_t* mask, int32_t B, const int32_t nb[3], int32_t* vid, int16_t* off_q,
+                       double* t_in_out, double* t_out_out, int64_t cap) {
+    const BrickMask bm = {mask, B, {nb[0], nb[1], nb[2]}};
+    return dda_core(dims, G0, G1, Z, L, &bm, vid, off_q, t_in_out, t_out_out, cap);
+}
+
+static int64_t dda_core(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3], double Z, double L,
+                        const BrickMask* bm, int32_t* vid, int16_t* off_q, double* t_in_out, double* t_out_out,
+                        int64_t cap) {
     int64_t c[3], num[3], den[3];
     int step[3];
     for (int k = 0; k < 3; ++k) {
@@ -112,7 +148,8 @@ int64_t orc_dda(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3],
         }
         const int last = (amin < 0) || (num[amin] >= den[amin]);
         const double t_out = last ? 1.0 : (double)num[amin] / (double)den[amin];
-        if (n < cap) {
+        const int emit = cell_allocated(bm, c);
+        if (emit && n < cap) {
             if (vid) vid[n] = (int32_t)(c[0] + (int64_t)dims[0] * (c[1] + (int64_t)dims[1] * c[2]));
             if (off_q) {
                 const double d_mid = (0.5 * (t_in + t_out)) * L;
@@ -125,7 +162,7 @@ int64_t orc_dda(const int32_t dims[3], const int64_t G0[3], const int64_t G1[3],
             if (t_in_out) t_in_out[n] = t_in;
             if (t_out_out) t_out_out[n] = t_out;
         }
-        ++n;
+        if (emit) ++n;
         if (last) break;
         const int64_t na = num[amin], da = den[amin];
         for (int k = 0; k < 3; ++k) { /* step every axis tied at t_min, simultaneously */
@@ -363,12 +400,62 @@ void orc_kf_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const
     orc_kf_beliefs(F, V, lbar, T);
 }
 
+/* ------------------------------------------------------------------ NEXT #4: brick allocation
+ * SPEC allocate_for_depth_image ("new bricks are allocated in a region around the
+ * reprojected 3D depth point cloud"; reading R23): for every pixel of the frame with a valid depth
+ * whose measured point p (grid units, B1) lies inside the grid, with r = margin_k sigma(Z) / res
+ * (the 3 sigma of P:205, in voxels), every brick containing a cell of the box
+ * [floor(p - r), floor(p + r)] (clamped to the grid) is allocated.  That box contains every cell
+ * within distance r of p, so "every voxel within r_alloc of a reprojected point belongs to an
+ * allocated brick" holds.  All pixels count, whatever their rank (the map is global).  Returns
+ * the number of newly allocated bricks. */
+int64_t orc_alloc_bricks(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+                         const double Twc[12], int32_t W, int32_t H, const float* depth, int32_t B,
+                         const int32_t nb[3], uint8_t* mask) {
+    int64_t added = 0;
+    for (int32_t v = 0; v < H; ++v)
+        for (int32_t u = 0; u < W; ++u) {
+            const double z = (double)depth[(int64_t)v * W + u];
+            if (!isfinite(z) || !(z > 0.0)) continue;
+            const double xc = ((double)u - K[2]) / K[0];
+            const double yc = ((double)v - K[3]) / K[1];
+            const double rho = sqrt((xc * xc + yc * yc) + 1.0);
+            const double Z = z * rho;
+            const double sZ = (par[6] + par[7] * Z) + (par[8] * Z) * Z;
+            const double r = (par[5] * sZ) / geo[0];
+            int64_t lo[3], hi[3];
+            int inside = 1;
+            for (int k = 0; k < 3; ++k) {
+                const double Dk = (Twc[4 * k + 0] * xc + Twc[4 * k + 1] * yc) + Twc[4 * k + 2];
+                const double pk = ((Twc[4 * k + 3] + z * Dk) - geo[1 + k]) / geo[0];
+                if (pk < 0.0 || pk >= (double)dims[k]) inside = 0;
+                lo[k] = (int64_t)floor(pk - r);
+                hi[k] = (int64_t)floor(pk + r);
+                if (lo[k] < 0) lo[k] = 0;
+                if (hi[k] > dims[k] - 1) hi[k] = dims[k] - 1;
+            }
+            if (!inside) continue;
+            for (int64_t bz = lo[2] / B; bz <= hi[2] / B; ++bz)
+                for (int64_t by = lo[1] / B; by <= hi[1] / B; ++by)
+                    for (int64_t bx = lo[0] / B; bx <= hi[0] / B; ++bx) {
+                        uint8_t* m = mask + bx + (int64_t)nb[0] * (by + (int64_t)nb[1] * bz);
+                        if (!*m) {
+                            *m = 1;
+                            ++added;
+                        }
+                    }
+        }
+    return added;
+}
+
 /* ------------------------------------------------------------------ frames -> CSR */
 /* Pass 1 over one frame: per pixel status (0 kept, 1 invalid, 2 dropped), cell count and
  * range Z.  Only rows with v % world == rank are visited (others get status 3). */
 void orc_frame_count(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
                      const double Twc[12], int32_t W, int32_t H, const float* depth, int32_t rank,
-                     int32_t world, int8_t* status, int64_t* count, double* Z_out, double* L_out) {
+                     int32_t world, int8_t* status, int64_t* count, double* Z_out, double* L_out,
+                     const uint8_t* mask, int32_t B, const int32_t* nb) {
+    const BrickMask bm = {mask, B, {nb ? nb[0] : 0, nb ? nb[1] : 0, nb ? nb[2] : 0}};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int32_t v = 0; v < H; ++v) {
         for (int32_t u = 0; u < W; ++u) {
@@ -387,7 +474,7 @@ void orc_frame_count(const int32_t dims[3], const double geo[4], const double pa
             if (s != 0) continue;
             Z_out[p] = Z;
             L_out[p] = L;
-            count[p] = orc_dda(dims, G0, G1, Z, L, NULL, NULL, NULL, NULL, 0);
+            count[p] = dda_core(dims, G0, G1, Z, L, &bm, NULL, NULL, NULL, NULL, 0);
         }
     }
 }
@@ -395,7 +482,8 @@ void orc_frame_count(const int32_t dims[3], const double geo[4], const double pa
 /* Pass 2: write vid/off_q of every kept pixel at offset[p] (offset < 0: skip). */
 void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
                     const double Twc[12], int32_t W, int32_t H, const float* depth, const int64_t* offset,
-                    int32_t* vid, int16_t* off_q) {
+                    int32_t* vid, int16_t* off_q, const uint8_t* mask, int32_t B, const int32_t* nb) {
+    const BrickMask bm = {mask, B, {nb ? nb[0] : 0, nb ? nb[1] : 0, nb ? nb[2] : 0}};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int32_t v = 0; v < H; ++v) {
         for (int32_t u = 0; u < W; ++u) {
@@ -404,7 +492,7 @@ void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par
             int64_t G0[3], G1[3];
             double Z = 0.0, L = 0.0;
             if (orc_ray_setup(dims, geo, par, K, Twc, u, v, depth[p], G0, G1, &Z, &L) != 0) continue;
-            orc_dda(dims, G0, G1, Z, L, vid + offset[p], off_q + offset[p], NULL, NULL, INT64_MAX);
+            dda_core(dims, G0, G1, Z, L, &bm, vid + offset[p], off_q + offset[p], NULL, NULL, INT64_MAX);
         }
     }
 }
