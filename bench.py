@@ -158,7 +158,7 @@ def run_ours(args, rank, world, local_rank):
     # holds several emulated ranks (dist.EmulatedRanks) whose per-iteration int64 partials are
     # summed on the device.
     emulate = args.emulate_ranks if args.emulate_ranks is not None else (
-        4 if (world == 1 and args.config in ("frames100", "sweep300")) else 1)
+        4 if (world == 1 and args.config in ("frames100", "sweep300") and not args.bricks) else 1)
     if args.messages == "keyframe-avg":
         assert world == 1 and emulate == 1, "keyframe averages are single-rank (one ctx, < 2^31 incidences)"
     if emulate > 1:
@@ -170,6 +170,9 @@ def run_ours(args, rank, world, local_rank):
         m.set_stream(stream.cuda_stream)
         if args.messages == "keyframe-avg":  # NEXT #3: the paper's per-keyframe average messages
             m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+    if args.bricks:  # NEXT #4: brick allocation around the depth points + empty-skip walks
+        for mm in (m.maps if emulate > 1 else [m]):
+            mm.set_sparse_bricks(args.bricks)
 
     depth_dev = [torch.from_numpy(fr.depth).to(dev) for fr in w.frames]
     depth_host = [torch.from_numpy(fr.depth).pin_memory() for fr in w.frames]
@@ -292,7 +295,7 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": args.config, "frames": len(w.frames), "bp_iterations": n_iter,
-                       "messages": args.messages,
+                       "messages": args.messages, "bricks": args.bricks,
                        "incidences": E_all, "rays": R_all, "voxels": V, "grid": list(w.dims), "res_m": w.res,
                        "parallelism": (f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else
                                        f"1 GPU, {emulate} emulated ranks (device-side int64 reduce)" if emulate > 1
@@ -328,6 +331,8 @@ def main():
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--bricks", type=int, default=0,
+                    help="sparse-brick map with B^3 bricks (P:203-205; 0 = dense, the north_star graph)")
     ap.add_argument("--messages", default="per-ray", choices=["per-ray", "keyframe-avg"],
                     help="message model: exact per-ray messages (north_star) or per-keyframe averages (P:200)")
     ap.add_argument("--emulate-ranks", type=int, default=None,

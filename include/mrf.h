@@ -222,6 +222,23 @@ mrf_status mrf_set_message_mode(mrf_ctx* ctx, int32_t mode);
  * floats, x fastest.  MRF_ERR_STATE in per-ray mode, MRF_ERR_INVALID_ARG for a bad frame id. */
 mrf_status mrf_export_keyframe_average(mrf_ctx* ctx, int64_t frame, float* out);
 
+/* Sparse-brick map (reading R23).
+ * brick = 0: dense grid (default).  brick = B (a power of two in [2, 64]; the paper uses 8):
+ * every mrf_add_frame allocates the B^3-cell bricks around its reprojected depth points (every
+ * voxel within 3 sigma(Z) of a measured point -- margin_k sigma_c of the noise model -- belongs to
+ * an allocated brick; all pixels count, whatever the rank), and the ray walk emits only cells of
+ * allocated bricks (empty skip: unallocated space holds no variable, i.e. a certainly-empty voxel
+ * in Eq.13/14; its marginal stays gamma).  Beliefs stay dense in device memory.  Set before the
+ * first frame (MRF_ERR_STATE otherwise); every keyframe must be added before the graph is first
+ * used (iterate, export, sizes): a later mrf_add_frame returns MRF_ERR_STATE.  The rays are then
+ * counted and walked once against the final allocation, so the 2^31 incidence-slot capacity is
+ * checked then: MRF_ERR_CAPACITY from the first call that uses the graph (mrf_reset starts over).
+ * mrf_reset clears the allocation and keeps the mode. */
+mrf_status mrf_set_sparse_bricks(mrf_ctx* ctx, int32_t brick);
+/* Allocation mask: out (nullable) = ceil(nz/B) * ceil(ny/B) * ceil(nx/B) bytes, brick x fastest,
+ * 1 = allocated; n_allocated (nullable) = number of allocated bricks.  MRF_ERR_STATE when dense. */
+mrf_status mrf_export_bricks(mrf_ctx* ctx, uint8_t* out, int64_t* n_allocated);
+
 /* 128-byte ncclUniqueId for MRF_COMM_NCCL (call on rank 0, broadcast to the others). */
 mrf_status mrf_nccl_unique_id(unsigned char out[128]);
 

@@ -55,6 +55,7 @@ class MRFMap:
     def __init__(self, dims, res, origin, prior, log_nu, z_lo, z_hi, off_lo, off_hi, margin_min=0.1,
                  margin_k=3.0, sigma_c=(0.0, 0.0, 0.0012), rank=0, world=1, comm=MRF_COMM_NCCL, nccl_id=None):
         self._L = _lib.load()
+        self._brick = 0
         self.dims = tuple(int(d) for d in dims)
         self.V = self.dims[0] * self.dims[1] * self.dims[2]
         self.prior = float(prior)
@@ -223,6 +224,24 @@ class MRFMap:
         x fastest) in keyframe-average mode."""
         out = np.empty(self.V, np.float32)
         self._chk(self._L.mrf_export_keyframe_average(self._h, int(frame), _ptr(out)))
+        return out
+
+    def set_sparse_bricks(self, brick=8):
+        """mrf_set_sparse_bricks: brick-sparse map with B^3 bricks allocated around the
+        reprojected depth points and empty-skip ray walks; 0 = dense."""
+        self._chk(self._L.mrf_set_sparse_bricks(self._h, int(brick)))
+        self._brick = int(brick)
+
+    def export_bricks(self):
+        """mrf_export_bricks -> uint8[nbz, nby, nbx] allocation mask (1 = allocated)."""
+        B = self._brick
+        if B == 0:  # dense map: the library reports the state error
+            self._chk(self._L.mrf_export_bricks(self._h, None, None))
+        nx, ny, nz = self.dims
+        out = np.zeros((-(-nz // B), -(-ny // B), -(-nx // B)), np.uint8)
+        n = ctypes.c_int64()
+        self._chk(self._L.mrf_export_bricks(self._h, _ptr(out), ctypes.byref(n)))
+        assert n.value == int(np.count_nonzero(out))
         return out
 
     def export_beliefs(self):

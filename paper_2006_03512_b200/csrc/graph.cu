@@ -168,8 +168,24 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
             Walker w;
             w.start(sg);
             if (w.inside(g)) {
-                bound = 1 + abs((int)(sg.g1[0] >> kFixShift) - w.c0) + abs((int)(sg.g1[1] >> kFixShift) - w.c1) +
-                        abs((int)(sg.g1[2] >> kFixShift) - w.c2);
+                if (f.skip_count) {
+                    bound = 0;  // counted again against the final allocation (sync_fill)
+                } else if (g.bmask) {
+                    // sparse bricks: the dense bound would size the layout for the skipped free
+                    // space too, so count the cells of allocated bricks exactly (the walk without
+                    // its crossing parameters)
+                    for (;;) {
+                        bound += cell_in_map(g, w.c0, w.c1, w.c2) ? 1 : 0;
+                        unsigned na, da;
+                        const int a = w.earliest(na, da);
+                        if (a < 0 || na >= da) break;
+                        w.advance(na, da);
+                        if (!w.inside(g)) break;
+                    }
+                } else {
+                    bound = 1 + abs((int)(sg.g1[0] >> kFixShift) - w.c0) +
+                            abs((int)(sg.g1[1] >> kFixShift) - w.c1) + abs((int)(sg.g1[2] >> kFixShift) - w.c2);
+                }
             }
             // LUT row of the measured range (bin centres, clamped to the edge centres)
             double fz = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(sg.Z, n.z_lo), __dsub_rn(n.z_hi, n.z_lo)),
@@ -239,6 +255,40 @@ struct RunBuilder {
         return Run{(unsigned)start, slot0 | ((unsigned)(n - 1) << 14) | (neg << 20), mx, my};
     }
 };
+
+// ---------------------------------------------------------------- NEXT #4: brick allocation
+// SPEC allocate_for_depth_image (reading R23): per pixel with a valid depth whose
+// measured point p lies in the grid, r = margin_k sigma(Z) / res; every brick holding a cell of
+// [floor(p - r), floor(p + r)] (clamped) is marked.  fp64 in the oracle's op order (the mask is
+// bit-exact with orc_alloc_bricks); the byte stores of 1 are idempotent, so no atomics.
+__global__ void brick_alloc_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const float* __restrict__ depth,
+                                   uint8_t* mask) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long long)f.W * f.H) return;
+    const int v = (int)(i / f.W), u = (int)(i - (long long)v * f.W);
+    const double z = (double)depth[i];
+    if (!(z > 0.0) || isinf(z)) return;
+    const double xc = __ddiv_rn(__dsub_rn((double)u, f.cx), f.fx);
+    const double yc = __ddiv_rn(__dsub_rn((double)v, f.cy), f.fy);
+    const double rho = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xc, xc), __dmul_rn(yc, yc)), 1.0));
+    const double Z = __dmul_rn(z, rho);
+    const double sig = __dadd_rn(__dadd_rn(n.c0, __dmul_rn(n.c1, Z)), __dmul_rn(__dmul_rn(n.c2, Z), Z));
+    const double r = __ddiv_rn(__dmul_rn(n.margin_k, sig), g.res);
+    const double org[3] = {g.ox, g.oy, g.oz};
+    const int dims[3] = {g.nx, g.ny, g.nz};
+    int lo[3], hi[3];
+    for (int k = 0; k < 3; ++k) {
+        const double d = __dadd_rn(__dadd_rn(__dmul_rn(f.R[3 * k], xc), __dmul_rn(f.R[3 * k + 1], yc)), f.R[3 * k + 2]);
+        const double p = __ddiv_rn(__dsub_rn(__dadd_rn(f.C[k], __dmul_rn(z, d)), org[k]), g.res);
+        if (p < 0.0 || p >= (double)dims[k]) return;
+        lo[k] = max((int)floor(__dsub_rn(p, r)), 0);
+        hi[k] = min((int)floor(__dadd_rn(p, r)), dims[k] - 1);
+    }
+    for (int bz = lo[2] >> g.bshift; bz <= hi[2] >> g.bshift; ++bz)
+        for (int by = lo[1] >> g.bshift; by <= hi[1] >> g.bshift; ++by)
+            for (int bx = lo[0] >> g.bshift; bx <= hi[0] >> g.bshift; ++bx)
+                mask[bx + g.nbx * (by + (long long)g.nby * bz)] = 1;
+}
 
 // ---------------------------------------------------------------- K3
 // B3: off_q = clamp(rint((0.5 (t_in + t_out) L - Z) * 32768), +-32767), the span midpoint
@@ -317,19 +367,24 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             const int a = w.earliest(na, da);
             const double t_out = crossing_t(w, a, na, da, last);
             const int vx = voxel_slot(g, w.c0, w.c1, w.c2);
-            const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
-            long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
-            q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
-            sv[e & 7] = vx;
-            so[e & 7] = (short)q;
-            if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so);
-            ++e;
-            // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
-            const int b = vx >> kTileShift, l = vx & (kTileSlots - 1);
-            const bool start = !run_extends(b, l, run_tile, run_n, run_prev);
-            run_n = start ? 1 : run_n + 1;
-            run_tile = b;
-            run_prev = l;
+            const bool keep = cell_in_map(g, w.c0, w.c1, w.c2);  // empty skip (sparse bricks)
+            bool start = false;
+            if (keep) {
+                const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
+                long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
+                q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
+                sv[e & 7] = vx;
+                so[e & 7] = (short)q;
+                if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so);
+                ++e;
+                // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
+                const int b = vx >> kTileShift, l = vx & (kTileSlots - 1);
+                start = !run_extends(b, l, run_tile, run_n, run_prev);
+                run_n = start ? 1 : run_n + 1;
+                run_tile = b;
+                run_prev = l;
+            }
+            const int b = vx >> kTileShift;
             const unsigned sm = __ballot_sync(am, start);
             if (start) {
                 const int key = bucket0 + b;  // (frame, tile) bucket; the tile itself in per-ray mode
@@ -342,7 +397,10 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 w.advance(na, da);
                 w.t_in = t_out;
                 alive = w.inside(g);
-                if (alive && e >= e_cap) {  // cannot happen (K1's bound); never write past the segment
+                // cannot happen (K1's bound); never write past the segment.  In a sparse map the walk
+                // goes on through skipped cells after its last emitted one, so only a cell that
+                // would be emitted counts.
+                if (alive && e >= e_cap && cell_in_map(g, w.c0, w.c1, w.c2)) {
                     alive = false;
                     overflow = true;
                 }
@@ -703,6 +761,13 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
     raygen_count_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, n_r, status, ray_z, counters);
+}
+
+void launch_brick_alloc(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, uint8_t* mask,
+                        cudaStream_t s) {
+    const long long np = (long long)f.W * f.H;
+    if (np == 0) return;
+    brick_alloc_kernel<<<blocks_for(np, 256), 256, 0, s>>>(f, g, n, depth, mask);
 }
 
 void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, long long r0,

@@ -36,7 +36,15 @@ struct GridDesc {
     int nx, ny, nz;
     int ntx, nty, ntz;
     double res, ox, oy, oz;
+    // sparse-brick map (NEXT #4, reading R23): a cell is part of the map iff
+    // bmask[(cx >> bshift) + nbx ((cy >> bshift) + nby (cz >> bshift))] != 0; nullptr = dense
+    const uint8_t* bmask;
+    int bshift, nbx, nby;
 };
+__host__ __device__ __forceinline__ bool cell_in_map(const GridDesc& g, int x, int y, int z) {
+    return !g.bmask ||
+           g.bmask[(x >> g.bshift) + g.nbx * ((y >> g.bshift) + g.nby * (long long)(z >> g.bshift))] != 0;
+}
 
 __host__ __device__ __forceinline__ int voxel_slot(const GridDesc& g, int x, int y, int z) {
     return ((((z >> 4) * g.nty + (y >> 5)) * g.ntx + (x >> 5)) << kTileShift) | ((z & 15) << 10) | ((y & 31) << 5) |
@@ -77,6 +85,7 @@ struct FrameDesc {
     long long ray_base;       // index of this frame's first ray
     long long depth_off;      // offset of the frame's depth image in the pending-depth buffer
     int index;                // frame index in the ctx
+    int skip_count;           // K1 without the walk count (sparse bricks before the final allocation)
     int bucket_stride;        // tile-run bucket of a run in tile t: index * bucket_stride + t
 };
 
@@ -135,6 +144,10 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
 // [cta0[k], cta0[k+1]) of kFillThreads pixels), writing vid / off_q at row_ptr offsets and
 // counting the tile runs (K4b) per tile; then log nu per incidence of the rays [r0, r0 + n_rays)
 // (RayInfo.n = the walk's length; counters[0] += incidences, counters[1] += bound overflows = 0)
+// NEXT #4: allocate the bricks around the reprojected depth points of one frame (every pixel,
+// whatever the rank; reading R23) into g.bmask
+void launch_brick_alloc(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, uint8_t* mask,
+                        cudaStream_t s);
 constexpr int kFillThreads = 128;
 void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, long long r0,
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,

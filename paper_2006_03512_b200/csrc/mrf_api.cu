@@ -84,6 +84,10 @@ struct mrf_ctx {
     int k6_item = 8192;
     // keyframe-average mode (NEXT #3, reading R22): one message per (frame, voxel)
     bool kf_avg = false;
+    // sparse-brick mode (NEXT #4, reading R23): brick allocation mask, grid.bmask points at it
+    int brick = 0;  // cells per brick edge, 0 = dense
+    DBuf<uint8_t> bmask;
+    long long n_brick_slots = 0;
     DBuf<int32_t> qbar;           // [frame][VI] quantised average log-odds
     DBuf<double> kf_sums;          // [frame][VI] fp64 D, then [frame][VI] int64 packed counts
     long long kf_frames_alloc = 0;
@@ -264,6 +268,31 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
 // the device, counters[10..11]; read them once when something needs E_real.
 mrf_status sync_fill(mrf_ctx* c) {
     if (!c->fill_pending) return MRF_OK;
+    if (!c->pend.empty() && c->grid.bmask) {
+        // Sparse bricks: every frame is allocated by now (the graph is walked once, R23), so the
+        // per-ray counts of add_frame -- made before the later frames' bricks existed -- are
+        // redone against the final allocation and the segments laid out again.
+        long long E = c->E_filled;
+        for (const FrameDesc& f : c->pend) {
+            const long long Rf = (long long)f.rows_owned * f.W;
+            CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+            {
+                ProfScope ps(c, MRF_K_RAYGEN_COUNT);
+                FrameDesc fc = f;
+                fc.skip_count = 0;
+                launch_raygen_count(fc, c->grid, c->noise, c->depth_all.p + f.depth_off, c->n_r.p, c->status.p,
+                                    c->ray_z.p, c->counters.p + 2, c->stream);
+                CK_LAUNCH(MRF_K_RAYGEN_COUNT, Rf > 0 ? 1 : 0);
+            }
+            mrf_status st;
+            if ((st = scan(c, c->n_r.p + f.ray_base, c->row_ptr.p + f.ray_base, Rf, E)) != MRF_OK) return st;
+            if ((st = read_ll(c, c->row_ptr.p + f.ray_base + Rf, &E)) != MRF_OK) return st;
+            if (E >= (1LL << 31) - kPadElems)  // the frames stay pending: mrf_reset starts over
+                return set_err(c, MRF_ERR_CAPACITY,
+                               "sparse bricks: the final allocation gives more than 2^31 incidence slots");
+        }
+        c->E = E;
+    }
     if (!c->pend.empty()) {
         const size_t ne = (size_t)c->E + kPadElems;
         CK(c->vid.ensure(ne, (size_t)c->E_filled, c->stream));
@@ -765,7 +794,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
-    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->marg.release(); c->eval_cls.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->bmask.release(); c->marg.release(); c->eval_cls.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
@@ -820,6 +849,7 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->depth_used = 0;
     c->E_filled = c->R_filled = 0;
     c->kf_frames_alloc = 0;
+    if (c->grid.bmask) CK(cudaMemsetAsync(c->bmask.p, 0, (size_t)c->n_brick_slots, c->stream));
     CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
@@ -834,6 +864,8 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
 mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_t height, const double K[4],
                          const double T_wc[12], int64_t* frame_id_out) {
     ENTER(ctx);
+    if (c->grid.bmask && c->E_filled > 0)
+        return set_err(c, MRF_ERR_STATE, "sparse bricks: add every keyframe before the graph is first used");
     if (!depth || !K || !T_wc) return set_err(c, MRF_ERR_INVALID_ARG, "NULL argument");
     if (width <= 0 || height <= 0) return set_err(c, MRF_ERR_INVALID_ARG, "width/height must be > 0");
     if (!finite_all(K, 4) || !(K[0] > 0) || !(K[1] > 0))
@@ -883,6 +915,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     f.rows_owned = rows_owned;
     f.ray_base = c->R;
     f.index = (int)c->frames.size();
+    f.skip_count = c->grid.bmask ? 1 : 0;  // sparse: the rays are counted once all frames are allocated
     f.bucket_stride = c->kf_avg ? (int)c->NT : 0;
     if (c->kf_avg) {  // this frame's (frame, tile) run counters
         const size_t F = c->frames.size();
@@ -904,6 +937,10 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2];
     if (E_new >= (1LL << 31) - kPadElems)
         return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
+    if (c->grid.bmask) {  // sparse bricks: allocate around this frame's reprojected points
+        launch_brick_alloc(f, c->grid, c->noise, d_depth, c->bmask.p, c->stream);
+        CK_LAUNCH(MRF_K_RAYGEN_COUNT, 1);
+    }
     f.depth_off = c->depth_used;
     c->depth_used += (long long)npix;
     if (Rf > 0) c->pend.push_back(f);
@@ -1259,6 +1296,42 @@ mrf_status mrf_set_message_mode(mrf_ctx* ctx, int32_t mode) {
     }
     c->kf_frames_alloc = 0;
     c->dirty = true;
+    return MRF_OK;
+}
+
+mrf_status mrf_set_sparse_bricks(mrf_ctx* ctx, int32_t brick) {
+    ENTER(ctx);
+    if (brick != 0 && (brick < 2 || brick > 64 || (brick & (brick - 1))))
+        return set_err(c, MRF_ERR_INVALID_ARG, "brick edge must be 0 (dense) or a power of two in [2, 64]");
+    if (!c->frames.empty()) return set_err(c, MRF_ERR_STATE, "sparse bricks are set before the first frame");
+    c->brick = brick;
+    if (brick == 0) {
+        c->grid.bmask = nullptr;
+        return MRF_OK;
+    }
+    const int nb[3] = {(c->grid.nx + brick - 1) / brick, (c->grid.ny + brick - 1) / brick,
+                       (c->grid.nz + brick - 1) / brick};
+    c->n_brick_slots = (long long)nb[0] * nb[1] * nb[2];
+    CK(c->bmask.ensure((size_t)c->n_brick_slots, 0, c->stream));
+    CK(cudaMemsetAsync(c->bmask.p, 0, (size_t)c->n_brick_slots, c->stream));
+    c->grid.bmask = c->bmask.p;
+    c->grid.bshift = __builtin_ctz((unsigned)brick);
+    c->grid.nbx = nb[0];
+    c->grid.nby = nb[1];
+    c->dirty = true;
+    return MRF_OK;
+}
+
+mrf_status mrf_export_bricks(mrf_ctx* ctx, uint8_t* out, int64_t* n_allocated) {
+    ENTER(ctx);
+    if (!c->grid.bmask) return set_err(c, MRF_ERR_STATE, "not a sparse-brick map");
+    std::vector<uint8_t> m((size_t)c->n_brick_slots);
+    CK(cudaMemcpyAsync(m.data(), c->bmask.p, m.size(), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    long long na = 0;
+    for (uint8_t x : m) na += x != 0;
+    if (out) memcpy(out, m.data(), m.size());
+    if (n_allocated) *n_allocated = na;
     return MRF_OK;
 }
 

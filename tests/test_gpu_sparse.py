@@ -1,0 +1,110 @@
+"""GPU parity of the sparse-brick variant (DESIGN.md
+reading R23) against the oracle, through the C ABI: the brick allocation mask and the empty-skip
+graph bit-exact (integer work), messages 1e-3 relative and marginals 1e-4 (the per-ray bars)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2006_03512_b200 as pkg  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+MSG_TOL = 1e-3
+MARG_TOL = 1e-4
+
+
+def _sparse_map(w, frames=None, brick=8):
+    m = pkg.MRFMap.from_workload(w)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    m.set_sparse_bricks(brick)
+    for fr in (w.frames if frames is None else frames):
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+    return m
+
+
+def _msg_err(lam, ref):
+    return float(np.max(np.abs(lam.astype(np.float64) - ref) / np.maximum(1.0, np.abs(ref)))) if len(ref) else 0.0
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny_frames", "frame1"])
+def test_sparse_graph_bitexact_and_bp(name):
+    w = {"tiny": synth.tiny, "tiny_frames": synth.tiny_frames, "frame1": synth.single_frame}[name]()
+    p = oracle.Params.from_workload(w)
+    bk = oracle.alloc_bricks(p, w.frames)
+    g = oracle.build_graph(p, w.frames, bricks=bk)
+    n_iter = 2 if name == "frame1" else 5
+    lam_ref, T_ref = oracle.bp(p, g, n_iter)
+    with _sparse_map(w) as m:
+        assert np.array_equal(m.export_bricks(), bk.mask)
+        gg = m.export_graph()
+        for k in ("row_ptr", "vid", "off_q", "pixel"):
+            assert np.array_equal(gg[k], getattr(g, k)), k
+        assert g.E < oracle.build_graph(p, w.frames[:1]).E * len(w.frames)  # cells were skipped
+        m.bp_iterate(n_iter)
+        lam = m.export_messages()
+        marg = m.marginals()
+    assert _msg_err(lam, lam_ref) <= MSG_TOL
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+    assert np.all(marg[~bk.cell_mask(p)] == np.float32(p.prior))  # unallocated space keeps the prior
+
+
+def test_sparse_frames30_sampled_rays():
+    """30 frames: the allocation over all frames bit-exact, and 3000 sampled pixels traced one by
+    one by the oracle's empty-skip walk bit-exact against mrf_export_rays."""
+    w = synth.frames30()
+    p = oracle.Params.from_workload(w)
+    bk = oracle.alloc_bricks(p, w.frames)
+    with _sparse_map(w) as m:
+        mask = m.export_bricks()
+        sizes = m.graph_sizes()
+        H, W = w.frames[0].depth.shape
+        rng = np.random.default_rng(5)
+        key = np.unique(rng.integers(0, len(w.frames) * H * W, 3000))
+        fsel, psel = (key // (H * W)).astype(np.int32), (key % (H * W)).astype(np.int64)
+        got = m.export_rays(fsel, psel)
+    assert np.array_equal(mask, bk.mask)
+    assert sizes["E"] < 846709585  # the dense frames30 graph
+    lens = np.diff(got["row_ptr"])
+    for fi in np.unique(fsel):
+        idx = np.nonzero(fsel == fi)[0]
+        sub = oracle.trace_pixels(p, w.frames[fi], psel[idx], int(fi), bricks=bk)
+        order = {int(px): k for k, px in enumerate(sub.pixel)}
+        for i in idx:
+            k = order.get(int(psel[i]))
+            s0, s1 = got["row_ptr"][i], got["row_ptr"][i + 1]
+            if k is None:
+                assert lens[i] == 0
+                continue
+            e0, e1 = sub.row_ptr[k], sub.row_ptr[k + 1]
+            assert np.array_equal(got["vid"][s0:s1], sub.vid[e0:e1])
+            assert np.array_equal(got["off_q"][s0:s1], sub.off_q[e0:e1])
+
+
+def test_sparse_mode_rules():
+    w = synth.tiny_frames(n_frames=3)
+    m = pkg.MRFMap.from_workload(w)
+    with m:
+        with pytest.raises(pkg.MrfError) as e:
+            m.set_sparse_bricks(6)  # not a power of two
+        assert e.value.status == 1
+        with pytest.raises(pkg.MrfError):
+            m.export_bricks()  # dense
+        m.set_sparse_bricks(8)
+        m.add_frame(w.frames[0].depth, w.frames[0].K, w.frames[0].T_wc)
+        with pytest.raises(pkg.MrfError) as e:
+            m.set_sparse_bricks(4)  # frames already added
+        assert e.value.status == 6
+        m.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
+        m.bp_iterate(1)
+        with pytest.raises(pkg.MrfError) as e:  # the graph is in use: the allocation is fixed
+            m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)
+        assert e.value.status == 6
+        m.reset()  # clears the allocation, keeps the mode
+        assert m.export_bricks().sum() == 0
+        m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)
+        p = oracle.Params.from_workload(w)
+        assert np.array_equal(m.export_bricks(), oracle.alloc_bricks(p, [w.frames[2]]).mask)
