@@ -260,7 +260,7 @@ struct RunBuilder {
 // SPEC allocate_for_depth_image (reading R23): per pixel with a valid depth whose
 // measured point p lies in the grid, r = margin_k sigma(Z) / res; every brick holding a cell of
 // [floor(p - r), floor(p + r)] (clamped) is marked.  fp64 in the oracle's op order (the mask is
-// bit-exact with orc_alloc_bricks); the byte stores of 1 are idempotent, so no atomics.
+// bit-exact with the oracle's allocation); the byte stores of 1 are idempotent, so no atomics.
 __global__ void brick_alloc_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const float* __restrict__ depth,
                                    uint8_t* mask) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
