@@ -314,6 +314,7 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long l
 
 // One launch fills every frame added since the last fill (frames[k] owns the CTAs
 // [cta0[k], cta0[k+1])): one wave-quantisation tail per batch instead of per frame.
+template <bool SPARSE>
 __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc* __restrict__ frames,
                                                        const int* __restrict__ cta0, int n_frames, GridDesc g,
                                                        NoiseDesc n, const float* __restrict__ depth_all,
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             const int a = w.earliest(na, da);
             const double t_out = crossing_t(w, a, na, da, last);
             const int vx = voxel_slot(g, w.c0, w.c1, w.c2);
-            const bool keep = cell_in_map(g, w.c0, w.c1, w.c2);  // empty skip (sparse bricks)
+            const bool keep = !SPARSE || cell_in_map(g, w.c0, w.c1, w.c2);  // empty skip (sparse bricks)
             bool start = false;
             if (keep) {
                 const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 // cannot happen (K1's bound); never write past the segment.  In a sparse map the walk
                 // goes on through skipped cells after its last emitted one, so only a cell that
                 // would be emitted counts.
-                if (alive && e >= e_cap && cell_in_map(g, w.c0, w.c1, w.c2)) {
+                if (alive && e >= e_cap && (!SPARSE || cell_in_map(g, w.c0, w.c1, w.c2))) {
                     alive = false;
                     overflow = true;
                 }
@@ -774,9 +775,14 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s) {
-    if (n_ctas > 0)
-        dda_fill_kernel<<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, off_q,
-                                                        tile_runs, ray_z, counters);
+    if (n_ctas > 0) {
+        if (g.bmask)
+            dda_fill_kernel<true><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr,
+                                                                  vid, off_q, tile_runs, ray_z, counters);
+        else
+            dda_fill_kernel<false><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr,
+                                                                   vid, off_q, tile_runs, ray_z, counters);
+    }
     if (n_rays > 0) lnu_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(r0, n_rays, mp, row_ptr, ray_z, off_q, lnu);
 }
 
