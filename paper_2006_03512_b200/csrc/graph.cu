@@ -124,6 +124,60 @@ struct Walker {
         if (t1) { c1 += s1; n1 += (unsigned)kFixOne; }
         if (t2) { c2 += s2; n2 += (unsigned)kFixOne; }
     }
+    // Empty skip (sparse bricks): from a cell of an unallocated brick, jump to the first
+    // cell past the brick in one step -- exactly the state the cell-by-cell walk reaches.  Axis k
+    // leaves the brick (clamped to the grid) after m_k crossings, the m_k-th at the exact time
+    // (n_k + (m_k - 1) 2^16) / d_k; t* is the earliest of these; every axis then takes all its
+    // crossings at times <= t* (ties step together, as in advance()), and t_in = RN(t*), the
+    // crossing that enters the new cell.  Returns false if the segment ends inside the brick.
+    __device__ __forceinline__ static unsigned exit_steps(int c, int s, int dim, int bs) {
+        if (s > 0) return (unsigned)(min(((c >> bs) + 1) << bs, dim) - c);
+        return (unsigned)(c - ((c >> bs) << bs) + 1);
+    }
+    // 1 + floor((Ns d - n Ds) / (2^16 Ds)) crossings of an axis at times (n + i 2^16) / d <= Ns / Ds
+    // (0 if even the first is later): the quotient (small, <= the brick edge) estimated in fp64 with
+    // y = RN(1 / Ds) and corrected exactly in integers (a 64-bit integer division is ~100 ops)
+    __device__ __forceinline__ static unsigned long long crossings_upto(unsigned n, unsigned d, unsigned long long Ns,
+                                                                        unsigned Ds, double y) {
+        if (!d) return 0;
+        const unsigned long long lhs = Ns * d, rhs = (unsigned long long)n * Ds;  // t* >= n / d ?
+        if (lhs < rhs) return 0;
+        const unsigned long long diff = lhs - rhs, unit = (unsigned long long)kFixOne * Ds;
+        unsigned long long k = (unsigned long long)__dmul_rn(__dmul_rn((double)diff, y), 1.0 / 65536.0);
+        while (k * unit > diff) --k;
+        while ((k + 1) * unit <= diff) ++k;
+        return k + 1;
+    }
+    __device__ bool skip_brick(const GridDesc& g) {
+        const int bs = g.bshift;
+        int a = -1;
+        unsigned long long Ns = 0;
+        unsigned Ds = 1;
+        if (d0) {
+            a = 0;
+            Ns = n0 + (unsigned long long)(exit_steps(c0, s0, g.nx, bs) - 1) * kFixOne;
+            Ds = d0;
+        }
+        if (d1) {
+            const unsigned long long N = n1 + (unsigned long long)(exit_steps(c1, s1, g.ny, bs) - 1) * kFixOne;
+            if (a < 0 || N * Ds < Ns * d1) { a = 1; Ns = N; Ds = d1; }
+        }
+        if (d2) {
+            const unsigned long long N = n2 + (unsigned long long)(exit_steps(c2, s2, g.nz, bs) - 1) * kFixOne;
+            if (a < 0 || N * Ds < Ns * d2) { a = 2; Ns = N; Ds = d2; }
+        }
+        if (a < 0 || Ns >= Ds) return false;  // the segment ends in this brick
+        const double y = a == 0 ? y0 : (a == 1 ? y1 : y2);  // RN(1 / Ds)
+        const unsigned long long k0 = crossings_upto(n0, d0, Ns, Ds, y), k1 = crossings_upto(n1, d1, Ns, Ds, y),
+                                 k2 = crossings_upto(n2, d2, Ns, Ds, y);
+        c0 += s0 * (int)k0; n0 += (unsigned)(k0 * kFixOne);
+        c1 += s1 * (int)k1; n1 += (unsigned)(k1 * kFixOne);
+        c2 += s2 * (int)k2; n2 += (unsigned)(k2 * kFixOne);
+        const double n = (double)Ns, d = (double)Ds;
+        const double q = __dmul_rn(n, y);
+        t_in = __fma_rn(__fma_rn(-q, d, n), y, q);  // RN(Ns / Ds), as crossing_t
+        return true;
+    }
 };
 
 // t of the next crossing (num/den, correctly rounded) or 1 when the walk ends in this cell.
@@ -175,7 +229,11 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
                     // space too, so count the cells of allocated bricks exactly (the walk without
                     // its crossing parameters)
                     for (;;) {
-                        bound += cell_in_map(g, w.c0, w.c1, w.c2) ? 1 : 0;
+                        if (!cell_in_map(g, w.c0, w.c1, w.c2)) {  // empty skip
+                            if (!w.skip_brick(g) || !w.inside(g)) break;
+                            continue;
+                        }
+                        ++bound;
                         unsigned na, da;
                         const int a = w.earliest(na, da);
                         if (a < 0 || na >= da) break;
@@ -363,14 +421,15 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
         const unsigned am = __ballot_sync(kFull, alive);
         if (am == 0) break;
         if (alive) {
-            bool last;
-            unsigned na, da;
-            const int a = w.earliest(na, da);
-            const double t_out = crossing_t(w, a, na, da, last);
-            const int vx = voxel_slot(g, w.c0, w.c1, w.c2);
-            const bool keep = !SPARSE || cell_in_map(g, w.c0, w.c1, w.c2);  // empty skip (sparse bricks)
+            const bool keep = !SPARSE || cell_in_map(g, w.c0, w.c1, w.c2);
             bool start = false;
+            int b = 0;
             if (keep) {
+                bool last;
+                unsigned na, da;
+                const int a = w.earliest(na, da);
+                const double t_out = crossing_t(w, a, na, da, last);
+                const int vx = voxel_slot(g, w.c0, w.c1, w.c2);
                 const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
                 long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
                 q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
@@ -379,32 +438,33 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so);
                 ++e;
                 // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
-                const int b = vx >> kTileShift, l = vx & (kTileSlots - 1);
+                b = vx >> kTileShift;
+                const int l = vx & (kTileSlots - 1);
                 start = !run_extends(b, l, run_tile, run_n, run_prev);
                 run_n = start ? 1 : run_n + 1;
                 run_tile = b;
                 run_prev = l;
+                if (last) {
+                    alive = false;
+                } else {
+                    w.advance(na, da);
+                    w.t_in = t_out;
+                    alive = w.inside(g);
+                }
+            } else {  // empty skip: past the unallocated brick in one step (sparse bricks)
+                alive = w.skip_brick(g) && w.inside(g);
             }
-            const int b = vx >> kTileShift;
             const unsigned sm = __ballot_sync(am, start);
             if (start) {
                 const int key = bucket0 + b;  // (frame, tile) bucket; the tile itself in per-ray mode
                 const unsigned peers = __match_any_sync(sm, key);
                 if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[key], __popc(peers));
             }
-            if (last) {
+            // cannot happen (K1's count); never write past the segment.  In a sparse map only a
+            // cell that would be emitted counts.
+            if (alive && e >= e_cap && (!SPARSE || cell_in_map(g, w.c0, w.c1, w.c2))) {
                 alive = false;
-            } else {
-                w.advance(na, da);
-                w.t_in = t_out;
-                alive = w.inside(g);
-                // cannot happen (K1's bound); never write past the segment.  In a sparse map the walk
-                // goes on through skipped cells after its last emitted one, so only a cell that
-                // would be emitted counts.
-                if (alive && e >= e_cap && (!SPARSE || cell_in_map(g, w.c0, w.c1, w.c2))) {
-                    alive = false;
-                    overflow = true;
-                }
+                overflow = true;
             }
             if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so);  // partial tail
         }
