@@ -108,3 +108,26 @@ def test_sparse_mode_rules():
         m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)
         p = oracle.Params.from_workload(w)
         assert np.array_equal(m.export_bricks(), oracle.alloc_bricks(p, [w.frames[2]]).mask)
+
+
+def test_sparse_bricks_with_keyframe_averages():
+    """The two paper-model modes compose: keyframe-average messages over the empty-skip graph
+    of a sparse-brick map, against oracle.kf_bp on the oracle's sparse graph."""
+    w = synth.tiny_frames(n_frames=4)
+    p = oracle.Params.from_workload(w)
+    bk = oracle.alloc_bricks(p, w.frames)
+    g = oracle.build_graph(p, w.frames, bricks=bk)
+    lam_ref, lbar_ref, T_ref = oracle.kf_bp(p, g, 5, F=len(w.frames))
+    m = pkg.MRFMap.from_workload(w)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    m.set_sparse_bricks(8)
+    m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+    for fr in w.frames:
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+    with m:
+        assert np.array_equal(m.export_graph()["vid"], g.vid)
+        m.bp_iterate(5)
+        lam = m.export_messages()
+        marg = m.marginals()
+    assert _msg_err(lam, lam_ref) <= MSG_TOL
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
