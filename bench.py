@@ -173,6 +173,9 @@ def run_ours(args, rank, world, local_rank):
     if args.bricks:  # NEXT #4: brick allocation around the depth points + empty-skip walks
         for mm in (m.maps if emulate > 1 else [m]):
             mm.set_sparse_bricks(args.bricks)
+    if args.matrix_free:  # NEXT #1: keep only lambda + tile runs, re-walk per chunk of frames
+        for mm in (m.maps if emulate > 1 else [m]):
+            mm.set_matrix_free(args.matrix_free)
 
     depth_dev = [torch.from_numpy(fr.depth).to(dev) for fr in w.frames]
     depth_host = [torch.from_numpy(fr.depth).pin_memory() for fr in w.frames]
@@ -295,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": args.config, "frames": len(w.frames), "bp_iterations": n_iter,
-                       "messages": args.messages, "bricks": args.bricks,
+                       "messages": args.messages, "bricks": args.bricks, "matrix_free": args.matrix_free,
                        "incidences": E_all, "rays": R_all, "voxels": V, "grid": list(w.dims), "res_m": w.res,
                        "parallelism": (f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else
                                        f"1 GPU, {emulate} emulated ranks (device-side int64 reduce)" if emulate > 1
@@ -331,6 +334,8 @@ def main():
     ap.add_argument("--iters", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--matrix-free", type=int, default=0,
+                    help="frames per re-walked chunk (NEXT #1: only messages + tile runs stored; 0 = stored graph)")
     ap.add_argument("--bricks", type=int, default=0,
                     help="sparse-brick map with B^3 bricks (P:203-205; 0 = dense, the north_star graph)")
     ap.add_argument("--messages", default="per-ray", choices=["per-ray", "keyframe-avg"],

@@ -239,6 +239,20 @@ mrf_status mrf_set_sparse_bricks(mrf_ctx* ctx, int32_t brick);
  * 1 = allocated; n_allocated (nullable) = number of allocated bricks.  MRF_ERR_STATE when dense. */
 mrf_status mrf_export_bricks(mrf_ctx* ctx, uint8_t* out, int64_t* n_allocated);
 
+/* Matrix-free iteration (the paper re-traces every keyframe each pass,
+ * P:200).  frames_per_chunk = 0: the ray->voxel lists (vid, off_q, log nu: 10 bytes per
+ * incidence) are stored once (default).  frames_per_chunk = F > 0: only the messages (4 bytes per
+ * incidence) and the tile-run transpose (~1 byte per incidence) persist; the rays of each chunk
+ * of F frames are walked again by the DDA into a scratch the size of one chunk, for the
+ * transpose build and before every message pass.  Same results as the stored graph (the walk is
+ * the same integer DDA), at the cost of one DDA walk per iteration.  The depth images are kept
+ * (W*H floats per frame).  Set before the first frame (MRF_ERR_STATE otherwise);
+ * environment MRF_SYNC_DEBUG=1 synchronises after every matrix-free step and reports its status on
+ * stderr (debugging aid);
+ * mrf_export_graph / mrf_export_rays / mrf_export_transpose return MRF_ERR_STATE, and
+ * mrf_graph_sizes reports n_active_vox = -1. */
+mrf_status mrf_set_matrix_free(mrf_ctx* ctx, int32_t frames_per_chunk);
+
 /* 128-byte ncclUniqueId for MRF_COMM_NCCL (call on rank 0, broadcast to the others). */
 mrf_status mrf_nccl_unique_id(unsigned char out[128]);
 

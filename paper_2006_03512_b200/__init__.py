@@ -226,6 +226,11 @@ class MRFMap:
         self._chk(self._L.mrf_export_keyframe_average(self._h, int(frame), _ptr(out)))
         return out
 
+    def set_matrix_free(self, frames_per_chunk=4):
+        """mrf_set_matrix_free: keep only the messages and the tile runs; re-walk the rays of each
+        chunk of frames_per_chunk frames before every message pass (0 = stored graph)."""
+        self._chk(self._L.mrf_set_matrix_free(self._h, int(frames_per_chunk)))
+
     def set_sparse_bricks(self, brick=8):
         """mrf_set_sparse_bricks: brick-sparse map with B^3 bricks allocated around the
         reprojected depth points and empty-skip ray walks; 0 = dense."""

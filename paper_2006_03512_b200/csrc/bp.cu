@@ -337,10 +337,13 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     if (wi * RPW >= n) return;  // warp-uniform
     const int lane = threadIdx.x & 31, sl = lane & (G - 1);
     const long long ri = wi * RPW + lane / G;
+    // lanes past the end of the list take its last ray with no incidences of their own: their
+    // (masked) loads stay inside the incidence range the list covers -- which, in the
+    // matrix-free mode, is a scratch holding only the current chunk's slots
     int nr = 0, e0 = 0, fr = 0;
-    if (ri < n) {
-        const int r = __ldg(rays + ri);
-        nr = ray_z[r].n;
+    {
+        const int r = __ldg(rays + (ri < n ? ri : n - 1));
+        if (ri < n) nr = ray_z[r].n;
         e0 = (int)__ldg(row_ptr + r);
         if constexpr (AVG) fr = ray_z[r].frame;
     }

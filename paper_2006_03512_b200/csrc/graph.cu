@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 alive = w.skip_brick(g) && w.inside(g);
             }
             const unsigned sm = __ballot_sync(am, start);
-            if (start) {
+            if (start && tile_runs) {  // (no counting on the matrix-free re-walks)
                 const int key = bucket0 + b;  // (frame, tile) bucket; the tile itself in per-ray mode
                 const unsigned peers = __match_any_sync(sm, key);
                 if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[key], __popc(peers));
@@ -473,6 +473,15 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
     if (i < n_pix) {
         ne = (int)(e - e_ray);
         ray_z[f.ray_base + i].n = ne;
+        // The rest of the segment K1 sized (its bound can exceed the walk at ties and grid exits)
+        // gets voxel 0: K5 lanes gather T and the keyframe averages through every slot of their
+        // chunk, masked elements included, so no slot of a segment may hold a stale id.
+        for (long long z = (e + 7) & ~7LL; z < e_cap; z += 8) {
+            int4* dv = reinterpret_cast<int4*>(vid + z);
+            dv[0] = make_int4(0, 0, 0, 0);
+            dv[1] = make_int4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(off_q + z) = make_uint4(0u, 0u, 0u, 0u);
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(kFull, ne, o);
@@ -748,6 +757,39 @@ __global__ void class_scatter_kernel(long long n_rays, const RayInfo* __restrict
     if (k >= 0) out[off.off[k] + (long long)base + __popc(peers & ((1u << lane) - 1u))] = (int32_t)r;
 }
 
+// Matrix-free class lists (NEXT #1): key = (frame / fpc) * kNumClasses + class, so that each
+// chunk of fpc frames has its own class lists (off[key] from the host scan of counts[key]).
+__global__ void class_count_mf_kernel(long long n_rays, const RayInfo* __restrict__ info, int fpc,
+                                      unsigned long long* counts) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    int k = -1;
+    if (r < n_rays) {
+        const RayInfo ri = info[r];
+        const int cl = ray_class(ri.n);
+        k = cl < 0 ? -1 : (ri.frame / fpc) * kNumClasses + cl;
+    }
+    const unsigned peers = __match_any_sync(kFull, k);
+    if (k >= 0 && lane == __ffs(peers) - 1) atomicAdd(&counts[k], (unsigned long long)__popc(peers));
+}
+__global__ void class_scatter_mf_kernel(long long n_rays, const RayInfo* __restrict__ info, int fpc,
+                                        const long long* __restrict__ off, unsigned long long* cursor, int32_t* out) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    int k = -1;
+    if (r < n_rays) {
+        const RayInfo ri = info[r];
+        const int cl = ray_class(ri.n);
+        k = cl < 0 ? -1 : (ri.frame / fpc) * kNumClasses + cl;
+    }
+    const unsigned peers = __match_any_sync(kFull, k);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long base = 0;
+    if (k >= 0 && lane == leader) base = atomicAdd(&cursor[k], (unsigned long long)__popc(peers));
+    base = __shfl_sync(kFull, base, leader);
+    if (k >= 0) out[off[k] + (long long)base + __popc(peers & ((1u << lane) - 1u))] = (int32_t)r;
+}
+
 __global__ void compact_kernel(long long n, const int32_t* __restrict__ flags, const long long* __restrict__ pos,
                                int32_t* out) {
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -896,6 +938,17 @@ void launch_class_scatter(long long n_rays, const RayInfo* info, const ClassOffs
                           int32_t* out, cudaStream_t s) {
     if (n_rays == 0) return;
     class_scatter_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, off, cursor, out);
+}
+
+void launch_class_count_mf(long long n_rays, const RayInfo* info, int fpc, unsigned long long* counts, cudaStream_t s) {
+    if (n_rays == 0) return;
+    class_count_mf_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, fpc, counts);
+}
+
+void launch_class_scatter_mf(long long n_rays, const RayInfo* info, int fpc, const long long* off,
+                             unsigned long long* cursor, int32_t* out, cudaStream_t s) {
+    if (n_rays == 0) return;
+    class_scatter_mf_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, info, fpc, off, cursor, out);
 }
 
 void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s) {

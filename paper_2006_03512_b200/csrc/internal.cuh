@@ -239,6 +239,10 @@ struct ClassOffsets {
     long long off[kNumClasses];
 };
 void launch_class_count(long long n_rays, const RayInfo* info, unsigned long long* counts, cudaStream_t s);
+// matrix-free (NEXT #1): class lists per chunk of fpc frames, key = (frame / fpc) * kNumClasses + class
+void launch_class_count_mf(long long n_rays, const RayInfo* info, int fpc, unsigned long long* counts, cudaStream_t s);
+void launch_class_scatter_mf(long long n_rays, const RayInfo* info, int fpc, const long long* off,
+                             unsigned long long* cursor, int32_t* out, cudaStream_t s);
 void launch_class_scatter(long long n_rays, const RayInfo* info, const ClassOffsets& off, unsigned long long* cursor,
                           int32_t* out, cudaStream_t s);
 void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,

@@ -84,6 +84,22 @@ struct mrf_ctx {
     int k6_item = 8192;
     // keyframe-average mode (NEXT #3, reading R22): one message per (frame, voxel)
     bool kf_avg = false;
+    // matrix-free mode (NEXT #1): only lambda and the tile runs persist; vid / off_q / log nu are
+    // re-walked per chunk of mf frames into scratch for the transpose build and for every K5 pass
+    struct MfChunk {
+        int f0, f1;
+        long long r0, r1, e0, e1;
+    };
+    int mf = 0;  // frames per chunk, 0 = off
+    std::vector<FrameDesc> mf_frames;
+    std::vector<long long> mf_frame_e;  // row_ptr at each frame's first ray (+ the end)
+    std::vector<MfChunk> mf_chunks;
+    DBuf<int32_t> s_vid;
+    DBuf<int16_t> s_off;
+    DBuf<float> s_lnu;
+    DBuf<int> d_cta_tmp;
+    DBuf<long long> mf_cls_off_d;
+    std::vector<long long> mf_cls_n, mf_cls_off;
     // sparse-brick mode (NEXT #4, reading R23): brick allocation mask, grid.bmask points at it
     int brick = 0;  // cells per brick edge, 0 = dense
     DBuf<uint8_t> bmask;
@@ -264,6 +280,67 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
     return MRF_OK;
 }
 
+// ---- matrix-free mode (NEXT #1)
+static void mf_dbg(mrf_ctx* c, const char* what) {
+    static const bool on = getenv("MRF_SYNC_DEBUG") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    fprintf(stderr, "[mf] %s: %s\n", what, cudaGetErrorString(e));
+}
+// Chunks of c->mf frames over every frame so far; the scratch holds the largest chunk's slots.
+mrf_status mf_rechunk(mrf_ctx* c) {
+    const int nf = (int)c->mf_frames.size();
+    c->mf_frame_e.assign((size_t)nf + 1, 0);
+    for (int k = 0; k <= nf; ++k) {
+        const long long r = k < nf ? c->mf_frames[k].ray_base : c->R;
+        CK(cudaMemcpyAsync(&c->mf_frame_e[k], c->row_ptr.p + r, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    c->mf_chunks.clear();
+    long long big = 0;
+    for (int f0 = 0; f0 < nf; f0 += c->mf) {
+        const int f1 = std::min(f0 + c->mf, nf);
+        mrf_ctx::MfChunk ch{f0, f1, c->mf_frames[f0].ray_base,
+                            f1 < nf ? c->mf_frames[f1].ray_base : c->R, c->mf_frame_e[f0], c->mf_frame_e[f1]};
+        big = std::max(big, ch.e1 - ch.e0);
+        c->mf_chunks.push_back(ch);
+    }
+    CK(c->s_vid.ensure((size_t)big + kPadElems, 0, c->stream));
+    CK(c->s_off.ensure((size_t)big + kPadElems, 0, c->stream));
+    CK(c->s_lnu.ensure((size_t)big + kPadElems, 0, c->stream));
+    // the slack after the largest chunk is read (masked) by the last rays' lanes: valid ids
+    CK(cudaMemsetAsync(c->s_vid.p, 0, sizeof(int32_t) * c->s_vid.cap, c->stream));
+    CK(c->d_frames.ensure((size_t)std::max(nf, 1), 0, c->stream));
+    if (nf)
+        CK(cudaMemcpyAsync(c->d_frames.p, c->mf_frames.data(), sizeof(FrameDesc) * nf, cudaMemcpyHostToDevice,
+                           c->stream));
+    return MRF_OK;
+}
+
+// Walk frames [f0, f1) of one chunk (the DDA fill + log nu) into the scratch, which stands for
+// the incidence slots [e0, ...) of chunk `ch` (pointers shifted by e0).  count: also count the
+// tile runs and the incidences (first walk of new frames only).
+mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool count) {
+    if (f0 >= f1) return MRF_OK;
+    std::vector<int> cta0((size_t)(f1 - f0) + 1, 0);
+    for (int k = f0; k < f1; ++k) {
+        const long long n_pix = (long long)c->mf_frames[k].rows_owned * c->mf_frames[k].W;
+        cta0[k - f0 + 1] = cta0[k - f0] + (int)((n_pix + kFillThreads - 1) / kFillThreads);
+    }
+    CK(c->d_cta_tmp.ensure(cta0.size(), 0, c->stream));
+    CK(cudaMemcpyAsync(c->d_cta_tmp.p, cta0.data(), sizeof(int) * cta0.size(), cudaMemcpyHostToDevice, c->stream));
+    const long long r0 = c->mf_frames[f0].ray_base;
+    const long long r1 = f1 < (int)c->mf_frames.size() ? c->mf_frames[f1].ray_base : c->R;
+    ProfScope ps(c, MRF_K_DDA_FILL);
+    launch_dda_fill(c->d_frames.p + f0, c->d_cta_tmp.p, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
+                    c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->s_vid.p - ch.e0, c->s_off.p - ch.e0,
+                    c->s_lnu.p - ch.e0, count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12),
+                    c->stream);
+    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (r1 > r0 ? 1 : 0));
+    mf_dbg(c, count ? "walk(count)" : "walk");
+    return MRF_OK;
+}
+
 // The DDA fills count their incidences (and any bound overflow, which K1's bound excludes) on
 // the device, counters[10..11]; read them once when something needs E_real.
 mrf_status sync_fill(mrf_ctx* c) {
@@ -293,9 +370,26 @@ mrf_status sync_fill(mrf_ctx* c) {
         }
         c->E = E;
     }
+    if (!c->pend.empty() && c->mf) {
+        // matrix-free: only lambda is stored per incidence; the new frames are walked once into
+        // the scratch to count their runs and incidences
+        CK(c->lam.ensure((size_t)c->E + kPadElems, (size_t)c->E_filled, c->stream));
+        CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
+        const int first_new = (int)c->mf_frames.size();
+        c->mf_frames.insert(c->mf_frames.end(), c->pend.begin(), c->pend.end());
+        c->pend.clear();
+        mrf_status st;
+        if ((st = mf_rechunk(c)) != MRF_OK) return st;
+        for (const auto& ch : c->mf_chunks)
+            if ((st = mf_walk(c, ch, std::max(ch.f0, first_new), ch.f1, true)) != MRF_OK) return st;
+        c->E_filled = c->E;
+        c->R_filled = c->R;
+    }
     if (!c->pend.empty()) {
         const size_t ne = (size_t)c->E + kPadElems;
         CK(c->vid.ensure(ne, (size_t)c->E_filled, c->stream));
+        // the slack after the last segment is read (masked) by the last rays' K5 lanes
+        CK(cudaMemsetAsync(c->vid.p + c->E, 0, sizeof(int32_t) * kPadElems, c->stream));
         CK(c->off_q.ensure(ne, (size_t)c->E_filled, c->stream));
         CK(c->lnu.ensure(ne, (size_t)c->E_filled, c->stream));
         CK(c->lam.ensure(ne, (size_t)c->E_filled, c->stream));
@@ -390,9 +484,20 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     CK(cudaMemsetAsync(c->tile_cursor.p, 0, sizeof(int32_t) * NT, c->stream));
     {
         ProfScope ps(c, MRF_K_TRANSPOSE);
-        launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p,
-                        c->kf_avg ? (int)c->NT : 0, c->runs.p, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        if (c->mf) {  // per chunk: walk into the scratch, then place the chunk's runs
+            for (const auto& ch : c->mf_chunks) {
+                mrf_status sw;
+                if ((sw = mf_walk(c, ch, ch.f0, ch.f1, false)) != MRF_OK) return sw;
+                launch_run_fill(ch.r1 - ch.r0, c->row_ptr.p + ch.r0, c->ray_z.p + ch.r0, c->s_vid.p - ch.e0,
+                                c->tile_ptr.p, c->tile_cursor.p, c->kf_avg ? (int)c->NT : 0, c->runs.p, c->stream);
+                CK_LAUNCH(MRF_K_TRANSPOSE, ch.r1 > ch.r0 ? 1 : 0);
+                mf_dbg(c, "run_fill");
+            }
+        } else {
+            launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p,
+                            c->kf_avg ? (int)c->NT : 0, c->runs.p, c->stream);
+            CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        }
     }
     // K6 work list, j-major: item j of every tile, then item j+1 ...  Runs land in a tile in
     // roughly ray order, so the items that run concurrently read nearby message ranges (L2 reuse).
@@ -442,6 +547,54 @@ mrf_status prepare(mrf_ctx* c) {
         CK(c->stages.ensure((size_t)std::max(1LL, c->n_stages), 0, c->stream));
         launch_stage_fill(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->pos.p, c->stages.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    }
+    if (c->mf) {  // K5 classes per chunk: counting sort by (chunk, class)
+        const long long NK = (long long)c->mf_chunks.size() * kNumClasses;
+        CK(c->class_cnt.ensure((size_t)std::max(1LL, 2 * NK), 0, c->stream));
+        CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * NK * sizeof(unsigned long long), c->stream));
+        launch_class_count_mf(c->R, c->ray_z.p, c->mf, c->class_cnt.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        c->mf_cls_n.assign((size_t)NK, 0);
+        c->mf_cls_off.assign((size_t)NK, 0);
+        if (NK)
+            CK(cudaMemcpyAsync(c->mf_cls_n.data(), c->class_cnt.p, NK * sizeof(long long), cudaMemcpyDeviceToHost,
+                               c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        long long tot = 0;
+        for (long long k = 0; k < NK; ++k) {
+            c->mf_cls_off[k] = tot;
+            tot += c->mf_cls_n[k];
+        }
+        CK(c->mf_cls_off_d.ensure((size_t)std::max(1LL, NK), 0, c->stream));
+        if (NK)
+            CK(cudaMemcpyAsync(c->mf_cls_off_d.p, c->mf_cls_off.data(), NK * sizeof(long long), cudaMemcpyHostToDevice,
+                               c->stream));
+        CK(c->class_all.ensure((size_t)std::max(1LL, tot), 0, c->stream));
+        launch_class_scatter_mf(c->R, c->ray_z.p, c->mf, c->mf_cls_off_d.p, c->class_cnt.p + NK, c->class_all.p,
+                                c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        const int kl = kNumClasses - 1;
+        long long n_long = 0;
+        CK(cudaMemsetAsync(c->counters.p + 6, 0, sizeof(unsigned long long), c->stream));
+        for (size_t ch = 0; ch < c->mf_chunks.size(); ++ch) {
+            const long long k = (long long)ch * kNumClasses + kl;
+            n_long = std::max(n_long, c->mf_cls_n[k]);
+            if (c->mf_cls_n[k] > 0) {
+                launch_span_max(c->mf_cls_n[k], c->class_all.p + c->mf_cls_off[k], c->ray_z.p, c->counters.p + 6,
+                                c->stream);
+                CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+            }
+        }
+        if (n_long > 0) {
+            long long span = 0;
+            if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
+            const long long tile = 512;
+            c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
+            c->n_warps_long = (int)std::min<long long>(n_long, 148LL * 16);
+            CK(c->long_scratch.ensure((size_t)(c->long_scratch_per_warp * c->n_warps_long), 0, c->stream));
+        }
+        c->dirty = false;
+        return MRF_OK;
     }
     // K5 length classes: counting sort of the ray ids by class
     CK(c->class_cnt.ensure(2 * kNumClasses, 0, c->stream));
@@ -501,6 +654,7 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
                        c->stream);
         launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_bitems > 0 ? 1 : 0) + 1);
+        mf_dbg(c, "kf sums");
         return MRF_OK;
     }
     CK(cudaMemsetAsync(out, 0, sizeof(long long) * c->VI, c->stream));
@@ -522,6 +676,25 @@ mrf_status ray_messages(mrf_ctx* c) {
     }
     c->mp.qbar = c->kf_avg ? c->qbar.p : nullptr;
     c->mp.qbar_vi = c->VI;
+    if (c->mf) {  // per chunk: re-walk into the scratch, then the chunk's class kernels
+        for (size_t ci = 0; ci < c->mf_chunks.size(); ++ci) {
+            const auto& ch = c->mf_chunks[ci];
+            mrf_status st;
+            if ((st = mf_walk(c, ch, ch.f0, ch.f1, false)) != MRF_OK) return st;
+            ProfScope ps(c, MRF_K_RAY_MSG);
+            for (int k = 0; k < kNumClasses; ++k) {
+                const long long key = (long long)ci * kNumClasses + k;
+                if (c->mf_cls_n[key] == 0) continue;
+                launch_ray_messages(k, c->mf_cls_n[key], c->class_all.p + c->mf_cls_off[key], c->row_ptr.p,
+                                    c->ray_z.p, c->s_vid.p - ch.e0, c->s_lnu.p - ch.e0, c->lam.p, c->T.p, c->mp,
+                                    c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long, c->k5_math,
+                                    c->stream);
+                CK_LAUNCH(MRF_K_RAY_MSG, 1);
+                mf_dbg(c, "k5 class");
+            }
+        }
+        return MRF_OK;
+    }
     ProfScope ps(c, MRF_K_RAY_MSG);
     const bool staged = c->k5_staged;
     if (staged && c->n_stages > 0) {
@@ -794,7 +967,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
-    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->bmask.release(); c->marg.release(); c->eval_cls.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->bmask.release(); c->s_vid.release(); c->s_off.release(); c->s_lnu.release(); c->d_cta_tmp.release(); c->mf_cls_off_d.release(); c->marg.release(); c->eval_cls.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
@@ -849,6 +1022,8 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->depth_used = 0;
     c->E_filled = c->R_filled = 0;
     c->kf_frames_alloc = 0;
+    c->mf_frames.clear();
+    c->mf_chunks.clear();
     if (c->grid.bmask) CK(cudaMemsetAsync(c->bmask.p, 0, (size_t)c->n_brick_slots, c->stream));
     CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
     c->n_invalid = c->n_dropped = c->n_kept = 0;
@@ -1086,7 +1261,9 @@ mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences,
     if (n_incidences) *n_incidences = c->E_real;
     if (n_invalid) *n_invalid = c->n_invalid;
     if (n_dropped) *n_dropped = c->n_dropped;
-    if (n_active_vox) {
+    if (n_active_vox && c->mf) {
+        *n_active_vox = -1;  // matrix-free: vid is not stored
+    } else if (n_active_vox) {
         CK(c->flags.ensure((size_t)c->VI + 1, 0, c->stream));
         CK(c->pos.ensure((size_t)c->VI + 1, 0, c->stream));
         mrf_status sh;
@@ -1105,6 +1282,7 @@ mrf_status mrf_graph_sizes(mrf_ctx* ctx, int64_t* n_rays, int64_t* n_incidences,
 
 mrf_status mrf_export_graph(mrf_ctx* ctx, int64_t* ray_pixel, int64_t* row_ptr, int32_t* vid, int16_t* off_q) {
     ENTER(ctx);
+    if (c->mf) return set_err(c, MRF_ERR_STATE, "matrix-free mode: the ray->voxel lists are not stored");
     HostLayout h;
     mrf_status st;
     if ((st = host_layout(c, h)) != MRF_OK) return st;
@@ -1143,6 +1321,7 @@ mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const 
                            int64_t* row_ptr, int32_t* vid, int16_t* off_q, float* lambda) {
     ENTER(ctx);
     if (n < 0 || (n > 0 && (!frame || !pixel)) || cap < 0) return set_err(c, MRF_ERR_INVALID_ARG, "bad ray selection");
+    if (c->mf) return set_err(c, MRF_ERR_STATE, "matrix-free mode: the ray->voxel lists are not stored");
     {
         mrf_status sf = sync_fill(c);
         if (sf != MRF_OK) return sf;
@@ -1195,6 +1374,7 @@ mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const 
 
 mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr) {
     ENTER(ctx);
+    if (c->mf) return set_err(c, MRF_ERR_STATE, "matrix-free mode: the ray->voxel lists are not stored");
     mrf_status st;
     if ((st = prepare(c)) != MRF_OK) return st;
     if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
@@ -1332,6 +1512,19 @@ mrf_status mrf_export_bricks(mrf_ctx* ctx, uint8_t* out, int64_t* n_allocated) {
     for (uint8_t x : m) na += x != 0;
     if (out) memcpy(out, m.data(), m.size());
     if (n_allocated) *n_allocated = na;
+    return MRF_OK;
+}
+
+mrf_status mrf_set_matrix_free(mrf_ctx* ctx, int32_t frames_per_chunk) {
+    ENTER(ctx);
+    if (frames_per_chunk < 0) return set_err(c, MRF_ERR_INVALID_ARG, "frames_per_chunk must be >= 0");
+    if (!c->frames.empty()) return set_err(c, MRF_ERR_STATE, "the matrix-free mode is set before the first frame");
+    c->mf = frames_per_chunk;
+    if (c->mf) {
+        c->k5_staged = false;  // the class / long-ray kernels read the scratch
+        c->k6_voxel = false;   // the per-voxel transpose needs vid
+    }
+    c->dirty = true;
     return MRF_OK;
 }
 

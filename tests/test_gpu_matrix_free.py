@@ -1,0 +1,83 @@
+"""Matrix-free iteration (the paper re-traces every keyframe each pass,
+P:200): only the messages and the tile runs persist, the rays are walked again per chunk of
+frames.  The walk is the same integer DDA and the reductions are exact integer sums, so the
+results must be BIT-IDENTICAL to the stored-graph path (itself parity-tested against the oracle
+in test_gpu_parity.py) -- in the per-ray, keyframe-average and sparse-brick modes."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2006_03512_b200 as pkg  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(w, n_iter, mf=0, kf=False, bricks=0, frames=None):
+    m = pkg.MRFMap.from_workload(w)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    if mf:
+        m.set_matrix_free(mf)
+    if kf:
+        m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+    if bricks:
+        m.set_sparse_bricks(bricks)
+    for fr in (w.frames if frames is None else frames):
+        m.add_frame(fr.depth, fr.K, fr.T_wc)
+    with m:
+        m.bp_iterate(n_iter)
+        sizes = m.graph_sizes(active=not mf)
+        return m.export_messages(), m.export_beliefs(), m.marginals(), sizes
+
+
+@pytest.mark.parametrize("mf", [1, 2, 3])
+def test_matrix_free_bit_identical(mf):
+    w = synth.tiny_frames(n_frames=4)
+    lam0, T0, m0, s0 = _run(w, 6)
+    lam1, T1, m1, s1 = _run(w, 6, mf=mf)
+    assert np.array_equal(lam0, lam1) and np.array_equal(T0, T1) and np.array_equal(m0, m1)
+    assert s1["E"] == s0["E"] and s1["n_rays"] == s0["n_rays"]
+
+
+def test_matrix_free_frame1_and_modes():
+    w = synth.single_frame()
+    a = _run(w, 3)
+    b = _run(w, 3, mf=1)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    t = synth.tiny_frames(n_frames=4)
+    for kw in (dict(kf=True), dict(bricks=8), dict(kf=True, bricks=8)):
+        x = _run(t, 4, **kw)
+        y = _run(t, 4, mf=2, **kw)
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), kw
+
+
+def test_matrix_free_warm_start_and_rules():
+    """Frames added after iterations (warm start) are walked and counted like the others; the
+    stored-graph exports are refused."""
+    w = synth.tiny_frames(n_frames=4)
+    res = []
+    for mf in (0, 2):
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        if mf:
+            m.set_matrix_free(mf)
+        with m:
+            for fr in w.frames[:3]:
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(3)
+            m.add_frame(w.frames[3].depth, w.frames[3].K, w.frames[3].T_wc)
+            m.bp_iterate(2)
+            res.append((m.export_messages(), m.export_beliefs()))
+            if mf:
+                with pytest.raises(pkg.MrfError) as e:
+                    m.export_graph()
+                assert e.value.status == 6
+                with pytest.raises(pkg.MrfError):
+                    m.export_rays(np.zeros(1, np.int32), np.zeros(1, np.int64))
+                assert m.graph_sizes()["n_active"] == -1
+                with pytest.raises(pkg.MrfError):
+                    m.set_matrix_free(1)  # frames already added
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
