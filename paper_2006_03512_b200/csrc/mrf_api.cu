@@ -94,9 +94,9 @@ struct mrf_ctx {
     std::vector<FrameDesc> mf_frames;
     std::vector<long long> mf_frame_e;  // row_ptr at each frame's first ray (+ the end)
     std::vector<MfChunk> mf_chunks;
-    DBuf<int32_t> s_vid;
-    DBuf<int16_t> s_off;
-    DBuf<float> s_lnu;
+    DBuf<int32_t> s_vid, s_vid2;  // two scratch sets: chunk i + 1 is walked while chunk i's K5 runs
+    DBuf<int16_t> s_off, s_off2;
+    DBuf<float> s_lnu, s_lnu2;
     DBuf<int> d_cta_tmp;
     DBuf<long long> mf_cls_off_d;
     std::vector<long long> mf_cls_n, mf_cls_off;
@@ -253,7 +253,7 @@ struct ProfScope {
     int kind;
     cudaEvent_t a = nullptr, b = nullptr;
     ProfScope(mrf_ctx* c_, int k) : c(c_), kind(k) {
-        if (!c->prof) return;
+        if (!c->prof || k < 0) return;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a, c->stream);
@@ -310,6 +310,12 @@ mrf_status mf_rechunk(mrf_ctx* c) {
     CK(c->s_lnu.ensure((size_t)big + kPadElems, 0, c->stream));
     // the slack after the largest chunk is read (masked) by the last rays' lanes: valid ids
     CK(cudaMemsetAsync(c->s_vid.p, 0, sizeof(int32_t) * c->s_vid.cap, c->stream));
+    if (c->k5_streams >= 2 && c->mf_chunks.size() > 1) {
+        CK(c->s_vid2.ensure((size_t)big + kPadElems, 0, c->stream));
+        CK(c->s_off2.ensure((size_t)big + kPadElems, 0, c->stream));
+        CK(c->s_lnu2.ensure((size_t)big + kPadElems, 0, c->stream));
+        CK(cudaMemsetAsync(c->s_vid2.p, 0, sizeof(int32_t) * c->s_vid2.cap, c->stream));
+    }
     CK(c->d_frames.ensure((size_t)std::max(nf, 1), 0, c->stream));
     if (nf)
         CK(cudaMemcpyAsync(c->d_frames.p, c->mf_frames.data(), sizeof(FrameDesc) * nf, cudaMemcpyHostToDevice,
@@ -320,22 +326,30 @@ mrf_status mf_rechunk(mrf_ctx* c) {
 // Walk frames [f0, f1) of one chunk (the DDA fill + log nu) into the scratch, which stands for
 // the incidence slots [e0, ...) of chunk `ch` (pointers shifted by e0).  count: also count the
 // tile runs and the incidences (first walk of new frames only).
-mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool count) {
+mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool count, cudaStream_t st = nullptr,
+                   int set = 0) {
     if (f0 >= f1) return MRF_OK;
+    const bool own = st == nullptr;  // on the ctx stream (profiled); else a pipeline stream
+    if (own) st = c->stream;
+    int32_t* sv = set ? c->s_vid2.p : c->s_vid.p;
+    int16_t* so = set ? c->s_off2.p : c->s_off.p;
+    float* sl = set ? c->s_lnu2.p : c->s_lnu.p;
     std::vector<int> cta0((size_t)(f1 - f0) + 1, 0);
     for (int k = f0; k < f1; ++k) {
         const long long n_pix = (long long)c->mf_frames[k].rows_owned * c->mf_frames[k].W;
         cta0[k - f0 + 1] = cta0[k - f0] + (int)((n_pix + kFillThreads - 1) / kFillThreads);
     }
-    CK(c->d_cta_tmp.ensure(cta0.size(), 0, c->stream));
-    CK(cudaMemcpyAsync(c->d_cta_tmp.p, cta0.data(), sizeof(int) * cta0.size(), cudaMemcpyHostToDevice, c->stream));
+    // one cta table per scratch set (the pipeline's two walks are in flight on one stream, so
+    // the tables are written in stream order anyway)
+    CK(c->d_cta_tmp.ensure(2 * (size_t)c->mf + 2, 0, c->stream));
+    int* dc = c->d_cta_tmp.p + set * ((size_t)c->mf + 1);
+    CK(cudaMemcpyAsync(dc, cta0.data(), sizeof(int) * cta0.size(), cudaMemcpyHostToDevice, st));
     const long long r0 = c->mf_frames[f0].ray_base;
     const long long r1 = f1 < (int)c->mf_frames.size() ? c->mf_frames[f1].ray_base : c->R;
-    ProfScope ps(c, MRF_K_DDA_FILL);
-    launch_dda_fill(c->d_frames.p + f0, c->d_cta_tmp.p, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
-                    c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->s_vid.p - ch.e0, c->s_off.p - ch.e0,
-                    c->s_lnu.p - ch.e0, count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12),
-                    c->stream);
+    ProfScope ps(c, own ? MRF_K_DDA_FILL : -1);
+    launch_dda_fill(c->d_frames.p + f0, dc, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
+                    c->depth_all.p, c->row_ptr.p, c->ray_z.p, sv - ch.e0, so - ch.e0, sl - ch.e0,
+                    count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), st);
     CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (r1 > r0 ? 1 : 0));
     mf_dbg(c, count ? "walk(count)" : "walk");
     return MRF_OK;
@@ -677,22 +691,43 @@ mrf_status ray_messages(mrf_ctx* c) {
     c->mp.qbar = c->kf_avg ? c->qbar.p : nullptr;
     c->mp.qbar_vi = c->VI;
     if (c->mf) {  // per chunk: re-walk into the scratch, then the chunk's class kernels
-        for (size_t ci = 0; ci < c->mf_chunks.size(); ++ci) {
+        ProfScope ps(c, MRF_K_RAY_MSG);  // walks + K5 of every chunk
+        const size_t nch = c->mf_chunks.size();
+        const bool pipe = c->k5_streams >= 2 && nch > 1;
+        // pipeline: walks on side[0], K5 on side[1]; walk i waits for the K5 of chunk i - 2 (same
+        // scratch set), K5 i waits for walk i; the ctx stream joins on the last K5
+        cudaStream_t A = pipe ? c->side[0] : c->stream, B = pipe ? c->side[1] : c->stream;
+        cudaEvent_t* ev_walk = c->ev_join;      // [2]
+        cudaEvent_t* ev_k5 = c->ev_join + 2;    // [2]
+        if (pipe) {
+            CK(cudaEventRecord(c->ev_fork, c->stream));
+            CK(cudaStreamWaitEvent(A, c->ev_fork, 0));
+            CK(cudaStreamWaitEvent(B, c->ev_fork, 0));
+        }
+        for (size_t ci = 0; ci < nch; ++ci) {
             const auto& ch = c->mf_chunks[ci];
+            const int set = pipe ? (int)(ci & 1) : 0;
             mrf_status st;
-            if ((st = mf_walk(c, ch, ch.f0, ch.f1, false)) != MRF_OK) return st;
-            ProfScope ps(c, MRF_K_RAY_MSG);
+            if (pipe && ci >= 2) CK(cudaStreamWaitEvent(A, ev_k5[set], 0));
+            if ((st = mf_walk(c, ch, ch.f0, ch.f1, false, pipe ? A : nullptr, set)) != MRF_OK) return st;
+            if (pipe) {
+                CK(cudaEventRecord(ev_walk[set], A));
+                CK(cudaStreamWaitEvent(B, ev_walk[set], 0));
+            }
+            const int32_t* sv = set ? c->s_vid2.p : c->s_vid.p;
+            const float* sl = set ? c->s_lnu2.p : c->s_lnu.p;
             for (int k = 0; k < kNumClasses; ++k) {
                 const long long key = (long long)ci * kNumClasses + k;
                 if (c->mf_cls_n[key] == 0) continue;
                 launch_ray_messages(k, c->mf_cls_n[key], c->class_all.p + c->mf_cls_off[key], c->row_ptr.p,
-                                    c->ray_z.p, c->s_vid.p - ch.e0, c->s_lnu.p - ch.e0, c->lam.p, c->T.p, c->mp,
-                                    c->long_scratch.p, c->long_scratch_per_warp, c->n_warps_long, c->k5_math,
-                                    c->stream);
+                                    c->ray_z.p, sv - ch.e0, sl - ch.e0, c->lam.p, c->T.p, c->mp, c->long_scratch.p,
+                                    c->long_scratch_per_warp, c->n_warps_long, c->k5_math, B);
                 CK_LAUNCH(MRF_K_RAY_MSG, 1);
                 mf_dbg(c, "k5 class");
             }
+            if (pipe) CK(cudaEventRecord(ev_k5[set], B));
         }
+        if (pipe) CK(cudaStreamWaitEvent(c->stream, ev_k5[(nch - 1) & 1], 0));
         return MRF_OK;
     }
     ProfScope ps(c, MRF_K_RAY_MSG);
@@ -967,7 +1002,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
     c->col_ptr.release(); c->item_ptr.release(); c->pos.release(); c->items.release();
-    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->bmask.release(); c->s_vid.release(); c->s_off.release(); c->s_lnu.release(); c->d_cta_tmp.release(); c->mf_cls_off_d.release(); c->marg.release(); c->eval_cls.release();
+    c->T.release(); c->T_part.release(); c->lutp.release(); c->depth_stage.release(); c->depth_all.release(); c->d_frames.release(); c->d_cta0.release(); c->qbar.release(); c->kf_sums.release(); c->bmask.release(); c->s_vid.release(); c->s_off.release(); c->s_lnu.release(); c->s_vid2.release(); c->s_off2.release(); c->s_lnu2.release(); c->d_cta_tmp.release(); c->mf_cls_off_d.release(); c->marg.release(); c->eval_cls.release();
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
