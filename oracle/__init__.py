@@ -11,7 +11,10 @@ Every function cites the SURVEY §8(c) step (B1..B7) / PAPER.md lines it follows
 the pins that tie it to the paper are in tests/test_oracle_*.py.  Parity status:
   B1 ray setup, B2 DDA, B3 offsets/LUT, B5 single-ray messages, B5+B6 on tree
   graphs, §III.D evaluation metric (vis_profile / eval_pixel), NEXT #3 keyframe averages
-  (kf_*: SPEC's worked examples, and equal to B5 when each keyframe has one ray per voxel): pinned.  B5+B6 on loopy graphs (several overlapping rays): parity
+  (kf_*: SPEC's worked examples, and equal to B5 when each keyframe has one ray per voxel),
+  NEXT #4 sparse bricks (alloc_bricks / dda_sparse: SPEC's allocation examples and coverage
+  post-condition, the filtered brute-force-pinned dense walk, skipped = certainly-empty): pinned.
+  NEXT #1 (matrix-free) needs no oracle of its own: it must equal the stored graph bit for bit.  B5+B6 on loopy graphs (several overlapping rays): parity
   unpinned beyond the invariants (loopy BP has no closed form).
 """
 
