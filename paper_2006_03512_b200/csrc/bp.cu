@@ -22,15 +22,16 @@
 // log nu_i is interpolated from the LUT once per frame by the DDA fill (graph.cu, lut_log_nu)
 // and read as one fp32 per incidence.
 //
-// Chunking: a chunk is 8 consecutive incidences of ONE ray, counted from the ray's start (ray
-// segments start at multiples of 8 slots), and the chunk scans are Hillis-Steele on the
-// ray-relative chunk index -- so every rounding depends only on the ray, never on where (or on
-// which rank) it is stored: beliefs are bit-identical for any rank count.  Masked elements are
-// identity maps.  Two layouts of the same arithmetic:
-//   * staged (default): stages of consecutive short rays are bulk-copied (TMA) into shared
-//     memory; thread = chunk; scans in shared memory (ray_msg_staged_kernel);
-//   * classes (MRF_K5=class): G lanes per ray by length class, scans by warp shuffles
-//     (ray_msg_kernel).
+// Chunking: a lane (or, in the staged layout, a thread) owns a chunk of consecutive incidences of
+// ONE ray, counted from the ray's start (ray segments start at multiples of 8 slots), and the
+// chunk scans are Hillis-Steele on the ray-relative chunk index -- so every rounding depends only
+// on the ray (and its length class), never on where (or on which rank) it is stored: beliefs are
+// bit-identical for any rank count.  Masked elements are identity maps.  Two layouts of the same
+// arithmetic:
+//   * classes (default): G lanes per ray by length class, K incidences per lane, scans by warp
+//     shuffles (ray_msg_kernel); the class kernels run concurrently on side streams;
+//   * staged (MRF_K5=staged, an ablation): stages of consecutive short rays bulk-copied (TMA)
+//     into shared memory, thread = 8-slot chunk, scans in shared memory (ray_msg_staged_kernel).
 // Rays longer than kShortMax run the tiled warp kernel (ray_msg_long_kernel) in both.
 #include <algorithm>
 
