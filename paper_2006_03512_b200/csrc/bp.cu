@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                                                                    const long long* __restrict__ tile_ptr,
                                                                    const Run* __restrict__ runs,
                                                                    const int32_t* __restrict__ lam, int per_item,
-                                                                   void* out, long long n_out) {
+                                                                   void* out, long long n_out, unsigned* next) {
     extern __shared__ int smem[];
     double* accd = reinterpret_cast<double*>(smem);        // MODE 1: D per slot (128 KB)
     int* accn = smem + 2 * kTileSlots;                     // MODE 1: packed counts (64 KB)
@@ -730,7 +730,11 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
     uint4* sdesc = reinterpret_cast<uint4*>(smem + kAccInts) + (threadIdx.x >> 5) * 32;  // this warp's batch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (long long it = blockIdx.x; it < n_items; it += gridDim.x) {
+    // items: the first per CTA by index, then dynamically (a CTA whose items ran short takes the
+    // next one instead of a fixed stride, so the uneven last chunks of the tiles do not leave SMs
+    // idle at the end); next == nullptr: fixed stride
+    __shared__ long long s_next;
+    for (long long it = blockIdx.x; it < n_items;) {
         const int2 item = __ldg(items + it);
         for (int i = threadIdx.x; i < kAccInts / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
         __syncthreads();
@@ -806,6 +810,13 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                     atomicAdd(Nt + i, (unsigned long long)(cn & 0xffffu) | ((unsigned long long)(cn >> 16) << 32));
                 }
             }
+        }
+        if (next) {
+            if (threadIdx.x == 0) s_next = (long long)gridDim.x + atomicAdd(next, 1u);
+            __syncthreads();
+            it = s_next;
+        } else {
+            it += gridDim.x;
         }
         __syncthreads();
     }
@@ -913,7 +924,7 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
 }
 
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, int per_item, long long* T, cudaStream_t s) {
+                        const int32_t* lam, int per_item, long long* T, unsigned* next, cudaStream_t s) {
     if (n_items == 0) return;
     static bool configured = false;
     if (!configured) {
@@ -921,12 +932,13 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
         configured = true;
     }
     const long long grid = n_items < 148LL ? n_items : 148LL;
+    if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
     tile_reduce_kernel<0><<<(unsigned)grid, kK6Threads, kK6Smem, s>>>(n_items, items, tile_ptr, runs, lam, per_item, T,
-                                                                       0);
+                                                                       0, next);
 }
 
 void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
-                    const int32_t* lam, int per_item, double* D, long long n_slots, cudaStream_t s) {
+                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, cudaStream_t s) {
     if (n_items == 0) return;
     static bool configured = false;
     if (!configured) {
@@ -934,8 +946,9 @@ void launch_kf_sums(long long n_items, const int2* items, const long long* bucke
         configured = true;
     }
     const long long grid = n_items < 148LL ? n_items : 148LL;
+    if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
     tile_reduce_kernel<1><<<(unsigned)grid, kK6Threads, kK6SmemKf, s>>>(n_items, items, bucket_ptr, runs, lam, per_item,
-                                                                         D, n_slots);
+                                                                         D, n_slots, next);
 }
 
 // Keyframe averages -> quantised log-odds per (frame, slot) and their sum per slot (thread per

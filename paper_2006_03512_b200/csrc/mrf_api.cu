@@ -82,6 +82,7 @@ struct mrf_ctx {
     bool k6_voxel = false;  // ablation: per-voxel transpose K6 instead of the tile-run K6 (MRF_K6=voxel)
     int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1)
     int k6_item = 8192;
+    bool k6_dynamic = true;  // MRF_K6_DYNAMIC=0: fixed-stride item order
     // keyframe-average mode (NEXT #3, reading R22): one message per (frame, voxel)
     bool kf_avg = false;
     // matrix-free mode (NEXT #1): only lambda and the tile runs persist; vid / off_q / log nu are
@@ -665,7 +666,7 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
         const long long F = (long long)c->frames.size(), n = F * c->VI;
         CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(double) * (size_t)n, c->stream));
         launch_kf_sums(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
-                       c->stream);
+                       c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr, c->stream);
         launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_bitems > 0 ? 1 : 0) + 1);
         mf_dbg(c, "kf sums");
@@ -676,7 +677,8 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
     } else {
-        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out, c->stream);
+        launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
+                           c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -899,6 +901,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* k6 = getenv("MRF_K6")) c->k6_voxel = strcmp(k6, "voxel") == 0;
     if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
     if (const char* ki = getenv("MRF_K6_ITEM")) c->k6_item = std::min(std::max(atoi(ki), 1024), kRunsPerItem);
+    if (const char* kd = getenv("MRF_K6_DYNAMIC")) c->k6_dynamic = atoi(kd) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
