@@ -83,6 +83,7 @@ struct mrf_ctx {
     int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1)
     int k6_item = 8192;       // runs per K6 work item (set per graph unless MRF_K6_ITEM fixes it)
     bool k6_item_fixed = false;
+    bool k6_lpt = true;  // MRF_K6_LPT=0: j-major item order only
     bool k6_dynamic = true;  // MRF_K6_DYNAMIC=0: fixed-stride item order
     // keyframe-average mode (NEXT #3, reading R22): one message per (frame, voxel)
     bool kf_avg = false;
@@ -536,6 +537,10 @@ mrf_status build_tile_runs(mrf_ctx* c) {
         }
         if (!any) break;
     }
+    if (c->k6_lpt) {  // largest items first (the dynamic schedule then ends on the small ones)
+        auto size = [&](const int2& it) { return std::min<long long>(c->k6_item, nr[it.x] - (long long)it.y * c->k6_item); };
+        std::stable_sort(items.begin(), items.end(), [&](const int2& a, const int2& b) { return size(a) > size(b); });
+    }
     c->n_bitems = (long long)items.size();
     CK(c->bitems.ensure((size_t)std::max(1LL, c->n_bitems), 0, c->stream));
     if (c->n_bitems)
@@ -911,6 +916,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         c->k6_item_fixed = true;
     }
     if (const char* kd = getenv("MRF_K6_DYNAMIC")) c->k6_dynamic = atoi(kd) != 0;
+    if (const char* kl = getenv("MRF_K6_LPT")) c->k6_lpt = atoi(kl) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
