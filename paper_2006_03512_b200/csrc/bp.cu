@@ -690,6 +690,9 @@ constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
 // steps (slot strides 32, 1024) change the bank (a bijection inside every 32-slot row); off by
 // default: K6 is ALU-bound and the 4 extra ALU ops cost more than the bank conflicts they
 // avoid (2.85 vs 2.74 ms per iteration at frames30).
+#ifndef MRF_K6_WARP_DYN
+#define MRF_K6_WARP_DYN 1
+#endif
 #ifndef MRF_K6_SWIZZLE
 #define MRF_K6_SWIZZLE 0
 #endif
@@ -734,14 +737,26 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     // next one instead of a fixed stride, so the uneven last chunks of the tiles do not leave SMs
     // idle at the end); next == nullptr: fixed stride
     __shared__ long long s_next;
+    __shared__ int s_batch;
     for (long long it = blockIdx.x; it < n_items;) {
         const int2 item = __ldg(items + it);
         for (int i = threadIdx.x; i < kAccInts / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
+#if MRF_K6_WARP_DYN
+        if (threadIdx.x == 0) s_batch = kK6Warps;
+#endif
         __syncthreads();
         const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * per_item;
         long long r1 = __ldg(tile_ptr + item.x + 1);
         if (r1 > r0 + per_item) r1 = r0 + per_item;
+#if MRF_K6_WARP_DYN
+        // batches of 32 runs: the first one per warp by index, then from a shared counter (the
+        // item ends at a barrier, so the warps should finish together)
+        for (long long bi = wid;;) {
+            const long long rb = r0 + 32LL * bi;
+            if (rb >= r1) break;
+#else
         for (long long rb = r0 + 32LL * wid; rb < r1; rb += 32LL * kK6Warps) {
+#endif
             const int nb = (int)min(32LL, r1 - rb);
             uint4 d{0u, 0u, 0u, 0u};
             if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
@@ -791,6 +806,11 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                 }
             }
             __syncwarp();
+#if MRF_K6_WARP_DYN
+            int nxt = 0;
+            if (lane == 0) nxt = atomicAdd(&s_batch, 1);
+            bi = __shfl_sync(kFull, nxt, 0);
+#endif
         }
         __syncthreads();
         if constexpr (MODE == 0) {
