@@ -164,6 +164,9 @@ void launch_vox_hist(long long n_rays, const long long* row_ptr, const RayInfo* 
 // K2: out[i] = offset + sum_{j<i} in[j] for i in [0, n]; out has n+1 entries.
 void launch_exclusive_scan(const int32_t* in, long long* out, long long n, long long offset,
                            long long* scratch, cudaStream_t s);
+// the same with the base read from device memory at *doff (may alias out[0]); n > 0
+void launch_exclusive_scan_dev(const int32_t* in, long long* out, long long n, const long long* doff,
+                               long long* scratch, cudaStream_t s);
 long long scan_scratch_elems(long long n);
 // K4: tr[col_ptr[v] + slot] = e for every incidence e (cursor zeroed by caller)
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,

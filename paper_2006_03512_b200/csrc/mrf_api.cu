@@ -132,6 +132,13 @@ struct mrf_ctx {
     long long R = 0, E = 0;  // rays (owned pixels) and incidence slots (ray segments padded to 4)
     long long E_real = 0;    // incidences (counted by the fills on the device; see sync_fill)
     bool fill_pending = false;
+    // frames added without a host round trip: their exact E (row_ptr[R]) and invalid / dropped
+    // counts (counters[2..3], accumulating) are read when something needs them (resolve_E);
+    // E_bound bounds what they added, so that the 2^31 capacity check needs no round trip while
+    // E + E_bound stays below it
+    bool E_unresolved = false;
+    long long E_bound = 0;
+    long long ray_slots_max = 0;  // pad8(1 + sum_k (dims_k + ceil(M / res))), M the largest margin
     long long n_invalid = 0, n_dropped = 0, n_kept = 0;
     DBuf<int32_t> n_r;
     DBuf<int8_t> status;
@@ -283,6 +290,22 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
     return MRF_OK;
 }
 
+// Exact E and invalid / dropped counts of the frames added since the last round trip.
+mrf_status resolve_E(mrf_ctx* c) {
+    if (!c->E_unresolved) return MRF_OK;
+    CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->E = c->pinned[0];
+    c->n_invalid += c->pinned[1];
+    c->n_dropped += c->pinned[2];
+    c->n_kept = c->R - c->n_invalid - c->n_dropped;
+    CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+    c->E_unresolved = false;
+    c->E_bound = 0;
+    return MRF_OK;
+}
+
 // ---- matrix-free mode (NEXT #1)
 static void mf_dbg(mrf_ctx* c, const char* what) {
     static const bool on = getenv("MRF_SYNC_DEBUG") != nullptr;
@@ -361,6 +384,10 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
 // The DDA fills count their incidences (and any bound overflow, which K1's bound excludes) on
 // the device, counters[10..11]; read them once when something needs E_real.
 mrf_status sync_fill(mrf_ctx* c) {
+    {
+        mrf_status sr = resolve_E(c);
+        if (sr != MRF_OK) return sr;
+    }
     if (!c->fill_pending) return MRF_OK;
     if (!c->pend.empty() && c->grid.bmask) {
         // Sparse bricks: every frame is allocated by now (the graph is walked once, R23), so the
@@ -385,6 +412,7 @@ mrf_status sync_fill(mrf_ctx* c) {
                 return set_err(c, MRF_ERR_CAPACITY,
                                "sparse bricks: the final allocation gives more than 2^31 incidence slots");
         }
+        CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));  // recounted frames
         c->E = E;
     }
     if (!c->pend.empty() && c->mf) {
@@ -863,6 +891,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         g_create_error = m;
         return MRF_ERR_INVALID_ARG;
     };
+    long long margin_cells = 0;  // ceil(largest traversal margin / res) + 1
     if (!out) return reject("out is NULL");
     *out = nullptr;
     if (!dims || !origin_m || !noise) return reject("NULL argument");
@@ -890,6 +919,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
                            std::fabs(noise->sigma_c[2]) * D * D;
         if (noise->margin_min > D || noise->margin_k * sig > D)
             return reject("traversal margin must stay below the grid diagonal (margin bound)");
+        margin_cells = (long long)std::ceil(std::max(noise->margin_min, noise->margin_k * sig) / resolution_m) + 1;
     }
     const long long nlut = (long long)noise->n_z * noise->n_off;
     for (long long i = 0; i < nlut; ++i)
@@ -909,6 +939,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
                resolution_m, origin_m[0], origin_m[1], origin_m[2]};
     c->NT = (long long)c->grid.ntx * c->grid.nty * c->grid.ntz;
     c->VI = c->NT * kTileSlots;
+    c->ray_slots_max = (1 + (long long)dims[0] + dims[1] + dims[2] + 3 * margin_cells + 7) & ~7LL;
     if (const char* k6 = getenv("MRF_K6")) c->k6_voxel = strcmp(k6, "voxel") == 0;
     if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
     if (const char* ki = getenv("MRF_K6_ITEM")) {
@@ -1071,6 +1102,9 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     ENTER(ctx);
     c->R = c->E = c->E_real = 0;
     c->fill_pending = false;
+    c->E_unresolved = false;
+    c->E_bound = 0;
+    CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
     c->pend.clear();
     c->depth_used = 0;
     c->E_filled = c->R_filled = 0;
@@ -1150,21 +1184,41 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
         CK(c->tile_runs.ensure((F + 1) * (size_t)c->NT, F * (size_t)c->NT, c->stream));
         CK(cudaMemsetAsync(c->tile_runs.p + F * c->NT, 0, sizeof(int32_t) * (size_t)c->NT, c->stream));
     }
+    // Capacity without a round trip while E + the bound of every unresolved frame stays below
+    // 2^31: K1 lays a ray out with pad8(1 + sum_k |c_end,k - c_0,k|) slots, the segment end lies
+    // within the traversal margin M of the measured point (inside the grid), so a frame adds at
+    // most Rf ray_slots_max slots (0 for a sparse-brick frame: counted at first use).
+    const long long U = c->grid.bmask ? 0 : Rf * c->ray_slots_max;
+    const bool fast = c->E + c->E_bound + U < (1LL << 31) - kPadElems;
     mrf_status st;
-    CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+    if (!fast && (st = resolve_E(c)) != MRF_OK) return st;
     {
         ProfScope ps(c, MRF_K_RAYGEN_COUNT);
         launch_raygen_count(f, c->grid, c->noise, d_depth, c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2,
                             c->stream);
         CK_LAUNCH(MRF_K_RAYGEN_COUNT, Rf > 0 ? 1 : 0);
     }
-    if ((st = scan(c, c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->E)) != MRF_OK) return st;
-    CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R + Rf, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    const long long E_new = c->pinned[0], inv = c->pinned[1], drp = c->pinned[2];
-    if (E_new >= (1LL << 31) - kPadElems)
-        return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
+    long long E_new = 0, inv = 0, drp = 0;
+    if (fast) {  // row_ptr[R] holds the running E on the device
+        if (Rf > 0) {
+            CK(c->scan_scratch.ensure((size_t)scan_scratch_elems(Rf), 0, c->stream));
+            ProfScope ps(c, MRF_K_SCAN);
+            launch_exclusive_scan_dev(c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->row_ptr.p + c->R,
+                                      c->scan_scratch.p, c->stream);
+            CK_LAUNCH(MRF_K_SCAN, 3);
+        }
+    } else {  // counters[2..3] hold this frame only (resolve_E cleared them)
+        if ((st = scan(c, c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->E)) != MRF_OK) return st;
+        CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R + Rf, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        E_new = c->pinned[0];
+        inv = c->pinned[1];
+        drp = c->pinned[2];
+        CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
+        if (E_new >= (1LL << 31) - kPadElems)
+            return set_err(c, MRF_ERR_CAPACITY, "incidence count would exceed 2^31 (int32 transpose indices)");
+    }
     if (c->grid.bmask) {  // sparse bricks: allocate around this frame's reprojected points
         launch_brick_alloc(f, c->grid, c->noise, d_depth, c->bmask.p, c->stream);
         CK_LAUNCH(MRF_K_RAYGEN_COUNT, 1);
@@ -1175,11 +1229,16 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
     c->frames.push_back({width, height, rows_owned, c->R, Rf});
     c->R += Rf;
-    c->E = E_new;
+    if (fast) {
+        c->E_unresolved = true;
+        c->E_bound += U;
+    } else {
+        c->E = E_new;
+        c->n_invalid += inv;
+        c->n_dropped += drp;
+        c->n_kept += Rf - inv - drp;
+    }
     c->fill_pending = true;
-    c->n_invalid += inv;
-    c->n_dropped += drp;
-    c->n_kept += Rf - inv - drp;
     c->dirty = true;
     c->hist_valid = false;
     return MRF_OK;

@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(1024) scan_sums_kernel(long long* sums, long l
 
 __global__ void __launch_bounds__(kThreads) tile_scan_kernel(const int32_t* __restrict__ in, long long n,
                                                              const long long* __restrict__ sums, long long offset,
-                                                             long long* out) {
+                                                             const long long* doff, long long* out) {
+    if (doff) offset += *doff;  // device-resident base (it may be out[0] itself: rewritten unchanged)
     __shared__ long long sw[kThreads / 32];
     const long long base = (long long)blockIdx.x * kTile + (long long)threadIdx.x * kPerThread;
     int v[kPerThread];
@@ -110,7 +111,16 @@ void launch_exclusive_scan(const int32_t* in, long long* out, long long n, long 
     const long long nb = (n + kTile - 1) / kTile;
     tile_sums_kernel<<<(unsigned)nb, kThreads, 0, s>>>(in, n, scratch);
     scan_sums_kernel<<<1, 1024, 0, s>>>(scratch, nb);
-    tile_scan_kernel<<<(unsigned)nb, kThreads, 0, s>>>(in, n, scratch, offset, out);
+    tile_scan_kernel<<<(unsigned)nb, kThreads, 0, s>>>(in, n, scratch, offset, nullptr, out);
+}
+
+void launch_exclusive_scan_dev(const int32_t* in, long long* out, long long n, const long long* doff,
+                               long long* scratch, cudaStream_t s) {
+    if (n <= 0) return;  // out[0] is *doff already (or must be written by the caller)
+    const long long nb = (n + kTile - 1) / kTile;
+    tile_sums_kernel<<<(unsigned)nb, kThreads, 0, s>>>(in, n, scratch);
+    scan_sums_kernel<<<1, 1024, 0, s>>>(scratch, nb);
+    tile_scan_kernel<<<(unsigned)nb, kThreads, 0, s>>>(in, n, scratch, 0, doff, out);
 }
 
 }  // namespace mrf
