@@ -476,3 +476,27 @@ def test_evaluate_matches_oracle(name, n_iter, tiny, frame1):
     rclsv, rnvv, rnav = oracle.eval_frame(p, fr, xmap, mode=1)
     assert np.array_equal(cls_v, rclsv) and (nv_v, na_v) == (rnvv, rnav)
     assert nv == int(np.sum(fr.depth > 0)) and 0 < na <= nv
+
+
+def test_capacity_limit_and_lazy_counts(frame1):
+    """Frames are accepted without a host round trip while a bound proves the 2^31 incidence
+    slots suffice; the frame that would overflow returns MRF_ERR_CAPACITY and leaves the state
+    unchanged; the lazily read sizes equal the per-frame ones times the frames accepted."""
+    w = frame1
+    fr = w.frames[0]
+    with _gpu_map(w) as one:
+        s1 = one.graph_sizes(active=False)
+        slots1 = one.layout_sizes()["n_slots"]
+    m = pkg.MRFMap.from_workload(w)
+    with m:
+        d = torch.from_numpy(fr.depth).cuda()
+        n = 0
+        with pytest.raises(pkg.MrfError) as e:
+            for _ in range(200):
+                m.add_frame(d, fr.K, fr.T_wc)
+                n += 1
+        assert e.value.status == 3  # MRF_ERR_CAPACITY
+        assert (n + 1) * slots1 >= 2 ** 31 - 64 > n * slots1  # exactly the first frame that overflows
+        s = m.graph_sizes(active=False)
+        assert s["n_rays"] == n * s1["n_rays"] and s["E"] == n * s1["E"]
+        assert s["n_invalid"] == n * s1["n_invalid"] and s["n_dropped"] == n * s1["n_dropped"]
