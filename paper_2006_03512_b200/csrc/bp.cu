@@ -738,9 +738,10 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     // idle at the end); next == nullptr: fixed stride
     __shared__ long long s_next;
     __shared__ int s_batch;
+    // the accumulator is zeroed once here, then by each item's flush as it reads it
+    for (int i = threadIdx.x; i < kAccInts / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
     for (long long it = blockIdx.x; it < n_items;) {
         const int2 item = __ldg(items + it);
-        for (int i = threadIdx.x; i < kAccInts / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
 #if MRF_K6_WARP_DYN
         if (threadIdx.x == 0) s_batch = kK6Warps;
 #endif
@@ -817,6 +818,8 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             long long* Tt = static_cast<long long*>(out) + ((long long)item.x << kTileShift);
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
                 const long long sum = (long long)acc_hi[swz(i)] * 65536 + (long long)acc_lo[swz(i)];
+                acc_hi[swz(i)] = 0;
+                acc_lo[swz(i)] = 0;
                 if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
             }
         } else {  // out: D (fp64) then the packed counts (int64: n_pos + 2^32 n_neg), each [bucket][slot]
@@ -825,20 +828,23 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             unsigned long long* Nt = reinterpret_cast<unsigned long long*>(static_cast<double*>(out) + n_out) + o;
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
                 const unsigned cn = (unsigned)accn[swz(i)];
+                const double dv = accd[swz(i)];
+                accn[swz(i)] = 0;
+                accd[swz(i)] = 0.0;
                 if (cn) {
-                    atomicAdd(Dt + i, accd[swz(i)]);
+                    atomicAdd(Dt + i, dv);
                     atomicAdd(Nt + i, (unsigned long long)(cn & 0xffffu) | ((unsigned long long)(cn >> 16) << 32));
                 }
             }
         }
-        if (next) {
+        if (next) {  // (this barrier also ends the flush before the next item's adds)
             if (threadIdx.x == 0) s_next = (long long)gridDim.x + atomicAdd(next, 1u);
             __syncthreads();
             it = s_next;
         } else {
             it += gridDim.x;
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
 
