@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(256) voxel_reduce_kernel(long long n_items, co
 // most voxels: processing several runs per instruction serialised on same-address atomics).
 // The in-tile slot comes from the run's step masks (no vid read): for incidence k,
 // slot0 + sx cx + 32 sy cy + 1024 sz (k - cx - cy), cx = popc(mx & (2^k - 1)) (accumulator
-// index swz(s), see below).  The slots then go to T with one int64 atomic each (a tile spans several items).  Integer sums:
+// index L::index(s): the padded layout of AccLayout, see below).  The slots then go to T with one int64 atomic each (a tile spans several items).  Integer sums:
 // exact, independent of order.
 constexpr int kK6Threads = 1024;
 constexpr int kK6Warps = kK6Threads / 32;
@@ -684,7 +684,7 @@ constexpr int kK6Warps = kK6Threads / 32;
 #define MRF_K6_W 16
 #endif
 constexpr int kK6W = MRF_K6_W;  // lanes per run in the add loop
-constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
+constexpr int kK6Desc = kK6Warps * 32 * 16;  // per warp: the batch's 32 run descriptors
 
 // slot -> accumulator index.  MRF_K6_SWIZZLE=1 XORs the low 5 bits with y ^ z so that y and z
 // steps (slot strides 32, 1024) change the bank (a bijection inside every 32-slot row); off by
@@ -697,6 +697,26 @@ constexpr int kK6Smem = 2 * kTileSlots * (int)sizeof(int) + kK6Warps * 32 * 16;
 #define MRF_K6_SWIZZLE 0
 #endif
 __device__ __forceinline__ int swz(int s) { return MRF_K6_SWIZZLE ? s ^ (((s >> 5) ^ (s >> 10)) & 31) : s; }
+// Accumulator layout of a tile's slots.  Plain (PAD = false): index = slot = x + 32 y + 1024 z, so
+// y and z steps stay in one shared-memory bank.  Padded: index = x + 35 y + 1127 z -- the bank
+// moves by 1, 3 and 7 for x, y and z steps (odd: a straight run never repeats a bank within 32
+// steps), at no ALU cost since the strides only change constants; 18024 entries instead of 16384.
+#ifndef MRF_K6_SY
+#define MRF_K6_SY 35
+#endif
+#ifndef MRF_K6_SZ
+#define MRF_K6_SZ 1127
+#endif
+template <bool PAD>
+struct AccLayout {
+    static constexpr int SY = PAD ? MRF_K6_SY : 32, SZ = PAD ? MRF_K6_SZ : 1024;
+    static constexpr int kSlots = PAD ? (31 + 31 * SY + 15 * SZ + 4) & ~3 : kTileSlots;  // multiple of 4
+    static_assert(!PAD || (SY >= 32 && SZ >= 32 + 31 * SY && (SY & 1) && (SZ & 1)), "injective, odd bank steps");
+    static constexpr int NS = PAD ? 15 : 14;                  // staged meta: index bits, then n - 1, signs
+    __device__ __forceinline__ static int index(int s) {
+        return PAD ? (s & 31) + SY * ((s >> 5) & 31) + SZ * (s >> 10) : swz(s);
+    }
+};
 
 // MODE 0: the beliefs, sum of q (int32 halves, exact).  MODE 1 (keyframe averages, reading R22):
 // per slot the counts of non-negative / negative messages (packed n_pos + 65536 n_neg, native
@@ -717,20 +737,22 @@ __device__ __forceinline__ double kf_small(int q) {
     const double s = y * (double)__frcp_rn(1.f + (float)y);  // relative ~2^-22
     return q >= 0 ? s : -s;
 }
-constexpr int kK6SmemKf = kTileSlots * (int)(sizeof(double) + sizeof(int)) + kK6Warps * 32 * 16;
+constexpr int kK6SmemKf = kTileSlots * (int)(sizeof(double) + sizeof(int));
 
-template <int MODE>
+template <int MODE, bool PAD>
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
                                                                    const long long* __restrict__ tile_ptr,
                                                                    const Run* __restrict__ runs,
                                                                    const int32_t* __restrict__ lam, int per_item,
                                                                    void* out, long long n_out, unsigned* next) {
     extern __shared__ int smem[];
+    using L = AccLayout<PAD>;
+    static_assert(MODE == 0 || !PAD, "keyframe-average sums use the plain layout (shared memory)");
     double* accd = reinterpret_cast<double*>(smem);        // MODE 1: D per slot (128 KB)
-    int* accn = smem + 2 * kTileSlots;                     // MODE 1: packed counts (64 KB)
-    constexpr int kAccInts = MODE == 0 ? 2 * kTileSlots : 3 * kTileSlots;
-    int* acc_lo = smem;                 // sum of (q & 0xffff), at swz(slot)
-    int* acc_hi = smem + kTileSlots;    // sum of (q >> 16)
+    int* accn = smem + 2 * L::kSlots;                      // MODE 1: packed counts (64 KB)
+    constexpr int kAccInts = MODE == 0 ? 2 * L::kSlots : 3 * L::kSlots;
+    int* acc_lo = smem;                 // sum of (q & 0xffff), at L::index(slot)
+    int* acc_hi = smem + L::kSlots;     // sum of (q >> 16)
     uint4* sdesc = reinterpret_cast<uint4*>(smem + kAccInts) + (threadIdx.x >> 5) * 32;  // this warp's batch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // items: the first per CTA by index, then dynamically (a CTA whose items ran short takes the
@@ -761,6 +783,8 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             const int nb = (int)min(32LL, r1 - rb);
             uint4 d{0u, 0u, 0u, 0u};
             if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
+            if constexpr (PAD)  // in-tile slot -> accumulator index, once per run
+                d.y = (unsigned)L::index((int)(d.y & (kTileSlots - 1))) | ((d.y >> 14) << L::NS);
             sdesc[lane] = d;
             __syncwarp();
             // Lane groups of kK6W lanes (32 / kK6W runs per instruction): in round r, group g takes
@@ -773,7 +797,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 const uint4 x = sdesc[j + NJ * hw];
-                const int n = j + NJ * hw < nb ? (int)((x.y >> 14) & 63u) + 1 : 0;
+                const int n = j + NJ * hw < nb ? (int)((x.y >> L::NS) & 63u) + 1 : 0;
 #pragma unroll
                 for (int rnd = 0; rnd < NR; ++rnd) {
                     const int k = hl + kK6W * rnd;
@@ -788,13 +812,14 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                 for (int j = 0; j < NJ; ++j) {
                     const uint4 x = sdesc[j + NJ * hw];
                     const unsigned meta = x.y;
-                    const int n = j + NJ * hw < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
+                    const int n = j + NJ * hw < nb ? (int)((meta >> L::NS) & 63u) + 1 : 0;
                     if (rnd > 0 && !__any_sync(kFull, k < n)) continue;  // every run of the column ended
                     if (k < n) {
                         const int cx = __popc(x.z & below_k), cy = __popc(x.w & below_k);
-                        const int sx = (meta >> 20) & 1 ? -cx : cx, sy = (meta >> 21) & 1 ? -cy : cy;
-                        const int cz = k - cx - cy, sz = (meta >> 22) & 1 ? -cz : cz;
-                        const int si = swz((int)(meta & (kTileSlots - 1)) + sx + 32 * sy + 1024 * sz);
+                        const int sx = (meta >> (L::NS + 6)) & 1 ? -cx : cx, sy = (meta >> (L::NS + 7)) & 1 ? -cy : cy;
+                        const int cz = k - cx - cy, sz = (meta >> (L::NS + 8)) & 1 ? -cz : cz;
+                        const int s0 = (int)(meta & ((1u << L::NS) - 1u)) + sx + L::SY * sy + L::SZ * sz;
+                        const int si = PAD ? s0 : swz(s0);
                         const int qv = q[rnd][j];
                         if constexpr (MODE == 0) {
                             atomicAdd(acc_lo + si, qv & 0xffff);
@@ -817,9 +842,10 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
         if constexpr (MODE == 0) {
             long long* Tt = static_cast<long long*>(out) + ((long long)item.x << kTileShift);
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
-                const long long sum = (long long)acc_hi[swz(i)] * 65536 + (long long)acc_lo[swz(i)];
-                acc_hi[swz(i)] = 0;
-                acc_lo[swz(i)] = 0;
+                const int a = L::index(i);
+                const long long sum = (long long)acc_hi[a] * 65536 + (long long)acc_lo[a];
+                acc_hi[a] = 0;
+                acc_lo[a] = 0;
                 if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
             }
         } else {  // out: D (fp64) then the packed counts (int64: n_pos + 2^32 n_neg), each [bucket][slot]
@@ -949,32 +975,34 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
     voxel_reduce_kernel<<<blocks_for(warps * 32, 256), 256, 0, s>>>(n_items, items, col_ptr, tr, lam, T);
 }
 
-void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, int per_item, long long* T, unsigned* next, cudaStream_t s) {
-    if (n_items == 0) return;
+template <int MODE, bool PAD>
+void launch_tile_reduce_t(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
+                          const int32_t* lam, int per_item, void* out, long long n_out, unsigned* next, cudaStream_t s) {
+    constexpr int smem = (MODE == 0 ? 2 * AccLayout<PAD>::kSlots * (int)sizeof(int) : kK6SmemKf) + kK6Desc;
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(tile_reduce_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6Smem);
+        cudaFuncSetAttribute(tile_reduce_kernel<MODE, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         configured = true;
     }
     const long long grid = n_items < 148LL ? n_items : 148LL;
     if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
-    tile_reduce_kernel<0><<<(unsigned)grid, kK6Threads, kK6Smem, s>>>(n_items, items, tile_ptr, runs, lam, per_item, T,
-                                                                       0, next);
+    tile_reduce_kernel<MODE, PAD><<<(unsigned)grid, kK6Threads, smem, s>>>(n_items, items, tile_ptr, runs, lam,
+                                                                              per_item, out, n_out, next);
+}
+
+void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
+                        const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad, cudaStream_t s) {
+    if (n_items == 0) return;
+    if (pad)
+        launch_tile_reduce_t<0, true>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, s);
+    else
+        launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, s);
 }
 
 void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
                     const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, cudaStream_t s) {
     if (n_items == 0) return;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(tile_reduce_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kK6SmemKf);
-        configured = true;
-    }
-    const long long grid = n_items < 148LL ? n_items : 148LL;
-    if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
-    tile_reduce_kernel<1><<<(unsigned)grid, kK6Threads, kK6SmemKf, s>>>(n_items, items, bucket_ptr, runs, lam, per_item,
-                                                                         D, n_slots, next);
+    launch_tile_reduce_t<1, false>(n_items, items, bucket_ptr, runs, lam, per_item, D, n_slots, next, s);
 }
 
 // Keyframe averages -> quantised log-odds per (frame, slot) and their sum per slot (thread per

@@ -255,7 +255,7 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, int per_item, long long* T, unsigned* next, cudaStream_t s);
+                        const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad, cudaStream_t s);
 // keyframe averages (reading R22): per [bucket = frame * NT + tile][slot], D += signed small
 // probability of each message (fp64, D[0 .. n_slots)) and the packed counts n_pos + 2^32 n_neg
 // (int64, at D + n_slots); both zeroed by the caller (bp.cu tile_reduce_kernel<1>)

@@ -85,6 +85,7 @@ struct mrf_ctx {
     bool k6_item_fixed = false;
     bool k6_lpt = true;  // MRF_K6_LPT=0: j-major item order only
     bool k6_dynamic = true;  // MRF_K6_DYNAMIC=0: fixed-stride item order
+    bool k6_pad = true;      // MRF_K6_PAD=0: plain accumulator layout (y, z steps in one bank)
     // keyframe-average mode (NEXT #3, reading R22): one message per (frame, voxel)
     bool kf_avg = false;
     // matrix-free mode (NEXT #1): only lambda and the tile runs persist; vid / off_q / log nu are
@@ -717,7 +718,8 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
     } else {
         launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
-                           c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->stream);
+                           c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->k6_pad,
+                           c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -947,6 +949,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         c->k6_item_fixed = true;
     }
     if (const char* kd = getenv("MRF_K6_DYNAMIC")) c->k6_dynamic = atoi(kd) != 0;
+    if (const char* kp = getenv("MRF_K6_PAD")) c->k6_pad = atoi(kp) != 0;
     if (const char* kl = getenv("MRF_K6_LPT")) c->k6_lpt = atoi(kl) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
