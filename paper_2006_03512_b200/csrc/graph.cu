@@ -354,8 +354,11 @@ __global__ void brick_alloc_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const f
 // 8-slot chunk of shared memory and writes a whole chunk at once (two 16-byte vid stores, one
 // 16-byte off_q store; segments are 8-aligned, padding slots get 0): one scattered 4-byte and
 // one 2-byte store per step had the walk waiting on the store queue.
+// With MRF_FILL_LNU the chunk's log nu (B3) is interpolated here too: 8 independent table
+// lookups per flush (16 loads in flight) instead of a separate pass that re-reads off_q.
 __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long long e_chunk, int nvalid,
-                                            const int* sv, const short* so) {
+                                            const int* sv, const short* so, float* lnu, const MsgParams& mp, int iz,
+                                            float wz) {
     int v[8];
     short o[8];
 #pragma unroll
@@ -363,6 +366,19 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long l
         v[k] = k < nvalid ? sv[k] : 0;
         o[k] = k < nvalid ? so[k] : (short)0;
     }
+#if MRF_FILL_LNU
+    {
+        LutFetch lf[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) lf[k] = lut_fetch(mp, iz, o[k]);
+        float l[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) l[k] = k < nvalid ? lut_finish(lf[k], wz) : 0.f;
+        float4* dl = reinterpret_cast<float4*>(lnu + e_chunk);
+        dl[0] = make_float4(l[0], l[1], l[2], l[3]);
+        dl[1] = make_float4(l[4], l[5], l[6], l[7]);
+    }
+#endif
     int4* dv = reinterpret_cast<int4*>(vid + e_chunk);
     dv[0] = make_int4(v[0], v[1], v[2], v[3]);
     dv[1] = make_int4(v[4], v[5], v[6], v[7]);
@@ -378,7 +394,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                                                        NoiseDesc n, const float* __restrict__ depth_all,
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
                                                        int16_t* off_q, int32_t* tile_runs, RayInfo* ray_z,
-                                                       unsigned long long* counters) {
+                                                       unsigned long long* counters, MsgParams mp, float* lnu) {
     __shared__ int s_vid[kFillThreads][8];
     __shared__ short s_off[kFillThreads][8];
     __shared__ FrameDesc f;
@@ -405,6 +421,8 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
     int run_tile = -1, run_n = 0, run_prev = 0;  // current tile run (K4b count)
     const int bucket0 = f.index * f.bucket_stride;
     long long e = 0, e_cap = 0;
+    int iz = 0;
+    float wz = 0.f;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
@@ -413,6 +431,10 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             w.start(sg);
             alive = w.inside(g);
             e_cap = row_ptr[f.ray_base + i + 1];  // the segment K1 sized from its bound
+            if (MRF_FILL_LNU) {  // the depth coordinate of the table (K1)
+                iz = ray_z[f.ray_base + i].iz;
+                wz = ray_z[f.ray_base + i].wz;
+            }
         }
     }
     const long long e_ray = e;
@@ -435,7 +457,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
                 sv[e & 7] = vx;
                 so[e & 7] = (short)q;
-                if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so);
+                if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, iz, wz);
                 ++e;
                 // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
                 b = vx >> kTileShift;
@@ -466,7 +488,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 alive = false;
                 overflow = true;
             }
-            if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so);  // partial tail
+            if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so, lnu, mp, iz, wz);  // partial tail
         }
     }
     int ne = 0;
@@ -481,6 +503,11 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             dv[0] = make_int4(0, 0, 0, 0);
             dv[1] = make_int4(0, 0, 0, 0);
             *reinterpret_cast<uint4*>(off_q + z) = make_uint4(0u, 0u, 0u, 0u);
+            if (MRF_FILL_LNU) {
+                float4* dl = reinterpret_cast<float4*>(lnu + z);
+                dl[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                dl[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
     }
 #pragma unroll
@@ -880,12 +907,13 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
     if (n_ctas > 0) {
         if (g.bmask)
             dda_fill_kernel<true><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr,
-                                                                  vid, off_q, tile_runs, ray_z, counters);
+                                                                  vid, off_q, tile_runs, ray_z, counters, mp, lnu);
         else
             dda_fill_kernel<false><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr,
-                                                                   vid, off_q, tile_runs, ray_z, counters);
+                                                                   vid, off_q, tile_runs, ray_z, counters, mp, lnu);
     }
-    if (n_rays > 0) lnu_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(r0, n_rays, mp, row_ptr, ray_z, off_q, lnu);
+    if (!MRF_FILL_LNU && n_rays > 0)
+        lnu_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(r0, n_rays, mp, row_ptr, ray_z, off_q, lnu);
 }
 
 void launch_transpose_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,

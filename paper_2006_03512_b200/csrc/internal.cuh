@@ -115,6 +115,11 @@ struct MsgParams {
 
 // log nu at (measured range row iz + wz, quantised offset off_q): bilinear interpolation of the
 // input table in fp32, bin-centre coordinates clamped to the edge centres.
+// MRF_FILL_LNU = 1: the DDA fill interpolates log nu as it flushes each 8-slot chunk; 0: a separate
+// pass (lnu_fill_kernel) re-reads off_q.
+#ifndef MRF_FILL_LNU
+#define MRF_FILL_LNU 1
+#endif
 // Evaluated once per incidence by the DDA fill; K5 reads the result.
 // Split in two so that a caller can issue the table loads one step before it needs them.
 struct LutFetch {

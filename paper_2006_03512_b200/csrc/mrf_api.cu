@@ -377,7 +377,7 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
     launch_dda_fill(c->d_frames.p + f0, dc, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
                     c->depth_all.p, c->row_ptr.p, c->ray_z.p, sv - ch.e0, so - ch.e0, sl - ch.e0,
                     count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), st);
-    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (r1 > r0 ? 1 : 0));
+    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (!MRF_FILL_LNU && r1 > r0 ? 1 : 0));
     mf_dbg(c, count ? "walk(count)" : "walk");
     return MRF_OK;
 }
@@ -455,7 +455,7 @@ mrf_status sync_fill(mrf_ctx* c) {
             launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
                             c->lnu.p, c->tile_runs.p, c->counters.p + 10, c->stream);
-            CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (c->R > c->R_filled ? 1 : 0));
+            CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (!MRF_FILL_LNU && c->R > c->R_filled ? 1 : 0));
         }
         c->pend.clear();
         c->depth_used = 0;
