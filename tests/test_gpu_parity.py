@@ -161,6 +161,20 @@ def test_determinism(frame1):
         assert np.array_equal(a, b)
 
 
+def test_k6_accumulator_layouts_agree(frame1, monkeypatch):
+    """K6's padded shared-memory layout (default) and the plain one (MRF_K6_PAD=0, read at
+    mrf_create) give identical beliefs: the sums are exact integers, the layout only moves the
+    accumulator slots."""
+    outs = []
+    for pad in ("1", "0"):
+        monkeypatch.setenv("MRF_K6_PAD", pad)
+        with _gpu_map(frame1) as m:
+            m.bp_iterate(3)
+            outs.append((m.export_beliefs(), m.export_messages()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
 def test_warm_start_matches_oracle(frame1):
     """A frame added after iterations starts with lambda = 0 and keeps the others (warm
     start): the state right after mrf_add_frame is exactly (old messages, zeros), and the
