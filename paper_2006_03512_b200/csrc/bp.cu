@@ -71,35 +71,45 @@ __device__ __forceinline__ float lg2(float x) {
 #ifndef MRF_LOG1P_DEG7
 #define MRF_LOG1P_DEG7 1
 #endif
+// Working base of the K5 log domain.  MRF_K5_LOG2 = 1: every log-quantity of K5 (cavity, la, w,
+// l, Q, R, lambda) is carried in base-2 units (x / ln 2), so e^x and ln(1+y) become bare ex2 / lg2
+// -- no scaling multiply per MUFU op; the nats of the inputs (T, q, L0: exact integers and one
+// constant; log nu) are converted where they enter (folded into existing FMAs, one multiply for
+// l) and lambda is converted back to nats before quantisation.  0: natural-log units throughout.
+#ifndef MRF_K5_LOG2
+#define MRF_K5_LOG2 1
+#endif
+constexpr float kWS = MRF_K5_LOG2 ? kLog2e : 1.f;  // nats -> working units
+constexpr float kWInv = MRF_K5_LOG2 ? kLn2 : 1.f;  // working units -> nats
 __device__ __forceinline__ float log1pn(float y) {
 #if MRF_LOG1P_DEG7
     // degree 7 (relative error 3.3e-7 evaluated in fp32; the degree-8 fit below: 1.6e-7)
-    float r = -0.00853875931f;
-    r = fmaf(r, y, 0.0440874845f);
-    r = fmaf(r, y, -0.10767781f);
-    r = fmaf(r, y, 0.177448928f);
-    r = fmaf(r, y, -0.244953007f);
-    r = fmaf(r, y, 0.332754433f);
-    r = fmaf(r, y, -0.499974012f);
-    r = fmaf(r, y, 0.999999821f);
+    float r = (-0.00853875931f * kWS);
+    r = fmaf(r, y, (0.0440874845f * kWS));
+    r = fmaf(r, y, (-0.10767781f * kWS));
+    r = fmaf(r, y, (0.177448928f * kWS));
+    r = fmaf(r, y, (-0.244953007f * kWS));
+    r = fmaf(r, y, (0.332754433f * kWS));
+    r = fmaf(r, y, (-0.499974012f * kWS));
+    r = fmaf(r, y, (0.999999821f * kWS));
     return r * y;
 #else
-    float r = 0.00523269456f;
-    r = fmaf(r, y, -0.0295052417f);
-    r = fmaf(r, y, 0.0782259554f);
-    r = fmaf(r, y, -0.136632457f);
-    r = fmaf(r, y, 0.191060066f);
-    r = fmaf(r, y, -0.24842982f);
-    r = fmaf(r, y, 0.333190978f);
-    r = fmaf(r, y, -0.499994934f);
-    r = fmaf(r, y, 0.99999994f);
+    float r = (0.00523269456f * kWS);
+    r = fmaf(r, y, (-0.0295052417f * kWS));
+    r = fmaf(r, y, (0.0782259554f * kWS));
+    r = fmaf(r, y, (-0.136632457f * kWS));
+    r = fmaf(r, y, (0.191060066f * kWS));
+    r = fmaf(r, y, (-0.24842982f * kWS));
+    r = fmaf(r, y, (0.333190978f * kWS));
+    r = fmaf(r, y, (-0.499994934f * kWS));
+    r = fmaf(r, y, (0.99999994f * kWS));
     return r * y;
 #endif
 }
-// ln(1 + y), y in [0, 1], absolutely accurate (~1e-7) on the MUFU
-__device__ __forceinline__ float log1pf_abs(float y) { return kLn2 * lg2(1.f + y); }
-// e^x on the MUFU (ex2.approx, relative error ~2^-22)
-__device__ __forceinline__ float expn(float x) { return ex2(x * kLog2e); }
+// ln(1 + y), y in [0, 1], absolutely accurate (~1e-7) on the MUFU (working units)
+__device__ __forceinline__ float log1pf_abs(float y) { return MRF_K5_LOG2 ? lg2(1.f + y) : kLn2 * lg2(1.f + y); }
+// e^x on the MUFU (ex2.approx, relative error ~2^-22), x in working units
+__device__ __forceinline__ float expn(float x) { return MRF_K5_LOG2 ? ex2(x) : ex2(x * kLog2e); }
 // ln(e^a + e^b) = max + ln(1 + e^-|a-b|)
 template <bool ABS>
 __device__ __forceinline__ float lse(float a, float b) {
@@ -149,15 +159,16 @@ __device__ __forceinline__ void elem_terms(long long t, int q, float lnu, float 
     // x = hi 2^24 + lo with both parts exact in fp32 (32-bit conversions run on the ALU pipe;
     // the 64-bit I2F is a MUFU-class op)
     const long long x = t - (long long)q;
-    const float c = fmaf(__int2float_rn((int)(x >> 24)), 2.f, fmaf(__int2float_rn((int)(x & 0xffffff)), kQInv, L0));
+    const float c = fmaf(__int2float_rn((int)(x >> 24)), 2.f * kWS,
+                         fmaf(__int2float_rn((int)(x & 0xffffff)), kQInv * kWS, L0 * kWS));
 #else
-    const float c = fmaf(__ll2float_rn(t - (long long)q), kQInv, L0);
+    const float c = fmaf(__ll2float_rn(t - (long long)q), kQInv * kWS, L0 * kWS);
 #endif
     const float y = expn(-fabsf(c));
     const float L1 = M >= 2 ? log1pf_abs(y) : log1pn(y);  // ln(1 + e^-|c|)
     la = selp(ok, -(fmaxf(c, 0.f) + L1), 0.f);
-    w = selp(ok, lnu - (fmaxf(-c, 0.f) + L1), kNeg);
-    l = selp(ok, lnu, kNeg);
+    w = selp(ok, fmaf(lnu, kWS, -(fmaxf(-c, 0.f) + L1)), kNeg);
+    l = selp(ok, lnu * kWS, kNeg);
 }
 
 // Chunk composite of the suffix maps R -> e^{la} R + e^{w} (first applied last):
@@ -176,7 +187,7 @@ __device__ __forceinline__ void lane_composite(const float (&la)[K], const float
 #pragma unroll
     for (int j = 0; j < K; ++j) sum += expn(t[j] - m);
     aB = acc;
-    bB = m + lg2(sum) * kLn2;
+    bB = m + (MRF_K5_LOG2 ? lg2(sum) : lg2(sum) * kLn2);
 }
 
 // Both lane scans of a ray's G lanes at once (two independent shuffle chains per level):
@@ -245,8 +256,8 @@ __device__ __forceinline__ float lambda_n(float Q, float l, float R) {
     return (m1 - m2) + (log1pn(expn(-fabsf(Q - l))) - log1pn(expn(-fabsf(Q - R))));
 }
 
-__device__ __forceinline__ int32_t quantise(float lam) {
-    lam = fminf(fmaxf(lam, -kLambdaClip), kLambdaClip);
+__device__ __forceinline__ int32_t quantise(float lam) {  // lam in working units
+    lam = fminf(fmaxf(lam * kWInv, -kLambdaClip), kLambdaClip);
     return __float2int_rn(lam * kQScale);  // saturates at +2^31-1 for +256
 }
 
