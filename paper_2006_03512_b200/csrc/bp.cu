@@ -14,8 +14,9 @@
 // Eq.13/14; dividing both messages by V_i leaves the log-odds unchanged and keeps every
 // quantity O(1) in the log domain.  Both recurrences are affine maps x -> e^a x + e^b, so
 // 8-element chunks compose in closed form and the chunks of a ray are combined by scans (prefix
-// for Q, suffix for R).  Everything is in natural logs (the units of the input table): e^x as
-// ex2.approx on the MUFU; ln(1+y) either as a relative-accurate polynomial on the FMA pipe
+// for Q, suffix for R).  The inputs are in natural logs (the units of the input table); inside
+// K5 every log-quantity is carried in base-2 units (MRF_K5_LOG2, below), and lambda leaves in
+// nats: e^x as ex2.approx on the MUFU; ln(1+y) either as a relative-accurate polynomial on the FMA pipe
 // (log1pn) or, where only absolute accuracy matters, as lg2.approx on the MUFU (MATH levels
 // below); lambda without cancellation (lambda_n).
 //
