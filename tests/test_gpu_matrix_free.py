@@ -81,3 +81,28 @@ def test_matrix_free_warm_start_and_rules():
                 with pytest.raises(pkg.MrfError):
                     m.set_matrix_free(1)  # frames already added
     assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+
+
+def _oracle_leg(w, n_iter, mf):
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    lam_ref, T_ref = oracle.bp(p, g, n_iter)
+    lam, _, marg, sizes = _run(w, n_iter, mf=mf)
+    assert sizes["E"] == g.E and sizes["n_rays"] == g.n_rays
+    rel = np.abs(lam.astype(np.float64) - lam_ref) / np.maximum(1.0, np.abs(lam_ref))
+    assert rel.max() <= 1e-3, f"max rel msg err {rel.max():.3e}"
+    d = np.abs(marg - oracle.marginals(p, T_ref))
+    assert d.max() <= 1e-4, f"max marginal err {d.max():.3e}"
+
+
+@pytest.mark.parametrize("mf,n_iter", [(1, 1), (2, 3), (3, 10)])
+def test_matrix_free_matches_oracle_tiny_frames(mf, n_iter):
+    """Matrix-free against the fp64 oracle directly (not only against the stored graph): the
+    tiny scene seen from 4 keyframes, full trajectory."""
+    _oracle_leg(synth.tiny_frames(n_frames=4), n_iter, mf)
+
+
+def test_matrix_free_matches_oracle_frame1():
+    """The single-frame room (26 M incidences), full trajectory over 2 iterations (where the
+    loopy graph is still well conditioned)."""
+    _oracle_leg(synth.single_frame(), 2, 1)

@@ -15,6 +15,7 @@ import oracle  # noqa: E402
 import synth  # noqa: E402
 import paper_2006_03512_b200 as pkg  # noqa: E402
 from synth.scenes import Frame  # noqa: E402
+from tests import traj  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -123,32 +124,31 @@ def test_frame1_graph_and_bp_parity(frame1):
             assert d.max() <= MARG_TOL, f"one-step marginal err {d.max():.3e} from iteration {k}"
 
 
-def test_frame1_full_trajectory_within_conditioning_envelope(frame1):
-    """End-to-end after all 8 iterations.  This loopy graph amplifies perturbations ~1e4x by
-    iteration 8 (tests/test_oracle_conditioning.py), so the bar is the oracle's own spread
-    under fp32-sized noise (reading R16): the fp64 oracle re-run with noise of the
-    size the one-step GPU comparison measures on every message of every iteration -- rms
-    2e-7 absolute + 6e-8 relative (`python -m tests.parity_report onestep frame1 2`: rms
-    1.3e-7..2.3e-7 absolute for |lambda| < 10, 1.5e-6 for |lambda| in [10, 300)) -- max over
-    two noise seeds.  GPU deviation <= max(1e-4, 5 x that spread)."""
+def test_frame1_full_trajectory_count_rule(frame1):
+    """End-to-end after all 8 iterations of the loopy single-frame config, under the count /
+    quantile rule of tests/traj.py (reading R16): the GPU's count of voxels off
+    the fp64 oracle by > 1e-4 is at most 3x the count of the oracle re-run with fp32-sized noise
+    on every message of every iteration, and its p99.99 deviation is <= 1e-4.  (This graph
+    amplifies perturbations ~1e4x by iteration 8, tests/test_oracle_conditioning.py, so a
+    max-norm bar over every voxel is not attainable in fp32.)  n = 3, the paper's pass count
+    (P:200), is checked the same way."""
     w = frame1
     p = oracle.Params.from_workload(w)
     g = oracle.build_graph(p, w.frames)
-    _, T_ref = oracle.bp(p, g, w.n_iter)
-    m_ref = oracle.marginals(p, T_ref)
-    spread = 0.0
-    for seed in (1, 2):
-        rng = np.random.default_rng(seed)
-        lam = np.zeros(g.E)
-        for _ in range(w.n_iter):
-            lam, _ = oracle.bp(p, g, 1, lam=lam)
-            lam = lam + (2e-7 + 6e-8 * np.abs(lam)) * rng.standard_normal(g.E)
-        spread = max(spread, np.max(np.abs(oracle.marginals(p, oracle.accumulate(p, g, lam)) - m_ref)))
+    ref = traj.reference_trajectory(p, g, (3, w.n_iter))
+    noisy = traj.noisy_trajectories(p, g, (3, w.n_iter), seeds=(1, 2, 3, 4))
+    gpu = {}
     with _gpu_map(w) as m:
-        m.bp_iterate(w.n_iter)
-        dev = np.max(np.abs(m.marginals() - m_ref))
-    print(f"frame1 n={w.n_iter}: gpu max|dp| {dev:.3e}, oracle fp32-noise spread {spread:.3e}")
-    assert dev <= max(MARG_TOL, 5 * spread)
+        m.bp_iterate(3)
+        gpu[3] = m.marginals()
+        m.bp_iterate(w.n_iter - 3)
+        gpu[w.n_iter] = m.marginals()
+    for n in (3, w.n_iter):
+        st = traj.dev_stats(gpu[n], ref[n])
+        ns = [traj.dev_stats(nz[n], ref[n]) for nz in noisy]
+        print(f"frame1 n={n}: gpu {st}, noisy oracle {ns}")
+        assert st["p9999"] <= MARG_TOL, st
+        assert st["over"] <= traj.count_bar([x["over"] for x in ns]), (st, ns)
 
 
 def test_determinism(frame1):
