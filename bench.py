@@ -7,8 +7,12 @@ Units per step = E * n (message updates), E = incidences of all ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config frames30] [--impl ours|reference]
 
-N > 1: launched by torch.distributed.run, one rank per GPU, rays sharded by pixel row
-(v % world == rank) with an NCCL all-reduce of the int64 voxel sums every iteration.
+N > 1: one rank per GPU, rays sharded by pixel row (v % world == rank) with an NCCL all-reduce
+of the int64 voxel sums of the touched tiles every iteration.  Launched by the driver under
+torch.distributed.run; `--gpus N` without WORLD_SIZE in the environment re-launches itself
+that way (N ranks on 127.0.0.1).  NCCL's INFO lines (communicator set-up, NVLS) go to
+gpurun_out/nccl.<host>.<pid>.log unless NCCL_DEBUG is set.  `--dry-run` exercises the launch
+and rank plumbing on CPU (gloo, no kernels).
 --impl reference: the fp64 CPU oracle (oracle/) timed on the host cores on a bounded sample
 of the same workload (this tier has no reference implementation to install).
 """
@@ -40,6 +44,26 @@ def _peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def _cores():
@@ -95,19 +119,42 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- reference arm
 
-def _oracle_sample(w, max_frames=1, messages="per-ray"):
+def _oracle_sample(w, max_frames=1, messages="per-ray", threads=None, n_iter=None):
     """The oracle as it stands on a bounded sample: the first `max_frames` frames of the
-    workload, graph build + n iterations.  Returns (updates, seconds, E)."""
+    workload, graph build + n iterations, on `threads` OpenMP threads (None: all cores).
+    Returns (updates, seconds, E, threads used)."""
     import oracle
-    p = oracle.Params.from_workload(w)
-    t0 = time.perf_counter()
-    g = oracle.build_graph(p, w.frames[:max_frames])
-    if messages == "keyframe-avg":
-        oracle.kf_bp(p, g, w.n_iter, F=max_frames)
-    else:
-        oracle.bp(p, g, w.n_iter)
-    dt = time.perf_counter() - t0
-    return g.E * w.n_iter, dt, g.E
+    n_iter = w.n_iter if n_iter is None else n_iter
+    used = _cores() if threads is None else int(threads)
+    oracle.set_num_threads(used)
+    try:
+        p = oracle.Params.from_workload(w)
+        t0 = time.perf_counter()
+        g = oracle.build_graph(p, w.frames[:max_frames])
+        if messages == "keyframe-avg":
+            oracle.kf_bp(p, g, n_iter, F=max_frames)
+        else:
+            oracle.bp(p, g, n_iter)
+        dt = time.perf_counter() - t0
+    finally:
+        oracle.set_num_threads(_cores())
+    return g.E * n_iter, dt, g.E, used
+
+
+def cpu_baseline(w, config, messages):
+    """the fp64 oracle on the host, at all cores (first 5 frames of the workload)
+    and at 1 thread (first frame), graph build + the workload's iterations, as it stands."""
+    nf = min(5, len(w.frames))
+    u, dt, E, used = _oracle_sample(w, nf, messages)
+    u1, dt1, E1, _ = _oracle_sample(w, 1, messages, threads=1)
+    v, v1 = u / dt, u1 / dt1
+    return {"value": v, "unit": UNIT, "cores": used, "kind": "oracle", "cpu": _cpu_model(),
+            "ns_per_incidence_iteration": 1e9 / v,
+            "sample": f"subset: first {nf} of {len(w.frames)} frames of {config} (E={E}), graph build + "
+                      f"{w.n_iter} BP iterations, fp64, {used} OpenMP threads",
+            "single_thread": {"value": v1, "unit": UNIT, "cores": 1, "ns_per_incidence_iteration": 1e9 / v1,
+                              "sample": f"subset: first frame of {config} (E={E1}), graph build + "
+                                        f"{w.n_iter} BP iterations, fp64, 1 thread"}}
 
 
 def run_reference(args, rank, world):
@@ -119,17 +166,18 @@ def run_reference(args, rank, world):
         _oracle_sample(w, 1, args.messages)
     tot_u = tot_t = 0.0
     for _ in range(args.steps):
-        u, dt, E = _oracle_sample(w, 1, args.messages)
+        u, dt, E, cores = _oracle_sample(w, 1, args.messages)
         tot_u += u
         tot_t += dt
     v = tot_u / tot_t
-    cores = _cores()
-    sample = f"first frame of {args.config} (E={E}), graph build + {w.n_iter} BP iterations per step"
+    sample = (f"subset: first frame of {args.config} (E={E}), graph build + {w.n_iter} BP iterations per step, "
+              f"fp64, {cores} OpenMP threads ({_cpu_model()})")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": args.config, "sample": sample},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu": _cpu_model(), "ns_per_incidence_iteration": 1e9 / v},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -251,10 +299,11 @@ def run_ours(args, rank, world, local_rank):
     d2h = w.n_voxels * 4
 
     # ---- roofline of the dominant kernel (one launch group = one BP iteration over all classes)
-    # Algorithmic bytes of THIS design per iteration:
-    #   K5: vid 4 + log nu 4 + lambda read 4 + lambda write 4 per incidence, + T gather 8 per voxel
-    #   K6: lambda 4 per incidence + 16 per tile run (step-coded descriptor), + T write 8 per voxel
-    # and, for comparison, SURVEY §8(d)'s canonical model (22 B per incidence + 16 per voxel).
+    # roofline.frac counts the METHOD's bytes, SURVEY §8(d)'s canonical model:
+    #   K5: vid 4 + off_q 2 + lambda read 4 + lambda write 4 = 14 B per incidence, + T gather 8 per voxel
+    #   K6: tr 4 + lambda 4 = 8 B per incidence, + T write 8 per voxel
+    # This design's own bytes (K5 reads a 4-byte log nu instead of the 2-byte off_q; K6 reads 16 B
+    # per tile run instead of tr) are reported beside them under "design_bytes".
     peak, peak_kind = _peaks()
     V = w.n_voxels
     lay = m.layout_sizes()
@@ -263,12 +312,15 @@ def run_ours(args, rank, world, local_rank):
     n_k6, ms_k6 = prof["voxel_sum"]
     per_iter_k5 = ms_k5 / max(1, args.steps * n_iter)
     per_iter_k6 = ms_k6 / max(1, args.steps * n_iter)
-    bytes_k5 = 16 * E_local + 8 * V
-    bytes_k6 = 4 * E_local + 16 * n_runs + 8 * V
+    bytes_k5 = 14 * E_local + 8 * V
+    bytes_k6 = 8 * E_local + 8 * V
+    dbytes_k5 = 16 * E_local + 8 * V             # this design
+    dbytes_k6 = 4 * E_local + 16 * n_runs + 8 * V
     gbs = lambda b, t: b / (t / 1e3) / 1e9 if t > 0 else 0.0
     ach_k5, ach_k6 = gbs(bytes_k5, per_iter_k5), gbs(bytes_k6, per_iter_k6)
     ach_bp = gbs(bytes_k5 + bytes_k6, per_iter_k5 + per_iter_k6)
-    ach_22 = gbs(22 * E_local + 16 * V, per_iter_k5 + per_iter_k6)
+    dach_k5, dach_k6 = gbs(dbytes_k5, per_iter_k5), gbs(dbytes_k6, per_iter_k6)
+    dach_bp = gbs(dbytes_k5 + dbytes_k6, per_iter_k5 + per_iter_k6)
     dominant = "ray_messages" if ms_k5 >= ms_k6 else "voxel_sum"
     ach = ach_k5 if dominant == "ray_messages" else ach_k6
     # ncu DRAM bytes per launch (one --set full capture of this workload, profiles/ncu_summary.json)
@@ -308,19 +360,21 @@ def run_ours(args, rank, world, local_rank):
             "kernel_ms_per_step": kernel_ms,
             "roofline": {"bound": "hbm", "kernel": dominant, "achieved": ach, "peak": peak, "unit": "GB/s",
                          "frac": ach / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "bytes_model": "SURVEY §8(d): K5 14 B/incidence + 8 B/voxel, K6 8 B/incidence + 8 B/voxel",
                          "algorithmic_bytes_per_launch": bytes_k5 if dominant == "ray_messages" else bytes_k6,
                          "k5_frac": ach_k5 / peak, "k6_frac": ach_k6 / peak,
-                         "bp_iteration_frac": ach_bp / peak, "bp_iteration_frac_survey22B": ach_22 / peak,
+                         "bp_iteration_frac": ach_bp / peak,
+                         "design_bytes": {"model": "K5 16 B/incidence (log nu stored) + 8 B/voxel; "
+                                                   "K6 4 B/incidence + 16 B/tile run + 8 B/voxel",
+                                          "k5_frac": dach_k5 / peak, "k6_frac": dach_k6 / peak,
+                                          "bp_iteration_frac": dach_bp / peak},
                          "ms_k5": per_iter_k5, "ms_k6": per_iter_k6, "tile_runs": n_runs, **dram},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            u, dt, Es = _oracle_sample(w, 1, args.messages)
-            line["cpu_baseline"] = {"value": u / dt, "unit": UNIT, "cores": _cores(), "kind": "oracle",
-                                    "sample": f"first frame of {args.config} (E={Es}), graph build + "
-                                              f"{w.n_iter} BP iterations, fp64"}
+            line["cpu_baseline"] = cpu_baseline(w, args.config, args.messages)
         print(json.dumps(line), flush=True)
     m.close()
 
@@ -342,21 +396,79 @@ def main():
                     help="message model: exact per-ray messages (north_star) or per-keyframe averages (P:200)")
     ap.add_argument("--emulate-ranks", type=int, default=None,
                     help="ranks emulated on the one GPU (default: 4 for the 0.02 m configs, else 1)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rank plumbing only (gloo on CPU, no kernels): one JSON line from rank 0")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and args.gpus != world and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using {world} ranks", file=sys.stderr)
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
     if world > 1:
         import torch
         import torch.distributed as dist
+        _nccl_log_env()
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _self_launch(n):
+    """`--gpus N` outside torch.distributed.run: re-launch this script as N ranks (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def _nccl_log_env():
+    """Keep NCCL's INFO lines (communicator set-up: rings, NVLS, P2P/NVLink transports) in a file
+    per rank, out of stdout (rank 0's stdout carries the one JSON line)."""
+    if "NCCL_DEBUG" in os.environ:
+        return None
+    d = os.path.join(ROOT, "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    os.environ["NCCL_DEBUG"] = "INFO"
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
+    os.environ["NCCL_DEBUG_FILE"] = os.path.join(d, "nccl.%h.%p.log")
+    return os.environ["NCCL_DEBUG_FILE"]
+
+
+def run_dry(args, rank, world):
+    """The N-rank plumbing without a GPU: gloo process group, the row sharding of the workload's
+    frames (v % world == rank), the max-over-ranks timing reduction; rank 0 prints one line."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2006_03512_b200.dist import owned_rows
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    w = synth.make_workload(args.config)
+    t0 = time.perf_counter()
+    pix = sum(len(owned_rows(fr.height, rank, world)) * fr.width for fr in w.frames)
+    t = torch.tensor([1, pix, rank], dtype=torch.int64)
+    ms = torch.tensor([1e3 * (time.perf_counter() - t0)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks": int(t[0]), "rank_sum": int(t[2]),
+                          "pixels": int(t[1]), "pixels_expected": sum(fr.height * fr.width for fr in w.frames),
+                          "ms_max_over_ranks": float(ms), "config": {"workload": args.config}}), flush=True)
+    if world > 1:
         dist.destroy_process_group()
 
 

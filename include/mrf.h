@@ -56,7 +56,8 @@ typedef enum {
  * Traversal margin past the measured range: margin(Z) = max(margin_min, margin_k*sigma(Z)),
  * sigma(Z) = (c0 + c1 Z) + c2 Z^2  (3 sigma beyond the depth; reading R5). */
 typedef struct {
-    const float* log_nu;   /* [n_z][n_off] row-major, finite, host memory; copied at create */
+    const float* log_nu;   /* [n_z][n_off] row-major, finite, host memory; copied at create (entries
+                              below -1e30, e.g. -FLT_MAX for log 0, are taken as -1e30) */
     int32_t n_z, n_off;    /* >= 2 each */
     double z_lo, z_hi;     /* metres, z_hi > z_lo */
     double off_lo, off_hi; /* metres, -1 <= off_lo < off_hi <= 1 (span of the int16 offset code) */
@@ -70,7 +71,10 @@ typedef struct {
 /* Data-parallel sharding: rank keeps the rays of pixel rows v % world == rank.
  * comm = MRF_COMM_NCCL: an NCCL communicator is created from nccl_id (all ranks pass the same
  *   id, from mrf_nccl_unique_id on rank 0) and mrf_bp_iterate all-reduces the per-voxel int64
- *   partial sums every iteration.
+ *   partial sums every iteration -- only over the 32x32x16 tiles some rank touches (a touched-
+ *   tile mask ncclMax-reduced once per graph change, so every rank compacts identically).  The
+ *   communicator's asynchronous error state is polled after every collective; a failure is the
+ *   sticky MRF_ERR_NCCL.  Every rank must make the same sequence of calls (collectives inside).
  * comm = MRF_COMM_EXTERNAL: no communicator; the caller reduces the partials itself with
  *   mrf_bp_partial / mrf_bp_finish (used to emulate ranks on one GPU, and by tests). */
 enum { MRF_COMM_NCCL = 0, MRF_COMM_EXTERNAL = 1 };

@@ -100,8 +100,21 @@ def lib():
             L.orc_eval_pixel.restype = ctypes.c_int
             L.orc_eval_frame.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, dp, d, d, i32, i32, i32, i8p, i64p, i64p]
             L.orc_eval_frame.restype = None
+            L.orc_set_num_threads.argtypes = [i32]
+            L.orc_set_num_threads.restype = None
+            L.orc_max_threads.argtypes = []
+            L.orc_max_threads.restype = i32
             _lib = L
     return _lib
+
+
+def set_num_threads(n: int):
+    """OpenMP threads of the oracle's parallel loops (independent rays / voxels only)."""
+    lib().orc_set_num_threads(int(n))
+
+
+def max_threads() -> int:
+    return int(lib().orc_max_threads())
 
 
 def _ptr(a, t):

@@ -24,9 +24,15 @@
  *                                                          mask = dense walk, skipped cells = empty
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+
+/* Thread count of the OpenMP loops (bench.py times the oracle at 1 thread and at all cores;
+ * no arithmetic depends on it: independent rays / voxels only). */
+void orc_set_num_threads(int32_t n) { omp_set_num_threads(n > 0 ? n : 1); }
+int32_t orc_max_threads(void) { return (int32_t)omp_get_max_threads(); }
 
 #define FIX_ONE 65536LL /* 16 fractional bits of the fixed-point grid coordinates (B1) */
 

@@ -772,7 +772,8 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                                                                    const long long* __restrict__ tile_ptr,
                                                                    const Run* __restrict__ runs,
                                                                    const int32_t* __restrict__ lam, int per_item,
-                                                                   void* out, long long n_out, unsigned* next) {
+                                                                   void* out, long long n_out, unsigned* next,
+                                                                   const int32_t* __restrict__ tile_map) {
     extern __shared__ int smem[];
     using L = AccLayout<PAD>;
     static_assert(MODE == 0 || !PAD, "keyframe-average sums use the plain layout (shared memory)");
@@ -868,7 +869,10 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
         }
         __syncthreads();
         if constexpr (MODE == 0) {
-            long long* Tt = static_cast<long long*>(out) + ((long long)item.x << kTileShift);
+            // world > 1: the tile's slots go to its position among the tiles some rank touches
+            // (the compacted all-reduce buffer); else to the tile itself
+            const long long tpos = tile_map ? (long long)__ldg(tile_map + item.x) : (long long)item.x;
+            long long* Tt = static_cast<long long*>(out) + (tpos << kTileShift);
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
                 const int a = L::index(i);
                 const long long sum = (long long)acc_hi[a] * 65536 + (long long)acc_lo[a];
@@ -921,6 +925,23 @@ __global__ void lambda_to_float_kernel(long long n, const int32_t* __restrict__ 
 
 inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
+// Per-device opt-in of the large dynamic shared memory (the attribute is per device: a process
+// may drive ctxs on several GPUs) and the device's SM count (grid sizing).
+struct DevCfg {
+    int sms = 0;
+    bool k6[2][2] = {};
+};
+DevCfg& dev_cfg() {
+    static thread_local DevCfg cfg[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    DevCfg& c = cfg[dev & 63];
+    if (!c.sms) cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (!c.sms) c.sms = 148;
+    return c;
+}
+
+
 template <int M, bool AVG, int k>
 void launch_class_k(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr, const RayInfo* ray_z,
                     const int32_t* vid, const float* lnu, int32_t* lam, const long long* T, const MsgParams& mp,
@@ -954,16 +975,13 @@ template <int M>
 void launch_staged_m(long long n_stages, const Stage* stages, const long long* row_ptr, const RayInfo* info,
                      const int32_t* vid, const float* lnu, int32_t* lam, const long long* T, const MsgParams& mp,
                      cudaStream_t s) {
-    static bool configured = false;
-    static int sms = 148;
-    if (!configured) {
-        cudaFuncSetAttribute(ray_msg_staged_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        configured = true;
-    }
-    const long long grid = std::min<long long>(n_stages, (long long)kStageCtas * sms);
+    // the attribute is per device: set it on every launch (cheap host call; the staged kernel is
+    // an ablation, not the default path)
+    cudaFuncSetAttribute(ray_msg_staged_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long grid = std::min<long long>(n_stages, (long long)kStageCtas * std::max(sms, 1));
     ray_msg_staged_kernel<M><<<(unsigned)grid, kStageThreads, kStageSmem, s>>>(n_stages, stages, row_ptr, info, vid,
                                                                               lnu, lam, T, mp);
 }
@@ -999,38 +1017,58 @@ void launch_ray_messages_staged(long long n_stages, const Stage* stages, const l
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s) {
     if (n_items == 0) return;
-    long long warps = n_items < 148LL * 64 ? n_items : 148LL * 64;
+    const long long cap = (long long)dev_cfg().sms * 64;
+    long long warps = n_items < cap ? n_items : cap;
     voxel_reduce_kernel<<<blocks_for(warps * 32, 256), 256, 0, s>>>(n_items, items, col_ptr, tr, lam, T);
 }
 
 template <int MODE, bool PAD>
 void launch_tile_reduce_t(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                          const int32_t* lam, int per_item, void* out, long long n_out, unsigned* next, cudaStream_t s) {
+                          const int32_t* lam, int per_item, void* out, long long n_out, unsigned* next,
+                          const int32_t* tile_map, cudaStream_t s) {
     constexpr int smem = (MODE == 0 ? 2 * AccLayout<PAD>::kSlots * (int)sizeof(int) : kK6SmemKf) + kK6Desc;
-    static bool configured = false;
-    if (!configured) {
+    DevCfg& dc = dev_cfg();
+    if (!dc.k6[MODE][PAD]) {
         cudaFuncSetAttribute(tile_reduce_kernel<MODE, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        configured = true;
+        dc.k6[MODE][PAD] = true;
     }
-    const long long grid = n_items < 148LL ? n_items : 148LL;
+    const long long grid = n_items < (long long)dc.sms ? n_items : (long long)dc.sms;
     if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
     tile_reduce_kernel<MODE, PAD><<<(unsigned)grid, kK6Threads, smem, s>>>(n_items, items, tile_ptr, runs, lam,
-                                                                              per_item, out, n_out, next);
+                                                                              per_item, out, n_out, next, tile_map);
 }
 
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad, cudaStream_t s) {
+                        const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad,
+                        const int32_t* tile_map, cudaStream_t s) {
     if (n_items == 0) return;
     if (pad)
-        launch_tile_reduce_t<0, true>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, s);
+        launch_tile_reduce_t<0, true>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, s);
     else
-        launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, s);
+        launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, s);
 }
 
 void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
                     const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, cudaStream_t s) {
     if (n_items == 0) return;
-    launch_tile_reduce_t<1, false>(n_items, items, bucket_ptr, runs, lam, per_item, D, n_slots, next, s);
+    launch_tile_reduce_t<1, false>(n_items, items, bucket_ptr, runs, lam, per_item, D, n_slots, next, nullptr, s);
+}
+
+// world > 1: the all-reduced sums of the touched tiles (compact order) back to their tiles
+__global__ void tile_scatter_kernel(long long n, const int32_t* __restrict__ tile_of, const longlong2* __restrict__ src,
+                                    longlong2* dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // pair index
+    if (i >= n) return;
+    constexpr int kPairs = kTileSlots / 2;
+    const long long ci = i / kPairs;
+    dst[(long long)__ldg(tile_of + ci) * kPairs + (i - ci * kPairs)] = src[i];
+}
+
+void launch_tile_scatter(long long n_tiles, const int32_t* tile_of, const long long* src, long long* T, cudaStream_t s) {
+    if (n_tiles == 0) return;
+    const long long n = n_tiles * (kTileSlots / 2);
+    tile_scatter_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, tile_of, reinterpret_cast<const longlong2*>(src),
+                                                           reinterpret_cast<longlong2*>(T));
 }
 
 // Keyframe averages -> quantised log-odds per (frame, slot) and their sum per slot (thread per

@@ -871,6 +871,30 @@ __global__ void stage_fill_kernel(long long n_rays, const long long* __restrict_
 
 inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) / b); }
 
+// mrf_export_rays: per selected ray its padded start and record, then its incidences gathered
+// into contiguous staging arrays (warp per ray) -- a few large copies instead of per-ray ones
+__global__ void ray_select_kernel(long long n, const long long* __restrict__ rid, const long long* __restrict__ row_ptr,
+                                  const RayInfo* __restrict__ info, long long* e0, RayInfo* out) {
+    const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const long long r = rid[k];
+    e0[k] = row_ptr[r];
+    out[k] = info[r];
+}
+__global__ void ray_gather_kernel(long long n, const long long* __restrict__ e0, const long long* __restrict__ off,
+                                  const int32_t* __restrict__ vid, const int16_t* __restrict__ off_q,
+                                  const int32_t* __restrict__ lam, int32_t* ovid, int16_t* ooff, int32_t* olam) {
+    const long long k = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (k >= n) return;
+    const int lane = threadIdx.x & 31;
+    const long long a = e0[k], o = off[k], len = off[k + 1] - off[k];
+    for (long long j = lane; j < len; j += 32) {
+        if (ovid) ovid[o + j] = vid[a + j];
+        if (ooff) ooff[o + j] = off_q[a + j];
+        if (olam) olam[o + j] = lam[a + j];
+    }
+}
+
 }  // namespace
 
 void launch_stage_flags(long long n_rays, const long long* row_ptr, const RayInfo* info, int32_t* flags,
@@ -988,6 +1012,18 @@ void launch_span_max(long long n, const int32_t* rays, const RayInfo* info, unsi
                      cudaStream_t s) {
     if (n == 0) return;
     span_max_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, rays, info, out);
+}
+
+void launch_ray_select(long long n, const long long* rid, const long long* row_ptr, const RayInfo* info, long long* e0,
+                       RayInfo* out, cudaStream_t s) {
+    if (n == 0) return;
+    ray_select_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, rid, row_ptr, info, e0, out);
+}
+
+void launch_ray_gather(long long n, const long long* e0, const long long* off, const int32_t* vid, const int16_t* off_q,
+                       const int32_t* lam, int32_t* ovid, int16_t* ooff, int32_t* olam, cudaStream_t s) {
+    if (n == 0) return;
+    ray_gather_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(n, e0, off, vid, off_q, lam, ovid, ooff, olam);
 }
 
 }  // namespace mrf

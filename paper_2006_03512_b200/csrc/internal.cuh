@@ -184,6 +184,12 @@ void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items,
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,
                       cudaStream_t s);
 void launch_compact(long long n, const int32_t* flags, const long long* pos, int32_t* out, cudaStream_t s);
+// mrf_export_rays: e0[k] = row_ptr[rid[k]], out[k] = info[rid[k]]; then the incidences of ray k
+// [e0[k], e0[k] + off[k+1] - off[k]) into the staging arrays at off[k] (null outputs skipped)
+void launch_ray_select(long long n, const long long* rid, const long long* row_ptr, const RayInfo* info, long long* e0,
+                       RayInfo* out, cudaStream_t s);
+void launch_ray_gather(long long n, const long long* e0, const long long* off, const int32_t* vid, const int16_t* off_q,
+                       const int32_t* lam, int32_t* ovid, int16_t* ooff, int32_t* olam, cudaStream_t s);
 // misc
 void launch_active_flags(long long V, const int32_t* vox_count, int32_t* flags, cudaStream_t s);
 void launch_span_max(long long n, const int32_t* rays, const RayInfo* info, unsigned long long* out,
@@ -259,8 +265,13 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
                          int n_warps_long, int math, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
+// tile_map (nullable): tile -> position among the tiles written (world > 1: the tiles some rank
+// touches, compacted for the all-reduce); nullptr = the tile itself
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
-                        const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad, cudaStream_t s);
+                        const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad,
+                        const int32_t* tile_map, cudaStream_t s);
+// T[tile_of[i] tile] = src[i-th compact tile] for i < n_tiles (16384 slots each)
+void launch_tile_scatter(long long n_tiles, const int32_t* tile_of, const long long* src, long long* T, cudaStream_t s);
 // keyframe averages (reading R22): per [bucket = frame * NT + tile][slot], D += signed small
 // probability of each message (fp64, D[0 .. n_slots)) and the packed counts n_pos + 2^32 n_neg
 // (int64, at D + n_slots); both zeroed by the caller (bp.cu tile_reduce_kernel<1>)

@@ -74,6 +74,7 @@ struct ProfEvent {
 
 struct mrf_ctx {
     int device = 0;
+    int sms = 148;  // multiprocessors of the ctx's device (grid sizing)
     GridDesc grid{};
     NoiseDesc noise{};
     long long V = 0;   // voxels (nx*ny*nz)
@@ -127,6 +128,7 @@ struct mrf_ctx {
     int k5_streams = 8;  // MRF_K5_STREAMS (1 = all classes on `stream`)
     cudaStream_t side[kMaxSide] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[kMaxSide] = {};
+    cudaEvent_t ev_mf[4] = {};  // matrix-free pipeline: walk done [2], K5 done [2] (per scratch set)
     std::string err;
     mrf_status sticky = MRF_OK;
 
@@ -160,6 +162,17 @@ struct mrf_ctx {
     DBuf<int2> bitems;
     long long n_runs = 0, n_bitems = 0;
     DBuf<long long> T, T_part;
+    // world > 1 (NCCL): the all-reduce covers only the tiles some rank touches:
+    // a touched-tile mask, ncclMax-reduced once per graph change, gives tile -> compact position;
+    // K6 writes its sums there, NCCL reduces n_act_tiles * 16384 slots in place, and a scatter
+    // puts them back into T
+    bool compact = false;
+    bool force_compact = false;  // MRF_COMPACT=1: the same compacted path at world == 1 (tests)
+    long long n_act_tiles = 0;
+    std::vector<int32_t> tile_nr;   // runs per tile (host copy, from build_tile_runs)
+    DBuf<int32_t> tile_map, tile_of;
+    DBuf<uint8_t> touched;
+    DBuf<long long> T_c;
     DBuf<float2> lutp;
     DBuf<float> depth_stage, marg;
     // frames added since the last fill: the walk (K3) of all of them runs as one launch when
@@ -549,12 +562,13 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     // dozen items per SM are needed for the dynamic schedule to even out the tiles' last chunks
     // (frames30: 8192 -> 24576 runs, 2.46 -> 2.39 ms; at 8 ranks 8192 stays best).
     if (!c->k6_item_fixed)
-        c->k6_item = (int)std::min<long long>(24576, std::max<long long>(8192, c->n_runs / (148 * 13)));
+        c->k6_item = (int)std::min<long long>(24576, std::max<long long>(8192, c->n_runs / ((long long)c->sms * 13)));
     // K6 work list, j-major: item j of every tile, then item j+1 ...  Runs land in a tile in
     // roughly ray order, so the items that run concurrently read nearby message ranges (L2 reuse).
     std::vector<int32_t> nr((size_t)NT);
     CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    c->tile_nr = nr;
     std::vector<int2> items;
     for (int j = 0;; ++j) {
         bool any = false;
@@ -578,6 +592,48 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     return MRF_OK;
 }
 
+// NCCL failures surface asynchronously (a peer lost, a timeout): poll after every collective
+mrf_status nccl_async_check(mrf_ctx* c) {
+    ncclResult_t ar = ncclSuccess;
+    NCK(ncclCommGetAsyncError(c->comm, &ar));
+    if (ar != ncclSuccess && ar != ncclInProgress)
+        return set_err(c, MRF_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+    return MRF_OK;
+}
+
+// world > 1 (NCCL): the tiles some rank touches, agreed by an ncclMax of the per-tile touched
+// flags (identical on every rank), and the maps tile -> compact position -> tile.  Once per graph
+// change; every rank calls it at the same point (prepare, from the same ABI call).
+mrf_status build_active_tiles(mrf_ctx* c) {
+    const long long NT = c->NT;
+    std::vector<uint8_t> h((size_t)NT, 0);
+    for (long long t = 0; t < NT && t < (long long)c->tile_nr.size(); ++t) h[(size_t)t] = c->tile_nr[(size_t)t] > 0;
+    CK(c->touched.ensure((size_t)NT, 0, c->stream));
+    if (c->world > 1) {
+        CK(cudaMemcpyAsync(c->touched.p, h.data(), (size_t)NT, cudaMemcpyHostToDevice, c->stream));
+        NCK(ncclAllReduce(c->touched.p, c->touched.p, (size_t)NT, ncclUint8, ncclMax, c->comm, c->stream));
+        CK(cudaMemcpyAsync(h.data(), c->touched.p, (size_t)NT, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        mrf_status sa = nccl_async_check(c);
+        if (sa != MRF_OK) return sa;
+    }
+    std::vector<int32_t> map((size_t)NT, -1), of;
+    for (long long t = 0; t < NT; ++t)
+        if (h[(size_t)t]) {
+            map[(size_t)t] = (int32_t)of.size();
+            of.push_back((int32_t)t);
+        }
+    c->n_act_tiles = (long long)of.size();
+    CK(c->tile_map.ensure((size_t)NT, 0, c->stream));
+    CK(c->tile_of.ensure((size_t)std::max<long long>(1, c->n_act_tiles), 0, c->stream));
+    CK(c->T_c.ensure((size_t)std::max<long long>(1, c->n_act_tiles) * kTileSlots, 0, c->stream));
+    CK(cudaMemcpyAsync(c->tile_map.p, map.data(), sizeof(int32_t) * NT, cudaMemcpyHostToDevice, c->stream));
+    if (c->n_act_tiles)
+        CK(cudaMemcpyAsync(c->tile_of.p, of.data(), sizeof(int32_t) * of.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return MRF_OK;
+}
+
 // Build the transpose used by K6, its work list and the K5 length classes (on graph change).
 mrf_status prepare(mrf_ctx* c) {
     if (!c->dirty) return MRF_OK;
@@ -589,6 +645,9 @@ mrf_status prepare(mrf_ctx* c) {
     } else {
         if ((st = build_tile_runs(c)) != MRF_OK) return st;
     }
+    c->compact = !c->k6_voxel && ((c->world > 1 && c->comm_mode == MRF_COMM_NCCL) ||
+                                  (c->world == 1 && c->force_compact && !c->kf_avg));
+    if (c->compact && (st = build_active_tiles(c)) != MRF_OK) return st;
     // K5 classes by ray length (stable compaction keeps pixel order inside a class)
     CK(c->flags.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
     CK(c->pos.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
@@ -645,7 +704,7 @@ mrf_status prepare(mrf_ctx* c) {
             if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
             const long long tile = 512;
             c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
-            c->n_warps_long = (int)std::min<long long>(n_long, 148LL * 16);
+            c->n_warps_long = (int)std::min<long long>(n_long, (long long)c->sms * 16);
             CK(c->long_scratch.ensure((size_t)(c->long_scratch_per_warp * c->n_warps_long), 0, c->stream));
         }
         c->dirty = false;
@@ -678,7 +737,7 @@ mrf_status prepare(mrf_ctx* c) {
         if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
         const long long tile = 512;
         c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
-        c->n_warps_long = (int)std::min<long long>(c->class_n[kl], 148LL * 16);
+        c->n_warps_long = (int)std::min<long long>(c->class_n[kl], (long long)c->sms * 16);
         CK(c->long_scratch.ensure((size_t)(c->long_scratch_per_warp * c->n_warps_long), 0, c->stream));
     }
     c->dirty = false;
@@ -698,7 +757,8 @@ mrf_status ensure_kf(mrf_ctx* c) {
     return MRF_OK;
 }
 
-mrf_status voxel_sums(mrf_ctx* c, long long* out) {
+// compact: write the touched tiles' sums in compact order (world > 1, see build_active_tiles)
+mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
     ProfScope ps(c, MRF_K_VOXEL_SUM);
     if (c->kf_avg) {  // per-(frame, slot) averages, then T = sum over frames (reading R22)
         mrf_status st;
@@ -712,14 +772,14 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out) {
         mf_dbg(c, "kf sums");
         return MRF_OK;
     }
-    CK(cudaMemsetAsync(out, 0, sizeof(long long) * c->VI, c->stream));
+    CK(cudaMemsetAsync(out, 0, sizeof(long long) * (compact ? c->n_act_tiles * kTileSlots : c->VI), c->stream));
     if (c->k6_voxel) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
     } else {
         launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
                            c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->k6_pad,
-                           c->stream);
+                           compact ? c->tile_map.p : nullptr, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -740,8 +800,8 @@ mrf_status ray_messages(mrf_ctx* c) {
         // pipeline: walks on side[0], K5 on side[1]; walk i waits for the K5 of chunk i - 2 (same
         // scratch set), K5 i waits for walk i; the ctx stream joins on the last K5
         cudaStream_t A = pipe ? c->side[0] : c->stream, B = pipe ? c->side[1] : c->stream;
-        cudaEvent_t* ev_walk = c->ev_join;      // [2]
-        cudaEvent_t* ev_k5 = c->ev_join + 2;    // [2]
+        cudaEvent_t* ev_walk = c->ev_mf;      // [2]
+        cudaEvent_t* ev_k5 = c->ev_mf + 2;    // [2]
         if (pipe) {
             CK(cudaEventRecord(c->ev_fork, c->stream));
             CK(cudaStreamWaitEvent(A, c->ev_fork, 0));
@@ -815,20 +875,46 @@ mrf_status ray_messages(mrf_ctx* c) {
     return MRF_OK;
 }
 
+// T = sum over ranks of the K6 partials.  compact: in place over the touched tiles (T_c), then
+// scattered into T; otherwise (per-voxel K6 ablation) over every belief slot, T_part -> T.
 mrf_status allreduce_T(mrf_ctx* c) {
     ProfScope ps(c, MRF_K_ALLREDUCE);
-    NCK(ncclAllReduce(c->T_part.p, c->T.p, (size_t)c->VI, ncclInt64, ncclSum, c->comm, c->stream));
-    c->prof_launch[MRF_K_ALLREDUCE] += 1;
-    return MRF_OK;
+    if (c->compact) {
+        if (c->n_act_tiles) {
+            if (c->world > 1) {
+                NCK(ncclAllReduce(c->T_c.p, c->T_c.p, (size_t)(c->n_act_tiles * kTileSlots), ncclInt64, ncclSum,
+                                  c->comm, c->stream));
+                c->prof_launch[MRF_K_ALLREDUCE] += 1;
+            }
+            launch_tile_scatter(c->n_act_tiles, c->tile_of.p, c->T_c.p, c->T.p, c->stream);
+            CK_LAUNCH(MRF_K_ALLREDUCE, 1);
+        }
+        if (c->world == 1) return MRF_OK;
+    } else {
+        NCK(ncclAllReduce(c->T_part.p, c->T.p, (size_t)c->VI, ncclInt64, ncclSum, c->comm, c->stream));
+        c->prof_launch[MRF_K_ALLREDUCE] += 1;
+    }
+    return nccl_async_check(c);
+}
+
+// K6 over the current messages, then (world > 1) the all-reduce: T of every rank.
+mrf_status reduce_T(mrf_ctx* c) {
+    mrf_status st;
+    if (c->compact) {
+        if ((st = voxel_sums(c, c->T_c.p, true)) != MRF_OK) return st;
+        return allreduce_T(c);
+    }
+    if (c->world == 1) return voxel_sums(c, c->T.p);
+    if ((st = voxel_sums(c, c->T_part.p)) != MRF_OK) return st;
+    return allreduce_T(c);
 }
 
 // Rebuild T from the current messages (all ranks).
 mrf_status rebuild_T(mrf_ctx* c) {
     mrf_status st;
     if ((st = prepare(c)) != MRF_OK) return st;
-    if (c->world == 1) return voxel_sums(c, c->T.p);
+    if (c->world == 1 || c->comm_mode == MRF_COMM_NCCL) return reduce_T(c);
     if ((st = voxel_sums(c, c->T_part.p)) != MRF_OK) return st;
-    if (c->comm_mode == MRF_COMM_NCCL) return allreduce_T(c);
     return MRF_OK;  // external mode: caller reduces (mrf_bp_partial / mrf_bp_finish)
 }
 
@@ -937,6 +1023,10 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
 
     mrf_ctx* c = new mrf_ctx();
     cudaGetDevice(&c->device);
+    if (cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, c->device) != cudaSuccess || c->sms <= 0) {
+        cudaGetLastError();
+        c->sms = 148;
+    }
     c->grid = {dims[0], dims[1], dims[2], (dims[0] + 31) / 32, (dims[1] + 31) / 32, (dims[2] + 15) / 16,
                resolution_m, origin_m[0], origin_m[1], origin_m[2]};
     c->NT = (long long)c->grid.ntx * c->grid.nty * c->grid.ntz;
@@ -951,6 +1041,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* kd = getenv("MRF_K6_DYNAMIC")) c->k6_dynamic = atoi(kd) != 0;
     if (const char* kp = getenv("MRF_K6_PAD")) c->k6_pad = atoi(kp) != 0;
     if (const char* kl = getenv("MRF_K6_LPT")) c->k6_lpt = atoi(kl) != 0;
+    if (const char* kc = getenv("MRF_COMPACT")) c->force_compact = atoi(kc) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
@@ -975,6 +1066,8 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* ks = getenv("MRF_K5_STREAMS")) c->k5_streams = std::min(std::max(atoi(ks), 1), mrf_ctx::kMaxSide);
     if (c->k5_streams > 1) {
         bool ok = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) == cudaSuccess;
+        for (int i = 0; ok && i < 4; ++i)
+            ok = cudaEventCreateWithFlags(&c->ev_mf[i], cudaEventDisableTiming) == cudaSuccess;
         for (int i = 0; ok && i < c->k5_streams; ++i)
             ok = cudaStreamCreateWithFlags(&c->side[i], cudaStreamNonBlocking) == cudaSuccess &&
                  cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) == cudaSuccess;
@@ -1010,7 +1103,10 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         std::vector<float2> h((size_t)nz * (no - 1));
         for (int i = 0; i < nz; ++i) {
             const float* row = noise->log_nu + (size_t)i * no;
-            for (int j = 0; j < no - 1; ++j) h[(size_t)i * (no - 1) + j] = make_float2(row[j], row[j + 1]);
+            // entries below -1e30 (e.g. -FLT_MAX standing for log 0) are raised to -1e30: K5 scales
+            // log nu by log2(e), which would overflow them to -inf (and -inf - -inf = NaN)
+            for (int j = 0; j < no - 1; ++j)
+                h[(size_t)i * (no - 1) + j] = make_float2(std::max(row[j], -1e30f), std::max(row[j + 1], -1e30f));
         }
         CK(c->lutp.ensure(h.size(), 0, c->stream));
         CK(cudaMemcpyAsync(c->lutp.p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, c->stream));
@@ -1058,6 +1154,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->scan_scratch.release(); c->counters.release(); c->long_scratch.release();
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
+    c->tile_map.release(); c->tile_of.release(); c->touched.release(); c->T_c.release();
     c->class_all.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -1067,6 +1164,8 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
         if (c->ev_join[i]) cudaEventDestroy(c->ev_join[i]);
     }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    for (int i = 0; i < 4; ++i)
+        if (c->ev_mf[i]) cudaEventDestroy(c->ev_mf[i]);
     delete c;
     return MRF_OK;
 }
@@ -1256,12 +1355,7 @@ mrf_status mrf_bp_iterate(mrf_ctx* ctx, int32_t n) {
     if ((st = prepare(c)) != MRF_OK) return st;
     for (int it = 0; it < n; ++it) {
         if ((st = ray_messages(c)) != MRF_OK) return st;
-        if (c->world == 1) {
-            if ((st = voxel_sums(c, c->T.p)) != MRF_OK) return st;
-        } else {
-            if ((st = voxel_sums(c, c->T_part.p)) != MRF_OK) return st;
-            if ((st = allreduce_T(c)) != MRF_OK) return st;
-        }
+        if ((st = reduce_T(c)) != MRF_OK) return st;
     }
     return MRF_OK;
 }
@@ -1450,29 +1544,51 @@ mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const 
             return set_err(c, MRF_ERR_INVALID_ARG, "pixel not owned by this rank");
         rid[(size_t)k] = fr.ray_base + (v / c->world) * fr.W + u;
     }
-    // per selected ray: padded start and length
+    // per selected ray: padded start and record (one gather kernel, two copies)
     std::vector<long long> e0((size_t)n);
     std::vector<RayInfo> info((size_t)n);
-    for (long long k = 0; k < n; ++k) {
-        CK(cudaMemcpyAsync(&e0[(size_t)k], c->row_ptr.p + rid[(size_t)k], sizeof(long long), cudaMemcpyDeviceToHost,
-                           c->stream));
-        CK(cudaMemcpyAsync(&info[(size_t)k], c->ray_z.p + rid[(size_t)k], sizeof(RayInfo), cudaMemcpyDeviceToHost,
-                           c->stream));
+    DBuf<long long> d_sel;   // rid [n] | e0 [n] | off [n + 1]
+    DBuf<RayInfo> d_info;
+    struct Free {
+        DBuf<long long>& a;
+        DBuf<RayInfo>& b;
+        ~Free() { a.release(); b.release(); }
+    } free_{d_sel, d_info};
+    CK(d_sel.ensure((size_t)(3 * n + 1), 0, c->stream));
+    CK(d_info.ensure((size_t)std::max<long long>(n, 1), 0, c->stream));
+    if (n) {
+        CK(cudaMemcpyAsync(d_sel.p, rid.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, c->stream));
+        launch_ray_select(n, d_sel.p, c->row_ptr.p, c->ray_z.p, d_sel.p + n, d_info.p, c->stream);
+        CK_LAUNCH(MRF_K_SCAN, 1);
+        CK(cudaMemcpyAsync(e0.data(), d_sel.p + n, sizeof(long long) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(info.data(), d_info.p, sizeof(RayInfo) * n, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
     }
-    CK(cudaStreamSynchronize(c->stream));
     std::vector<long long> off((size_t)n + 1, 0);
     for (long long k = 0; k < n; ++k) off[(size_t)k + 1] = off[(size_t)k] + info[(size_t)k].n;
     if (row_ptr) std::copy(off.begin(), off.end(), row_ptr);
     if (off[(size_t)n] > cap && (vid || off_q || lambda)) return set_err(c, MRF_ERR_CAPACITY, "rays exceed cap");
-    for (long long k = 0; k < n; ++k) {
-        const int len = info[(size_t)k].n;
-        if (!len) continue;
-        const long long a = e0[(size_t)k], o = off[(size_t)k];
-        if (vid) CK(cudaMemcpyAsync(vid + o, c->vid.p + a, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, c->stream));
-        if (off_q)
-            CK(cudaMemcpyAsync(off_q + o, c->off_q.p + a, sizeof(int16_t) * len, cudaMemcpyDeviceToHost, c->stream));
+    const long long tot_e = off[(size_t)n];
+    if (tot_e && (vid || off_q || lambda)) {
+        // the incidences, gathered into contiguous staging arrays on the device
+        DBuf<int32_t> s32;  // vid [tot] | lam [tot]
+        DBuf<int16_t> s16;
+        struct Free2 {
+            DBuf<int32_t>& a;
+            DBuf<int16_t>& b;
+            ~Free2() { a.release(); b.release(); }
+        } free2_{s32, s16};
+        CK(s32.ensure((size_t)(2 * tot_e), 0, c->stream));
+        CK(s16.ensure((size_t)tot_e, 0, c->stream));
+        CK(cudaMemcpyAsync(d_sel.p + 2 * n, off.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+        launch_ray_gather(n, d_sel.p + n, d_sel.p + 2 * n, c->vid.p, c->off_q.p, c->lam.p, vid ? s32.p : nullptr,
+                          off_q ? s16.p : nullptr, lambda ? s32.p + tot_e : nullptr, c->stream);
+        CK_LAUNCH(MRF_K_SCAN, 1);
+        if (vid) CK(cudaMemcpyAsync(vid, s32.p, sizeof(int32_t) * tot_e, cudaMemcpyDeviceToHost, c->stream));
+        if (off_q) CK(cudaMemcpyAsync(off_q, s16.p, sizeof(int16_t) * tot_e, cudaMemcpyDeviceToHost, c->stream));
         if (lambda)  // raw int32 q first, converted below
-            CK(cudaMemcpyAsync(lambda + o, c->lam.p + a, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(lambda, s32.p + tot_e, sizeof(int32_t) * tot_e, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));  // before the staging buffers are freed
     }
     CK(cudaStreamSynchronize(c->stream));
     const long long tot = off[(size_t)n];
