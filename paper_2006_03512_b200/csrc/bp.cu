@@ -77,9 +77,6 @@ __device__ __forceinline__ float lg2(float x) {
 // -- no scaling multiply per MUFU op; the nats of the inputs (T, q, L0: exact integers and one
 // constant; log nu) are converted where they enter (folded into existing FMAs, one multiply for
 // l) and lambda is converted back to nats before quantisation.  0: natural-log units throughout.
-#ifndef MRF_K5_LOG2
-#define MRF_K5_LOG2 1
-#endif
 constexpr float kWS = MRF_K5_LOG2 ? kLog2e : 1.f;  // nats -> working units
 constexpr float kWInv = MRF_K5_LOG2 ? kLn2 : 1.f;  // working units -> nats
 __device__ __forceinline__ float log1pn(float y) {
@@ -167,9 +164,10 @@ __device__ __forceinline__ void elem_terms(long long t, int q, float lnu, float 
 #endif
     const float y = expn(-fabsf(c));
     const float L1 = M >= 2 ? log1pf_abs(y) : log1pn(y);  // ln(1 + e^-|c|)
+    // lnu arrives in working units (the fill stores log nu * kLnuScale, internal.cuh)
     la = selp(ok, -(fmaxf(c, 0.f) + L1), 0.f);
-    w = selp(ok, fmaf(lnu, kWS, -(fmaxf(-c, 0.f) + L1)), kNeg);
-    l = selp(ok, lnu * kWS, kNeg);
+    w = selp(ok, lnu - (fmaxf(-c, 0.f) + L1), kNeg);
+    l = selp(ok, lnu, kNeg);
 }
 
 // Chunk composite of the suffix maps R -> e^{la} R + e^{w} (first applied last):
@@ -257,9 +255,9 @@ __device__ __forceinline__ float lambda_n(float Q, float l, float R) {
     return (m1 - m2) + (log1pn(expn(-fabsf(Q - l))) - log1pn(expn(-fabsf(Q - R))));
 }
 
-__device__ __forceinline__ int32_t quantise(float lam) {  // lam in working units
-    lam = fminf(fmaxf(lam * kWInv, -kLambdaClip), kLambdaClip);
-    return __float2int_rn(lam * kQScale);  // saturates at +2^31-1 for +256
+__device__ __forceinline__ int32_t quantise(float lam) {  // lam in working units -> round(clip(nats) 2^23)
+    constexpr float kS = kWInv * kQScale, kC = kLambdaClip * kQScale;
+    return __float2int_rn(fminf(fmaxf(lam * kS, -kC), kC));  // saturates at +2^31-1 for +256
 }
 
 // ---------------------------------------------------------------- K5: class kernels

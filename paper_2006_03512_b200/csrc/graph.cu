@@ -386,16 +386,28 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long l
     *reinterpret_cast<uint4*>(off_q + e_chunk) = make_uint4(pk(o[0], o[1]), pk(o[2], o[3]), pk(o[4], o[5]), pk(o[6], o[7]));
 }
 
+// Resident CTAs of 128 threads per SM: 6 (<= 80 registers) for the plain walk; 5 (<= 96) when it
+// also builds the tile runs (RUNS), whose state spilled at 80 (frames30: fill 10.43 ms at 6,
+// 10.02 ms at 5 per 30-frame step; without runs 8.1 ms at 6).
+#ifndef MRF_FILL_MIN_BLOCKS
+#define MRF_FILL_MIN_BLOCKS 6
+#endif
+#ifndef MRF_FILL_MIN_BLOCKS_RUNS
+#define MRF_FILL_MIN_BLOCKS_RUNS 5
+#endif
 // One launch fills every frame added since the last fill (frames[k] owns the CTAs
 // [cta0[k], cta0[k+1])): one wave-quantisation tail per batch instead of per frame.
-template <bool SPARSE>
-__global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc* __restrict__ frames,
+template <bool SPARSE, bool RUNS>
+__global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS : MRF_FILL_MIN_BLOCKS) dda_fill_kernel(const FrameDesc* __restrict__ frames,
                                                        const int* __restrict__ cta0, int n_frames, GridDesc g,
                                                        NoiseDesc n, const float* __restrict__ depth_all,
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
                                                        int16_t* off_q, int32_t* tile_runs, RayInfo* ray_z,
-                                                       unsigned long long* counters, MsgParams mp, float* lnu) {
+                                                       unsigned long long* counters, MsgParams mp, float* lnu,
+                                                       RunSink sink) {
     __shared__ int s_vid[kFillThreads][8];
+    __shared__ Run s_done[RUNS ? kFillThreads : 1];  // a run that ended at this step, per thread
+    __shared__ int s_done_key[RUNS ? kFillThreads : 1];
     __shared__ short s_off[kFillThreads][8];
     __shared__ FrameDesc f;
     __shared__ int s_fi;
@@ -418,7 +430,13 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
     bool alive = false;
     Segment sg;
     Walker w;
-    int run_tile = -1, run_n = 0, run_prev = 0;  // current tile run (K4b count)
+    // current tile run (K4b: counted per bucket, and emitted to the sink when it ends): tile, length,
+    // in-tile slots of its first and last element, first incidence slot, x / y step masks; the
+    // step signs are the ray's (a DDA walk is monotone on every axis)
+    int run_tile = -1, run_n = 0, run_prev = 0, run_slot0 = 0;
+    unsigned run_e = 0, run_mx = 0, run_my = 0, run_neg = 0;
+    unsigned long long sink_base = 0;  // the warp's block of run slots (RunSink::emit)
+    int sink_left = 0;
     const int bucket0 = f.index * f.bucket_stride;
     long long e = 0, e_cap = 0;
     int iz = 0;
@@ -431,6 +449,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             w.start(sg);
             alive = w.inside(g);
             e_cap = row_ptr[f.ray_base + i + 1];  // the segment K1 sized from its bound
+            run_neg = ((unsigned)(w.s0 < 0) | ((unsigned)(w.s1 < 0) << 1) | ((unsigned)(w.s2 < 0) << 2)) << 20;
             if (MRF_FILL_LNU) {  // the depth coordinate of the table (K1)
                 iz = ray_z[f.ray_base + i].iz;
                 wz = ray_z[f.ray_base + i].wz;
@@ -442,6 +461,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
     for (;;) {
         const unsigned am = __ballot_sync(kFull, alive);
         if (am == 0) break;
+        bool has_done = false;  // a run ended at this step (to the sink, below, with all lanes)
         if (alive) {
             const bool keep = !SPARSE || cell_in_map(g, w.c0, w.c1, w.c2);
             bool start = false;
@@ -458,14 +478,33 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 sv[e & 7] = vx;
                 so[e & 7] = (short)q;
                 if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, iz, wz);
-                ++e;
-                // K4b count: runs per tile (a warp's concurrent run starts in one tile share an atomic)
+                // K4b: runs per tile (a warp's concurrent run starts in one tile share an atomic);
+                // a run that ends here goes to the sink
                 b = vx >> kTileShift;
                 const int l = vx & (kTileSlots - 1);
+                const int ad = abs(l - run_prev);
                 start = !run_extends(b, l, run_tile, run_n, run_prev);
-                run_n = start ? 1 : run_n + 1;
-                run_tile = b;
+                if (start) {
+                    if (RUNS && run_tile >= 0) {  // the run that ends here waits in shared memory
+                        s_done[threadIdx.x] = Run{run_e, (unsigned)run_slot0 | ((unsigned)(run_n - 1) << 14) | run_neg,
+                                                  run_mx, run_my};
+                        s_done_key[threadIdx.x] = bucket0 + run_tile;
+                        has_done = true;
+                    }
+                    run_tile = b;
+                    run_n = 1;
+                    run_slot0 = l;
+                    run_e = (unsigned)e;
+                    run_mx = run_my = 0;
+                } else {
+                    if (RUNS) {
+                        run_mx |= (unsigned)(ad == 1) << (run_n - 1);
+                        run_my |= (unsigned)(ad == 32) << (run_n - 1);
+                    }
+                    ++run_n;
+                }
                 run_prev = l;
+                ++e;
                 if (last) {
                     alive = false;
                 } else {
@@ -482,6 +521,7 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
                 const unsigned peers = __match_any_sync(sm, key);
                 if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[key], __popc(peers));
             }
+
             // cannot happen (K1's count); never write past the segment.  In a sparse map only a
             // cell that would be emitted counts.
             if (alive && e >= e_cap && (!SPARSE || cell_in_map(g, w.c0, w.c1, w.c2))) {
@@ -490,6 +530,12 @@ __global__ void __launch_bounds__(kFillThreads) dda_fill_kernel(const FrameDesc*
             }
             if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so, lnu, mp, iz, wz);  // partial tail
         }
+        if (RUNS) sink.emit(has_done, s_done[threadIdx.x], s_done_key[threadIdx.x], lane, sink_base, sink_left);
+    }
+    if (RUNS) {  // every ray's last run
+        const bool last_run = run_tile >= 0;
+        sink.emit(last_run, Run{run_e, (unsigned)run_slot0 | ((unsigned)(run_n - 1) << 14) | run_neg, run_mx, run_my},
+                  bucket0 + run_tile, lane, sink_base, sink_left);
     }
     int ne = 0;
     if (i < n_pix) {
@@ -750,6 +796,54 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
     }
 }
 
+// Sparse bricks, keyframes added after the graph was used (reading R24): every ray is walked again
+// against the grown allocation; its old incidences are a subsequence of the new ones (cells of
+// newly allocated bricks are inserted, nothing is removed), in the same order along the ray.
+// Thread per old ray: each new incidence takes the message of the same voxel in the old list,
+// or 0 (a new incidence).
+__global__ void __launch_bounds__(256) lambda_merge_kernel(long long n_rays, const long long* __restrict__ rp_old,
+                                                           const RayInfo* __restrict__ ri_old,
+                                                           const int32_t* __restrict__ vid_old,
+                                                           const int32_t* __restrict__ lam_old,
+                                                           const long long* __restrict__ rp_new,
+                                                           const RayInfo* __restrict__ ri_new,
+                                                           const int32_t* __restrict__ vid_new, int32_t* lam_new,
+                                                           unsigned long long* lost) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rays) return;
+    const long long eo = rp_old[r], en = rp_new[r];
+    const int no = ri_old[r].n, nn = ri_new[r].n;
+    int j = 0;
+    for (int k = 0; k < nn; ++k) {
+        const int v = vid_new[en + k];
+        int q = 0;
+        if (j < no && vid_old[eo + j] == v) q = lam_old[eo + j++];
+        lam_new[en + k] = q;
+    }
+    if (j < no) atomicAdd(lost, (unsigned long long)(no - j));  // cannot happen (allocation only grows)
+}
+
+// The runs the DDA fills emitted (unsorted, with their bucket keys) placed by bucket: the
+// tile-run transpose without re-reading vid.  Thread per run; a warp's runs of one bucket share
+// one cursor atomic.
+__global__ void __launch_bounds__(256) run_bucket_kernel(long long n, const Run* __restrict__ src,
+                                                         const int32_t* __restrict__ keys,
+                                                         const long long* __restrict__ tile_ptr, int32_t* cursor,
+                                                         Run* dst) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int key = i < n ? __ldg(keys + i) : -1;  // -1: an unused slot of a warp's block
+    const bool act = key >= 0;
+    const unsigned am = __ballot_sync(kFull, act);
+    if (!act) return;
+    const unsigned peers = __match_any_sync(am, key);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    dst[tile_ptr[key] + base + __popc(peers & ((1u << lane) - 1u))] = src[i];
+}
+
 __global__ void item_fill_kernel(long long V, const int32_t* __restrict__ n_items,
                                  const long long* __restrict__ item_ptr, int2* items) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -927,14 +1021,18 @@ void launch_brick_alloc(const FrameDesc& f, const GridDesc& g, const NoiseDesc& 
 void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, long long r0,
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
-                     int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s) {
+                     int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters,
+                     const RunSink& sink, cudaStream_t s) {
     if (n_ctas > 0) {
-        if (g.bmask)
-            dda_fill_kernel<true><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr,
-                                                                  vid, off_q, tile_runs, ray_z, counters, mp, lnu);
-        else
-            dda_fill_kernel<false><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr,
-                                                                   vid, off_q, tile_runs, ray_z, counters, mp, lnu);
+#define MRF_FILL_LAUNCH(SP, RU)                                                                                     \
+    dda_fill_kernel<SP, RU><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, \
+                                                            off_q, tile_runs, ray_z, counters, mp, lnu, sink)
+        if (g.bmask) {
+            if (sink.runs) MRF_FILL_LAUNCH(true, true); else MRF_FILL_LAUNCH(true, false);
+        } else {
+            if (sink.runs) MRF_FILL_LAUNCH(false, true); else MRF_FILL_LAUNCH(false, false);
+        }
+#undef MRF_FILL_LAUNCH
     }
     if (!MRF_FILL_LNU && n_rays > 0)
         lnu_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(r0, n_rays, mp, row_ptr, ray_z, off_q, lnu);
@@ -1024,6 +1122,20 @@ void launch_ray_gather(long long n, const long long* e0, const long long* off, c
                        const int32_t* lam, int32_t* ovid, int16_t* ooff, int32_t* olam, cudaStream_t s) {
     if (n == 0) return;
     ray_gather_kernel<<<blocks_for(n * 32, 256), 256, 0, s>>>(n, e0, off, vid, off_q, lam, ovid, ooff, olam);
+}
+
+void launch_run_bucket(long long n, const Run* src, const int32_t* keys, const long long* tile_ptr, int32_t* cursor,
+                       Run* dst, cudaStream_t s) {
+    if (n == 0) return;
+    run_bucket_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, src, keys, tile_ptr, cursor, dst);
+}
+
+void launch_lambda_merge(long long n_rays, const long long* rp_old, const RayInfo* ri_old, const int32_t* vid_old,
+                         const int32_t* lam_old, const long long* rp_new, const RayInfo* ri_new, const int32_t* vid_new,
+                         int32_t* lam_new, unsigned long long* lost, cudaStream_t s) {
+    if (n_rays == 0) return;
+    lambda_merge_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, rp_old, ri_old, vid_old, lam_old, rp_new,
+                                                                ri_new, vid_new, lam_new, lost);
 }
 
 }  // namespace mrf

@@ -71,6 +71,44 @@ struct Run {
     unsigned mx, my;
 };
 
+// Where the DDA fill puts the tile runs it builds (K4b without a vid re-read): appended, unsorted,
+// to runs[0 .. cap) with their bucket keys.  Each warp reserves blocks of kSinkBlock slots from a
+// global cursor (*count, the slots reserved so far) and fills them in order; the unused tail of a
+// block keeps key -1 (the keys are preset to -1) and is skipped by the bucket pass.  Slots at or
+// past cap are dropped and the caller falls back to the vid re-read.  runs == nullptr: no emission.
+constexpr int kSinkBlock = 128;
+struct RunSink {
+    Run* runs;
+    int32_t* keys;
+    unsigned long long* count;
+    long long cap;
+#ifdef __CUDACC__
+    // Called by all 32 lanes (wbase / wleft: the warp's current block, warp-uniform registers);
+    // lanes with `has` set append (run, key).
+    __device__ __forceinline__ void emit(bool has, const Run& r, int key, int lane, unsigned long long& wbase,
+                                         int& wleft) const {
+        const unsigned em = __ballot_sync(0xffffffffu, has);
+        if (!em) return;
+        const int k = __popc(em);
+        if (k > wleft) {  // a new block (the rest of the old one stays unused, key -1)
+            unsigned long long b = 0;
+            if (lane == 0) b = atomicAdd(count, (unsigned long long)kSinkBlock);
+            wbase = __shfl_sync(0xffffffffu, b, 0);
+            wleft = kSinkBlock;
+        }
+        if (has) {
+            const long long pos = (long long)wbase + __popc(em & ((1u << lane) - 1u));
+            if (pos < cap) {
+                runs[pos] = r;
+                keys[pos] = key;
+            }
+        }
+        wbase += (unsigned long long)k;
+        wleft -= k;
+    }
+#endif
+};
+
 struct NoiseDesc {
     double z_lo, z_hi, off_lo, off_hi, margin_min, margin_k, c0, c1, c2;
     int n_z, n_off;
@@ -120,7 +158,13 @@ struct MsgParams {
 #ifndef MRF_FILL_LNU
 #define MRF_FILL_LNU 1
 #endif
-// Evaluated once per incidence by the DDA fill; K5 reads the result.
+// Evaluated once per incidence by the DDA fill; K5 reads the result, stored in K5's working units:
+// MRF_K5_LOG2 = 1 (default) carries every log-quantity of K5 in base 2 (bp.cu), so the fill stores
+// log2 nu = ln nu * log2(e) and K5 uses it without a scaling multiply.
+#ifndef MRF_K5_LOG2
+#define MRF_K5_LOG2 1
+#endif
+constexpr float kLnuScale = MRF_K5_LOG2 ? 1.4426950408889634f : 1.f;
 // Split in two so that a caller can issue the table loads one step before it needs them.
 struct LutFetch {
     float wo;
@@ -136,7 +180,7 @@ __device__ __forceinline__ LutFetch lut_fetch(const MsgParams& mp, int iz, int o
 __device__ __forceinline__ float lut_finish(const LutFetch& f, float wz) {
     const float ra = fmaf(f.wo, f.ta.y - f.ta.x, f.ta.x);
     const float rb = fmaf(f.wo, f.tb.y - f.tb.x, f.tb.x);
-    return fmaf(wz, rb - ra, ra);
+    return fmaf(wz, rb - ra, ra) * kLnuScale;
 }
 
 // ---- launchers (all asynchronous on `s`)
@@ -157,7 +201,8 @@ constexpr int kFillThreads = 128;
 void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, long long r0,
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
-                     int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters, cudaStream_t s);
+                     int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters,
+                     const RunSink& sink, cudaStream_t s);
 // K9 §III.D evaluation of one frame against T: cls per pixel (-1 invalid, 0/1), counts[0..1] +=
 // (valid, accurate) (zeroed by the caller)
 void launch_eval(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, const long long* T,
@@ -179,6 +224,15 @@ void launch_transpose_fill(long long n_rays, const long long* row_ptr, const Ray
 // tile-run transpose (K4b): runs per tile, then the run list grouped by tile
 void launch_run_fill(long long n_rays, const long long* row_ptr, const RayInfo* info, const int32_t* vid,
                      const long long* tile_ptr, int32_t* cursor, int bucket_stride, Run* runs, cudaStream_t s);
+// sparse bricks, re-walk after new keyframes (reading R24): lam_new of old ray r's incidences from
+// its old list (same voxel -> its message, else 0); *lost += old incidences not found (never)
+void launch_lambda_merge(long long n_rays, const long long* rp_old, const RayInfo* ri_old, const int32_t* vid_old,
+                         const int32_t* lam_old, const long long* rp_new, const RayInfo* ri_new, const int32_t* vid_new,
+                         int32_t* lam_new, unsigned long long* lost, cudaStream_t s);
+// the runs of a RunSink placed by bucket key: dst[tile_ptr[key] + cursor[key]++] (cursor zeroed by
+// the caller)
+void launch_run_bucket(long long n, const Run* src, const int32_t* keys, const long long* tile_ptr, int32_t* cursor,
+                       Run* dst, cudaStream_t s);
 // K6 work list: n_items[i] = ceil(count[i] / chunk); items (i, j) from item_ptr
 void launch_item_counts(long long V, const int32_t* vox_count, int32_t* n_items, int chunk, cudaStream_t s);
 void launch_item_fill(long long V, const int32_t* n_items, const long long* item_ptr, int2* items,

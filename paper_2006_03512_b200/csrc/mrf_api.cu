@@ -109,6 +109,14 @@ struct mrf_ctx {
     int brick = 0;  // cells per brick edge, 0 = dense
     DBuf<uint8_t> bmask;
     long long n_brick_slots = 0;
+    // keyframes added after the graph was used (reading R24): every filled frame (depth kept) is
+    // walked again against the grown allocation; the old layout is kept until the messages moved
+    std::vector<FrameDesc> sp_frames;
+    bool sp_rebuild = false;
+    DBuf<long long> rp_old;
+    DBuf<RayInfo> ri_old;
+    DBuf<int32_t> vid_old, lam_old;
+    long long sp_R_old = 0;
     DBuf<int32_t> qbar;           // [frame][VI] quantised average log-odds
     DBuf<double> kf_sums;          // [frame][VI] fp64 D, then [frame][VI] int64 packed counts
     long long kf_frames_alloc = 0;
@@ -159,6 +167,16 @@ struct mrf_ctx {
     DBuf<int32_t> tile_runs, tile_cursor;
     DBuf<long long> tile_ptr;
     DBuf<Run> runs;
+    // tile runs as the DDA fills build them (unsorted, with bucket keys): the transpose is then a
+    // bucket pass over them (run_bucket) instead of a vid re-read (run_fill).  runs_ok: every run
+    // since the last reset reached the sink (its capacity is sized from run_ratio runs per new
+    // slot; an overflow falls back to run_fill and raises run_ratio).  MRF_RUN_FILL=1: always
+    // run_fill (ablation).
+    DBuf<Run> runs_all;
+    DBuf<int32_t> run_keys;
+    long long runs_emitted = 0, runs_cap = 0;
+    bool runs_ok = true, run_fill_forced = false;
+    double run_ratio = 0.125;
     DBuf<int2> bitems;
     long long n_runs = 0, n_bitems = 0;
     DBuf<long long> T, T_part;
@@ -363,6 +381,33 @@ mrf_status mf_rechunk(mrf_ctx* c) {
     return MRF_OK;
 }
 
+// The sink of the next fill over new_slots incidence slots (capacity from run_ratio; see runs_ok).
+mrf_status run_sink(mrf_ctx* c, long long new_slots, RunSink& sink) {
+    sink = RunSink{nullptr, nullptr, nullptr, 0};
+    if (c->run_fill_forced || !c->runs_ok) return MRF_OK;
+    const long long need = c->runs_emitted + (long long)std::ceil((double)new_slots * c->run_ratio) + 65536;
+    if (need > c->runs_cap) {
+        CK(c->runs_all.ensure((size_t)need, (size_t)std::min(c->runs_emitted, c->runs_cap), c->stream));
+        CK(c->run_keys.ensure((size_t)need, (size_t)std::min(c->runs_emitted, c->runs_cap), c->stream));
+        c->runs_cap = (long long)std::min(c->runs_all.cap, c->run_keys.cap);
+    }
+    // unused slots of the warps' blocks keep key -1
+    CK(cudaMemsetAsync(c->run_keys.p + c->runs_emitted, 0xff, sizeof(int32_t) * (size_t)(c->runs_cap - c->runs_emitted),
+                       c->stream));
+    sink = RunSink{c->runs_all.p, c->run_keys.p, c->counters.p + 16, c->runs_cap};
+    return MRF_OK;
+}
+
+// After a fill (counters read back): how many runs the sink took; an overflow disables it until
+// the next reset (the transpose falls back to run_fill) and raises run_ratio for the next time.
+void run_sink_done(mrf_ctx* c, long long emitted_total, long long new_slots) {
+    if (c->run_fill_forced || !c->runs_ok) return;
+    const long long added = emitted_total - c->runs_emitted;
+    if (new_slots > 0) c->run_ratio = std::max(c->run_ratio, 1.25 * (double)added / (double)new_slots);
+    if (emitted_total > c->runs_cap) c->runs_ok = false;
+    c->runs_emitted = emitted_total;
+}
+
 // Walk frames [f0, f1) of one chunk (the DDA fill + log nu) into the scratch, which stands for
 // the incidence slots [e0, ...) of chunk `ch` (pointers shifted by e0).  count: also count the
 // tile runs and the incidences (first walk of new frames only).
@@ -386,10 +431,21 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
     CK(cudaMemcpyAsync(dc, cta0.data(), sizeof(int) * cta0.size(), cudaMemcpyHostToDevice, st));
     const long long r0 = c->mf_frames[f0].ray_base;
     const long long r1 = f1 < (int)c->mf_frames.size() ? c->mf_frames[f1].ray_base : c->R;
+    RunSink sink{nullptr, nullptr, nullptr, 0};
+    if (count) {  // the first walk of new frames builds their tile runs
+        mrf_status ss = run_sink(c, c->mf_frame_e[f1] - c->mf_frame_e[f0], sink);
+        if (ss != MRF_OK) return ss;
+    }
     ProfScope ps(c, own ? MRF_K_DDA_FILL : -1);
     launch_dda_fill(c->d_frames.p + f0, dc, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
                     c->depth_all.p, c->row_ptr.p, c->ray_z.p, sv - ch.e0, so - ch.e0, sl - ch.e0,
-                    count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), st);
+                    count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), sink, st);
+    if (count) {  // the sink's count is read back per chunk walk (few chunks; first use only)
+        long long emitted = 0;
+        mrf_status sr = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 16), &emitted);
+        if (sr != MRF_OK) return sr;
+        run_sink_done(c, emitted, c->mf_frame_e[f1] - c->mf_frame_e[f0]);
+    }
     CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (!MRF_FILL_LNU && r1 > r0 ? 1 : 0));
     mf_dbg(c, count ? "walk(count)" : "walk");
     return MRF_OK;
@@ -403,10 +459,34 @@ mrf_status sync_fill(mrf_ctx* c) {
         if (sr != MRF_OK) return sr;
     }
     if (!c->fill_pending) return MRF_OK;
+    long long new_slots = -1;  // slots walked by the stored-graph fill below (its run sink)
     if (!c->pend.empty() && c->grid.bmask) {
-        // Sparse bricks: every frame is allocated by now (the graph is walked once, R23), so the
-        // per-ray counts of add_frame -- made before the later frames' bricks existed -- are
-        // redone against the final allocation and the segments laid out again.
+        // Sparse bricks: every frame is allocated by now (R23), so the per-ray counts of add_frame
+        // -- made before the later frames' bricks existed -- are redone against the allocation and
+        // the segments laid out again.  Frames added after the graph was used grow the allocation
+        // under the rays already walked: then every frame is walked again (R24) and the messages
+        // move to the new layout (lambda_merge, after the fill).
+        if (c->sp_rebuild) {
+            const long long R0 = c->R_filled;
+            c->sp_R_old = R0;
+            CK(c->rp_old.ensure((size_t)R0 + 1, 0, c->stream));
+            CK(c->ri_old.ensure((size_t)std::max<long long>(R0, 1), 0, c->stream));
+            CK(cudaMemcpyAsync(c->rp_old.p, c->row_ptr.p, sizeof(long long) * (R0 + 1), cudaMemcpyDeviceToDevice,
+                               c->stream));
+            if (R0)
+                CK(cudaMemcpyAsync(c->ri_old.p, c->ray_z.p, sizeof(RayInfo) * R0, cudaMemcpyDeviceToDevice, c->stream));
+            std::swap(c->vid, c->vid_old);
+            std::swap(c->lam, c->lam_old);
+            c->pend.insert(c->pend.begin(), c->sp_frames.begin(), c->sp_frames.end());
+            c->sp_frames.clear();
+            c->E_filled = 0;
+            c->R_filled = 0;
+            CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * (size_t)(c->NT * c->n_bucket_groups()), c->stream));
+            CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
+            CK(cudaMemsetAsync(c->counters.p + 16, 0, sizeof(unsigned long long), c->stream));
+            c->runs_emitted = 0;
+            c->runs_ok = true;
+        }
         long long E = c->E_filled;
         for (const FrameDesc& f : c->pend) {
             const long long Rf = (long long)f.rows_owned * f.W;
@@ -463,21 +543,50 @@ mrf_status sync_fill(mrf_ctx* c) {
         CK(c->d_cta0.ensure((size_t)nf + 1, 0, c->stream));
         CK(cudaMemcpyAsync(c->d_frames.p, c->pend.data(), sizeof(FrameDesc) * nf, cudaMemcpyHostToDevice, c->stream));
         CK(cudaMemcpyAsync(c->d_cta0.p, cta0.data(), sizeof(int) * (nf + 1), cudaMemcpyHostToDevice, c->stream));
+        RunSink sink;
+        {
+            mrf_status ss = run_sink(c, c->E - c->E_filled, sink);
+            if (ss != MRF_OK) return ss;
+        }
+        new_slots = c->E - c->E_filled;
         {
             ProfScope ps(c, MRF_K_DDA_FILL);
             launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
-                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, c->stream);
+                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, c->stream);
             CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (!MRF_FILL_LNU && c->R > c->R_filled ? 1 : 0));
         }
+        if (c->grid.bmask) {  // the depth images stay: a later keyframe may grow the allocation (R24)
+            c->sp_frames.insert(c->sp_frames.end(), c->pend.begin(), c->pend.end());
+        } else {
+            c->depth_used = 0;
+        }
         c->pend.clear();
-        c->depth_used = 0;
         c->E_filled = c->E;
         c->R_filled = c->R;
+        if (c->sp_rebuild) {  // the old rays' messages to the new layout; new incidences start at 0
+            CK(cudaMemsetAsync(c->counters.p + 17, 0, sizeof(unsigned long long), c->stream));
+            launch_lambda_merge(c->sp_R_old, c->rp_old.p, c->ri_old.p, c->vid_old.p, c->lam_old.p, c->row_ptr.p,
+                                c->ray_z.p, c->vid.p, c->lam.p, c->counters.p + 17, c->stream);
+            CK_LAUNCH(MRF_K_DDA_FILL, c->sp_R_old > 0 ? 1 : 0);
+            long long lost = 0;
+            mrf_status sr = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 17), &lost);
+            if (sr != MRF_OK) return sr;
+            c->vid_old.release();
+            c->lam_old.release();
+            c->sp_rebuild = false;
+            if (lost) {
+                c->sticky = MRF_ERR_STATE;
+                c->err = "internal: a re-walked ray lost incidences of its earlier walk";
+                return MRF_ERR_STATE;
+            }
+        }
     }
     CK(cudaMemcpyAsync(c->pinned, c->counters.p + 10, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 2, c->counters.p + 16, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->fill_pending = false;
+    if (new_slots >= 0) run_sink_done(c, c->pinned[2], new_slots);
     c->E_real = c->pinned[0];
     if (c->pinned[1]) {
         c->sticky = MRF_ERR_STATE;
@@ -541,7 +650,13 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     if ((st = read_ll(c, c->tile_ptr.p + NT, &c->n_runs)) != MRF_OK) return st;
     CK(c->runs.ensure((size_t)std::max(1LL, c->n_runs), 0, c->stream));
     CK(cudaMemsetAsync(c->tile_cursor.p, 0, sizeof(int32_t) * NT, c->stream));
-    {
+    const bool from_sink = c->runs_ok && !c->run_fill_forced;
+    if (from_sink) {  // the runs the fills built, placed by bucket (no vid re-read, no re-walk)
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_run_bucket(c->runs_emitted, c->runs_all.p, c->run_keys.p, c->tile_ptr.p, c->tile_cursor.p, c->runs.p,
+                          c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->runs_emitted > 0 ? 1 : 0);
+    } else {
         ProfScope ps(c, MRF_K_TRANSPOSE);
         if (c->mf) {  // per chunk: walk into the scratch, then place the chunk's runs
             for (const auto& ch : c->mf_chunks) {
@@ -1042,6 +1157,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* kp = getenv("MRF_K6_PAD")) c->k6_pad = atoi(kp) != 0;
     if (const char* kl = getenv("MRF_K6_LPT")) c->k6_lpt = atoi(kl) != 0;
     if (const char* kc = getenv("MRF_COMPACT")) c->force_compact = atoi(kc) != 0;
+    if (const char* rf = getenv("MRF_RUN_FILL")) c->run_fill_forced = atoi(rf) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
@@ -1090,12 +1206,12 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(c->tile_runs.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
-        CK(c->counters.ensure(16, 0, c->stream));
+        CK(c->counters.ensure(32, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
         CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
         CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
-        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 16, c->stream));
+        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 32, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
         // LUT as (L[i][j], L[i][j+1]) pairs: one 8-byte load per LUT row in K5.  The values are
         // the input table's floats, unscaled and unshifted.
@@ -1155,6 +1271,8 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->tile_runs.release(); c->tile_cursor.release(); c->tile_ptr.release();
     c->runs.release(); c->bitems.release(); c->stages.release();
     c->tile_map.release(); c->tile_of.release(); c->touched.release(); c->T_c.release();
+    c->runs_all.release(); c->run_keys.release();
+    c->rp_old.release(); c->ri_old.release(); c->vid_old.release(); c->lam_old.release();
     c->class_all.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -1213,8 +1331,15 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->kf_frames_alloc = 0;
     c->mf_frames.clear();
     c->mf_chunks.clear();
+    c->sp_frames.clear();
+    c->sp_rebuild = false;
+    c->vid_old.release();
+    c->lam_old.release();
     if (c->grid.bmask) CK(cudaMemsetAsync(c->bmask.p, 0, (size_t)c->n_brick_slots, c->stream));
     CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->counters.p + 16, 0, sizeof(unsigned long long), c->stream));
+    c->runs_emitted = 0;
+    c->runs_ok = true;
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
     CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * c->NT, c->stream));
@@ -1228,8 +1353,9 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
 mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_t height, const double K[4],
                          const double T_wc[12], int64_t* frame_id_out) {
     ENTER(ctx);
-    if (c->grid.bmask && c->E_filled > 0)
-        return set_err(c, MRF_ERR_STATE, "sparse bricks: add every keyframe before the graph is first used");
+    if (c->grid.bmask && c->mf && c->E_filled > 0)
+        return set_err(c, MRF_ERR_STATE,
+                       "sparse bricks with matrix-free walks: add every keyframe before the graph is first used");
     if (!depth || !K || !T_wc) return set_err(c, MRF_ERR_INVALID_ARG, "NULL argument");
     if (width <= 0 || height <= 0) return set_err(c, MRF_ERR_INVALID_ARG, "width/height must be > 0");
     if (!finite_all(K, 4) || !(K[0] > 0) || !(K[1] > 0))
@@ -1340,6 +1466,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
         c->n_dropped += drp;
         c->n_kept += Rf - inv - drp;
     }
+    if (c->grid.bmask && c->E_filled > 0) c->sp_rebuild = true;  // R24: re-walk every frame at the next fill
     c->fill_pending = true;
     c->dirty = true;
     c->hist_valid = false;

@@ -514,3 +514,34 @@ def test_capacity_limit_and_lazy_counts(frame1):
         s = m.graph_sizes(active=False)
         assert s["n_rays"] == n * s1["n_rays"] and s["E"] == n * s1["E"]
         assert s["n_invalid"] == n * s1["n_invalid"] and s["n_dropped"] == n * s1["n_dropped"]
+
+
+@pytest.mark.parametrize("mode", ["dense", "kfavg", "sparse", "mf"])
+def test_runs_from_fill_match_run_fill(mode, monkeypatch):
+    """The tile runs the DDA fill builds (placed by a bucket pass) give the same transpose as the
+    vid re-read (MRF_RUN_FILL=1): same run count, beliefs and messages bit-identical (exact integer
+    sums; the order of runs inside a tile is free)."""
+    w = synth.single_frame() if mode == "dense" else synth.tiny_frames(n_frames=4)
+    outs = []
+    for forced in ("0", "1"):
+        monkeypatch.setenv("MRF_RUN_FILL", forced)
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        if mode == "kfavg":
+            m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+        if mode == "sparse":
+            m.set_sparse_bricks(8)
+        if mode == "mf":
+            m.set_matrix_free(2)
+        with m:
+            frames = w.frames if mode == "sparse" else w.frames[:-1]
+            for fr in frames:
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(2)
+            if mode != "sparse":  # warm start: a second fill appends its runs
+                fr = w.frames[-1]
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(2)
+            outs.append((m.layout_sizes()["n_runs"], m.export_beliefs(), m.export_messages()))
+    assert outs[0][0] == outs[1][0]
+    assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])

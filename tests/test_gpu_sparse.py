@@ -100,9 +100,17 @@ def test_sparse_mode_rules():
         assert e.value.status == 6
         m.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
         m.bp_iterate(1)
-        with pytest.raises(pkg.MrfError) as e:  # the graph is in use: the allocation is fixed
-            m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)
-        assert e.value.status == 6
+        m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)  # after use: re-walk (R24)
+        m.bp_iterate(1)
+        mf = pkg.MRFMap.from_workload(w)
+        with mf:  # sparse + matrix-free: the allocation is fixed once the graph is used
+            mf.set_sparse_bricks(8)
+            mf.set_matrix_free(1)
+            mf.add_frame(w.frames[0].depth, w.frames[0].K, w.frames[0].T_wc)
+            mf.bp_iterate(1)
+            with pytest.raises(pkg.MrfError) as e:
+                mf.add_frame(w.frames[1].depth, w.frames[1].K, w.frames[1].T_wc)
+            assert e.value.status == 6
         m.reset()  # clears the allocation, keeps the mode
         assert m.export_bricks().sum() == 0
         m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)
@@ -129,5 +137,57 @@ def test_sparse_bricks_with_keyframe_averages():
         m.bp_iterate(5)
         lam = m.export_messages()
         marg = m.marginals()
+    assert _msg_err(lam, lam_ref) <= MSG_TOL
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+def _carry_messages(g_old, lam_old, g_new, V):
+    """Warm start across a re-walk (reading R24): each incidence of the new graph takes the message
+    of the same (frame, pixel, voxel) in the old graph, 0 if it is new (host-side reference)."""
+    def keys(g):
+        ray = np.repeat(np.arange(g.n_rays), np.diff(g.row_ptr))
+        return (g.frame[ray].astype(np.int64) << 52) | (g.pixel[ray].astype(np.int64) << 32) | g.vid.astype(np.int64)
+    ko, kn = keys(g_old), keys(g_new)
+    order = np.argsort(ko)
+    pos = np.searchsorted(ko[order], kn)
+    pos = np.minimum(pos, len(ko) - 1)
+    hit = ko[order][pos] == kn
+    out = np.zeros(g_new.E, np.float64)
+    out[hit] = np.asarray(lam_old, np.float64)[order][pos[hit]]
+    assert hit.sum() == g_old.E  # every old incidence survives (the allocation only grows)
+    return out
+
+
+@pytest.mark.parametrize("name,k,n_after", [("tiny_frames", 2, 2), ("frames30_3", 1, 1)])
+def test_sparse_keyframes_after_use(name, k, n_after):
+    """P:205 "When adding new depth images, new bricks are allocated" (reading R24): keyframes added
+    after iterating grow the allocation under rays already walked.  Every frame is walked again
+    against the grown allocation: the graph equals the oracle's empty-skip graph over all frames
+    (bit-exact); every old incidence keeps its message and the new ones start at 0 (the host-side
+    (frame, pixel, voxel) mapping, exact); the beliefs are unchanged by the re-walk; the next
+    iterations match the oracle continued from that state."""
+    w = synth.tiny_frames(n_frames=4) if name == "tiny_frames" else synth.frames30(n_frames=3)
+    p = oracle.Params.from_workload(w)
+    g_old = oracle.build_graph(p, w.frames[:k], bricks=oracle.alloc_bricks(p, w.frames[:k]))
+    bk = oracle.alloc_bricks(p, w.frames)
+    g_new = oracle.build_graph(p, w.frames, bricks=bk)
+    assert g_new.E > g_old.E
+    with _sparse_map(w, frames=w.frames[:k]) as m:
+        m.bp_iterate(3)
+        lam_old = m.export_messages()
+        T_old = m.export_beliefs()
+        for fr in w.frames[k:]:
+            m.add_frame(fr.depth, fr.K, fr.T_wc)
+        assert np.array_equal(m.export_bricks(), bk.mask)
+        gg = m.export_graph()
+        for key in ("row_ptr", "vid", "off_q", "pixel", "frame"):
+            assert np.array_equal(gg[key], getattr(g_new, key)), key
+        lam_start = m.export_messages()
+        assert np.array_equal(lam_start.astype(np.float64), _carry_messages(g_old, lam_old, g_new, p.V))
+        assert np.array_equal(m.export_beliefs(), T_old)
+        m.bp_iterate(n_after)
+        lam = m.export_messages()
+        marg = m.marginals()
+    lam_ref, T_ref = oracle.bp(p, g_new, n_after, lam=lam_start.astype(np.float64))
     assert _msg_err(lam, lam_ref) <= MSG_TOL
     assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
