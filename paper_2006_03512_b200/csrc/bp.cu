@@ -307,7 +307,7 @@ __device__ __forceinline__ void stk(int32_t* p, const int (&v)[K], long long nv)
 
 // Loads of one lane's chunk [s, s+K) (s < e1): vid, q, log nu, then the belief gathers.
 template <int K, int M>
-__device__ __forceinline__ void load_chunk(long long s, long long e1, float L0, const int32_t* __restrict__ vid,
+__device__ __forceinline__ void load_chunk(long long s, long long e1, const MsgParams& mp, const int32_t* __restrict__ vid,
                                            const float* __restrict__ lnu, const int32_t* __restrict__ lam,
                                            const long long* __restrict__ T, const int32_t* __restrict__ qrow,
                                            float (&la)[K], float (&w)[K], float (&l)[K]) {
@@ -322,9 +322,12 @@ __device__ __forceinline__ void load_chunk(long long s, long long e1, float L0, 
     ldk<K>(reinterpret_cast<const int32_t*>(lnu) + s, ln);
     long long t[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) t[j] = (s + j < e1) ? __ldg(T + v[j]) : 0;
+    for (int j = 0; j < K; ++j) {
+        MRF_ASSERT(s + j >= e1 || (v[j] >= 0 && v[j] < mp.chk_vi && (qrow || s + j < mp.chk_lam)));
+        t[j] = (s + j < e1) ? __ldg(T + v[j]) : 0;
+    }
 #pragma unroll
-    for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), L0, s + j < e1, la[j], w[j], l[j]);
+    for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, s + j < e1, la[j], w[j], l[j]);
 }
 template <int K>
 __device__ __forceinline__ void identity_chunk(float (&la)[K], float (&w)[K], float (&l)[K]) {
@@ -395,10 +398,14 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
         // by select afterwards
         long long t[K];
 #pragma unroll
-        for (int j = 0; j < K; ++j) t[j] = __ldg(T + v[j]);
+        for (int j = 0; j < K; ++j) {
+            MRF_ASSERT(v[j] >= 0 && v[j] < mp.chk_vi);
+            t[j] = __ldg(T + v[j]);
+        }
 #pragma unroll
         for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
     }
+    MRF_ASSERT(!AVG && nv > 0 ? (long long)s + nv <= mp.chk_lam : true);
     float aB, bB, Rin, Qin;
     lane_composite<K>(la, w, aB, bB);
     lane_scans<G, M, false>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         for (int t = n_tiles - 1; t >= 0; --t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             identity_chunk<kLongK>(la, w, l);
-            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, qrow, la, w, l);
+            if (s < e1) load_chunk<kLongK, M>(s, e1, mp, vid, lnu, lam, T, qrow, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
             lane_scans<32, M>(aB, bB, lane, Rc, kNeg, Rin, Qin, &Rc_out, &Qc_out);
             Rc = Rc_out;
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         for (int t = 0; t < n_tiles; ++t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             identity_chunk<kLongK>(la, w, l);
-            if (s < e1) load_chunk<kLongK, M>(s, e1, mp.L0, vid, lnu, lam, T, qrow, la, w, l);
+            if (s < e1) load_chunk<kLongK, M>(s, e1, mp, vid, lnu, lam, T, qrow, la, w, l);
             lane_composite<kLongK>(la, w, aB, bB);
             lane_scans<32, M>(aB, bB, lane, kNeg, Qc, Rin, Qin, &Rc_out, &Qc_out);
             Qc = Qc_out;
@@ -771,7 +778,8 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                                                                    const Run* __restrict__ runs,
                                                                    const int32_t* __restrict__ lam, int per_item,
                                                                    void* out, long long n_out, unsigned* next,
-                                                                   const int32_t* __restrict__ tile_map) {
+                                                                   const int32_t* __restrict__ tile_map, long long chk_lam,
+                                                                   long long chk_out_tiles) {
     extern __shared__ int smem[];
     using L = AccLayout<PAD>;
     static_assert(MODE == 0 || !PAD, "keyframe-average sums use the plain layout (shared memory)");
@@ -810,6 +818,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             const int nb = (int)min(32LL, r1 - rb);
             uint4 d{0u, 0u, 0u, 0u};
             if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
+            MRF_ASSERT(lane >= nb || (long long)d.x + ((d.y >> 14) & 63u) + 1 <= chk_lam);
             if constexpr (PAD)  // in-tile slot -> accumulator index, once per run
                 d.y = (unsigned)L::index((int)(d.y & (kTileSlots - 1))) | ((d.y >> 14) << L::NS);
             sdesc[lane] = d;
@@ -847,6 +856,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                         const int cz = k - cx - cy, sz = (meta >> (L::NS + 8)) & 1 ? -cz : cz;
                         const int s0 = (int)(meta & ((1u << L::NS) - 1u)) + sx + L::SY * sy + L::SZ * sz;
                         const int si = PAD ? s0 : swz(s0);
+                        MRF_ASSERT(si >= 0 && si < L::kSlots);
                         const int qv = q[rnd][j];
                         if constexpr (MODE == 0) {
                             atomicAdd(acc_lo + si, qv & 0xffff);
@@ -870,6 +880,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             // world > 1: the tile's slots go to its position among the tiles some rank touches
             // (the compacted all-reduce buffer); else to the tile itself
             const long long tpos = tile_map ? (long long)__ldg(tile_map + item.x) : (long long)item.x;
+            MRF_ASSERT(tpos >= 0 && tpos < chk_out_tiles);
             long long* Tt = static_cast<long long*>(out) + (tpos << kTileShift);
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
                 const int a = L::index(i);
@@ -1023,7 +1034,7 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
 template <int MODE, bool PAD>
 void launch_tile_reduce_t(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                           const int32_t* lam, int per_item, void* out, long long n_out, unsigned* next,
-                          const int32_t* tile_map, cudaStream_t s) {
+                          const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s) {
     constexpr int smem = (MODE == 0 ? 2 * AccLayout<PAD>::kSlots * (int)sizeof(int) : kK6SmemKf) + kK6Desc;
     DevCfg& dc = dev_cfg();
     if (!dc.k6[MODE][PAD]) {
@@ -1033,23 +1044,28 @@ void launch_tile_reduce_t(long long n_items, const int2* items, const long long*
     const long long grid = n_items < (long long)dc.sms ? n_items : (long long)dc.sms;
     if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
     tile_reduce_kernel<MODE, PAD><<<(unsigned)grid, kK6Threads, smem, s>>>(n_items, items, tile_ptr, runs, lam,
-                                                                              per_item, out, n_out, next, tile_map);
+                                                                              per_item, out, n_out, next, tile_map,
+                                                                              chk_lam, chk_out_tiles);
 }
 
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                         const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad,
-                        const int32_t* tile_map, cudaStream_t s) {
+                        const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s) {
     if (n_items == 0) return;
     if (pad)
-        launch_tile_reduce_t<0, true>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, s);
+        launch_tile_reduce_t<0, true>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, chk_lam,
+                                      chk_out_tiles, s);
     else
-        launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, s);
+        launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, chk_lam,
+                                       chk_out_tiles, s);
 }
 
 void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
-                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, cudaStream_t s) {
+                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, long long chk_lam,
+                    cudaStream_t s) {
     if (n_items == 0) return;
-    launch_tile_reduce_t<1, false>(n_items, items, bucket_ptr, runs, lam, per_item, D, n_slots, next, nullptr, s);
+    launch_tile_reduce_t<1, false>(n_items, items, bucket_ptr, runs, lam, per_item, D, n_slots, next, nullptr, chk_lam,
+                                   n_slots >> kTileShift, s);
 }
 
 // world > 1: the all-reduced sums of the touched tiles (compact order) back to their tiles
@@ -1059,6 +1075,7 @@ __global__ void tile_scatter_kernel(long long n, const int32_t* __restrict__ til
     if (i >= n) return;
     constexpr int kPairs = kTileSlots / 2;
     const long long ci = i / kPairs;
+    MRF_ASSERT(__ldg(tile_of + ci) >= 0);
     dst[(long long)__ldg(tile_of + ci) * kPairs + (i - ci * kPairs)] = src[i];
 }
 

@@ -472,6 +472,7 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 const int a = w.earliest(na, da);
                 const double t_out = crossing_t(w, a, na, da, last);
                 const int vx = voxel_slot(g, w.c0, w.c1, w.c2);
+                MRF_ASSERT(vx >= 0 && (vx >> kTileShift) < g.ntx * g.nty * g.ntz && e < e_cap);
                 const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
                 long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
                 q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
@@ -841,6 +842,7 @@ __global__ void __launch_bounds__(256) run_bucket_kernel(long long n, const Run*
     int base = 0;
     if (lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
     base = __shfl_sync(peers, base, leader);
+    MRF_ASSERT(tile_ptr[key] + base + __popc(peers & ((1u << lane) - 1u)) < tile_ptr[key + 1]);
     dst[tile_ptr[key] + base + __popc(peers & ((1u << lane) - 1u))] = src[i];
 }
 

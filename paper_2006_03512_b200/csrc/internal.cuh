@@ -8,8 +8,25 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace mrf {
+
+// Checked build (MRF_CHECK=1, libmrf_checked.so; SURVEY §4 T8 -- compute-sanitizer is closed on
+// this pool): the data-dependent indices of the hot kernels (belief-slot gathers, message slots of
+// runs and chunks, accumulator indices, run placement) are bounds-checked on the device; a failed
+// check prints the site and traps, which the ABI returns as a sticky MRF_ERR_CUDA.
+#ifndef MRF_CHECK
+#define MRF_CHECK 0
+#endif
+#define MRF_ASSERT(cond)                                                                      \
+    do {                                                                                      \
+        if (MRF_CHECK && !(cond)) {                                                           \
+            printf("MRF_CHECK failed: %s at %s:%d (block %d, thread %d)\n", #cond, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                        \
+            __trap();                                                                         \
+        }                                                                                     \
+    } while (0)
 
 // ---- fixed-point conventions (DESIGN.md §Data layout)
 constexpr int kFixShift = 16;                 // grid coordinates carry 16 fractional bits
@@ -149,6 +166,8 @@ struct MsgParams {
     // qbar[frame * qbar_vi + v] instead of the ray's own message; nullptr in per-ray mode
     const int32_t* qbar;
     long long qbar_vi;
+    // checked build: the message slots [0, chk_lam) and belief slots [0, chk_vi) that exist
+    long long chk_lam, chk_vi;
 };
 
 // log nu at (measured range row iz + wz, quantised offset off_q): bilinear interpolation of the
@@ -323,14 +342,15 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
 // touches, compacted for the all-reduce); nullptr = the tile itself
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                         const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad,
-                        const int32_t* tile_map, cudaStream_t s);
+                        const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s);
 // T[tile_of[i] tile] = src[i-th compact tile] for i < n_tiles (16384 slots each)
 void launch_tile_scatter(long long n_tiles, const int32_t* tile_of, const long long* src, long long* T, cudaStream_t s);
 // keyframe averages (reading R22): per [bucket = frame * NT + tile][slot], D += signed small
 // probability of each message (fp64, D[0 .. n_slots)) and the packed counts n_pos + 2^32 n_neg
 // (int64, at D + n_slots); both zeroed by the caller (bp.cu tile_reduce_kernel<1>)
 void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
-                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, cudaStream_t s);
+                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, long long chk_lam,
+                    cudaStream_t s);
 // qbar[f][v] = quantised clip(ln(sum mu(1) / sum mu(0)), +-256) (0 without a ray), T[v] = sum_f qbar
 void launch_kf_finalize(long long F, long long VI, const double* D, int32_t* qbar, long long* T, cudaStream_t s);
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s);

@@ -881,7 +881,8 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
         const long long F = (long long)c->frames.size(), n = F * c->VI;
         CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(double) * (size_t)n, c->stream));
         launch_kf_sums(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
-                       c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr, c->stream);
+                       c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr, (long long)c->lam.cap,
+                       c->stream);
         launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_bitems > 0 ? 1 : 0) + 1);
         mf_dbg(c, "kf sums");
@@ -894,7 +895,8 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
     } else {
         launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
                            c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->k6_pad,
-                           compact ? c->tile_map.p : nullptr, c->stream);
+                           compact ? c->tile_map.p : nullptr, (long long)c->lam.cap, compact ? c->n_act_tiles : c->NT,
+                           c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -908,6 +910,8 @@ mrf_status ray_messages(mrf_ctx* c) {
     }
     c->mp.qbar = c->kf_avg ? c->qbar.p : nullptr;
     c->mp.qbar_vi = c->VI;
+    c->mp.chk_lam = (long long)c->lam.cap;  // checked build (MRF_CHECK): what exists
+    c->mp.chk_vi = c->VI;
     if (c->mf) {  // per chunk: re-walk into the scratch, then the chunk's class kernels
         ProfScope ps(c, MRF_K_RAY_MSG);  // walks + K5 of every chunk
         const size_t nch = c->mf_chunks.size();

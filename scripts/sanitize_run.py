@@ -1,4 +1,4 @@
-"""Workload for compute-sanitizer: the tiny scene from 4 keyframes through every
+"""Workload for compute-sanitizer and for the bounds-checked build: the tiny scene from 4 keyframes through every
 K5 / K6 path and mode of the library -- the class kernels, the long-ray tiled kernel (a
 corridor), the TMA-staged K5 (MRF_K5=staged), the per-voxel K6 ablation (MRF_K6=voxel), the
 compacted reduction (MRF_COMPACT=1), keyframe averages, sparse bricks, matrix-free walks, the
@@ -30,7 +30,7 @@ def corridor():
 
 
 def run(mode):
-    w = corridor() if mode == "long" else synth.tiny_frames(n_frames=4)
+    w = corridor() if mode == "long" else (synth.frames30(n_frames=3) if mode == "room" else synth.tiny_frames(n_frames=4))
     m = pkg.MRFMap.from_workload(w)
     with m:
         if mode == "kfavg":
