@@ -37,6 +37,7 @@
 #include <algorithm>
 
 #include "internal.cuh"
+#include "walk.cuh"
 
 namespace mrf {
 namespace {
@@ -419,18 +420,132 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_
     stk<K>(lam + s, out, nv);
 }
 
+// ---------------------------------------------------------------- K5 matrix-free (K12)
+// The paper re-traces every keyframe in every pass.  Here a lane re-walks ITS chunk of
+// the ray inside the message kernel: the chunk's first cell is stored (ck: 4 bytes per chunk, one
+// per K incidences, written by the first walk), the walker's exact state in that cell follows from
+// the cell and the ray's segment (Walker::restart), and K steps of the same integer DDA give the
+// chunk's voxel slots and offsets; log nu is interpolated from the table (L1) as the fill does.
+// No vid / off_q / log-nu array exists: per iteration K5 moves lambda (read + write), the
+// checkpoints and the per-ray records.  Bit-identical to the stored graph (same walk, same
+// interpolation, same message arithmetic).
+template <int K>
+__device__ __forceinline__ void walk_chunk(const WalkParams& wp, const RaySeg& sg, const MsgParams& mp, int iz, float wz,
+                                           int vck, bool first, int nv, int (&v)[K], int (&ln)[K]) {
+    int x, y, z;
+    slot_xyz(wp.g, vck, x, y, z);
+    Walker w;
+    w.restart(sg, x, y, z, first);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        unsigned na, da;
+        const int a = w.earliest(na, da);
+        bool last;
+        const double t_out = crossing_t(w, a, na, da, last);
+        const bool ok = j < nv;
+        // cells past the ray's end may lie outside the grid: slot 0 (masked afterwards)
+        v[j] = ok ? voxel_slot(wp.g, w.c0, w.c1, w.c2) : 0;
+        const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
+        long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
+        q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
+        ln[j] = __float_as_int(ok ? lut_finish(lut_fetch(mp, iz, (int)q), wz) : 0.f);
+        w.advance(na, da);
+        w.t_in = t_out;
+    }
+}
+
+// the long-ray kernel's chunk [s, s + K) (s < e1), re-walked: chunk index (s - e0) / K of the ray
+template <int K, int M>
+__device__ __forceinline__ void load_chunk_walk(long long s, long long e0, long long e1, const MsgParams& mp,
+                                                const WalkParams& wp, const RaySeg& sg, const RayInfo& info,
+                                                const int32_t* __restrict__ lam, const long long* __restrict__ T,
+                                                const int32_t* __restrict__ qrow, float (&la)[K], float (&w)[K],
+                                                float (&l)[K]) {
+    const int c = (int)((s - e0) / K);
+    const int nv = (int)min((long long)K, e1 - s);
+    int v[K], q[K], ln[K];
+    walk_chunk<K>(wp, sg, mp, info.iz, info.wz, __ldg(wp.ck + (e0 >> 2) + c), c == 0, nv, v, ln);
+    if (qrow) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) q[j] = __ldg(qrow + v[j]);
+    } else {
+        ldk<K>(lam + s, q);
+    }
+    long long t[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        MRF_ASSERT(j >= nv || (v[j] >= 0 && v[j] < mp.chk_vi && (qrow || s + j < mp.chk_lam)));
+        t[j] = __ldg(T + v[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
+}
+
+template <int G, int K, int M, bool AVG>
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_walk_kernel(long long n, const int32_t* __restrict__ rays,
+                                                         const long long* __restrict__ row_ptr,
+                                                         const RayInfo* __restrict__ ray_z, int32_t* lam,
+                                                         const long long* __restrict__ T, MsgParams mp, WalkParams wp) {
+    constexpr int RPW = 32 / G;
+    const long long wi = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wi * RPW >= n) return;  // warp-uniform
+    const int lane = threadIdx.x & 31, sl = lane & (G - 1);
+    const long long ri = wi * RPW + lane / G;
+    const int r = __ldg(rays + (ri < n ? ri : n - 1));
+    const RayInfo info = ray_z[r];
+    const int nr = ri < n ? info.n : 0;
+    const int e0 = (int)__ldg(row_ptr + r);
+    const int s = e0 + sl * K;
+    const int nv = min(max(nr - sl * K, 0), K);
+    const int sr = nv > 0 ? s : e0;
+    float la[K], w[K], l[K], lR[K], lQ[K];
+    {
+        int v[K], q[K], ln[K];
+        const RaySeg sg = wp.seg[r];
+        const int vck = __ldg(wp.ck + (e0 >> 2) + (nv > 0 ? sl : 0));
+        walk_chunk<K>(wp, sg, mp, info.iz, info.wz, vck, nv <= 0 || sl == 0, nv, v, ln);
+        if constexpr (AVG) {
+            const int32_t* qrow = mp.qbar + (long long)info.frame * mp.qbar_vi;
+#pragma unroll
+            for (int j = 0; j < K; ++j) q[j] = __ldg(qrow + v[j]);
+        } else {
+            ldk<K>(lam + sr, q);
+        }
+        long long t[K];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            MRF_ASSERT(v[j] >= 0 && v[j] < mp.chk_vi);
+            t[j] = __ldg(T + v[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
+    }
+    MRF_ASSERT(!AVG && nv > 0 ? (long long)s + nv <= mp.chk_lam : true);
+    float aB, bB, Rin, Qin;
+    lane_composite<K>(la, w, aB, bB);
+    lane_scans<G, M, false>(aB, bB, sl, kNeg, kNeg, Rin, Qin, nullptr, nullptr);
+    lane_recurrences<K, M>(la, w, Rin, Qin, lR, lQ);
+    int out[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int x = quantise(lambda_n(lQ[j], l[j], lR[j]));
+        out[j] = j < nv ? x : 0;
+    }
+    stk<K>(lam + s, out, nv);
+}
+
 // ---------------------------------------------------------------- K5: long rays (tiled)
 constexpr int kLongK = 8;
 constexpr int kLongTile = 32 * kLongK;
 
-template <int M, bool AVG>
+template <int M, bool AVG, bool WALK>
 __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const int32_t* __restrict__ rays,
                                                            const long long* __restrict__ row_ptr,
                                                            const RayInfo* __restrict__ ray_z,
                                                            const int32_t* __restrict__ vid,
                                                            const float* __restrict__ lnu, int32_t* lam,
                                                            const long long* __restrict__ T, MsgParams mp,
-                                                           float* scratch, long long scratch_per_warp) {
+                                                           float* scratch, long long scratch_per_warp, WalkParams wp) {
     const long long gw = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long n_warps = ((long long)gridDim.x * blockDim.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -439,6 +554,9 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         const int r = __ldg(rays + wi);
         const long long e0 = __ldg(row_ptr + r), e1 = e0 + ray_z[r].n;
         const int32_t* qrow = AVG ? mp.qbar + (long long)ray_z[r].frame * mp.qbar_vi : nullptr;
+        const RayInfo info = ray_z[r];
+        RaySeg sg{};
+        if constexpr (WALK) sg = wp.seg[r];
         const int n_tiles = (int)((e1 - e0 + kLongTile - 1) / kLongTile);
         float la[kLongK], w[kLongK], l[kLongK], lR[kLongK], lQ[kLongK];
         float aB, bB, Rin, Qin, Rc_out, Qc_out;
@@ -447,7 +565,10 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         for (int t = n_tiles - 1; t >= 0; --t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             identity_chunk<kLongK>(la, w, l);
-            if (s < e1) load_chunk<kLongK, M>(s, e1, mp, vid, lnu, lam, T, qrow, la, w, l);
+            if (s < e1) {
+                if constexpr (WALK) load_chunk_walk<kLongK, M>(s, e0, e1, mp, wp, sg, info, lam, T, qrow, la, w, l);
+                else load_chunk<kLongK, M>(s, e1, mp, vid, lnu, lam, T, qrow, la, w, l);
+            }
             lane_composite<kLongK>(la, w, aB, bB);
             lane_scans<32, M>(aB, bB, lane, Rc, kNeg, Rin, Qin, &Rc_out, &Qc_out);
             Rc = Rc_out;
@@ -462,7 +583,10 @@ __global__ void __launch_bounds__(256) ray_msg_long_kernel(long long n, const in
         for (int t = 0; t < n_tiles; ++t) {
             const long long s = e0 + (long long)t * kLongTile + (long long)lane * kLongK;
             identity_chunk<kLongK>(la, w, l);
-            if (s < e1) load_chunk<kLongK, M>(s, e1, mp, vid, lnu, lam, T, qrow, la, w, l);
+            if (s < e1) {
+                if constexpr (WALK) load_chunk_walk<kLongK, M>(s, e0, e1, mp, wp, sg, info, lam, T, qrow, la, w, l);
+                else load_chunk<kLongK, M>(s, e1, mp, vid, lnu, lam, T, qrow, la, w, l);
+            }
             lane_composite<kLongK>(la, w, aB, bB);
             lane_scans<32, M>(aB, bB, lane, kNeg, Qc, Rin, Qin, &Rc_out, &Qc_out);
             Qc = Qc_out;
@@ -975,8 +1099,36 @@ void launch_ray_messages_m(int cls, long long n_rays, const int32_t* rays, const
         launch_class_k<M, AVG, 0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
     } else {
         const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
-        ray_msg_long_kernel<M, AVG><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
-                                                      scratch_per_warp);
+        ray_msg_long_kernel<M, AVG, false><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+                                                             scratch_per_warp, WalkParams{});
+    }
+}
+
+template <int M, bool AVG, int k>
+void launch_walk_class_k(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr, const RayInfo* ray_z,
+                         int32_t* lam, const long long* T, const MsgParams& mp, const WalkParams& wp, cudaStream_t s) {
+    if constexpr (k < kNumShort) {
+        if (cls == k) {
+            constexpr int G = class_G(k), K = class_K(k);
+            const unsigned grid = blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256);
+            ray_msg_walk_kernel<G, K, M, AVG><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, lam, T, mp, wp);
+            return;
+        }
+        launch_walk_class_k<M, AVG, k + 1>(cls, n_rays, rays, row_ptr, ray_z, lam, T, mp, wp, s);
+    }
+}
+
+template <int M, bool AVG>
+void launch_ray_messages_walk_m(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+                                const RayInfo* ray_z, int32_t* lam, const long long* T, const MsgParams& mp,
+                                const WalkParams& wp, float* scratch, long long scratch_per_warp, int n_warps_long,
+                                cudaStream_t s) {
+    if (cls < kNumShort) {
+        launch_walk_class_k<M, AVG, 0>(cls, n_rays, rays, row_ptr, ray_z, lam, T, mp, wp, s);
+    } else {
+        const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
+        ray_msg_long_kernel<M, AVG, true><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, nullptr, nullptr, lam, T, mp,
+                                                            scratch, scratch_per_warp, wp);
     }
 }
 
@@ -1011,6 +1163,22 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
     else
         launch_ray_messages_m<1, false>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
                                         scratch_per_warp, n_warps_long, s);
+}
+
+void launch_ray_messages_walk(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+                              const RayInfo* ray_z, int32_t* lam, const long long* T, const MsgParams& mp,
+                              const WalkParams& wp, float* scratch, long long scratch_per_warp, int n_warps_long,
+                              int math, cudaStream_t s) {
+    if (n_rays == 0) return;
+    if (mp.qbar)
+        launch_ray_messages_walk_m<1, true>(cls, n_rays, rays, row_ptr, ray_z, lam, T, mp, wp, scratch,
+                                            scratch_per_warp, n_warps_long, s);
+    else if (math == 0)
+        launch_ray_messages_walk_m<0, false>(cls, n_rays, rays, row_ptr, ray_z, lam, T, mp, wp, scratch,
+                                             scratch_per_warp, n_warps_long, s);
+    else
+        launch_ray_messages_walk_m<1, false>(cls, n_rays, rays, row_ptr, ray_z, lam, T, mp, wp, scratch,
+                                             scratch_per_warp, n_warps_long, s);
 }
 
 void launch_ray_messages_staged(long long n_stages, const Stage* stages, const long long* row_ptr,

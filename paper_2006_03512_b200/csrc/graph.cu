@@ -10,6 +10,7 @@
 // so the warp's rays start in the same voxel and fan out slowly -- voxel-histogram and
 // transpose-cursor atomics are aggregated per warp with __match_any_sync.
 #include "internal.cuh"
+#include "walk.cuh"
 
 namespace mrf {
 namespace {
@@ -19,10 +20,6 @@ constexpr unsigned kFull = 0xffffffffu;
 // ---------------------------------------------------------------- B1: pixel -> segment
 // All fp64 steps use explicitly rounded intrinsics (no FMA contraction), in the order
 // stated in DESIGN.md §Graph build, so the quantised end points are reproducible.
-struct Segment {
-    long long g0[3], g1[3];
-    double Z, L;
-};
 
 // 0 = kept, 1 = invalid pixel, 2 = dropped (measured point outside the grid)
 __device__ __forceinline__ int pixel_segment(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, int u,
@@ -53,145 +50,6 @@ __device__ __forceinline__ int pixel_segment(const FrameDesc& f, const GridDesc&
     sg.Z = Z;
     sg.L = L;
     return 0;
-}
-
-// ---------------------------------------------------------------- B2: integer 3D-DDA
-// State of the walk: current cell, per-axis step direction, and the exact crossing parameter
-// of the next boundary on each axis as the rational num/den (den = |dG| > 0).  Held in scalar
-// registers (no runtime-indexed arrays, which would live in local memory), 32-bit: mrf_create
-// bounds the segment length (margin(D) <= D for the grid diagonal D, dims <= 8192), so
-// den < 2^31 and num <= den + 2^16 fit in uint32 and the exact products in one IMAD.WIDE.U32.
-struct Walker {
-    unsigned n0, n1, n2, d0, d1, d2;  // d = 0: the axis never crosses
-    int c0, c1, c2, s0, s1, s2;       // cell, step direction
-    double y0, y1, y2;                // RN(1 / d) per axis (crossing_t)
-    double t_in;
-
-    __device__ __forceinline__ static void axis_start(long long g0, long long g1, int& c, int& s, unsigned& n,
-                                                      unsigned& d) {
-        const long long dg = g1 - g0;
-        long long cc = g0 >> kFixShift;  // arithmetic shift == floor
-        const bool on_face = (g0 & (kFixOne - 1)) == 0;
-        if (dg < 0 && on_face) cc -= 1;  // cell that contains t = 0+
-        c = (int)cc;
-        if (dg > 0) {
-            s = 1;
-            n = (unsigned)(((cc + 1) << kFixShift) - g0);
-            d = (unsigned)dg;
-        } else if (dg < 0) {
-            s = -1;
-            n = (unsigned)(g0 - (cc << kFixShift));
-            d = (unsigned)(-dg);
-        } else {
-            s = 0;
-            n = 1;
-            d = 0;
-        }
-    }
-    __device__ __forceinline__ void start(const Segment& sg) {
-        axis_start(sg.g0[0], sg.g1[0], c0, s0, n0, d0);
-        axis_start(sg.g0[1], sg.g1[1], c1, s1, n1, d1);
-        axis_start(sg.g0[2], sg.g1[2], c2, s2, n2, d2);
-        y0 = __drcp_rn((double)(d0 ? d0 : 1u));
-        y1 = __drcp_rn((double)(d1 ? d1 : 1u));
-        y2 = __drcp_rn((double)(d2 ? d2 : 1u));
-        t_in = 0.0;
-    }
-    __device__ __forceinline__ bool inside(const GridDesc& g) const {
-        return (unsigned)c0 < (unsigned)g.nx && (unsigned)c1 < (unsigned)g.ny && (unsigned)c2 < (unsigned)g.nz;
-    }
-    // n_a / d_a < n_b / d_b, exactly
-    __device__ __forceinline__ static bool before(unsigned na, unsigned da, unsigned nb, unsigned db) {
-        return (unsigned long long)na * db < (unsigned long long)nb * da;
-    }
-    // The earliest next crossing as (num, den) and its axis (-1 if no axis crosses).
-    __device__ __forceinline__ int earliest(unsigned& na, unsigned& da) const {
-        int a = -1;
-        na = 1;
-        da = 0;
-        if (d0) { a = 0; na = n0; da = d0; }
-        if (d1 && (a < 0 || before(n1, d1, na, da))) { a = 1; na = n1; da = d1; }
-        if (d2 && (a < 0 || before(n2, d2, na, da))) { a = 2; na = n2; da = d2; }
-        return a;
-    }
-    // Advance every axis whose crossing ties with (na, da) (simultaneous steps on corners/edges).
-    __device__ __forceinline__ void advance(unsigned na, unsigned da) {
-        const unsigned long long r = (unsigned long long)na;
-        const bool t0 = d0 && (unsigned long long)n0 * da == r * d0;
-        const bool t1 = d1 && (unsigned long long)n1 * da == r * d1;
-        const bool t2 = d2 && (unsigned long long)n2 * da == r * d2;
-        if (t0) { c0 += s0; n0 += (unsigned)kFixOne; }
-        if (t1) { c1 += s1; n1 += (unsigned)kFixOne; }
-        if (t2) { c2 += s2; n2 += (unsigned)kFixOne; }
-    }
-    // Empty skip (sparse bricks): from a cell of an unallocated brick, jump to the first
-    // cell past the brick in one step -- exactly the state the cell-by-cell walk reaches.  Axis k
-    // leaves the brick (clamped to the grid) after m_k crossings, the m_k-th at the exact time
-    // (n_k + (m_k - 1) 2^16) / d_k; t* is the earliest of these; every axis then takes all its
-    // crossings at times <= t* (ties step together, as in advance()), and t_in = RN(t*), the
-    // crossing that enters the new cell.  Returns false if the segment ends inside the brick.
-    __device__ __forceinline__ static unsigned exit_steps(int c, int s, int dim, int bs) {
-        if (s > 0) return (unsigned)(min(((c >> bs) + 1) << bs, dim) - c);
-        return (unsigned)(c - ((c >> bs) << bs) + 1);
-    }
-    // 1 + floor((Ns d - n Ds) / (2^16 Ds)) crossings of an axis at times (n + i 2^16) / d <= Ns / Ds
-    // (0 if even the first is later): the quotient (small, <= the brick edge) estimated in fp64 with
-    // y = RN(1 / Ds) and corrected exactly in integers (a 64-bit integer division is ~100 ops)
-    __device__ __forceinline__ static unsigned long long crossings_upto(unsigned n, unsigned d, unsigned long long Ns,
-                                                                        unsigned Ds, double y) {
-        if (!d) return 0;
-        const unsigned long long lhs = Ns * d, rhs = (unsigned long long)n * Ds;  // t* >= n / d ?
-        if (lhs < rhs) return 0;
-        const unsigned long long diff = lhs - rhs, unit = (unsigned long long)kFixOne * Ds;
-        unsigned long long k = (unsigned long long)__dmul_rn(__dmul_rn((double)diff, y), 1.0 / 65536.0);
-        while (k * unit > diff) --k;
-        while ((k + 1) * unit <= diff) ++k;
-        return k + 1;
-    }
-    __device__ bool skip_brick(const GridDesc& g) {
-        const int bs = g.bshift;
-        int a = -1;
-        unsigned long long Ns = 0;
-        unsigned Ds = 1;
-        if (d0) {
-            a = 0;
-            Ns = n0 + (unsigned long long)(exit_steps(c0, s0, g.nx, bs) - 1) * kFixOne;
-            Ds = d0;
-        }
-        if (d1) {
-            const unsigned long long N = n1 + (unsigned long long)(exit_steps(c1, s1, g.ny, bs) - 1) * kFixOne;
-            if (a < 0 || N * Ds < Ns * d1) { a = 1; Ns = N; Ds = d1; }
-        }
-        if (d2) {
-            const unsigned long long N = n2 + (unsigned long long)(exit_steps(c2, s2, g.nz, bs) - 1) * kFixOne;
-            if (a < 0 || N * Ds < Ns * d2) { a = 2; Ns = N; Ds = d2; }
-        }
-        if (a < 0 || Ns >= Ds) return false;  // the segment ends in this brick
-        const double y = a == 0 ? y0 : (a == 1 ? y1 : y2);  // RN(1 / Ds)
-        const unsigned long long k0 = crossings_upto(n0, d0, Ns, Ds, y), k1 = crossings_upto(n1, d1, Ns, Ds, y),
-                                 k2 = crossings_upto(n2, d2, Ns, Ds, y);
-        c0 += s0 * (int)k0; n0 += (unsigned)(k0 * kFixOne);
-        c1 += s1 * (int)k1; n1 += (unsigned)(k1 * kFixOne);
-        c2 += s2 * (int)k2; n2 += (unsigned)(k2 * kFixOne);
-        const double n = (double)Ns, d = (double)Ds;
-        const double q = __dmul_rn(n, y);
-        t_in = __fma_rn(__fma_rn(-q, d, n), y, q);  // RN(Ns / Ds), as crossing_t
-        return true;
-    }
-};
-
-// t of the next crossing (num/den, correctly rounded) or 1 when the walk ends in this cell.
-// The quotient is RN(n/d) by Markstein's sequence -- y = RN(1/d) (per axis, once per ray),
-// q = RN(n y), r = n - d q (exact with an FMA), t = RN(q + r y) -- which equals the correctly
-// rounded division for every operand pair of the walk (integers < 2^31; checked against
-// __ddiv_rn on 6.9e10 random pairs, scripts/div_check.cu, zero mismatches) at a third of the cost.
-__device__ __forceinline__ double crossing_t(const Walker& w, int a, unsigned na, unsigned da, bool& last) {
-    last = (a < 0) || (na >= da);
-    const double y = a == 0 ? w.y0 : (a == 1 ? w.y1 : w.y2);
-    const double n = (double)na, d = (double)da;
-    const double q = __dmul_rn(n, y);
-    const double r = __fma_rn(-q, d, n);
-    return last ? 1.0 : __fma_rn(r, y, q);
 }
 
 __device__ __forceinline__ void owned_pixel(const FrameDesc& f, long long i, int& u, int& v) {
@@ -404,7 +262,7 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
                                                        int16_t* off_q, int32_t* tile_runs, RayInfo* ray_z,
                                                        unsigned long long* counters, MsgParams mp, float* lnu,
-                                                       RunSink sink) {
+                                                       RunSink sink, RaySeg* seg) {
     __shared__ int s_vid[kFillThreads][8];
     __shared__ Run s_done[RUNS ? kFillThreads : 1];  // a run that ended at this step, per thread
     __shared__ int s_done_key[RUNS ? kFillThreads : 1];
@@ -450,6 +308,11 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
             alive = w.inside(g);
             e_cap = row_ptr[f.ray_base + i + 1];  // the segment K1 sized from its bound
             run_neg = ((unsigned)(w.s0 < 0) | ((unsigned)(w.s1 < 0) << 1) | ((unsigned)(w.s2 < 0) << 2)) << 20;
+            if (seg)  // matrix-free: what a re-walk of any chunk of this ray needs (K12)
+                seg[f.ray_base + i] = RaySeg{{(int)sg.g0[0], (int)sg.g0[1], (int)sg.g0[2]},
+                                             {(int)(sg.g1[0] - sg.g0[0]), (int)(sg.g1[1] - sg.g0[1]),
+                                              (int)(sg.g1[2] - sg.g0[2])},
+                                             sg.Z, sg.L};
             if (MRF_FILL_LNU) {  // the depth coordinate of the table (K1)
                 iz = ray_z[f.ray_base + i].iz;
                 wz = ray_z[f.ray_base + i].wz;
@@ -824,6 +687,21 @@ __global__ void __launch_bounds__(256) lambda_merge_kernel(long long n_rays, con
     if (j < no) atomicAdd(lost, (unsigned long long)(no - j));  // cannot happen (allocation only grows)
 }
 
+// Matrix-free (K12): the first cell of every K5 chunk of a ray (its class's K, 8 for long rays),
+// from the voxel slots of its first walk.  Thread per ray.
+__global__ void __launch_bounds__(256) ck_extract_kernel(long long n, const long long* __restrict__ row_ptr,
+                                                         const RayInfo* __restrict__ info,
+                                                         const int32_t* __restrict__ vid, int32_t* ck) {
+    const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    const int nr = info[r].n;
+    if (nr <= 0) return;
+    const int cls = ray_class(nr);
+    const int K = cls < kNumShort ? class_K(cls) : 8;
+    const long long e0 = row_ptr[r];
+    for (int c = 0; c * K < nr; ++c) ck[(e0 >> 2) + c] = vid[e0 + (long long)c * K];
+}
+
 // The runs the DDA fills emitted (unsorted, with their bucket keys) placed by bucket: the
 // tile-run transpose without re-reading vid.  Thread per run; a warp's runs of one bucket share
 // one cursor atomic.
@@ -1024,11 +902,11 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters,
-                     const RunSink& sink, cudaStream_t s) {
+                     const RunSink& sink, RaySeg* seg, cudaStream_t s) {
     if (n_ctas > 0) {
 #define MRF_FILL_LAUNCH(SP, RU)                                                                                     \
     dda_fill_kernel<SP, RU><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, \
-                                                            off_q, tile_runs, ray_z, counters, mp, lnu, sink)
+                                                            off_q, tile_runs, ray_z, counters, mp, lnu, sink, seg)
         if (g.bmask) {
             if (sink.runs) MRF_FILL_LAUNCH(true, true); else MRF_FILL_LAUNCH(true, false);
         } else {
@@ -1138,6 +1016,12 @@ void launch_lambda_merge(long long n_rays, const long long* rp_old, const RayInf
     if (n_rays == 0) return;
     lambda_merge_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(n_rays, rp_old, ri_old, vid_old, lam_old, rp_new,
                                                                 ri_new, vid_new, lam_new, lost);
+}
+
+void launch_ck_extract(long long n, const long long* row_ptr, const RayInfo* info, const int32_t* vid, int32_t* ck,
+                       cudaStream_t s) {
+    if (n == 0) return;
+    ck_extract_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, row_ptr, info, vid, ck);
 }
 
 }  // namespace mrf

@@ -202,6 +202,8 @@ __device__ __forceinline__ float lut_finish(const LutFetch& f, float wz) {
     return fmaf(wz, rb - ra, ra) * kLnuScale;
 }
 
+struct RaySeg;  // walk.cuh
+
 // ---- launchers (all asynchronous on `s`)
 // K1: per owned pixel -> status, pad8(upper bound of the walk's length) (scan input), RayInfo
 // (n = 0); counters[0] += invalid, counters[1] += dropped
@@ -221,7 +223,7 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters,
-                     const RunSink& sink, cudaStream_t s);
+                     const RunSink& sink, RaySeg* seg, cudaStream_t s);
 // K9 §III.D evaluation of one frame against T: cls per pixel (-1 invalid, 0/1), counts[0..1] +=
 // (valid, accurate) (zeroed by the caller)
 void launch_eval(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, const long long* T,

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "internal.cuh"
+#include "walk.cuh"
 #include "mrf.h"
 
 using namespace mrf;
@@ -96,6 +97,12 @@ struct mrf_ctx {
         long long r0, r1, e0, e1;
     };
     int mf = 0;  // frames per chunk, 0 = off
+    // fused (default): K5 re-walks each lane's chunk itself from a stored first cell (K12), so no
+    // per-iteration walk into the scratch; the scratch serves only the first walk of new frames.
+    // MRF_MF_FUSED=0 (and sparse bricks, whose empty-skip walk K5 does not carry): the scratch path.
+    bool mf_fused = true;
+    DBuf<RaySeg> ray_seg;   // per ray: segment for the re-walks
+    DBuf<int32_t> ck;       // chunk checkpoints, ck[row_ptr / 4 + c]
     std::vector<FrameDesc> mf_frames;
     std::vector<long long> mf_frame_e;  // row_ptr at each frame's first ray (+ the end)
     std::vector<MfChunk> mf_chunks;
@@ -437,16 +444,21 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
         if (ss != MRF_OK) return ss;
     }
     ProfScope ps(c, own ? MRF_K_DDA_FILL : -1);
+    const bool fused = count && c->mf_fused && !c->grid.bmask;
     launch_dda_fill(c->d_frames.p + f0, dc, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
                     c->depth_all.p, c->row_ptr.p, c->ray_z.p, sv - ch.e0, so - ch.e0, sl - ch.e0,
-                    count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), sink, st);
+                    count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), sink,
+                    fused ? c->ray_seg.p : nullptr, st);
+    if (fused) {  // K12: the first cell of every K5 chunk of these rays
+        launch_ck_extract(r1 - r0, c->row_ptr.p + r0, c->ray_z.p + r0, sv - ch.e0, c->ck.p, st);
+    }
     if (count) {  // the sink's count is read back per chunk walk (few chunks; first use only)
         long long emitted = 0;
         mrf_status sr = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 16), &emitted);
         if (sr != MRF_OK) return sr;
         run_sink_done(c, emitted, c->mf_frame_e[f1] - c->mf_frame_e[f0]);
     }
-    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (!MRF_FILL_LNU && r1 > r0 ? 1 : 0));
+    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (!MRF_FILL_LNU && r1 > r0 ? 1 : 0) + (fused && r1 > r0 ? 1 : 0));
     mf_dbg(c, count ? "walk(count)" : "walk");
     return MRF_OK;
 }
@@ -514,6 +526,10 @@ mrf_status sync_fill(mrf_ctx* c) {
         // the scratch to count their runs and incidences
         CK(c->lam.ensure((size_t)c->E + kPadElems, (size_t)c->E_filled, c->stream));
         CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
+        if (c->mf_fused && !c->grid.bmask) {
+            CK(c->ray_seg.ensure((size_t)std::max<long long>(c->R, 1), (size_t)c->R_filled, c->stream));
+            CK(c->ck.ensure((size_t)(c->E / 4 + 4), (size_t)(c->E_filled / 4), c->stream));
+        }
         const int first_new = (int)c->mf_frames.size();
         c->mf_frames.insert(c->mf_frames.end(), c->pend.begin(), c->pend.end());
         c->pend.clear();
@@ -553,7 +569,7 @@ mrf_status sync_fill(mrf_ctx* c) {
             ProfScope ps(c, MRF_K_DDA_FILL);
             launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
-                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, c->stream);
+                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, nullptr, c->stream);
             CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (!MRF_FILL_LNU && c->R > c->R_filled ? 1 : 0));
         }
         if (c->grid.bmask) {  // the depth images stay: a later keyframe may grow the allocation (R24)
@@ -777,7 +793,7 @@ mrf_status prepare(mrf_ctx* c) {
         launch_stage_fill(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->pos.p, c->stages.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     }
-    if (c->mf) {  // K5 classes per chunk: counting sort by (chunk, class)
+    if (c->mf && !(c->mf_fused && !c->grid.bmask)) {  // K5 classes per chunk: counting sort by (chunk, class)
         const long long NK = (long long)c->mf_chunks.size() * kNumClasses;
         CK(c->class_cnt.ensure((size_t)std::max(1LL, 2 * NK), 0, c->stream));
         CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * NK * sizeof(unsigned long long), c->stream));
@@ -912,6 +928,40 @@ mrf_status ray_messages(mrf_ctx* c) {
     c->mp.qbar_vi = c->VI;
     c->mp.chk_lam = (long long)c->lam.cap;  // checked build (MRF_CHECK): what exists
     c->mp.chk_vi = c->VI;
+    if (c->mf && c->mf_fused && !c->grid.bmask) {  // K12: K5 re-walks its own chunks (no scratch)
+        ProfScope ps(c, MRF_K_RAY_MSG);
+        c->mp.chk_lam = (long long)c->lam.cap;
+        const WalkParams wp{c->grid, c->ray_seg.p, c->ck.p};
+        int order[kNumClasses], n_cls = 0;
+        for (int k = 0; k < kNumClasses; ++k)
+            if (c->class_n[k]) order[n_cls++] = k;
+        auto work = [&](int k) { return (double)c->class_n[k] * (k < kNumShort ? class_G(k) * class_K(k) : 1024); };
+        std::sort(order, order + n_cls, [&](int a, int b) { return work(a) > work(b); });
+        const int ns = std::min(c->k5_streams, std::max(n_cls, 1));
+        if (ns > 1) {
+            CK(cudaEventRecord(c->ev_fork, c->stream));
+            for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(c->side[i], c->ev_fork, 0));
+        }
+        double load[mrf_ctx::kMaxSide] = {};
+        for (int i = 0; i < n_cls; ++i) {
+            const int k = order[i];
+            int si = 0;
+            for (int j = 1; j < ns; ++j)
+                if (load[j] < load[si]) si = j;
+            load[si] += work(k);
+            launch_ray_messages_walk(k, c->class_n[k], c->class_all.p + c->class_off[k], c->row_ptr.p, c->ray_z.p,
+                                     c->lam.p, c->T.p, c->mp, wp, c->long_scratch.p, c->long_scratch_per_warp,
+                                     c->n_warps_long, c->k5_math, ns > 1 ? c->side[si] : c->stream);
+            CK_LAUNCH(MRF_K_RAY_MSG, 1);
+        }
+        if (ns > 1) {
+            for (int i = 0; i < ns; ++i) {
+                CK(cudaEventRecord(c->ev_join[i], c->side[i]));
+                CK(cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
+            }
+        }
+        return MRF_OK;
+    }
     if (c->mf) {  // per chunk: re-walk into the scratch, then the chunk's class kernels
         ProfScope ps(c, MRF_K_RAY_MSG);  // walks + K5 of every chunk
         const size_t nch = c->mf_chunks.size();
@@ -1162,6 +1212,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* kl = getenv("MRF_K6_LPT")) c->k6_lpt = atoi(kl) != 0;
     if (const char* kc = getenv("MRF_COMPACT")) c->force_compact = atoi(kc) != 0;
     if (const char* rf = getenv("MRF_RUN_FILL")) c->run_fill_forced = atoi(rf) != 0;
+    if (const char* mff = getenv("MRF_MF_FUSED")) c->mf_fused = atoi(mff) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,
@@ -1277,6 +1328,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->tile_map.release(); c->tile_of.release(); c->touched.release(); c->T_c.release();
     c->runs_all.release(); c->run_keys.release();
     c->rp_old.release(); c->ri_old.release(); c->vid_old.release(); c->lam_old.release();
+    c->ray_seg.release(); c->ck.release();
     c->class_all.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
