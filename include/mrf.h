@@ -180,7 +180,9 @@ mrf_status mrf_export_rays(mrf_ctx* ctx, int64_t n, const int32_t* frame, const 
  * voxel is unspecified).  Builds the transpose if needed.  Synchronises. */
 mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr);
 
-/* Messages lambda_e (nats) of this rank in canonical order, host buffer of E floats. */
+/* Messages lambda_e (nats) of this rank in canonical order, host buffer of E floats.
+ * MRF_ERR_STATE in keyframe-average mode with matrix-free walks (no per-incidence messages are
+ * kept there; mrf_export_keyframe_average exports the state). */
 mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda);
 
 /* Replace the messages (host buffer of E floats, nats; quantised to 2^-23 and clipped to
@@ -214,10 +216,14 @@ int64_t mrf_belief_slots(const mrf_ctx* ctx);
  *     voxel from a single keyframe send the same average message"): per (frame, voxel) the
  *     average of the normalised messages of the frame's rays, lbar = ln(mean mu(1) / mean mu(0))
  *     (uniform when the frame has no ray through the voxel); T_v = sum over frames of lbar; a
- *     ray of frame f sees the cavity L0 + T_v - lbar[f][v].  mu(1), mu(0) are summed in fp64 (so
- *     the average does not depend on the summation order beyond fp64 rounding, far below the
- *     2^-23 quantisation of lbar); messages are still computed and stored per incidence.  Costs
- *     20 bytes per (frame, belief slot) of device memory.
+ *     ray of frame f sees the cavity L0 + T_v - lbar[f][v].  The sums of mu(1), mu(0) are exact
+ *     integer sums of fixed-point small probabilities (2^-30, relative to the largest term when
+ *     the messages have one sign, so down to e^-256), so the average does not depend on the
+ *     summation order.  Costs 20 bytes per (frame, belief slot) of device memory.  With the stored
+ *     graph the messages are still stored per incidence (mrf_export_messages works); with
+ *     matrix-free walks (mrf_set_matrix_free) they are not kept at all -- only a scratch of one
+ *     chunk of frames between the message pass and the averaging of that chunk -- which is the
+ *     paper's storage: keyframes re-traced every pass, one average message per (keyframe, voxel).
  * Set before the first frame (MRF_ERR_STATE otherwise); single rank only (MRF_ERR_INVALID_ARG
  * with world > 1).  Frame ids are the mrf_add_frame order (frame_id_out). */
 enum { MRF_MSG_PER_RAY = 0, MRF_MSG_KEYFRAME_AVG = 1 };
@@ -233,10 +239,14 @@ mrf_status mrf_export_keyframe_average(mrf_ctx* ctx, int64_t frame, float* out);
  * an allocated brick; all pixels count, whatever the rank), and the ray walk emits only cells of
  * allocated bricks (empty skip: unallocated space holds no variable, i.e. a certainly-empty voxel
  * in Eq.13/14; its marginal stays gamma).  Beliefs stay dense in device memory.  Set before the
- * first frame (MRF_ERR_STATE otherwise); every keyframe must be added before the graph is first
- * used (iterate, export, sizes): a later mrf_add_frame returns MRF_ERR_STATE.  The rays are then
- * counted and walked once against the final allocation, so the 2^31 incidence-slot capacity is
- * checked then: MRF_ERR_CAPACITY from the first call that uses the graph (mrf_reset starts over).
+ * first frame (MRF_ERR_STATE otherwise).  The rays are counted and walked against the allocation
+ * of every frame added so far when the graph is next used (iterate, export, sizes), so the 2^31
+ * incidence-slot capacity is checked then: MRF_ERR_CAPACITY from that call (mrf_reset starts
+ * over).  A frame added after the graph was used grows the allocation under rays already walked
+ * (reading R24): every frame is walked again at the next use, each old incidence keeps its
+ * message and the cells of new bricks start at 0 (the beliefs do not change); the depth images
+ * are kept for this (W*H floats per frame).  With matrix-free walks the allocation is fixed once
+ * the graph is used (a later mrf_add_frame returns MRF_ERR_STATE).
  * mrf_reset clears the allocation and keeps the mode. */
 mrf_status mrf_set_sparse_bricks(mrf_ctx* ctx, int32_t brick);
 /* Allocation mask: out (nullable) = ceil(nz/B) * ceil(ny/B) * ceil(nx/B) bytes, brick x fastest,
@@ -246,10 +256,14 @@ mrf_status mrf_export_bricks(mrf_ctx* ctx, uint8_t* out, int64_t* n_allocated);
 /* Matrix-free iteration (the paper re-traces every keyframe each pass,
  * P:200).  frames_per_chunk = 0: the ray->voxel lists (vid, off_q, log nu: 10 bytes per
  * incidence) are stored once (default).  frames_per_chunk = F > 0: only the messages (4 bytes per
- * incidence) and the tile-run transpose (~1 byte per incidence) persist; the rays of each chunk
- * of F frames are walked again by the DDA into a scratch the size of one chunk, for the
- * transpose build and before every message pass.  Same results as the stored graph (the walk is
- * the same integer DDA), at the cost of one DDA walk per iteration.  The depth images are kept
+ * incidence) and the tile-run transpose (~1 byte per incidence) persist, plus a 40-byte segment
+ * per ray and the first cell of every message-kernel chunk (<= 1 byte per incidence): the message
+ * kernel re-walks each chunk of a ray with the same integer DDA in registers (K12).  New frames
+ * are walked once into a scratch of one chunk of F frames (counting, tile runs, checkpoints).
+ * Same results as the stored graph, bit for bit, at the cost of one DDA walk per iteration
+ * (environment MRF_MF_FUSED=0: the chunks are walked into the scratch before every message pass
+ * instead; also the path taken with sparse bricks).  With keyframe-average messages the
+ * per-incidence messages are not stored either (mrf_set_message_mode).  The depth images are kept
  * (W*H floats per frame).  Set before the first frame (MRF_ERR_STATE otherwise);
  * environment MRF_SYNC_DEBUG=1 synchronises after every matrix-free step and reports its status on
  * stderr (debugging aid);

@@ -353,11 +353,21 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
 // G lanes per ray (32/G rays per warp), K incidences per lane: capacity G*K.  Incidence indices
 // are 32-bit (a ctx holds < 2^31 slots), and the per-element masks are selects on the lane's
 // valid count nv, so the only divergence is a lane without a chunk skipping its loads.
+// Resident CTAs of 256 threads per SM: K <= 8 classes fit 40 registers without spills, so 6 CTAs
+// (48 warps; frames30 K5 3.418 -> 3.366 ms per iteration against 4 CTAs); K <= 6 fit 32: 7 CTAs
+// (-> 3.281 ms); K > 8: 2 CTAs.  The matrix-free walk kernels carry the walker too: 5 CTAs
+// (<= 51 registers; 4: 98.1, 5: 96.8 ms of K5 per 10 iterations).
 #ifndef MRF_K5_MIN_BLOCKS
-#define MRF_K5_MIN_BLOCKS 4
+#define MRF_K5_MIN_BLOCKS 6
+#endif
+#ifndef MRF_K5_MIN_BLOCKS_SMALL
+#define MRF_K5_MIN_BLOCKS_SMALL 7
+#endif
+#ifndef MRF_K5_WALK_MIN_BLOCKS
+#define MRF_K5_WALK_MIN_BLOCKS 5
 #endif
 template <int G, int K, int M, bool AVG>
-__global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS : MRF_K5_MIN_BLOCKS_SMALL))) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ ray_z,
                                                          const int32_t* __restrict__ vid,
@@ -482,7 +492,7 @@ __device__ __forceinline__ void load_chunk_walk(long long s, long long e0, long 
 }
 
 template <int G, int K, int M, bool AVG>
-__global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_MIN_BLOCKS)) ray_msg_walk_kernel(long long n, const int32_t* __restrict__ rays,
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_WALK_MIN_BLOCKS)) ray_msg_walk_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ ray_z, int32_t* lam,
                                                          const long long* __restrict__ T, MsgParams mp, WalkParams wp) {
@@ -875,26 +885,23 @@ struct AccLayout {
     }
 };
 
-// MODE 0: the beliefs, sum of q (int32 halves, exact).  MODE 1 (keyframe averages, reading R22):
-// per slot the counts of non-negative / negative messages (packed n_pos + 65536 n_neg, native
-// int32 shared atomics) and D = sum over non-negative messages of their small probability
-// s = mu(0) minus the same over negative messages (s = mu(1)), s = e^-|lambda| / (1 + e^-|lambda|)
-// in fp64 (down to e^-256), summed in an fp64 shared accumulator (shared float atomics of either
-// width are CAS loops on sm_100a) and flushed with fp64 global atomics.  Then
-//     sum mu(1) = n_pos - D,   sum mu(0) = n_neg + D,
-// both well conditioned: with n_neg = 0, sum mu(0) = D is a sum of positive terms; with both
-// counts >= 1 each sum is >= 1/2.  The value depends on the summation order only through fp64
-// rounding, far below the 2^-23 quantisation of the average.
-__device__ __forceinline__ double kf_small(int q) {
-    // y = e^-|lambda| = 2^-t, t = n + f: 2^-f by ex2.approx (relative 2^-22), 2^-n exactly in
-    // the fp64 exponent (|lambda| <= 256: n <= 369, far inside the fp64 range)
-    const float t = fabsf((float)q * kQInv) * kLog2e;
-    const float n = floorf(t);
-    const double y = (double)ex2(n - t) * __hiloint2double((1023 - (int)n) << 20, 0);
-    const double s = y * (double)__frcp_rn(1.f + (float)y);  // relative ~2^-22
-    return q >= 0 ? s : -s;
-}
-constexpr int kK6SmemKf = kTileSlots * (int)(sizeof(double) + sizeof(int));
+// MODE 0: the beliefs, sum of q (int32 halves, exact).
+// Keyframe averages (reading R22), two integer passes over the same (frame, tile) buckets:
+//   MODE 2: per slot the counts of non-negative / negative messages (packed n_pos + 65536 n_neg)
+//     and the smallest |q| (native int32 shared atomics) -> N (int64 n_pos + 2^32 n_neg) and M
+//     (uint32 min |q|) per (frame, slot);
+//   then per (frame, slot) the scale a = |lambda_min| if all its messages have one sign, else -1
+//     (kf_scale_kernel);
+//   MODE 3: D = sum of the messages' small probabilities s = e^-|lambda| / (1 + e^-|lambda|) in
+//     fixed point 2^-30, relative to s(a) when the slot's messages have one sign (a sum of
+//     same-signed terms, kept relative-accurate down to e^-256), absolute and signed
+//     (+ for lambda >= 0, - below) when they are mixed (then both sums below are >= 1/2):
+//     int32 halves in shared memory (native atomics), int64 per (frame, slot).
+// kf_finalize: sum mu(1) = n_pos - D, sum mu(0) = n_neg + D (mixed), or the one-signed forms with
+// S = s(a) D, in fp64.  Round 1 summed D in fp64 with CAS-loop shared atomics (7.1 ms per
+// iteration at frames30).
+constexpr float kKfFix = 1073741824.0f;  // 2^30
+constexpr double kKfFixInv = 1.0 / 1073741824.0;
 
 template <int MODE, bool PAD>
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
@@ -907,11 +914,12 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     extern __shared__ int smem[];
     using L = AccLayout<PAD>;
     static_assert(MODE == 0 || !PAD, "keyframe-average sums use the plain layout (shared memory)");
-    double* accd = reinterpret_cast<double*>(smem);        // MODE 1: D per slot (128 KB)
-    int* accn = smem + 2 * L::kSlots;                      // MODE 1: packed counts (64 KB)
-    constexpr int kAccInts = MODE == 0 ? 2 * L::kSlots : 3 * L::kSlots;
-    int* acc_lo = smem;                 // sum of (q & 0xffff), at L::index(slot)
-    int* acc_hi = smem + L::kSlots;     // sum of (q >> 16)
+    constexpr int kAccInts = MODE == 3 ? 3 * L::kSlots : 2 * L::kSlots;
+    int* acc_lo = smem;                 // MODE 0 / 3: sum of (v & 0xffff), at L::index(slot)
+    int* acc_hi = smem + L::kSlots;     // MODE 0 / 3: sum of (v >> 16)
+    int* accn = smem;                   // MODE 2: packed counts
+    unsigned* accm = reinterpret_cast<unsigned*>(smem + L::kSlots);  // MODE 2: min |q|
+    float* accs = reinterpret_cast<float*>(smem + 2 * L::kSlots);     // MODE 3: the bucket's scales
     uint4* sdesc = reinterpret_cast<uint4*>(smem + kAccInts) + (threadIdx.x >> 5) * 32;  // this warp's batch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // items: the first per CTA by index, then dynamically (a CTA whose items ran short takes the
@@ -921,11 +929,23 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     __shared__ int s_batch;
     // the accumulator is zeroed once here, then by each item's flush as it reads it
     for (int i = threadIdx.x; i < kAccInts / 4; i += kK6Threads) reinterpret_cast<int4*>(smem)[i] = int4{0, 0, 0, 0};
+    if constexpr (MODE >= 2) {
+        // the zeroing above and the writes below (MODE 2: min |q| starts at the maximum; MODE 3:
+        // the first item's scales) touch the same words from different threads
+        __syncthreads();
+        if constexpr (MODE == 2)
+            for (int i = threadIdx.x; i < L::kSlots; i += kK6Threads) accm[i] = 0xffffffffu;
+    }
     for (long long it = blockIdx.x; it < n_items;) {
         const int2 item = __ldg(items + it);
 #if MRF_K6_WARP_DYN
         if (threadIdx.x == 0) s_batch = kK6Warps;
 #endif
+        if constexpr (MODE == 3) {  // the bucket's per-slot scales (kf_scale_kernel)
+            const float* A = reinterpret_cast<const float*>(static_cast<long long*>(out) + 2 * n_out) +
+                             ((long long)item.x << kTileShift);
+            for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) accs[swz(i)] = __ldg(A + i);
+        }
         __syncthreads();
         const long long r0 = __ldg(tile_ptr + item.x) + (long long)item.y * per_item;
         long long r1 = __ldg(tile_ptr + item.x + 1);
@@ -985,9 +1005,20 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                         if constexpr (MODE == 0) {
                             atomicAdd(acc_lo + si, qv & 0xffff);
                             atomicAdd(acc_hi + si, qv >> 16);
-                        } else {
-                            atomicAdd(accd + si, kf_small(qv));
+                        } else if constexpr (MODE == 2) {
                             atomicAdd(accn + si, qv >= 0 ? 1 : 65536);
+                            atomicMin(accm + si, qv >= 0 ? (unsigned)qv : 0u - (unsigned)qv);
+                        } else {
+                            // s(|lambda|) / s(a) in fixed point (a = -1: mixed signs, absolute s)
+                            const float a = accs[si];
+                            const float al = (float)(qv >= 0 ? (unsigned)qv : 0u - (unsigned)qv) * (kQInv * kLog2e);
+                            const float ap = fmaxf(a, 0.f) * kLog2e;
+                            const float c = a < 0.f ? 1.f : 1.f + ex2(-ap);
+                            const float term = ex2(ap - al) * c * __frcp_rn(1.f + ex2(-al));
+                            int v = __float2int_rn(term * kKfFix);
+                            if (a < 0.f && qv < 0) v = -v;
+                            atomicAdd(acc_lo + si, v & 0xffff);
+                            atomicAdd(acc_hi + si, v >> 16);
                         }
                     }
                 }
@@ -1013,19 +1044,28 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                 acc_lo[a] = 0;
                 if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(Tt + i), (unsigned long long)sum);
             }
-        } else {  // out: D (fp64) then the packed counts (int64: n_pos + 2^32 n_neg), each [bucket][slot]
+        } else if constexpr (MODE == 2) {  // out: N (int64 n_pos + 2^32 n_neg) [n_out], D [n_out], M (uint32) [n_out]
             const long long o = (long long)item.x << kTileShift;
-            double* Dt = static_cast<double*>(out) + o;
-            unsigned long long* Nt = reinterpret_cast<unsigned long long*>(static_cast<double*>(out) + n_out) + o;
+            unsigned long long* Nt = static_cast<unsigned long long*>(out) + o;
+            unsigned* Mt = reinterpret_cast<unsigned*>(static_cast<unsigned long long*>(out) + 2 * n_out) + o;
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
                 const unsigned cn = (unsigned)accn[swz(i)];
-                const double dv = accd[swz(i)];
+                const unsigned mq = accm[swz(i)];
                 accn[swz(i)] = 0;
-                accd[swz(i)] = 0.0;
+                accm[swz(i)] = 0xffffffffu;
                 if (cn) {
-                    atomicAdd(Dt + i, dv);
                     atomicAdd(Nt + i, (unsigned long long)(cn & 0xffffu) | ((unsigned long long)(cn >> 16) << 32));
+                    atomicMin(Mt + i, mq);
                 }
+            }
+        } else {  // MODE 3: D (int64, 2^-30) [n_out .. 2 n_out)
+            const long long o = (long long)item.x << kTileShift;
+            unsigned long long* Dt = static_cast<unsigned long long*>(out) + n_out + o;
+            for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
+                const long long sum = (long long)acc_hi[swz(i)] * 65536 + (long long)acc_lo[swz(i)];
+                acc_hi[swz(i)] = 0;
+                acc_lo[swz(i)] = 0;
+                if (sum) atomicAdd(Dt + i, (unsigned long long)sum);
             }
         }
         if (next) {  // (this barrier also ends the flush before the next item's adds)
@@ -1062,7 +1102,7 @@ inline unsigned blocks_for(long long n, int b) { return (unsigned)((n + b - 1) /
 // may drive ctxs on several GPUs) and the device's SM count (grid sizing).
 struct DevCfg {
     int sms = 0;
-    bool k6[2][2] = {};
+    bool k6[4][2] = {};
 };
 DevCfg& dev_cfg() {
     static thread_local DevCfg cfg[64];
@@ -1203,7 +1243,7 @@ template <int MODE, bool PAD>
 void launch_tile_reduce_t(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                           const int32_t* lam, int per_item, void* out, long long n_out, unsigned* next,
                           const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s) {
-    constexpr int smem = (MODE == 0 ? 2 * AccLayout<PAD>::kSlots * (int)sizeof(int) : kK6SmemKf) + kK6Desc;
+    constexpr int smem = (MODE == 3 ? 3 : 2) * AccLayout<PAD>::kSlots * (int)sizeof(int) + kK6Desc;
     DevCfg& dc = dev_cfg();
     if (!dc.k6[MODE][PAD]) {
         cudaFuncSetAttribute(tile_reduce_kernel<MODE, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1228,12 +1268,34 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
                                        chk_out_tiles, s);
 }
 
-void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
-                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, long long chk_lam,
-                    cudaStream_t s) {
+void launch_kf_sums(int pass, long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
+                    const int32_t* lam, int per_item, long long* sums, long long n_slots, unsigned* next,
+                    long long chk_lam, cudaStream_t s) {
     if (n_items == 0) return;
-    launch_tile_reduce_t<1, false>(n_items, items, bucket_ptr, runs, lam, per_item, D, n_slots, next, nullptr, chk_lam,
-                                   n_slots >> kTileShift, s);
+    if (pass == 0)
+        launch_tile_reduce_t<2, false>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots, next, nullptr,
+                                       chk_lam, n_slots >> kTileShift, s);
+    else
+        launch_tile_reduce_t<3, false>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots, next, nullptr,
+                                       chk_lam, n_slots >> kTileShift, s);
+}
+
+// between the passes: M (min |q|) -> the scale a (nats, float, in place) per (frame, slot):
+// |lambda_min| when the slot's messages have one sign, -1 when mixed (or none)
+__global__ void kf_scale_kernel(long long n, const unsigned long long* __restrict__ N, unsigned* M) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long cn = N[i];
+    const bool one_sign = cn != 0 && ((cn & 0xffffffffull) == 0 || (cn >> 32) == 0);
+    const float a = one_sign ? (float)((double)M[i] * kQInvD) : -1.f;
+    M[i] = __float_as_uint(a);
+}
+
+void launch_kf_scale(long long n_slots, long long first, long long count, long long* sums, cudaStream_t s) {
+    if (count <= 0) return;
+    kf_scale_kernel<<<blocks_for(count, 256), 256, 0, s>>>(
+        count, reinterpret_cast<const unsigned long long*>(sums) + first,
+        reinterpret_cast<unsigned*>(sums + 2 * n_slots) + first);
 }
 
 // world > 1: the all-reduced sums of the touched tiles (compact order) back to their tiles
@@ -1255,9 +1317,10 @@ void launch_tile_scatter(long long n_tiles, const int32_t* tile_of, const long l
 }
 
 // Keyframe averages -> quantised log-odds per (frame, slot) and their sum per slot (thread per
-// slot, frames in order: T is an exact integer sum).
-__global__ void kf_finalize_kernel(long long F, long long VI, const double* __restrict__ D,
-                                   const unsigned long long* __restrict__ N, int32_t* qbar, long long* T) {
+// slot, frames in order: T is an exact integer sum).  sums = [N | D | A] per (frame, slot).
+__global__ void kf_finalize_kernel(long long F, long long VI, const unsigned long long* __restrict__ N,
+                                   const long long* __restrict__ D, const float* __restrict__ A, int32_t* qbar,
+                                   long long* T) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= VI) return;
     long long t = 0;
@@ -1266,9 +1329,17 @@ __global__ void kf_finalize_kernel(long long F, long long VI, const double* __re
         const unsigned long long cn = N[k];
         int qb = 0;
         if (cn) {
-            const double d = D[k];
-            const double s1 = (double)(cn & 0xffffffffull) - d, s0 = (double)(cn >> 32) + d;  // sum mu(1), mu(0)
-            const double lb = fmin(fmax(log(s1) - log(s0), -(double)kLambdaClip), (double)kLambdaClip);
+            const double np = (double)(cn & 0xffffffffull), nn = (double)(cn >> 32);
+            const double d = (double)D[k] * kKfFixInv;
+            double lb;
+            if (np > 0.0 && nn > 0.0) {  // mixed signs: sum mu(1) = n_pos - D, sum mu(0) = n_neg + D
+                lb = log(np - d) - log(nn + d);
+            } else {  // one sign: S = s(a) d, ln s(a) = -a - ln(1 + e^-a)
+                const double a = (double)A[k];
+                const double ls = -a - log1p(exp(-a)) + log(d);
+                lb = np > 0.0 ? log(np - exp(ls)) - ls : ls - log(nn - exp(ls));
+            }
+            lb = fmin(fmax(lb, -(double)kLambdaClip), (double)kLambdaClip);
             qb = lb >= (double)kLambdaClip ? 0x7fffffff : (int)__double2ll_rn(lb * (double)kQScale);
         }
         qbar[k] = qb;
@@ -1277,10 +1348,12 @@ __global__ void kf_finalize_kernel(long long F, long long VI, const double* __re
     T[v] = t;
 }
 
-void launch_kf_finalize(long long F, long long VI, const double* D, int32_t* qbar, long long* T, cudaStream_t s) {
+void launch_kf_finalize(long long F, long long VI, const long long* sums, int32_t* qbar, long long* T, cudaStream_t s) {
     if (VI == 0) return;
+    const long long n = F * VI;
     kf_finalize_kernel<<<(unsigned)((VI + 255) / 256), 256, 0, s>>>(
-        F, VI, D, reinterpret_cast<const unsigned long long*>(D + F * VI), qbar, T);
+        F, VI, reinterpret_cast<const unsigned long long*>(sums), sums + n,
+        reinterpret_cast<const float*>(sums + 2 * n), qbar, T);
 }
 
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s) {

@@ -347,14 +347,18 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
                         const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s);
 // T[tile_of[i] tile] = src[i-th compact tile] for i < n_tiles (16384 slots each)
 void launch_tile_scatter(long long n_tiles, const int32_t* tile_of, const long long* src, long long* T, cudaStream_t s);
-// keyframe averages (reading R22): per [bucket = frame * NT + tile][slot], D += signed small
-// probability of each message (fp64, D[0 .. n_slots)) and the packed counts n_pos + 2^32 n_neg
-// (int64, at D + n_slots); both zeroed by the caller (bp.cu tile_reduce_kernel<1>)
-void launch_kf_sums(long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
-                    const int32_t* lam, int per_item, double* D, long long n_slots, unsigned* next, long long chk_lam,
-                    cudaStream_t s);
+// keyframe averages (reading R22), two integer passes over the (frame * NT + tile) buckets into
+// sums = [N: int64 n_pos + 2^32 n_neg | D: int64, 2^-30 | M / A: uint32 min |q|, then float scale]
+// per [bucket][slot] (n_slots = F * VI each; N, D zeroed and M set to 0xffffffff by the caller):
+// pass 0 the counts and min |q|, then launch_kf_scale, then pass 1 the fixed-point sums of the
+// small probabilities (bp.cu tile_reduce_kernel<2 / 3>)
+void launch_kf_sums(int pass, long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
+                    const int32_t* lam, int per_item, long long* sums, long long n_slots, unsigned* next,
+                    long long chk_lam, cudaStream_t s);
+// (the (frame, slot) entries [first, first + count) of the n_slots)
+void launch_kf_scale(long long n_slots, long long first, long long count, long long* sums, cudaStream_t s);
 // qbar[f][v] = quantised clip(ln(sum mu(1) / sum mu(0)), +-256) (0 without a ray), T[v] = sum_f qbar
-void launch_kf_finalize(long long F, long long VI, const double* D, int32_t* qbar, long long* T, cudaStream_t s);
+void launch_kf_finalize(long long F, long long VI, const long long* sums, int32_t* qbar, long long* T, cudaStream_t s);
 void launch_marginals(const GridDesc& g, const long long* T, double L0, float* out, cudaStream_t s);
 void launch_lambda_to_float(long long n, const int32_t* q, float* out, cudaStream_t s);
 

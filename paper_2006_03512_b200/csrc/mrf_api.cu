@@ -103,6 +103,12 @@ struct mrf_ctx {
     bool mf_fused = true;
     DBuf<RaySeg> ray_seg;   // per ray: segment for the re-walks
     DBuf<int32_t> ck;       // chunk checkpoints, ck[row_ptr / 4 + c]
+    // keyframe averages + fused matrix-free walks (the paper's storage): the per-incidence
+    // messages are not state (K5 reads the keyframe averages), so they live only in a one-chunk
+    // scratch between K5 and K6' of the chunk; the K6' items are grouped by chunk
+    DBuf<int32_t> lam_chunk;
+    std::vector<long long> kf_item_off;  // K6' items of chunk ci: [kf_item_off[ci], kf_item_off[ci + 1])
+    bool kf_chunked() const { return kf_avg && mf && mf_fused && !grid.bmask; }
     std::vector<FrameDesc> mf_frames;
     std::vector<long long> mf_frame_e;  // row_ptr at each frame's first ray (+ the end)
     std::vector<MfChunk> mf_chunks;
@@ -125,7 +131,7 @@ struct mrf_ctx {
     DBuf<int32_t> vid_old, lam_old;
     long long sp_R_old = 0;
     DBuf<int32_t> qbar;           // [frame][VI] quantised average log-odds
-    DBuf<double> kf_sums;          // [frame][VI] fp64 D, then [frame][VI] int64 packed counts
+    DBuf<long long> kf_sums;       // [frame][VI] x {N int64, D int64 (2^-30), M/A uint32} (bp.cu)
     long long kf_frames_alloc = 0;
     long long n_bucket_groups() const { return kf_avg ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
@@ -373,6 +379,7 @@ mrf_status mf_rechunk(mrf_ctx* c) {
     CK(c->s_vid.ensure((size_t)big + kPadElems, 0, c->stream));
     CK(c->s_off.ensure((size_t)big + kPadElems, 0, c->stream));
     CK(c->s_lnu.ensure((size_t)big + kPadElems, 0, c->stream));
+    if (c->kf_chunked()) CK(c->lam_chunk.ensure((size_t)big + kPadElems, 0, c->stream));
     // the slack after the largest chunk is read (masked) by the last rays' lanes: valid ids
     CK(cudaMemsetAsync(c->s_vid.p, 0, sizeof(int32_t) * c->s_vid.cap, c->stream));
     if (c->k5_streams >= 2 && c->mf_chunks.size() > 1) {
@@ -524,8 +531,10 @@ mrf_status sync_fill(mrf_ctx* c) {
     if (!c->pend.empty() && c->mf) {
         // matrix-free: only lambda is stored per incidence; the new frames are walked once into
         // the scratch to count their runs and incidences
-        CK(c->lam.ensure((size_t)c->E + kPadElems, (size_t)c->E_filled, c->stream));
-        CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
+        if (!c->kf_chunked()) {  // (keyframe averages + fused walks: no per-incidence messages)
+            CK(c->lam.ensure((size_t)c->E + kPadElems, (size_t)c->E_filled, c->stream));
+            CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
+        }
         if (c->mf_fused && !c->grid.bmask) {
             CK(c->ray_seg.ensure((size_t)std::max<long long>(c->R, 1), (size_t)c->R_filled, c->stream));
             CK(c->ck.ensure((size_t)(c->E / 4 + 4), (size_t)(c->E_filled / 4), c->stream));
@@ -715,6 +724,14 @@ mrf_status build_tile_runs(mrf_ctx* c) {
         auto size = [&](const int2& it) { return std::min<long long>(c->k6_item, nr[it.x] - (long long)it.y * c->k6_item); };
         std::stable_sort(items.begin(), items.end(), [&](const int2& a, const int2& b) { return size(a) > size(b); });
     }
+    if (c->kf_chunked()) {  // items grouped by the frame chunk of their (frame, tile) bucket
+        auto chunk = [&](const int2& it) { return (long long)(it.x / c->NT) / c->mf; };
+        std::stable_sort(items.begin(), items.end(), [&](const int2& a, const int2& b) { return chunk(a) < chunk(b); });
+        const long long nch = (long long)c->mf_chunks.size();
+        c->kf_item_off.assign((size_t)nch + 1, 0);
+        for (const int2& it : items) ++c->kf_item_off[(size_t)chunk(it) + 1];
+        for (long long k = 0; k < nch; ++k) c->kf_item_off[(size_t)k + 1] += c->kf_item_off[(size_t)k];
+    }
     c->n_bitems = (long long)items.size();
     CK(c->bitems.ensure((size_t)std::max(1LL, c->n_bitems), 0, c->stream));
     if (c->n_bitems)
@@ -793,7 +810,7 @@ mrf_status prepare(mrf_ctx* c) {
         launch_stage_fill(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->pos.p, c->stages.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     }
-    if (c->mf && !(c->mf_fused && !c->grid.bmask)) {  // K5 classes per chunk: counting sort by (chunk, class)
+    if (c->mf && (!(c->mf_fused && !c->grid.bmask) || c->kf_chunked())) {  // K5 classes per (chunk, class)
         const long long NK = (long long)c->mf_chunks.size() * kNumClasses;
         CK(c->class_cnt.ensure((size_t)std::max(1LL, 2 * NK), 0, c->stream));
         CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * NK * sizeof(unsigned long long), c->stream));
@@ -883,7 +900,7 @@ mrf_status ensure_kf(mrf_ctx* c) {
     const size_t n = (size_t)(F * c->VI), used = (size_t)(c->kf_frames_alloc * c->VI);
     CK(c->qbar.ensure(n, used, c->stream));
     CK(cudaMemsetAsync(c->qbar.p + used, 0, sizeof(int32_t) * (n - used), c->stream));
-    CK(c->kf_sums.ensure(2 * n, 0, c->stream));
+    CK(c->kf_sums.ensure(2 * n + (n + 1) / 2, 0, c->stream));
     c->kf_frames_alloc = F;
     return MRF_OK;
 }
@@ -895,12 +912,16 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
         mrf_status st;
         if ((st = ensure_kf(c)) != MRF_OK) return st;
         const long long F = (long long)c->frames.size(), n = F * c->VI;
-        CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(double) * (size_t)n, c->stream));
-        launch_kf_sums(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
-                       c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr, (long long)c->lam.cap,
-                       c->stream);
+        CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(long long) * (size_t)n, c->stream));
+        CK(cudaMemsetAsync(c->kf_sums.p + 2 * n, 0xff, sizeof(unsigned) * (size_t)n, c->stream));
+        unsigned* nxt = c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr;
+        launch_kf_sums(0, c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
+                       nxt, (long long)c->lam.cap, c->stream);
+        launch_kf_scale(n, 0, n, c->kf_sums.p, c->stream);
+        launch_kf_sums(1, c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
+                       nxt, (long long)c->lam.cap, c->stream);
         launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, out, c->stream);
-        CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_bitems > 0 ? 1 : 0) + 1);
+        CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_bitems > 0 ? 2 : 0) + 2);
         mf_dbg(c, "kf sums");
         return MRF_OK;
     }
@@ -1041,6 +1062,53 @@ mrf_status ray_messages(mrf_ctx* c) {
             CK(cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
         }
     }
+    return MRF_OK;
+}
+
+// One flooding iteration in keyframe-average mode with fused matrix-free walks (kf_chunked): per
+// chunk of frames, K5 (walk kernels, the keyframe cavity) writes the chunk's messages into the
+// scratch, then K6' adds them into the (frame, slot) sums; then the averages and T.
+mrf_status kf_iteration(mrf_ctx* c) {
+    mrf_status st;
+    if ((st = ensure_kf(c)) != MRF_OK) return st;
+    const long long F = (long long)c->frames.size(), n = F * c->VI;
+    c->mp.qbar = c->qbar.p;
+    c->mp.qbar_vi = c->VI;
+    c->mp.chk_vi = c->VI;
+    CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(long long) * (size_t)n, c->stream));
+    CK(cudaMemsetAsync(c->kf_sums.p + 2 * n, 0xff, sizeof(unsigned) * (size_t)n, c->stream));
+    const WalkParams wp{c->grid, c->ray_seg.p, c->ck.p};
+    for (size_t ci = 0; ci < c->mf_chunks.size(); ++ci) {
+        const auto& ch = c->mf_chunks[ci];
+        int32_t* lam = c->lam_chunk.p - ch.e0;  // absolute slots [e0, e1) of this chunk
+        c->mp.chk_lam = ch.e1;
+        {
+            ProfScope ps(c, MRF_K_RAY_MSG);
+            for (int k = 0; k < kNumClasses; ++k) {
+                const long long key = (long long)ci * kNumClasses + k;
+                if (c->mf_cls_n[key] == 0) continue;
+                launch_ray_messages_walk(k, c->mf_cls_n[key], c->class_all.p + c->mf_cls_off[key], c->row_ptr.p,
+                                         c->ray_z.p, lam, c->T.p, c->mp, wp, c->long_scratch.p,
+                                         c->long_scratch_per_warp, c->n_warps_long, c->k5_math, c->stream);
+                CK_LAUNCH(MRF_K_RAY_MSG, 1);
+            }
+        }
+        {
+            ProfScope ps(c, MRF_K_VOXEL_SUM);
+            const long long i0 = c->kf_item_off[ci], i1 = c->kf_item_off[ci + 1];
+            unsigned* nxt = c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr;
+            launch_kf_sums(0, i1 - i0, c->bitems.p + i0, c->tile_ptr.p, c->runs.p, lam, c->k6_item, c->kf_sums.p, n,
+                           nxt, ch.e1, c->stream);
+            launch_kf_scale(n, (long long)ch.f0 * c->VI, (long long)(ch.f1 - ch.f0) * c->VI, c->kf_sums.p, c->stream);
+            launch_kf_sums(1, i1 - i0, c->bitems.p + i0, c->tile_ptr.p, c->runs.p, lam, c->k6_item, c->kf_sums.p, n,
+                           nxt, ch.e1, c->stream);
+            CK_LAUNCH(MRF_K_VOXEL_SUM, (i1 > i0 ? 2 : 0) + 1);
+        }
+        mf_dbg(c, "kf chunk");
+    }
+    ProfScope ps(c, MRF_K_VOXEL_SUM);
+    launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, c->T.p, c->stream);
+    CK_LAUNCH(MRF_K_VOXEL_SUM, 1);
     return MRF_OK;
 }
 
@@ -1328,7 +1396,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->tile_map.release(); c->tile_of.release(); c->touched.release(); c->T_c.release();
     c->runs_all.release(); c->run_keys.release();
     c->rp_old.release(); c->ri_old.release(); c->vid_old.release(); c->lam_old.release();
-    c->ray_seg.release(); c->ck.release();
+    c->ray_seg.release(); c->ck.release(); c->lam_chunk.release();
     c->class_all.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -1537,6 +1605,10 @@ mrf_status mrf_bp_iterate(mrf_ctx* ctx, int32_t n) {
     mrf_status st;
     if ((st = prepare(c)) != MRF_OK) return st;
     for (int it = 0; it < n; ++it) {
+        if (c->kf_chunked()) {
+            if ((st = kf_iteration(c)) != MRF_OK) return st;
+            continue;
+        }
         if ((st = ray_messages(c)) != MRF_OK) return st;
         if ((st = reduce_T(c)) != MRF_OK) return st;
     }
@@ -1826,6 +1898,10 @@ mrf_status mrf_export_transpose(mrf_ctx* ctx, int64_t* col_ptr, int32_t* tr) {
 mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda) {
     ENTER(ctx);
     if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    if (c->kf_chunked())
+        return set_err(c, MRF_ERR_STATE,
+                       "keyframe averages with matrix-free walks keep no per-incidence messages "
+                       "(mrf_export_keyframe_average exports the state)");
     if (!c->E) return MRF_OK;
     HostLayout h;
     mrf_status st;
@@ -1841,6 +1917,8 @@ mrf_status mrf_export_messages(mrf_ctx* ctx, float* lambda) {
 mrf_status mrf_import_messages(mrf_ctx* ctx, const float* lambda) {
     ENTER(ctx);
     if (!lambda) return set_err(c, MRF_ERR_INVALID_ARG, "NULL input");
+    if (c->kf_chunked())
+        return set_err(c, MRF_ERR_STATE, "keyframe averages with matrix-free walks keep no per-incidence messages");
     {
         mrf_status sf = sync_fill(c);
         if (sf != MRF_OK) return sf;

@@ -33,11 +33,11 @@ def run(mode):
     w = corridor() if mode == "long" else (synth.frames30(n_frames=3) if mode == "room" else synth.tiny_frames(n_frames=4))
     m = pkg.MRFMap.from_workload(w)
     with m:
-        if mode == "kfavg":
+        if mode in ("kfavg", "kfmf"):
             m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
         if mode == "sparse":
             m.set_sparse_bricks(8)
-        if mode == "mf":
+        if mode in ("mf", "kfmf"):
             m.set_matrix_free(2)
         for fr in w.frames[:-1] if len(w.frames) > 1 and mode != "sparse" else w.frames:
             m.add_frame(fr.depth, fr.K, fr.T_wc)
@@ -47,10 +47,11 @@ def run(mode):
             m.add_frame(fr.depth, fr.K, fr.T_wc)
         m.bp_iterate(2)
         m.marginals()
-        lam = m.export_messages()
-        m.import_messages(lam)
+        if mode != "kfmf":  # (keyframe averages + matrix-free walks keep no per-incidence messages)
+            lam = m.export_messages()
+            m.import_messages(lam)
         m.bp_iterate(1)
-        if mode not in ("mf",):
+        if mode not in ("mf", "kfmf"):
             g = m.export_graph()
             m.export_rays(g["frame"][:50], g["pixel"][:50])
             m.export_transpose()

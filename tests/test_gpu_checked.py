@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 MODES = [("default", {}), ("staged", {"MRF_K5": "staged"}), ("voxel", {"MRF_K6": "voxel"}),
          ("compact", {"MRF_COMPACT": "1"}), ("runfill", {"MRF_RUN_FILL": "1"}), ("long", {}), ("kfavg", {}),
-         ("sparse", {}), ("mf", {}), ("room", {})]
+         ("sparse", {}), ("mf", {}), ("kfmf", {}), ("room", {})]
 
 
 @pytest.mark.parametrize("mode,env", MODES, ids=[m for m, _ in MODES])

@@ -165,3 +165,29 @@ def test_kfavg_import_and_warm_start(tf4):
     lam_ref, lbar_ref, T_ref = oracle.kf_bp(p, g, 2, F=F, lbar=lb0)
     assert _msg_err(lam, lam_ref) <= MSG_TOL
     assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+@pytest.mark.parametrize("mf", [0, 1])
+def test_kfavg_deterministic(tf4, mf):
+    """The keyframe averages are exact integer sums (counts, min |q|, fixed-point small
+    probabilities): byte-identical averages and beliefs across runs, every iteration, with the
+    stored graph and with matrix-free walks (chunked, no per-incidence messages)."""
+    F = len(tf4.frames)
+    runs = []
+    for _ in range(3):
+        m = pkg.MRFMap.from_workload(tf4)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+        if mf:
+            m.set_matrix_free(mf)
+        out = []
+        with m:
+            for fr in tf4.frames:
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            for _ in range(4):
+                m.bp_iterate(1)
+                out.append((np.stack([m.export_keyframe_average(f) for f in range(F)]), m.export_beliefs()))
+        runs.append(out)
+    for other in runs[1:]:
+        for (a, ta), (b, tb) in zip(runs[0], other):
+            assert np.array_equal(a, b) and np.array_equal(ta, tb)

@@ -30,7 +30,11 @@ def _run(w, n_iter, mf=0, kf=False, bricks=0, frames=None):
     with m:
         m.bp_iterate(n_iter)
         sizes = m.graph_sizes(active=not mf)
-        return m.export_messages(), m.export_beliefs(), m.marginals(), sizes
+        if kf and mf and not bricks:  # keyframe averages + fused walks: the averages are the state
+            lam = np.stack([m.export_keyframe_average(f) for f in range(len(frames or w.frames))])
+        else:
+            lam = m.export_messages()
+        return lam, m.export_beliefs(), m.marginals(), sizes
 
 
 @pytest.mark.parametrize("mf", [1, 2, 3])
@@ -51,7 +55,19 @@ def test_matrix_free_frame1_and_modes():
     for kw in (dict(kf=True), dict(bricks=8), dict(kf=True, bricks=8)):
         x = _run(t, 4, **kw)
         y = _run(t, 4, mf=2, **kw)
-        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), kw
+        if kw.get("kf") and not kw.get("bricks"):  # (per-incidence messages are not kept: compare averages)
+            F = len(t.frames)
+            m = pkg.MRFMap.from_workload(t)
+            m.set_stream(torch.cuda.current_stream().cuda_stream)
+            m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+            with m:
+                for fr in t.frames:
+                    m.add_frame(fr.depth, fr.K, fr.T_wc)
+                m.bp_iterate(4)
+                xa = np.stack([m.export_keyframe_average(f) for f in range(F)])
+            assert np.array_equal(xa, y[0]) and np.array_equal(x[1], y[1]), kw
+        else:
+            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), kw
 
 
 def test_matrix_free_warm_start_and_rules():
@@ -106,3 +122,54 @@ def test_matrix_free_matches_oracle_frame1():
     """The single-frame room (26 M incidences), full trajectory over 2 iterations (where the
     loopy graph is still well conditioned)."""
     _oracle_leg(synth.single_frame(), 2, 1)
+
+
+@pytest.mark.parametrize("mf", [1, 3])
+def test_keyframe_average_matrix_free_storage_and_parity(mf):
+    """The paper's own storage (keyframes re-traced every pass, "an auxiliary buffer that
+    stores the average outgoing message"): keyframe averages with fused matrix-free walks keep no
+    per-incidence messages -- only a one-chunk scratch between K5 and K6' -- and give keyframe
+    averages and beliefs bit-identical to the stored keyframe-average path, which matches the
+    oracle's kf_bp; warm start (a keyframe added after iterating) included."""
+    w = synth.tiny_frames(n_frames=4)
+    F = len(w.frames)
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    _, lbar_ref, T_ref = oracle.kf_bp(p, g, 5, F=F)
+    outs = []
+    for m_f in (0, mf):
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+        if m_f:
+            m.set_matrix_free(m_f)
+        with m:
+            for fr in w.frames:
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(5)
+            lbar = np.stack([m.export_keyframe_average(f) for f in range(F)])
+            outs.append((lbar, m.export_beliefs(), m.marginals()))
+            if m_f:
+                with pytest.raises(pkg.MrfError) as e:
+                    m.export_messages()
+                assert e.value.status == 6
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    err = np.abs(outs[1][0].astype(np.float64).reshape(-1) - lbar_ref.reshape(-1)) / np.maximum(1.0, np.abs(lbar_ref.reshape(-1)))
+    assert err.max() <= 1e-3
+    assert np.max(np.abs(outs[1][2] - oracle.marginals(p, T_ref))) <= 1e-4
+    # warm start: 3 keyframes, iterate, add the 4th, iterate -- equal to the stored path
+    res = []
+    for m_f in (0, mf):
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+        if m_f:
+            m.set_matrix_free(m_f)
+        with m:
+            for fr in w.frames[:3]:
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(3)
+            m.add_frame(w.frames[3].depth, w.frames[3].K, w.frames[3].T_wc)
+            m.bp_iterate(2)
+            res.append((np.stack([m.export_keyframe_average(f) for f in range(F)]), m.export_beliefs()))
+    assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
