@@ -461,6 +461,11 @@ __device__ __forceinline__ void walk_chunk(const WalkParams& wp, const RaySeg& s
         ln[j] = __float_as_int(ok ? lut_finish(lut_fetch(mp, iz, (int)q), wz) : 0.f);
         w.advance(na, da);
         w.t_in = t_out;
+        // sparse bricks (g.bmask set): the next emitted cell lies past any unallocated brick, reached
+        // by the same one-step empty skip as the first walk (bit-identical); dense: no iteration
+        if (j + 1 < nv)
+            while (!cell_in_map(wp.g, w.c0, w.c1, w.c2))
+                if (!w.skip_brick(wp.g) || !w.inside(wp.g)) break;
     }
 }
 
@@ -474,7 +479,7 @@ __device__ __forceinline__ void load_chunk_walk(long long s, long long e0, long 
     const int c = (int)((s - e0) / K);
     const int nv = (int)min((long long)K, e1 - s);
     int v[K], q[K], ln[K];
-    walk_chunk<K>(wp, sg, mp, info.iz, info.wz, __ldg(wp.ck + (e0 >> 2) + c), c == 0, nv, v, ln);
+    walk_chunk<K>(wp, sg, mp, info.iz, info.wz, __ldg(wp.ck + (e0 >> 2) + c), false, nv, v, ln);
     if (qrow) {
 #pragma unroll
         for (int j = 0; j < K; ++j) q[j] = __ldg(qrow + v[j]);
@@ -513,7 +518,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_WALK_MIN_BLOCKS)) ray
         int v[K], q[K], ln[K];
         const RaySeg sg = wp.seg[r];
         const int vck = __ldg(wp.ck + (e0 >> 2) + (nv > 0 ? sl : 0));
-        walk_chunk<K>(wp, sg, mp, info.iz, info.wz, vck, nv <= 0 || sl == 0, nv, v, ln);
+        walk_chunk<K>(wp, sg, mp, info.iz, info.wz, vck, false, nv, v, ln);  // (t_in of a ray's first cell: 0 by restart)
         if constexpr (AVG) {
             const int32_t* qrow = mp.qbar + (long long)info.frame * mp.qbar_vi;
 #pragma unroll

@@ -97,9 +97,9 @@ struct mrf_ctx {
         long long r0, r1, e0, e1;
     };
     int mf = 0;  // frames per chunk, 0 = off
-    // fused (default): K5 re-walks each lane's chunk itself from a stored first cell (K12), so no
-    // per-iteration walk into the scratch; the scratch serves only the first walk of new frames.
-    // MRF_MF_FUSED=0 (and sparse bricks, whose empty-skip walk K5 does not carry): the scratch path.
+    // fused (default): K5 re-walks each lane's chunk itself from a stored first cell (K12, with the
+    // empty skip in sparse-brick maps), so no per-iteration walk into the scratch; the scratch
+    // serves only the first walk of new frames.  MRF_MF_FUSED=0: the scratch path.
     bool mf_fused = true;
     DBuf<RaySeg> ray_seg;   // per ray: segment for the re-walks
     DBuf<int32_t> ck;       // chunk checkpoints, ck[row_ptr / 4 + c]
@@ -108,7 +108,7 @@ struct mrf_ctx {
     // scratch between K5 and K6' of the chunk; the K6' items are grouped by chunk
     DBuf<int32_t> lam_chunk;
     std::vector<long long> kf_item_off;  // K6' items of chunk ci: [kf_item_off[ci], kf_item_off[ci + 1])
-    bool kf_chunked() const { return kf_avg && mf && mf_fused && !grid.bmask; }
+    bool kf_chunked() const { return kf_avg && mf && mf_fused; }
     std::vector<FrameDesc> mf_frames;
     std::vector<long long> mf_frame_e;  // row_ptr at each frame's first ray (+ the end)
     std::vector<MfChunk> mf_chunks;
@@ -451,7 +451,7 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
         if (ss != MRF_OK) return ss;
     }
     ProfScope ps(c, own ? MRF_K_DDA_FILL : -1);
-    const bool fused = count && c->mf_fused && !c->grid.bmask;
+    const bool fused = count && c->mf_fused;
     launch_dda_fill(c->d_frames.p + f0, dc, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
                     c->depth_all.p, c->row_ptr.p, c->ray_z.p, sv - ch.e0, so - ch.e0, sl - ch.e0,
                     count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), sink,
@@ -535,7 +535,7 @@ mrf_status sync_fill(mrf_ctx* c) {
             CK(c->lam.ensure((size_t)c->E + kPadElems, (size_t)c->E_filled, c->stream));
             CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
         }
-        if (c->mf_fused && !c->grid.bmask) {
+        if (c->mf_fused) {
             CK(c->ray_seg.ensure((size_t)std::max<long long>(c->R, 1), (size_t)c->R_filled, c->stream));
             CK(c->ck.ensure((size_t)(c->E / 4 + 4), (size_t)(c->E_filled / 4), c->stream));
         }
@@ -810,7 +810,7 @@ mrf_status prepare(mrf_ctx* c) {
         launch_stage_fill(c->R, c->row_ptr.p, c->ray_z.p, c->flags.p, c->pos.p, c->stages.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
     }
-    if (c->mf && (!(c->mf_fused && !c->grid.bmask) || c->kf_chunked())) {  // K5 classes per (chunk, class)
+    if (c->mf && (!(c->mf_fused) || c->kf_chunked())) {  // K5 classes per (chunk, class)
         const long long NK = (long long)c->mf_chunks.size() * kNumClasses;
         CK(c->class_cnt.ensure((size_t)std::max(1LL, 2 * NK), 0, c->stream));
         CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * NK * sizeof(unsigned long long), c->stream));
@@ -949,7 +949,7 @@ mrf_status ray_messages(mrf_ctx* c) {
     c->mp.qbar_vi = c->VI;
     c->mp.chk_lam = (long long)c->lam.cap;  // checked build (MRF_CHECK): what exists
     c->mp.chk_vi = c->VI;
-    if (c->mf && c->mf_fused && !c->grid.bmask) {  // K12: K5 re-walks its own chunks (no scratch)
+    if (c->mf && c->mf_fused) {  // K12: K5 re-walks its own chunks (no scratch)
         ProfScope ps(c, MRF_K_RAY_MSG);
         c->mp.chk_lam = (long long)c->lam.cap;
         const WalkParams wp{c->grid, c->ray_seg.p, c->ck.p};

@@ -66,7 +66,9 @@ struct Walker {
     // The walk's exact state in cell (x, y, z) of the segment: the next boundary numerator of an
     // axis is a function of the cell alone (n = (c + 1) 2^16 - G0 stepping up, G0 - c 2^16 stepping
     // down), and t_in is the latest earlier crossing, RN((n_a - 2^16) / d_a) as crossing_t rounds
-    // it (0 for the ray's first cell).  Bit-identical to the state the walk from the start reaches.
+    // it -- 0 in the segment's start cell, where no axis has crossed yet (n_k <= 2^16), and the
+    // crossing an empty skip entered by in a sparse map (skip_brick rounds it the same way).
+    // Bit-identical to the state the walk from the start reaches.  (first = true forces t_in = 0.)
     __device__ __forceinline__ static void axis_at(int g0, int dg, int c, int& s, unsigned& n, unsigned& d) {
         if (dg > 0) {
             s = 1;

@@ -30,7 +30,7 @@ def _run(w, n_iter, mf=0, kf=False, bricks=0, frames=None):
     with m:
         m.bp_iterate(n_iter)
         sizes = m.graph_sizes(active=not mf)
-        if kf and mf and not bricks:  # keyframe averages + fused walks: the averages are the state
+        if kf:  # keyframe averages: the state (with matrix-free walks no messages are kept)
             lam = np.stack([m.export_keyframe_average(f) for f in range(len(frames or w.frames))])
         else:
             lam = m.export_messages()
@@ -55,19 +55,7 @@ def test_matrix_free_frame1_and_modes():
     for kw in (dict(kf=True), dict(bricks=8), dict(kf=True, bricks=8)):
         x = _run(t, 4, **kw)
         y = _run(t, 4, mf=2, **kw)
-        if kw.get("kf") and not kw.get("bricks"):  # (per-incidence messages are not kept: compare averages)
-            F = len(t.frames)
-            m = pkg.MRFMap.from_workload(t)
-            m.set_stream(torch.cuda.current_stream().cuda_stream)
-            m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
-            with m:
-                for fr in t.frames:
-                    m.add_frame(fr.depth, fr.K, fr.T_wc)
-                m.bp_iterate(4)
-                xa = np.stack([m.export_keyframe_average(f) for f in range(F)])
-            assert np.array_equal(xa, y[0]) and np.array_equal(x[1], y[1]), kw
-        else:
-            assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), kw
+        assert np.array_equal(x[0], y[0]) and np.array_equal(x[1], y[1]), kw
 
 
 def test_matrix_free_warm_start_and_rules():
