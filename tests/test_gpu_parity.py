@@ -545,3 +545,69 @@ def test_runs_from_fill_match_run_fill(mode, monkeypatch):
             outs.append((m.layout_sizes()["n_runs"], m.export_beliefs(), m.export_messages()))
     assert outs[0][0] == outs[1][0]
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
+
+
+def _single_cell_rays():
+    """1 m voxels, camera at a cell centre looking +x, every depth 0.2 m (+ the 0.1 m margin): every
+    ray ends inside the camera's cell -- rays of ONE incidence (N = 1: Eq.14's message has no
+    other voxel, so lambda = +256 by the clip, reading R9)."""
+    dims, res = (4, 4, 4), 1.0
+    C = np.array([2.5, 2.5, 2.5])
+    R = np.array([[0.0, 0.0, 1.0], [-1.0, 0.0, 0.0], [0.0, -1.0, 0.0]])
+    W, H, K = 5, 3, (50.0, 50.0, 2.0, 1.0)
+    depth = np.full((H, W), 0.2, np.float32)
+    depth[1, 1] = 0.0  # an invalid pixel
+    lut = synth.build_log_nu_lut(16, 64, 0.0, 4.0, -0.5, 0.5, (0.01, 0.0, 0.0), 0.0)
+    return synth.Workload("cell", dims, res, (0, 0, 0), 0.3, lut, 0.0, 4.0, -0.5, 0.5, 0.1, 3.0,
+                          (0.01, 0.0, 0.0), 4, [Frame(depth, np.array(K), np.concatenate([R, C[:, None]], 1).reshape(-1))])
+
+
+def test_single_incidence_rays():
+    w = _single_cell_rays()
+    p = oracle.Params.from_workload(w)
+    g = oracle.build_graph(p, w.frames)
+    assert g.n_rays == 14 and np.all(np.diff(g.row_ptr) == 1)
+    lam_ref, T_ref = oracle.bp(p, g, 3)
+    assert np.all(lam_ref == 256.0)
+    with _gpu_map(w) as m:
+        _assert_graph_equal(m.export_graph(), g)
+        m.bp_iterate(3)
+        lam = m.export_messages()
+        marg = m.marginals()
+    assert np.all(lam == np.float32(256.0))
+    assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+@pytest.mark.parametrize("mode", ["mf", "kf", "kfmf", "sparse"])
+def test_all_invalid_frames_in_every_mode(tiny, mode):
+    """Frames whose pixels are all invalid (0, NaN) add no ray in any mode; the map then behaves
+    as with the valid frame alone (oracle parity), and an empty map keeps the prior."""
+    fr = tiny.frames[0]
+    bad = [Frame(np.zeros_like(fr.depth), fr.K, fr.T_wc), Frame(np.full_like(fr.depth, np.nan), fr.K, fr.T_wc)]
+    p = oracle.Params.from_workload(tiny)
+    bk = oracle.alloc_bricks(p, [fr]) if mode == "sparse" else None
+    g = oracle.build_graph(p, [fr], bricks=bk)
+    for frames in (bad, bad + [fr]):
+        m = pkg.MRFMap.from_workload(tiny)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        if "kf" in mode:
+            m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+        if "mf" in mode:
+            m.set_matrix_free(2)
+        if mode == "sparse":
+            m.set_sparse_bricks(8)
+        with m:
+            for f in frames:
+                m.add_frame(f.depth, f.K, f.T_wc)
+            m.bp_iterate(3)
+            marg = m.marginals()
+            s = m.graph_sizes(active=False)
+        if len(frames) == 2:
+            assert s["E"] == 0 and s["n_rays"] == 0 and np.all(marg == np.float32(tiny.prior))
+        else:
+            assert s["E"] == g.E and s["n_rays"] == g.n_rays
+            if "kf" in mode:
+                _, _, T_ref = oracle.kf_bp(p, g, 3, F=3)  # (frame ids 0, 1 hold no ray)
+            else:
+                _, T_ref = oracle.bp(p, g, 3)
+            assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
