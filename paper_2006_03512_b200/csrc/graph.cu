@@ -59,11 +59,9 @@ __device__ __forceinline__ void owned_pixel(const FrameDesc& f, long long i, int
 }
 
 // ---------------------------------------------------------------- K1
-__global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
-                                                           const float* __restrict__ depth, int32_t* n_r,
-                                                           int8_t* status, RayInfo* ray_z,
-                                                           unsigned long long* counters) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void raygen_count_body(const FrameDesc& f, long long i, const GridDesc& g,
+                                                  const NoiseDesc& n, const float* __restrict__ depth, int32_t* n_r,
+                                                  int8_t* status, RayInfo* ray_z, unsigned long long* counters) {
     const long long n_pix = (long long)f.rows_owned * f.W;
     int st = 3;
     if (i < n_pix) {
@@ -124,6 +122,37 @@ __global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc
         if (inv) atomicAdd(&counters[0], (unsigned long long)__popc(inv));
         if (drp) atomicAdd(&counters[1], (unsigned long long)__popc(drp));
     }
+}
+
+__global__ void __launch_bounds__(128) raygen_count_kernel(FrameDesc f, GridDesc g, NoiseDesc n,
+                                                           const float* __restrict__ depth, int32_t* n_r,
+                                                           int8_t* status, RayInfo* ray_z,
+                                                           unsigned long long* counters) {
+    raygen_count_body(f, (long long)blockIdx.x * blockDim.x + threadIdx.x, g, n, depth, n_r, status, ray_z, counters);
+}
+
+// K1 of every frame added since the last batch in one launch (frames[k] owns the CTAs
+// [cta0[k], cta0[k+1]) of 128 pixels; its depth image at depth_all + depth_off)
+__global__ void __launch_bounds__(128) raygen_count_batch_kernel(const FrameDesc* __restrict__ frames,
+                                                                 const int* __restrict__ cta0, int n_frames,
+                                                                 GridDesc g, NoiseDesc n,
+                                                                 const float* __restrict__ depth_all, int32_t* n_r,
+                                                                 int8_t* status, RayInfo* ray_z,
+                                                                 unsigned long long* counters) {
+    __shared__ FrameDesc f;
+    __shared__ int s_c0;
+    if (threadIdx.x == 0) {
+        int lo = 0, hi = n_frames - 1;  // last k with cta0[k] <= blockIdx.x
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(cta0 + mid) <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+        }
+        f = frames[lo];
+        s_c0 = __ldg(cta0 + lo);
+    }
+    __syncthreads();
+    raygen_count_body(f, (long long)((int)blockIdx.x - s_c0) * 128 + threadIdx.x, g, n, depth_all + f.depth_off, n_r,
+                      status, ray_z, counters);
 }
 
 // Tile runs (K4b): a run ends where the tile changes (a ray crosses a convex tile once), after
@@ -889,6 +918,14 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
     const long long n_pix = (long long)f.rows_owned * f.W;
     if (n_pix == 0) return;
     raygen_count_kernel<<<blocks_for(n_pix, 128), 128, 0, s>>>(f, g, n, depth, n_r, status, ray_z, counters);
+}
+
+void launch_raygen_count_batch(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, const GridDesc& g,
+                               const NoiseDesc& n, const float* depth_all, int32_t* n_r, int8_t* status, RayInfo* ray_z,
+                               unsigned long long* counters, cudaStream_t s) {
+    if (n_ctas == 0) return;
+    raygen_count_batch_kernel<<<n_ctas, 128, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, n_r, status, ray_z,
+                                                     counters);
 }
 
 void launch_brick_alloc(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, uint8_t* mask,

@@ -210,6 +210,11 @@ struct RaySeg;  // walk.cuh
 void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth,
                          int32_t* n_r, int8_t* status, RayInfo* ray_z, unsigned long long* counters,
                          cudaStream_t s);
+// the same for several frames in one launch (frames[k] owns the CTAs [cta0[k], cta0[k+1]) of 128
+// pixels, its depth at depth_all + frames[k].depth_off)
+void launch_raygen_count_batch(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, const GridDesc& g,
+                               const NoiseDesc& n, const float* depth_all, int32_t* n_r, int8_t* status, RayInfo* ray_z,
+                               unsigned long long* counters, cudaStream_t s);
 // K3: the walk of every pending frame (device FrameDesc array, frame k owning the CTAs
 // [cta0[k], cta0[k+1]) of kFillThreads pixels), writing vid / off_q at row_ptr offsets and
 // counting the tile runs (K4b) per tile; then log nu per incidence of the rays [r0, r0 + n_rays)

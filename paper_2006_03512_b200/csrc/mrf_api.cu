@@ -191,6 +191,7 @@ struct mrf_ctx {
     bool runs_ok = true, run_fill_forced = false;
     double run_ratio = 0.125;
     DBuf<int2> bitems;
+    std::vector<int2> h_items;  // host copy of the K6 work list
     long long n_runs = 0, n_bitems = 0;
     DBuf<long long> T, T_part;
     // world > 1 (NCCL): the all-reduce covers only the tiles some rank touches:
@@ -212,6 +213,13 @@ struct mrf_ctx {
     long long depth_used = 0;
     std::vector<FrameDesc> pend;
     DBuf<FrameDesc> d_frames;
+    // frames whose K1 (ray setup + length bound) and row scan have not run yet: they run as one
+    // launch + one scan when something needs the layout (flush_k1) -- add_frame itself launches
+    // nothing while the capacity bound holds
+    std::vector<FrameDesc> k1_pend;
+    DBuf<FrameDesc> d_k1_frames;
+    DBuf<int> d_k1_cta0;
+    long long k1_R0 = 0;
     DBuf<int> d_cta0;
     long long E_filled = 0, R_filled = 0;  // incidences / rays already walked
     DBuf<int8_t> eval_cls;
@@ -335,8 +343,43 @@ mrf_status read_ll(mrf_ctx* c, const long long* dev, long long* out) {
     return MRF_OK;
 }
 
+// K1 and the row scan of the frames added since the last batch (one launch each).
+mrf_status flush_k1(mrf_ctx* c) {
+    if (c->k1_pend.empty()) return MRF_OK;
+    const int nf = (int)c->k1_pend.size();
+    std::vector<int> cta0((size_t)nf + 1, 0);
+    for (int k = 0; k < nf; ++k) {
+        const long long n_pix = (long long)c->k1_pend[k].rows_owned * c->k1_pend[k].W;
+        cta0[k + 1] = cta0[k] + (int)((n_pix + 127) / 128);
+    }
+    CK(c->d_k1_frames.ensure((size_t)nf, 0, c->stream));
+    CK(c->d_k1_cta0.ensure((size_t)nf + 1, 0, c->stream));
+    CK(cudaMemcpyAsync(c->d_k1_frames.p, c->k1_pend.data(), sizeof(FrameDesc) * nf, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_k1_cta0.p, cta0.data(), sizeof(int) * (nf + 1), cudaMemcpyHostToDevice, c->stream));
+    {
+        ProfScope ps(c, MRF_K_RAYGEN_COUNT);
+        launch_raygen_count_batch(c->d_k1_frames.p, c->d_k1_cta0.p, nf, cta0[nf], c->grid, c->noise, c->depth_all.p,
+                                  c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2, c->stream);
+        CK_LAUNCH(MRF_K_RAYGEN_COUNT, cta0[nf] > 0 ? 1 : 0);
+    }
+    const long long n = c->R - c->k1_R0;
+    if (n > 0) {  // row_ptr[k1_R0] holds the running E on the device
+        CK(c->scan_scratch.ensure((size_t)scan_scratch_elems(n), 0, c->stream));
+        ProfScope ps(c, MRF_K_SCAN);
+        launch_exclusive_scan_dev(c->n_r.p + c->k1_R0, c->row_ptr.p + c->k1_R0, n, c->row_ptr.p + c->k1_R0,
+                                  c->scan_scratch.p, c->stream);
+        CK_LAUNCH(MRF_K_SCAN, 3);
+    }
+    c->k1_pend.clear();  // (pageable host -> device copies are staged before they return)
+    return MRF_OK;
+}
+
 // Exact E and invalid / dropped counts of the frames added since the last round trip.
 mrf_status resolve_E(mrf_ctx* c) {
+    {
+        mrf_status sk = flush_k1(c);
+        if (sk != MRF_OK) return sk;
+    }
     if (!c->E_unresolved) return MRF_OK;
     CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
@@ -672,7 +715,13 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
     CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
     if ((st = scan(c, c->tile_runs.p, c->tile_ptr.p, NT, 0)) != MRF_OK) return st;
-    if ((st = read_ll(c, c->tile_ptr.p + NT, &c->n_runs)) != MRF_OK) return st;
+    // the runs per bucket on the host (one round trip: their sum is n_runs, and they make the K6
+    // work list below)
+    std::vector<int32_t> nr((size_t)NT);
+    CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->n_runs = 0;
+    for (int32_t x : nr) c->n_runs += x;
     CK(c->runs.ensure((size_t)std::max(1LL, c->n_runs), 0, c->stream));
     CK(cudaMemsetAsync(c->tile_cursor.p, 0, sizeof(int32_t) * NT, c->stream));
     const bool from_sink = c->runs_ok && !c->run_fill_forced;
@@ -705,11 +754,9 @@ mrf_status build_tile_runs(mrf_ctx* c) {
         c->k6_item = (int)std::min<long long>(24576, std::max<long long>(8192, c->n_runs / ((long long)c->sms * 13)));
     // K6 work list, j-major: item j of every tile, then item j+1 ...  Runs land in a tile in
     // roughly ray order, so the items that run concurrently read nearby message ranges (L2 reuse).
-    std::vector<int32_t> nr((size_t)NT);
-    CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
     c->tile_nr = nr;
-    std::vector<int2> items;
+    std::vector<int2>& items = c->h_items;  // (kept: the copy below is asynchronous)
+    items.clear();
     for (int j = 0;; ++j) {
         bool any = false;
         for (long long t = 0; t < NT; ++t) {
@@ -736,7 +783,6 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     CK(c->bitems.ensure((size_t)std::max(1LL, c->n_bitems), 0, c->stream));
     if (c->n_bitems)
         CK(cudaMemcpyAsync(c->bitems.p, items.data(), sizeof(int2) * items.size(), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
     return MRF_OK;
 }
 
@@ -1397,6 +1443,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->runs_all.release(); c->run_keys.release();
     c->rp_old.release(); c->ri_old.release(); c->vid_old.release(); c->lam_old.release();
     c->ray_seg.release(); c->ck.release(); c->lam_chunk.release();
+    c->d_k1_frames.release(); c->d_k1_cta0.release();
     c->class_all.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
@@ -1450,6 +1497,7 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->E_bound = 0;
     CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
     c->pend.clear();
+    c->k1_pend.clear();
     c->depth_used = 0;
     c->E_filled = c->R_filled = 0;
     c->kf_frames_alloc = 0;
@@ -1543,23 +1591,19 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     const long long U = c->grid.bmask ? 0 : Rf * c->ray_slots_max;
     const bool fast = c->E + c->E_bound + U < (1LL << 31) - kPadElems;
     mrf_status st;
-    if (!fast && (st = resolve_E(c)) != MRF_OK) return st;
-    {
-        ProfScope ps(c, MRF_K_RAYGEN_COUNT);
-        launch_raygen_count(f, c->grid, c->noise, d_depth, c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2,
-                            c->stream);
-        CK_LAUNCH(MRF_K_RAYGEN_COUNT, Rf > 0 ? 1 : 0);
-    }
+    if (!fast && (st = resolve_E(c)) != MRF_OK) return st;  // (runs the pending K1s first)
+    f.depth_off = c->depth_used;
     long long E_new = 0, inv = 0, drp = 0;
-    if (fast) {  // row_ptr[R] holds the running E on the device
-        if (Rf > 0) {
-            CK(c->scan_scratch.ensure((size_t)scan_scratch_elems(Rf), 0, c->stream));
-            ProfScope ps(c, MRF_K_SCAN);
-            launch_exclusive_scan_dev(c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->row_ptr.p + c->R,
-                                      c->scan_scratch.p, c->stream);
-            CK_LAUNCH(MRF_K_SCAN, 3);
-        }
+    if (fast) {  // K1 and the row scan run later, batched with the other pending frames (flush_k1)
+        if (c->k1_pend.empty()) c->k1_R0 = c->R;
+        if (Rf > 0) c->k1_pend.push_back(f);
     } else {  // counters[2..3] hold this frame only (resolve_E cleared them)
+        {
+            ProfScope ps(c, MRF_K_RAYGEN_COUNT);
+            launch_raygen_count(f, c->grid, c->noise, d_depth, c->n_r.p, c->status.p, c->ray_z.p, c->counters.p + 2,
+                                c->stream);
+            CK_LAUNCH(MRF_K_RAYGEN_COUNT, Rf > 0 ? 1 : 0);
+        }
         if ((st = scan(c, c->n_r.p + c->R, c->row_ptr.p + c->R, Rf, c->E)) != MRF_OK) return st;
         CK(cudaMemcpyAsync(c->pinned, c->row_ptr.p + c->R + Rf, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(c->pinned + 1, c->counters.p + 2, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
@@ -1575,7 +1619,6 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
         launch_brick_alloc(f, c->grid, c->noise, d_depth, c->bmask.p, c->stream);
         CK_LAUNCH(MRF_K_RAYGEN_COUNT, 1);
     }
-    f.depth_off = c->depth_used;
     c->depth_used += (long long)npix;
     if (Rf > 0) c->pend.push_back(f);
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
