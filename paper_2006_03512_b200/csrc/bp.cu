@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                                                                    const int32_t* __restrict__ lam, int per_item,
                                                                    void* out, long long n_out, unsigned* next,
                                                                    const int32_t* __restrict__ tile_map, long long chk_lam,
-                                                                   long long chk_out_tiles) {
+                                                                   long long chk_out_tiles, int n_tiles) {
     extern __shared__ int smem[];
     using L = AccLayout<PAD>;
     static_assert(MODE == 0 || !PAD, "keyframe-average sums use the plain layout (shared memory)");
@@ -1039,7 +1039,8 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
         if constexpr (MODE == 0) {
             // world > 1: the tile's slots go to its position among the tiles some rank touches
             // (the compacted all-reduce buffer); else to the tile itself
-            const long long tpos = tile_map ? (long long)__ldg(tile_map + item.x) : (long long)item.x;
+            const int tile = item.x % n_tiles;  // (buckets may be (frame, tile) pairs, frame-major)
+            const long long tpos = tile_map ? (long long)__ldg(tile_map + tile) : (long long)tile;
             MRF_ASSERT(tpos >= 0 && tpos < chk_out_tiles);
             long long* Tt = static_cast<long long*>(out) + (tpos << kTileShift);
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
@@ -1247,7 +1248,8 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
 template <int MODE, bool PAD>
 void launch_tile_reduce_t(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                           const int32_t* lam, int per_item, void* out, long long n_out, unsigned* next,
-                          const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s) {
+                          const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, int n_tiles,
+                          cudaStream_t s) {
     constexpr int smem = (MODE == 3 ? 3 : 2) * AccLayout<PAD>::kSlots * (int)sizeof(int) + kK6Desc;
     DevCfg& dc = dev_cfg();
     if (!dc.k6[MODE][PAD]) {
@@ -1258,19 +1260,20 @@ void launch_tile_reduce_t(long long n_items, const int2* items, const long long*
     if (next) cudaMemsetAsync(next, 0, sizeof(unsigned), s);
     tile_reduce_kernel<MODE, PAD><<<(unsigned)grid, kK6Threads, smem, s>>>(n_items, items, tile_ptr, runs, lam,
                                                                               per_item, out, n_out, next, tile_map,
-                                                                              chk_lam, chk_out_tiles);
+                                                                              chk_lam, chk_out_tiles, n_tiles);
 }
 
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                         const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad,
-                        const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s) {
+                        const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, int n_tiles,
+                        cudaStream_t s) {
     if (n_items == 0) return;
     if (pad)
         launch_tile_reduce_t<0, true>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, chk_lam,
-                                      chk_out_tiles, s);
+                                      chk_out_tiles, n_tiles, s);
     else
         launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, chk_lam,
-                                       chk_out_tiles, s);
+                                       chk_out_tiles, n_tiles, s);
 }
 
 void launch_kf_sums(int pass, long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,
@@ -1279,10 +1282,10 @@ void launch_kf_sums(int pass, long long n_items, const int2* items, const long l
     if (n_items == 0) return;
     if (pass == 0)
         launch_tile_reduce_t<2, false>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots, next, nullptr,
-                                       chk_lam, n_slots >> kTileShift, s);
+                                       chk_lam, n_slots >> kTileShift, 1 << 30, s);
     else
         launch_tile_reduce_t<3, false>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots, next, nullptr,
-                                       chk_lam, n_slots >> kTileShift, s);
+                                       chk_lam, n_slots >> kTileShift, 1 << 30, s);
 }
 
 // between the passes: M (min |q|) -> the scale a (nats, float, in place) per (frame, slot):

@@ -347,9 +347,11 @@ void launch_voxel_reduce(long long n_items, const int2* items, const long long* 
                          const int32_t* lam, long long* T, cudaStream_t s);
 // tile_map (nullable): tile -> position among the tiles written (world > 1: the tiles some rank
 // touches, compacted for the all-reduce); nullptr = the tile itself
+// (buckets b of tile b % n_tiles: tiles, or (frame, tile) pairs frame-major)
 void launch_tile_reduce(long long n_items, const int2* items, const long long* tile_ptr, const Run* runs,
                         const int32_t* lam, int per_item, long long* T, unsigned* next, bool pad,
-                        const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, cudaStream_t s);
+                        const int32_t* tile_map, long long chk_lam, long long chk_out_tiles, int n_tiles,
+                        cudaStream_t s);
 // T[tile_of[i] tile] = src[i-th compact tile] for i < n_tiles (16384 slots each)
 void launch_tile_scatter(long long n_tiles, const int32_t* tile_of, const long long* src, long long* T, cudaStream_t s);
 // keyframe averages (reading R22), two integer passes over the (frame * NT + tile) buckets into

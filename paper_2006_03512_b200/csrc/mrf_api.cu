@@ -133,7 +133,11 @@ struct mrf_ctx {
     DBuf<int32_t> qbar;           // [frame][VI] quantised average log-odds
     DBuf<long long> kf_sums;       // [frame][VI] x {N int64, D int64 (2^-30), M/A uint32} (bp.cu)
     long long kf_frames_alloc = 0;
-    long long n_bucket_groups() const { return kf_avg ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
+    // tile-run buckets by (frame, tile), frame-major: always for keyframe averages; in per-ray mode
+    // with MRF_K6_FRAMES=1 (K6 items then cover one frame's rays of a tile)
+    bool frame_buckets = false;
+    bool fb() const { return kf_avg || frame_buckets; }
+    long long n_bucket_groups() const { return fb() ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
     bool hist_valid = false; // vox_count (voxel degrees) computed for the current graph
@@ -737,13 +741,13 @@ mrf_status build_tile_runs(mrf_ctx* c) {
                 mrf_status sw;
                 if ((sw = mf_walk(c, ch, ch.f0, ch.f1, false)) != MRF_OK) return sw;
                 launch_run_fill(ch.r1 - ch.r0, c->row_ptr.p + ch.r0, c->ray_z.p + ch.r0, c->s_vid.p - ch.e0,
-                                c->tile_ptr.p, c->tile_cursor.p, c->kf_avg ? (int)c->NT : 0, c->runs.p, c->stream);
+                                c->tile_ptr.p, c->tile_cursor.p, c->fb() ? (int)c->NT : 0, c->runs.p, c->stream);
                 CK_LAUNCH(MRF_K_TRANSPOSE, ch.r1 > ch.r0 ? 1 : 0);
                 mf_dbg(c, "run_fill");
             }
         } else {
             launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, c->tile_ptr.p, c->tile_cursor.p,
-                            c->kf_avg ? (int)c->NT : 0, c->runs.p, c->stream);
+                            c->fb() ? (int)c->NT : 0, c->runs.p, c->stream);
             CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
         }
     }
@@ -801,7 +805,8 @@ mrf_status nccl_async_check(mrf_ctx* c) {
 mrf_status build_active_tiles(mrf_ctx* c) {
     const long long NT = c->NT;
     std::vector<uint8_t> h((size_t)NT, 0);
-    for (long long t = 0; t < NT && t < (long long)c->tile_nr.size(); ++t) h[(size_t)t] = c->tile_nr[(size_t)t] > 0;
+    for (long long b = 0; b < (long long)c->tile_nr.size(); ++b)  // (buckets: tiles, or (frame, tile) pairs)
+        if (c->tile_nr[(size_t)b] > 0) h[(size_t)(b % NT)] = 1;
     CK(c->touched.ensure((size_t)NT, 0, c->stream));
     if (c->world > 1) {
         CK(cudaMemcpyAsync(c->touched.p, h.data(), (size_t)NT, cudaMemcpyHostToDevice, c->stream));
@@ -979,7 +984,7 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
         launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
                            c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->k6_pad,
                            compact ? c->tile_map.p : nullptr, (long long)c->lam.cap, compact ? c->n_act_tiles : c->NT,
-                           c->stream);
+                           (int)c->NT, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_bitems > 0 ? 1 : 0);
     }
     return MRF_OK;
@@ -1325,6 +1330,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* kp = getenv("MRF_K6_PAD")) c->k6_pad = atoi(kp) != 0;
     if (const char* kl = getenv("MRF_K6_LPT")) c->k6_lpt = atoi(kl) != 0;
     if (const char* kc = getenv("MRF_COMPACT")) c->force_compact = atoi(kc) != 0;
+    if (const char* kf = getenv("MRF_K6_FRAMES")) c->frame_buckets = atoi(kf) != 0;
     if (const char* rf = getenv("MRF_RUN_FILL")) c->run_fill_forced = atoi(rf) != 0;
     if (const char* mff = getenv("MRF_MF_FUSED")) c->mf_fused = atoi(mff) != 0;
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
@@ -1578,8 +1584,8 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     f.ray_base = c->R;
     f.index = (int)c->frames.size();
     f.skip_count = c->grid.bmask ? 1 : 0;  // sparse: the rays are counted once all frames are allocated
-    f.bucket_stride = c->kf_avg ? (int)c->NT : 0;
-    if (c->kf_avg) {  // this frame's (frame, tile) run counters
+    f.bucket_stride = c->fb() ? (int)c->NT : 0;
+    if (c->fb()) {  // this frame's (frame, tile) run counters
         const size_t F = c->frames.size();
         CK(c->tile_runs.ensure((F + 1) * (size_t)c->NT, F * (size_t)c->NT, c->stream));
         CK(cudaMemsetAsync(c->tile_runs.p + F * c->NT, 0, sizeof(int32_t) * (size_t)c->NT, c->stream));

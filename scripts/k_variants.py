@@ -35,7 +35,7 @@ def main():
     depth = [torch.from_numpy(fr.depth).cuda() for fr in w.frames]
     E_alg = None
     ref = None
-    keys = ("MRF_K5", "MRF_K5_MATH", "MRF_K6", "MRF_L2_FETCH", "MRF_K6_ITEM", "MRF_K5_STREAMS", "MRF_K6_DYNAMIC", "MRF_K6_LPT", "MRF_K6_PAD")
+    keys = ("MRF_K5", "MRF_K5_MATH", "MRF_K6", "MRF_L2_FETCH", "MRF_K6_ITEM", "MRF_K5_STREAMS", "MRF_K6_DYNAMIC", "MRF_K6_LPT", "MRF_K6_PAD", "MRF_K6_FRAMES", "MRF_RUN_FILL")
     for var in a.variants:
         for k in keys:
             os.environ.pop(k, None)

@@ -611,3 +611,17 @@ def test_all_invalid_frames_in_every_mode(tiny, mode):
             else:
                 _, T_ref = oracle.bp(p, g, 3)
             assert np.max(np.abs(marg - oracle.marginals(p, T_ref))) <= MARG_TOL
+
+
+def test_k6_frame_buckets_agree(frame1, monkeypatch):
+    """K6 over (frame, tile) run buckets (MRF_K6_FRAMES=1: an item covers one frame's rays of a
+    tile) and over tile buckets give identical beliefs and messages (exact integer sums)."""
+    w = synth.frames30(n_frames=3)
+    outs = []
+    for fb in ("0", "1"):
+        monkeypatch.setenv("MRF_K6_FRAMES", fb)
+        with _gpu_map(w) as m:
+            m.bp_iterate(3)
+            outs.append((m.export_beliefs(), m.export_messages()))
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
