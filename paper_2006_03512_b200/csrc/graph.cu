@@ -243,7 +243,7 @@ __global__ void brick_alloc_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const f
 // one 2-byte store per step had the walk waiting on the store queue.
 // With MRF_FILL_LNU the chunk's log nu (B3) is interpolated here too: 8 independent table
 // lookups per flush (16 loads in flight) instead of a separate pass that re-reads off_q.
-__device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long long e_chunk, int nvalid,
+__device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, int e_chunk, int nvalid,
                                             const int* sv, const short* so, float* lnu, const MsgParams& mp, int iz,
                                             float wz) {
     int v[8];
@@ -273,14 +273,15 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, long l
     *reinterpret_cast<uint4*>(off_q + e_chunk) = make_uint4(pk(o[0], o[1]), pk(o[2], o[3]), pk(o[4], o[5]), pk(o[6], o[7]));
 }
 
-// Resident CTAs of 128 threads per SM: 6 (<= 80 registers) for the plain walk; 5 (<= 96) when it
-// also builds the tile runs (RUNS), whose state spilled at 80 (frames30: fill 10.43 ms at 6,
-// 10.02 ms at 5 per 30-frame step; without runs 8.1 ms at 6).
+// Resident CTAs of 128 threads per SM: 6 (<= 80 registers), also when the walk builds the tile
+// runs (RUNS): the values read only at chunk flushes and run ends (LUT row, a run's first slots)
+// live in shared memory, which took the run builder's spills at 80 registers from 56 to 4 bytes
+// (frames30: fill 9.90 ms at 5 CTAs, 9.46 ms at 6 per 30-frame step; without runs 8.2 ms).
 #ifndef MRF_FILL_MIN_BLOCKS
 #define MRF_FILL_MIN_BLOCKS 6
 #endif
 #ifndef MRF_FILL_MIN_BLOCKS_RUNS
-#define MRF_FILL_MIN_BLOCKS_RUNS 5
+#define MRF_FILL_MIN_BLOCKS_RUNS 6
 #endif
 // One launch fills every frame added since the last fill (frames[k] owns the CTAs
 // [cta0[k], cta0[k+1])): one wave-quantisation tail per batch instead of per frame.
@@ -295,6 +296,11 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
     __shared__ int s_vid[kFillThreads][8];
     __shared__ Run s_done[RUNS ? kFillThreads : 1];  // a run that ended at this step, per thread
     __shared__ int s_done_key[RUNS ? kFillThreads : 1];
+    // per-thread values read only at chunk flushes / run ends (kept out of registers: the walk
+    // with the run builder is register-bound)
+    __shared__ int s_iz[kFillThreads];
+    __shared__ float s_wz[kFillThreads];
+    __shared__ unsigned s_run_e[RUNS ? kFillThreads : 1], s_run_slot0[RUNS ? kFillThreads : 1];
     __shared__ short s_off[kFillThreads][8];
     __shared__ FrameDesc f;
     __shared__ int s_fi;
@@ -320,22 +326,22 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
     // current tile run (K4b: counted per bucket, and emitted to the sink when it ends): tile, length,
     // in-tile slots of its first and last element, first incidence slot, x / y step masks; the
     // step signs are the ray's (a DDA walk is monotone on every axis)
-    int run_tile = -1, run_n = 0, run_prev = 0, run_slot0 = 0;
-    unsigned run_e = 0, run_mx = 0, run_my = 0, run_neg = 0;
+    int run_tile = -1, run_n = 0, run_prev = 0;
+    unsigned run_mx = 0, run_my = 0, run_neg = 0;
     unsigned long long sink_base = 0;  // the warp's block of run slots (RunSink::emit)
     int sink_left = 0;
     const int bucket0 = f.index * f.bucket_stride;
-    long long e = 0, e_cap = 0;
-    int iz = 0;
-    float wz = 0.f;
+    int e = 0, e_cap = 0;  // incidence slots (< 2^31 per ctx)
+    s_iz[threadIdx.x] = 0;
+    s_wz[threadIdx.x] = 0.f;
     if (i < n_pix) {
         int u, v;
         owned_pixel(f, i, u, v);
-        e = row_ptr[f.ray_base + i];
+        e = (int)row_ptr[f.ray_base + i];
         if (pixel_segment(f, g, n, u, v, depth[(long long)v * f.W + u], sg) == 0) {
             w.start(sg);
             alive = w.inside(g);
-            e_cap = row_ptr[f.ray_base + i + 1];  // the segment K1 sized from its bound
+            e_cap = (int)row_ptr[f.ray_base + i + 1];  // the segment K1 sized from its bound
             run_neg = ((unsigned)(w.s0 < 0) | ((unsigned)(w.s1 < 0) << 1) | ((unsigned)(w.s2 < 0) << 2)) << 20;
             if (seg)  // matrix-free: what a re-walk of any chunk of this ray needs (K12)
                 seg[f.ray_base + i] = RaySeg{{(int)sg.g0[0], (int)sg.g0[1], (int)sg.g0[2]},
@@ -343,12 +349,12 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                                               (int)(sg.g1[2] - sg.g0[2])},
                                              sg.Z, sg.L};
             if (MRF_FILL_LNU) {  // the depth coordinate of the table (K1)
-                iz = ray_z[f.ray_base + i].iz;
-                wz = ray_z[f.ray_base + i].wz;
+                s_iz[threadIdx.x] = ray_z[f.ray_base + i].iz;
+                s_wz[threadIdx.x] = ray_z[f.ray_base + i].wz;
             }
         }
     }
-    const long long e_ray = e;
+    const int e_ray = e;
     bool overflow = false;
     for (;;) {
         const unsigned am = __ballot_sync(kFull, alive);
@@ -370,7 +376,7 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
                 sv[e & 7] = vx;
                 so[e & 7] = (short)q;
-                if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, iz, wz);
+                if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x]);
                 // K4b: runs per tile (a warp's concurrent run starts in one tile share an atomic);
                 // a run that ends here goes to the sink
                 b = vx >> kTileShift;
@@ -379,15 +385,18 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 start = !run_extends(b, l, run_tile, run_n, run_prev);
                 if (start) {
                     if (RUNS && run_tile >= 0) {  // the run that ends here waits in shared memory
-                        s_done[threadIdx.x] = Run{run_e, (unsigned)run_slot0 | ((unsigned)(run_n - 1) << 14) | run_neg,
+                        s_done[threadIdx.x] = Run{s_run_e[threadIdx.x],
+                                                  s_run_slot0[threadIdx.x] | ((unsigned)(run_n - 1) << 14) | run_neg,
                                                   run_mx, run_my};
                         s_done_key[threadIdx.x] = bucket0 + run_tile;
                         has_done = true;
                     }
                     run_tile = b;
                     run_n = 1;
-                    run_slot0 = l;
-                    run_e = (unsigned)e;
+                    if (RUNS) {
+                        s_run_slot0[threadIdx.x] = (unsigned)l;
+                        s_run_e[threadIdx.x] = (unsigned)e;
+                    }
                     run_mx = run_my = 0;
                 } else {
                     if (RUNS) {
@@ -421,13 +430,16 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 alive = false;
                 overflow = true;
             }
-            if (!alive && (e & 7)) flush_chunk(vid, off_q, e & ~7LL, (int)(e & 7), sv, so, lnu, mp, iz, wz);  // partial tail
+            if (!alive && (e & 7))  // partial tail
+                flush_chunk(vid, off_q, e & ~7, e & 7, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x]);
         }
         if (RUNS) sink.emit(has_done, s_done[threadIdx.x], s_done_key[threadIdx.x], lane, sink_base, sink_left);
     }
     if (RUNS) {  // every ray's last run
         const bool last_run = run_tile >= 0;
-        sink.emit(last_run, Run{run_e, (unsigned)run_slot0 | ((unsigned)(run_n - 1) << 14) | run_neg, run_mx, run_my},
+        sink.emit(last_run,
+                  Run{s_run_e[threadIdx.x], s_run_slot0[threadIdx.x] | ((unsigned)(run_n - 1) << 14) | run_neg, run_mx,
+                      run_my},
                   bucket0 + run_tile, lane, sink_base, sink_left);
     }
     int ne = 0;
@@ -437,7 +449,7 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
         // The rest of the segment K1 sized (its bound can exceed the walk at ties and grid exits)
         // gets voxel 0: K5 lanes gather T and the keyframe averages through every slot of their
         // chunk, masked elements included, so no slot of a segment may hold a stale id.
-        for (long long z = (e + 7) & ~7LL; z < e_cap; z += 8) {
+        for (int z = (e + 7) & ~7; z < e_cap; z += 8) {
             int4* dv = reinterpret_cast<int4*>(vid + z);
             dv[0] = make_int4(0, 0, 0, 0);
             dv[1] = make_int4(0, 0, 0, 0);
