@@ -245,7 +245,7 @@ __global__ void brick_alloc_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const f
 // lookups per flush (16 loads in flight) instead of a separate pass that re-reads off_q.
 __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, int e_chunk, int nvalid,
                                             const int* sv, const short* so, float* lnu, const MsgParams& mp, int iz,
-                                            float wz) {
+                                            float wz, int32_t* lam0) {
     int v[8];
     short o[8];
 #pragma unroll
@@ -271,6 +271,11 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, int e_
     dv[1] = make_int4(v[4], v[5], v[6], v[7]);
     auto pk = [](short a, short b) { return (unsigned)(unsigned short)a | ((unsigned)(unsigned short)b << 16); };
     *reinterpret_cast<uint4*>(off_q + e_chunk) = make_uint4(pk(o[0], o[1]), pk(o[2], o[3]), pk(o[4], o[5]), pk(o[6], o[7]));
+    if (lam0) {  // new incidences start with lambda = 0 (B4): written here instead of a memset pass
+        int4* dl = reinterpret_cast<int4*>(lam0 + e_chunk);
+        dl[0] = make_int4(0, 0, 0, 0);
+        dl[1] = make_int4(0, 0, 0, 0);
+    }
 }
 
 // Resident CTAs of 128 threads per SM: 6 (<= 80 registers), also when the walk builds the tile
@@ -292,7 +297,8 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                                                        const long long* __restrict__ row_ptr, int32_t* vid,
                                                        int16_t* off_q, int32_t* tile_runs, RayInfo* ray_z,
                                                        unsigned long long* counters, MsgParams mp, float* lnu,
-                                                       RunSink sink, RaySeg* seg) {
+                                                       RunSink sink, RaySeg* seg, unsigned long long* class_counts,
+                                                       int32_t* lam0) {
     __shared__ int s_vid[kFillThreads][8];
     __shared__ Run s_done[RUNS ? kFillThreads : 1];  // a run that ended at this step, per thread
     __shared__ int s_done_key[RUNS ? kFillThreads : 1];
@@ -376,7 +382,8 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
                 sv[e & 7] = vx;
                 so[e & 7] = (short)q;
-                if ((e & 7) == 7) flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x]);
+                if ((e & 7) == 7)
+                    flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x], lam0);
                 // K4b: runs per tile (a warp's concurrent run starts in one tile share an atomic);
                 // a run that ends here goes to the sink
                 b = vx >> kTileShift;
@@ -431,7 +438,7 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 overflow = true;
             }
             if (!alive && (e & 7))  // partial tail
-                flush_chunk(vid, off_q, e & ~7, e & 7, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x]);
+                flush_chunk(vid, off_q, e & ~7, e & 7, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x], lam0);
         }
         if (RUNS) sink.emit(has_done, s_done[threadIdx.x], s_done_key[threadIdx.x], lane, sink_base, sink_left);
     }
@@ -459,7 +466,24 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 dl[0] = make_float4(0.f, 0.f, 0.f, 0.f);
                 dl[1] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            if (lam0) {
+                int4* dq = reinterpret_cast<int4*>(lam0 + z);
+                dq[0] = make_int4(0, 0, 0, 0);
+                dq[1] = make_int4(0, 0, 0, 0);
+            }
         }
+    }
+    if (class_counts) {  // the rays per K5 length class and the longest ray (no separate pass)
+        const int k = ne > 0 ? ray_class(ne) : -1;
+        const unsigned act = __ballot_sync(kFull, k >= 0);
+        if (k >= 0) {
+            const unsigned peers = __match_any_sync(act, k);
+            if (lane == __ffs(peers) - 1) atomicAdd(&class_counts[k], (unsigned long long)__popc(peers));
+        }
+        int mx = ne;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        if (lane == 0 && mx > 0) atomicMax(&class_counts[kNumClasses], (unsigned long long)mx);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ne += __shfl_xor_sync(kFull, ne, o);
@@ -951,11 +975,13 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters,
-                     const RunSink& sink, RaySeg* seg, cudaStream_t s) {
+                     const RunSink& sink, RaySeg* seg, unsigned long long* class_counts, int32_t* lam0,
+                     cudaStream_t s) {
     if (n_ctas > 0) {
 #define MRF_FILL_LAUNCH(SP, RU)                                                                                     \
     dda_fill_kernel<SP, RU><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, \
-                                                            off_q, tile_runs, ray_z, counters, mp, lnu, sink, seg)
+                                                            off_q, tile_runs, ray_z, counters, mp, lnu, sink, seg, \
+                                                            class_counts, lam0)
         if (g.bmask) {
             if (sink.runs) MRF_FILL_LAUNCH(true, true); else MRF_FILL_LAUNCH(true, false);
         } else {

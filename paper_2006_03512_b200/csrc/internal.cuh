@@ -215,6 +215,8 @@ void launch_raygen_count(const FrameDesc& f, const GridDesc& g, const NoiseDesc&
 void launch_raygen_count_batch(const FrameDesc* frames, const int* cta0, int n_frames, int n_ctas, const GridDesc& g,
                                const NoiseDesc& n, const float* depth_all, int32_t* n_r, int8_t* status, RayInfo* ray_z,
                                unsigned long long* counters, cudaStream_t s);
+// (class_counts, nullable: += rays per K5 length class [kNumClasses], max= longest ray at
+// [kNumClasses]; lam0, nullable: zeroes the messages of the walked slots)
 // K3: the walk of every pending frame (device FrameDesc array, frame k owning the CTAs
 // [cta0[k], cta0[k+1]) of kFillThreads pixels), writing vid / off_q at row_ptr offsets and
 // counting the tile runs (K4b) per tile; then log nu per incidence of the rays [r0, r0 + n_rays)
@@ -228,7 +230,8 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
                      long long n_rays, const GridDesc& g, const NoiseDesc& n, const MsgParams& mp,
                      const float* depth_all, const long long* row_ptr, RayInfo* ray_z, int32_t* vid,
                      int16_t* off_q, float* lnu, int32_t* tile_runs, unsigned long long* counters,
-                     const RunSink& sink, RaySeg* seg, cudaStream_t s);
+                     const RunSink& sink, RaySeg* seg, unsigned long long* class_counts, int32_t* lam0,
+                     cudaStream_t s);
 // K9 §III.D evaluation of one frame against T: cls per pixel (-1 invalid, 0/1), counts[0..1] +=
 // (valid, accurate) (zeroed by the caller)
 void launch_eval(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, const float* depth, const long long* T,

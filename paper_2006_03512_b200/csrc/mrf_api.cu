@@ -61,6 +61,8 @@ struct DBuf {
     }
 };
 
+constexpr int kClassCtr = 32;  // counters[32 .. 32 + kNumClasses]: rays per K5 class, longest ray
+
 struct FrameRec {
     int W, H, rows_owned;
     long long ray_base, n_rays;
@@ -160,6 +162,12 @@ struct mrf_ctx {
     long long R = 0, E = 0;  // rays (owned pixels) and incidence slots (ray segments padded to 4)
     long long E_real = 0;    // incidences (counted by the fills on the device; see sync_fill)
     bool fill_pending = false;
+    bool fill_rb_pending = false;    // the last fill's counters are on their way to pinned[32..57]
+    // rays per K5 length class and the longest ray, counted by the fills since the reset
+    // (counters[kClassCtr ..]); fill_classes_ok: read back with the last fill's counters
+    long long fill_class_n[kNumClasses + 1] = {};
+    bool fill_classes_ok = false;
+    long long fill_rb_new_slots = -1;
     // frames added without a host round trip: their exact E (row_ptr[R]) and invalid / dropped
     // counts (counters[2..3], accumulating) are read when something needs them (resolve_E);
     // E_bound bounds what they added, so that the 2^31 capacity check needs no round trip while
@@ -244,6 +252,7 @@ struct mrf_ctx {
 
     bool prof = false;
     std::vector<ProfEvent> events;
+    std::vector<cudaEvent_t> ev_pool;  // recycled profiling events (creating two per scope costs host time)
     long long prof_launch[MRF_K_COUNT] = {};
     double prof_ms[MRF_K_COUNT] = {};
     long long launches = 0;
@@ -319,10 +328,20 @@ struct ProfScope {
     mrf_ctx* c;
     int kind;
     cudaEvent_t a = nullptr, b = nullptr;
+    static cudaEvent_t get(mrf_ctx* c) {
+        cudaEvent_t e = nullptr;
+        if (!c->ev_pool.empty()) {
+            e = c->ev_pool.back();
+            c->ev_pool.pop_back();
+        } else {
+            cudaEventCreate(&e);
+        }
+        return e;
+    }
     ProfScope(mrf_ctx* c_, int k) : c(c_), kind(k) {
         if (!c->prof || k < 0) return;
-        cudaEventCreate(&a);
-        cudaEventCreate(&b);
+        a = get(c);
+        b = get(c);
         cudaEventRecord(a, c->stream);
     }
     ~ProfScope() {
@@ -502,7 +521,7 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
     launch_dda_fill(c->d_frames.p + f0, dc, f1 - f0, cta0.back(), r0, r1 - r0, c->grid, c->noise, c->mp,
                     c->depth_all.p, c->row_ptr.p, c->ray_z.p, sv - ch.e0, so - ch.e0, sl - ch.e0,
                     count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), sink,
-                    fused ? c->ray_seg.p : nullptr, st);
+                    fused ? c->ray_seg.p : nullptr, count ? c->counters.p + kClassCtr : nullptr, nullptr, st);
     if (fused) {  // K12: the first cell of every K5 chunk of these rays
         launch_ck_extract(r1 - r0, c->row_ptr.p + r0, c->ray_z.p + r0, sv - ch.e0, c->ck.p, st);
     }
@@ -517,9 +536,30 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
     return MRF_OK;
 }
 
+// The counters of the last fill (pinned[32..34]): incidences, bound overflows, tile runs emitted.
+mrf_status fill_readback(mrf_ctx* c) {
+    if (!c->fill_rb_pending) return MRF_OK;
+    CK(cudaStreamSynchronize(c->stream));
+    c->fill_rb_pending = false;
+    if (c->fill_rb_new_slots >= 0) run_sink_done(c, c->pinned[34], c->fill_rb_new_slots);
+    c->E_real = c->pinned[32];
+    for (int k = 0; k <= kNumClasses; ++k) c->fill_class_n[k] = c->pinned[36 + k];  // (+ longest ray)
+    c->fill_classes_ok = true;
+    if (c->pinned[33]) {
+        c->sticky = MRF_ERR_STATE;
+        c->err = "internal: a DDA walk exceeded its precomputed bound";
+        return MRF_ERR_STATE;
+    }
+    return MRF_OK;
+}
+
 // The DDA fills count their incidences (and any bound overflow, which K1's bound excludes) on
-// the device, counters[10..11]; read them once when something needs E_real.
-mrf_status sync_fill(mrf_ctx* c) {
+// the device, counters[10..11]; read them once when something needs E_real (need_counts = false:
+// later, by fill_readback).
+mrf_status sync_fill(mrf_ctx* c, bool need_counts = true) {
+    if (!c->fill_pending) {
+        if (need_counts) return fill_readback(c);
+    }
     {
         mrf_status sr = resolve_E(c);
         if (sr != MRF_OK) return sr;
@@ -550,6 +590,7 @@ mrf_status sync_fill(mrf_ctx* c) {
             CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * (size_t)(c->NT * c->n_bucket_groups()), c->stream));
             CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
             CK(cudaMemsetAsync(c->counters.p + 16, 0, sizeof(unsigned long long), c->stream));
+            CK(cudaMemsetAsync(c->counters.p + kClassCtr, 0, (kNumClasses + 1) * sizeof(unsigned long long), c->stream));
             c->runs_emitted = 0;
             c->runs_ok = true;
         }
@@ -603,8 +644,7 @@ mrf_status sync_fill(mrf_ctx* c) {
         CK(cudaMemsetAsync(c->vid.p + c->E, 0, sizeof(int32_t) * kPadElems, c->stream));
         CK(c->off_q.ensure(ne, (size_t)c->E_filled, c->stream));
         CK(c->lnu.ensure(ne, (size_t)c->E_filled, c->stream));
-        CK(c->lam.ensure(ne, (size_t)c->E_filled, c->stream));
-        CK(cudaMemsetAsync(c->lam.p + c->E_filled, 0, sizeof(int32_t) * (size_t)(c->E - c->E_filled), c->stream));
+        CK(c->lam.ensure(ne, (size_t)c->E_filled, c->stream));  // (the fill zeroes the new slots' messages)
         const int nf = (int)c->pend.size();
         std::vector<int> cta0((size_t)nf + 1, 0);
         for (int k = 0; k < nf; ++k) {
@@ -625,7 +665,8 @@ mrf_status sync_fill(mrf_ctx* c) {
             ProfScope ps(c, MRF_K_DDA_FILL);
             launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
-                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, nullptr, c->stream);
+                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, nullptr, c->counters.p + kClassCtr,
+                            c->lam.p, c->stream);
             CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (!MRF_FILL_LNU && c->R > c->R_filled ? 1 : 0));
         }
         if (c->grid.bmask) {  // the depth images stay: a later keyframe may grow the allocation (R24)
@@ -654,18 +695,16 @@ mrf_status sync_fill(mrf_ctx* c) {
             }
         }
     }
-    CK(cudaMemcpyAsync(c->pinned, c->counters.p + 10, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(c->pinned + 2, c->counters.p + 16, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    // the fill's counters come back with the next round trip (fill_readback): the transpose build
+    // makes one anyway, so the fill and what follows it are enqueued without a wait here
+    CK(cudaMemcpyAsync(c->pinned + 32, c->counters.p + 10, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 34, c->counters.p + 16, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned + 36, c->counters.p + kClassCtr, (kNumClasses + 1) * sizeof(long long),
+                       cudaMemcpyDeviceToHost, c->stream));
     c->fill_pending = false;
-    if (new_slots >= 0) run_sink_done(c, c->pinned[2], new_slots);
-    c->E_real = c->pinned[0];
-    if (c->pinned[1]) {
-        c->sticky = MRF_ERR_STATE;
-        c->err = "internal: a DDA walk exceeded its precomputed bound";
-        return MRF_ERR_STATE;
-    }
-    return MRF_OK;
+    c->fill_rb_pending = true;
+    c->fill_rb_new_slots = new_slots;
+    return need_counts ? fill_readback(c) : MRF_OK;
 }
 
 // Per-voxel transpose (col_ptr over belief slots, tr) + its K6 work list.  Built by prepare()
@@ -724,6 +763,7 @@ mrf_status build_tile_runs(mrf_ctx* c) {
     std::vector<int32_t> nr((size_t)NT);
     CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if ((st = fill_readback(c)) != MRF_OK) return st;  // (already here: no further wait)
     c->n_runs = 0;
     for (int32_t x : nr) c->n_runs += x;
     CK(c->runs.ensure((size_t)std::max(1LL, c->n_runs), 0, c->stream));
@@ -837,7 +877,7 @@ mrf_status build_active_tiles(mrf_ctx* c) {
 mrf_status prepare(mrf_ctx* c) {
     if (!c->dirty) return MRF_OK;
     mrf_status st;
-    if ((st = sync_fill(c)) != MRF_OK) return st;
+    if ((st = sync_fill(c, false)) != MRF_OK) return st;
     c->vtr_valid = false;
     if (c->k6_voxel) {
         if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
@@ -909,17 +949,25 @@ mrf_status prepare(mrf_ctx* c) {
         c->dirty = false;
         return MRF_OK;
     }
-    // K5 length classes: counting sort of the ray ids by class
+    // K5 length classes: counting sort of the ray ids by class (the counts come from the fills,
+    // read back with their counters -- no round trip of its own)
     CK(c->class_cnt.ensure(2 * kNumClasses, 0, c->stream));
     CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * kNumClasses * sizeof(unsigned long long), c->stream));
-    launch_class_count(c->R, c->ray_z.p, c->class_cnt.p, c->stream);
-    CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
-    CK(cudaMemcpyAsync(c->pinned, c->class_cnt.p, kNumClasses * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    if ((st = fill_readback(c)) != MRF_OK) return st;
+    if (!c->fill_classes_ok) {  // (counts not from the fills, e.g. nothing walked yet)
+        launch_class_count(c->R, c->ray_z.p, c->class_cnt.p, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+        CK(cudaMemcpyAsync(c->pinned, c->class_cnt.p, kNumClasses * sizeof(long long), cudaMemcpyDeviceToHost,
+                           c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        for (int k = 0; k < kNumClasses; ++k) c->fill_class_n[k] = c->pinned[k];
+        c->fill_class_n[kNumClasses] = -1;
+        CK(cudaMemsetAsync(c->class_cnt.p, 0, 2 * kNumClasses * sizeof(unsigned long long), c->stream));
+    }
     ClassOffsets off{};
     long long tot = 0;
     for (int k = 0; k < kNumClasses; ++k) {
-        c->class_n[k] = c->pinned[k];
+        c->class_n[k] = c->fill_class_n[k];
         c->class_off[k] = off.off[k] = tot;
         tot += c->class_n[k];
     }
@@ -929,11 +977,14 @@ mrf_status prepare(mrf_ctx* c) {
     // scratch for the tiled long-ray kernel
     const int kl = kNumClasses - 1;
     if (c->class_n[kl] > 0) {
-        CK(cudaMemsetAsync(c->counters.p + 6, 0, sizeof(unsigned long long), c->stream));
-        launch_span_max(c->class_n[kl], c->class_all.p + c->class_off[kl], c->ray_z.p, c->counters.p + 6, c->stream);
-        CK_LAUNCH(MRF_K_TRANSPOSE, 1);
-        long long span = 0;
-        if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
+        long long span = c->fill_class_n[kNumClasses];  // the longest ray, counted by the fills
+        if (span < 0) {
+            CK(cudaMemsetAsync(c->counters.p + 6, 0, sizeof(unsigned long long), c->stream));
+            launch_span_max(c->class_n[kl], c->class_all.p + c->class_off[kl], c->ray_z.p, c->counters.p + 6,
+                            c->stream);
+            CK_LAUNCH(MRF_K_TRANSPOSE, 1);
+            if ((st = read_ll(c, reinterpret_cast<long long*>(c->counters.p + 6), &span)) != MRF_OK) return st;
+        }
         const long long tile = 512;
         c->long_scratch_per_warp = (span + tile - 1) / tile * tile + tile;
         c->n_warps_long = (int)std::min<long long>(c->class_n[kl], (long long)c->sms * 16);
@@ -1381,12 +1432,12 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         CK(c->tile_runs.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
         CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
-        CK(c->counters.ensure(32, 0, c->stream));
+        CK(c->counters.ensure(64, 0, c->stream));
         CK(c->row_ptr.ensure(1, 0, c->stream));
         CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * VI, c->stream));
         CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * NT, c->stream));
         CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
-        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 32, c->stream));
+        CK(cudaMemsetAsync(c->counters.p, 0, sizeof(unsigned long long) * 64, c->stream));
         CK(cudaMallocHost(&c->pinned, 64 * sizeof(long long)));
         // LUT as (L[i][j], L[i][j+1]) pairs: one 8-byte load per LUT row in K5.  The values are
         // the input table's floats, unscaled and unshifted.
@@ -1437,6 +1488,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
         cudaEventDestroy(e.a);
         cudaEventDestroy(e.b);
     }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     c->n_r.release(); c->status.release(); c->ray_z.release(); c->row_ptr.release();
     c->vid.release(); c->off_q.release(); c->lnu.release(); c->lam.release(); c->tr.release();
     c->vox_count.release(); c->cursor.release(); c->n_items.release(); c->flags.release();
@@ -1504,6 +1556,7 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     CK(cudaMemsetAsync(c->counters.p + 2, 0, 2 * sizeof(unsigned long long), c->stream));
     c->pend.clear();
     c->k1_pend.clear();
+    c->fill_rb_pending = false;
     c->depth_used = 0;
     c->E_filled = c->R_filled = 0;
     c->kf_frames_alloc = 0;
@@ -1516,6 +1569,8 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     if (c->grid.bmask) CK(cudaMemsetAsync(c->bmask.p, 0, (size_t)c->n_brick_slots, c->stream));
     CK(cudaMemsetAsync(c->counters.p + 10, 0, 2 * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(c->counters.p + 16, 0, sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->counters.p + kClassCtr, 0, (kNumClasses + 1) * sizeof(unsigned long long), c->stream));
+    c->fill_classes_ok = false;
     c->runs_emitted = 0;
     c->runs_ok = true;
     c->n_invalid = c->n_dropped = c->n_kept = 0;
@@ -2109,8 +2164,8 @@ mrf_status mrf_profile_read(mrf_ctx* ctx, int64_t* launches, double* total_ms) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, e.a, e.b));
         c->prof_ms[e.kind] += ms;
-        cudaEventDestroy(e.a);
-        cudaEventDestroy(e.b);
+        c->ev_pool.push_back(e.a);
+        c->ev_pool.push_back(e.b);
     }
     c->events.clear();
     for (int k = 0; k < MRF_K_COUNT; ++k) {
