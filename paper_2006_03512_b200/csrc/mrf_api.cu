@@ -201,7 +201,8 @@ struct mrf_ctx {
     DBuf<int32_t> run_keys;
     long long runs_emitted = 0, runs_cap = 0;
     bool runs_ok = true, run_fill_forced = false;
-    double run_ratio = 0.125;
+    double run_ratio = 0.125;        // (MRF_RUN_RATIO: the first estimate; tests force an overflow)
+    long long run_slack = 65536;     // (MRF_RUN_SLACK)
     DBuf<int2> bitems;
     std::vector<int2> h_items;  // host copy of the K6 work list
     long long n_runs = 0, n_bitems = 0;
@@ -465,7 +466,7 @@ mrf_status mf_rechunk(mrf_ctx* c) {
 mrf_status run_sink(mrf_ctx* c, long long new_slots, RunSink& sink) {
     sink = RunSink{nullptr, nullptr, nullptr, 0};
     if (c->run_fill_forced || !c->runs_ok) return MRF_OK;
-    const long long need = c->runs_emitted + (long long)std::ceil((double)new_slots * c->run_ratio) + 65536;
+    const long long need = c->runs_emitted + (long long)std::ceil((double)new_slots * c->run_ratio) + c->run_slack;
     if (need > c->runs_cap) {
         CK(c->runs_all.ensure((size_t)need, (size_t)std::min(c->runs_emitted, c->runs_cap), c->stream));
         CK(c->run_keys.ensure((size_t)need, (size_t)std::min(c->runs_emitted, c->runs_cap), c->stream));
@@ -1384,6 +1385,8 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     if (const char* kf = getenv("MRF_K6_FRAMES")) c->frame_buckets = atoi(kf) != 0;
     if (const char* rf = getenv("MRF_RUN_FILL")) c->run_fill_forced = atoi(rf) != 0;
     if (const char* mff = getenv("MRF_MF_FUSED")) c->mf_fused = atoi(mff) != 0;
+    if (const char* rr = getenv("MRF_RUN_RATIO")) c->run_ratio = atof(rr);
+    if (const char* rs = getenv("MRF_RUN_SLACK")) c->run_slack = atoll(rs);
     if (const char* k5 = getenv("MRF_K5")) c->k5_staged = strcmp(k5, "staged") == 0;
     if (const char* l2 = getenv("MRF_L2_FETCH")) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(l2));
     c->noise = {noise->z_lo, noise->z_hi, noise->off_lo, noise->off_hi, noise->margin_min, noise->margin_k,

@@ -625,3 +625,23 @@ def test_k6_frame_buckets_agree(frame1, monkeypatch):
             outs.append((m.export_beliefs(), m.export_messages()))
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+def test_run_sink_overflow_falls_back(frame1, monkeypatch):
+    """The fill's run sink sized too small (forced: MRF_RUN_RATIO / MRF_RUN_SLACK) overflows: the
+    transpose falls back to the vid re-read and the beliefs are the same; the next graph (after a
+    reset) gets a sink sized from the observed runs per slot and uses it."""
+    w = frame1
+    with _gpu_map(w) as m:
+        m.bp_iterate(2)
+        ref = (m.export_beliefs(), m.export_messages())
+    monkeypatch.setenv("MRF_RUN_RATIO", "0.0001")
+    monkeypatch.setenv("MRF_RUN_SLACK", "0")
+    with _gpu_map(w) as m:
+        m.bp_iterate(2)
+        assert np.array_equal(m.export_beliefs(), ref[0]) and np.array_equal(m.export_messages(), ref[1])
+        m.reset()
+        for fr in w.frames:
+            m.add_frame(fr.depth, fr.K, fr.T_wc)
+        m.bp_iterate(2)
+        assert np.array_equal(m.export_beliefs(), ref[0]) and np.array_equal(m.export_messages(), ref[1])
