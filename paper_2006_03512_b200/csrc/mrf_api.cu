@@ -849,7 +849,7 @@ mrf_status build_active_tiles(mrf_ctx* c) {
     for (long long b = 0; b < (long long)c->tile_nr.size(); ++b)  // (buckets: tiles, or (frame, tile) pairs)
         if (c->tile_nr[(size_t)b] > 0) h[(size_t)(b % NT)] = 1;
     CK(c->touched.ensure((size_t)NT, 0, c->stream));
-    if (c->world > 1) {
+    if (c->comm) {
         CK(cudaMemcpyAsync(c->touched.p, h.data(), (size_t)NT, cudaMemcpyHostToDevice, c->stream));
         NCK(ncclAllReduce(c->touched.p, c->touched.p, (size_t)NT, ncclUint8, ncclMax, c->comm, c->stream));
         CK(cudaMemcpyAsync(h.data(), c->touched.p, (size_t)NT, cudaMemcpyDeviceToHost, c->stream));
@@ -886,7 +886,7 @@ mrf_status prepare(mrf_ctx* c) {
         if ((st = build_tile_runs(c)) != MRF_OK) return st;
     }
     c->compact = !c->k6_voxel && ((c->world > 1 && c->comm_mode == MRF_COMM_NCCL) ||
-                                  (c->world == 1 && c->force_compact && !c->kf_avg));
+                                  (c->world == 1 && (c->force_compact || c->comm) && !c->kf_avg));
     if (c->compact && (st = build_active_tiles(c)) != MRF_OK) return st;
     // K5 classes by ray length (stable compaction keeps pixel order inside a class)
     CK(c->flags.ensure((size_t)std::max(c->R, c->VI) + 1, 0, c->stream));
@@ -1221,7 +1221,7 @@ mrf_status allreduce_T(mrf_ctx* c) {
     ProfScope ps(c, MRF_K_ALLREDUCE);
     if (c->compact) {
         if (c->n_act_tiles) {
-            if (c->world > 1) {
+            if (c->comm) {
                 NCK(ncclAllReduce(c->T_c.p, c->T_c.p, (size_t)(c->n_act_tiles * kTileSlots), ncclInt64, ncclSum,
                                   c->comm, c->stream));
                 c->prof_launch[MRF_K_ALLREDUCE] += 1;
@@ -1229,7 +1229,7 @@ mrf_status allreduce_T(mrf_ctx* c) {
             launch_tile_scatter(c->n_act_tiles, c->tile_of.p, c->T_c.p, c->T.p, c->stream);
             CK_LAUNCH(MRF_K_ALLREDUCE, 1);
         }
-        if (c->world == 1) return MRF_OK;
+        if (!c->comm) return MRF_OK;
     } else {
         NCK(ncclAllReduce(c->T_part.p, c->T.p, (size_t)c->VI, ncclInt64, ncclSum, c->comm, c->stream));
         c->prof_launch[MRF_K_ALLREDUCE] += 1;
@@ -1466,10 +1466,21 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
         return MRF_OK;
     };
     if ((st = alloc()) != MRF_OK) return fail(st);
-    if (world > 1 && comm_mode == MRF_COMM_NCCL) {
+    // MRF_NCCL_WORLD1=1: a one-rank communicator at world 1, so that the NCCL data plane (the
+    // touched-tile mask and the compacted all-reduce, the async-error polling) runs on one GPU (tests)
+    const char* w1 = getenv("MRF_NCCL_WORLD1");
+    const bool nccl_w1 = world == 1 && w1 && atoi(w1) != 0;
+    if ((world > 1 && comm_mode == MRF_COMM_NCCL) || nccl_w1) {
         ncclUniqueId id;
         static_assert(sizeof(id.internal) == 128, "ncclUniqueId size");
-        memcpy(id.internal, dist->nccl_id, 128);
+        if (nccl_w1) {
+            if (ncclGetUniqueId(&id) != ncclSuccess) {
+                c->err = "ncclGetUniqueId failed";
+                return fail(MRF_ERR_NCCL);
+            }
+        } else {
+            memcpy(id.internal, dist->nccl_id, 128);
+        }
         ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
         if (r != ncclSuccess) {
             c->err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);

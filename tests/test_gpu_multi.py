@@ -41,6 +41,41 @@ def test_compacted_reduction_bit_identical_one_gpu(monkeypatch):
         assert np.array_equal(x, y)
 
 
+def test_nccl_data_plane_one_rank(monkeypatch):
+    """The NCCL data plane on one GPU (MRF_NCCL_WORLD1=1: a one-rank communicator): the ncclMax
+    of the touched-tile mask, the in-place ncclAllReduce of the compacted sums, the scatter and
+    the async-error polling all run, through the C ABI; beliefs, messages and marginals
+    bit-identical to the plain path, warm start included."""
+    w = synth.frames30(n_frames=3)
+    a = _run(w, 3)
+    monkeypatch.setenv("MRF_NCCL_WORLD1", "1")
+    b = _run(w, 3)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    m = pkg.MRFMap.from_workload(w)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    with m:
+        m.set_profiling(True)
+        for fr in w.frames[:2]:
+            m.add_frame(fr.depth, fr.K, fr.T_wc)
+        m.bp_iterate(1)
+        m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)  # the touched tiles change
+        m.bp_iterate(2)
+        prof = m.profile_read()
+        assert prof["allreduce"][0] >= 3  # the NCCL all-reduce ran every iteration
+        T = m.export_beliefs()
+    monkeypatch.delenv("MRF_NCCL_WORLD1")
+    m = pkg.MRFMap.from_workload(w)
+    m.set_stream(torch.cuda.current_stream().cuda_stream)
+    with m:
+        for fr in w.frames[:2]:
+            m.add_frame(fr.depth, fr.K, fr.T_wc)
+        m.bp_iterate(1)
+        m.add_frame(w.frames[2].depth, w.frames[2].K, w.frames[2].T_wc)
+        m.bp_iterate(2)
+        assert np.array_equal(m.export_beliefs(), T)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
