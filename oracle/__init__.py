@@ -68,11 +68,11 @@ def lib():
             L.orc_log_nu.restype = d
             L.orc_ray_messages.argtypes = [i64, dp, dp, dp, dp, dp]
             L.orc_ray_messages.restype = None
-            L.orc_ray_pass.argtypes = [i64, i64p, i32p, i16p, dp, fp, i32, i32, dp, d, dp, dp]
+            L.orc_ray_pass.argtypes = [i64, i64p, i32p, i16p, dp, fp, i32, i32, dp, d, dp, dp, dp]
             L.orc_ray_pass.restype = None
             L.orc_accumulate.argtypes = [i64, i32p, dp, i64, dp]
             L.orc_accumulate.restype = None
-            L.orc_bp.argtypes = [i64, i64p, i32p, i16p, dp, fp, i32, i32, dp, d, i64, i32, dp, dp]
+            L.orc_bp.argtypes = [i64, i64p, i32p, i16p, dp, fp, i32, i32, dp, d, i64, i32, dp, dp, dp]
             L.orc_bp.restype = None
             L.orc_marginals.argtypes = [i64, d, dp, dp]
             L.orc_marginals.restype = None
@@ -80,17 +80,17 @@ def lib():
             L.orc_kf_beliefs.restype = None
             L.orc_kf_average.argtypes = [i64, i64p, i32p, i32p, dp, i64, i64, dp]
             L.orc_kf_average.restype = None
-            L.orc_kf_pass.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, dp, dp]
+            L.orc_kf_pass.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, dp, dp, dp]
             L.orc_kf_pass.restype = None
-            L.orc_kf_bp.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, i32, dp, dp, dp]
+            L.orc_kf_bp.argtypes = [i64, i64p, i32p, i16p, dp, i32p, fp, i32, i32, dp, d, i64, i64, i32, dp, dp, dp, dp]
             L.orc_kf_bp.restype = None
             u8p = _P(ctypes.c_uint8)
             L.orc_frame_count.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32, i8p, i64p, dp, dp, u8p, i32,
-                                          i32p]
+                                          i32p, dp]
             L.orc_frame_count.restype = None
-            L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p, u8p, i32, i32p]
+            L.orc_frame_fill.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i64p, i32p, i16p, u8p, i32, i32p, dp]
             L.orc_frame_fill.restype = None
-            L.orc_alloc_bricks.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32p, u8p]
+            L.orc_alloc_bricks.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, i32, i32p, u8p, dp]
             L.orc_alloc_bricks.restype = i64
             L.orc_dda_sparse.argtypes = [i32p, i64p, i64p, d, d, u8p, i32, i32p, i32p, i16p, dp, dp, i64]
             L.orc_dda_sparse.restype = i64
@@ -98,7 +98,9 @@ def lib():
             L.orc_vis_profile.restype = i64
             L.orc_eval_pixel.argtypes = [i32p, dp, dp, dp, dp, i32, i32, ctypes.c_float, dp, d, d, i32, dp]
             L.orc_eval_pixel.restype = ctypes.c_int
-            L.orc_eval_frame.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, dp, d, d, i32, i32, i32, i8p, i64p, i64p]
+            L.orc_eval_frame.argtypes = [i32p, dp, dp, dp, dp, i32, i32, fp, dp, d, d, i32, i32, i32, i8p, i64p, i64p, dp]
+            L.orc_patch_log_nu.argtypes = [i64, i64p, i16p, dp, dp, d, dp]
+            L.orc_patch_log_nu.restype = None
             L.orc_eval_frame.restype = None
             L.orc_set_num_threads.argtypes = [i32]
             L.orc_set_num_threads.restype = None
@@ -129,7 +131,7 @@ class Params:
     """Grid + noise model, as plain arrays for the C entry points."""
 
     def __init__(self, dims, res, origin, prior, log_nu, z_lo, z_hi, off_lo, off_hi,
-                 margin_min, margin_k, sigma_c):
+                 margin_min, margin_k, sigma_c, patch=None):
         self.dims = _c(dims, np.int32)
         self.geo = _c([res, origin[0], origin[1], origin[2]], np.float64)
         self.par = _c([z_lo, z_hi, off_lo, off_hi, margin_min, margin_k,
@@ -138,17 +140,35 @@ class Params:
         self.prior = float(prior)
         self.L0 = math.log(prior / (1.0 - prior))  # prior log-odds of Eq.2
         self.V = int(np.prod(self.dims.astype(np.int64)))
+        # learnt per-patch noise model (NEXT #4 option, reading R25): synth.PatchNoise or None
+        self.patch = patch
 
     @classmethod
     def from_workload(cls, w):
         return cls(w.dims, w.res, w.origin, w.prior, w.log_nu, w.z_lo, w.z_hi, w.off_lo, w.off_hi,
-                   w.margin_min, w.margin_k, w.sigma_c)
+                   w.margin_min, w.margin_k, w.sigma_c, getattr(w, "patch", None))
+
+    def pix_sigma(self, W, H):
+        """Per-pixel sigma coefficients [H*W, 3] of the patch model (None without one)."""
+        if self.patch is None:
+            return None
+        return _c(self.patch.pixel_coeffs(W, H)[:, 3:6], np.float64)
+
+    def pix_par(self, W, u, v):
+        """par of one pixel (the patch's sigma coefficients in place of c0, c1, c2)."""
+        if self.patch is None:
+            return self.par
+        par = self.par.copy()
+        par[6:9] = self.patch.coeffs[v // self.patch.patch_px, u // self.patch.patch_px, 3:6]
+        return par
 
 
 # --------------------------------------------------------------------------- B1..B3
 
-def ray_setup(p: Params, K, T_wc, u, v, z):
-    """B1 for one pixel -> (status, G0[3], G1[3], Z, L)."""
+def ray_setup(p: Params, K, T_wc, u, v, z, W=None):
+    """B1 for one pixel -> (status, G0[3], G1[3], Z, L).  W: the frame width (the pixel's patch of a
+    per-patch noise model, reading R25)."""
+    par = p.pix_par(W, int(u), int(v)) if (p.patch is not None and W is not None) else p.par
     G0 = np.zeros(3, np.int64)
     G1 = np.zeros(3, np.int64)
     Z = ctypes.c_double(0.0)
@@ -156,7 +176,7 @@ def ray_setup(p: Params, K, T_wc, u, v, z):
     K = _c(K, np.float64)
     T = _c(T_wc, np.float64)
     s = lib().orc_ray_setup(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double),
-                            _ptr(p.par, ctypes.c_double), _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double),
+                            _ptr(par, ctypes.c_double), _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double),
                             int(u), int(v), float(z), _ptr(G0, ctypes.c_int64), _ptr(G1, ctypes.c_int64),
                             ctypes.byref(Z), ctypes.byref(L))
     return s, G0, G1, Z.value, L.value
@@ -191,10 +211,11 @@ class Graph:
     """Canonical-order CSR of one rank's rays: row_ptr over kept rays, vid, off_q,
     plus per-ray range Z and the flat pixel id (frame, v*W+u)."""
 
-    def __init__(self, row_ptr, vid, off_q, Z, frame, pixel, n_invalid, n_dropped):
+    def __init__(self, row_ptr, vid, off_q, Z, frame, pixel, n_invalid, n_dropped, coef=None):
         self.row_ptr, self.vid, self.off_q, self.Z = row_ptr, vid, off_q, Z
         self.frame, self.pixel = frame, pixel
         self.n_invalid, self.n_dropped = n_invalid, n_dropped
+        self.coef = coef  # per-ray patch coefficients [n_rays, 6] of the per-patch model (R25), or None
 
     @property
     def n_rays(self):
@@ -227,11 +248,12 @@ def alloc_bricks(p: Params, frames, B: int = 8, bricks: Bricks = None) -> Bricks
     bk.added = []
     for fr in frames:
         H, W = fr.depth.shape
+        ps = p.pix_sigma(W, H)
         bk.added.append(int(lib().orc_alloc_bricks(
             _ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
             _ptr(_c(fr.K, np.float64), ctypes.c_double), _ptr(_c(fr.T_wc, np.float64), ctypes.c_double), W, H,
             _ptr(_c(fr.depth, np.float32), ctypes.c_float), bk.B, _ptr(bk.nb, ctypes.c_int32),
-            _ptr(bk.mask, ctypes.c_uint8))))
+            _ptr(bk.mask, ctypes.c_uint8), _ptr(ps, ctypes.c_double) if ps is not None else None)))
     return bk
 
 
@@ -270,27 +292,32 @@ def build_graph(p: Params, frames, rank: int = 0, world: int = 1, bricks: Bricks
         count = np.zeros(H * W, np.int64)
         Z = np.zeros(H * W, np.float64)
         Lr = np.zeros(H * W, np.float64)
+        ps = p.pix_sigma(W, H)
+        psp = _ptr(ps, ctypes.c_double) if ps is not None else None
         L_.orc_frame_count(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                            _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
                            rank, world, _ptr(status, ctypes.c_int8), _ptr(count, ctypes.c_int64),
-                           _ptr(Z, ctypes.c_double), _ptr(Lr, ctypes.c_double), *bm)
+                           _ptr(Z, ctypes.c_double), _ptr(Lr, ctypes.c_double), *bm, psp)
         kept = np.nonzero(status == STATUS_KEPT)[0]
         n_inv += int(np.sum(status == STATUS_INVALID))
         n_drop += int(np.sum(status == STATUS_DROPPED))
-        parts.append((fi, depth, K, T, W, H, kept, count[kept], Z[kept]))
+        cf = p.patch.pixel_coeffs(W, H)[kept] if p.patch is not None else None
+        parts.append((fi, depth, K, T, W, H, kept, count[kept], Z[kept], cf, ps))
         total += int(count[kept].sum())
     vid = np.zeros(total, np.int32)
     off_q = np.zeros(total, np.int16)
     row_ptr = [np.zeros(1, np.int64)]
-    Zs, fids, pix = [], [], []
+    Zs, fids, pix, cfs = [], [], [], []
     base = 0
-    for fi, depth, K, T, W, H, kept, cnt, Z in parts:
+    for fi, depth, K, T, W, H, kept, cnt, Z, cf, ps in parts:
         offs = np.full(H * W, -1, np.int64)
         starts = base + np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64) if len(cnt) else np.zeros(0, np.int64)
         offs[kept] = starts
         L_.orc_frame_fill(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                           _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
-                          _ptr(offs, ctypes.c_int64), _ptr(vid, ctypes.c_int32), _ptr(off_q, ctypes.c_int16), *bm)
+                          _ptr(offs, ctypes.c_int64), _ptr(vid, ctypes.c_int32), _ptr(off_q, ctypes.c_int16), *bm,
+                          _ptr(ps, ctypes.c_double) if ps is not None else None)
+        cfs.append(cf)
         row_ptr.append(base + np.cumsum(cnt).astype(np.int64))
         base += int(cnt.sum())
         Zs.append(Z)
@@ -298,7 +325,8 @@ def build_graph(p: Params, frames, rank: int = 0, world: int = 1, bricks: Bricks
         pix.append(kept.astype(np.int64))
     return Graph(np.concatenate(row_ptr), vid, off_q, np.concatenate(Zs) if Zs else np.zeros(0),
                  np.concatenate(fids) if fids else np.zeros(0, np.int32),
-                 np.concatenate(pix) if pix else np.zeros(0, np.int64), n_inv, n_drop)
+                 np.concatenate(pix) if pix else np.zeros(0, np.int64), n_inv, n_drop,
+                 (np.concatenate(cfs) if cfs else np.zeros((0, 6))) if p.patch is not None else None)
 
 
 def trace_pixels(p: Params, frame, pixels, frame_index: int = 0, bricks: Bricks = None) -> Graph:
@@ -311,7 +339,7 @@ def trace_pixels(p: Params, frame, pixels, frame_index: int = 0, bricks: Bricks 
     n_inv = n_drop = 0
     for px in pixels:
         v, u = divmod(int(px), W)
-        s, G0, G1, Z, L = ray_setup(p, frame.K, frame.T_wc, u, v, float(frame.depth[v, u]))
+        s, G0, G1, Z, L = ray_setup(p, frame.K, frame.T_wc, u, v, float(frame.depth[v, u]), W)
         if s == STATUS_INVALID:
             n_inv += 1
             continue
@@ -325,11 +353,31 @@ def trace_pixels(p: Params, frame, pixels, frame_index: int = 0, bricks: Bricks 
         Zs.append(Z)
         pix.append(int(px))
     cat = lambda a, t: np.concatenate(a).astype(t) if a else np.zeros(0, t)  # noqa: E731
+    coef = None
+    if p.patch is not None:
+        coef = p.patch.pixel_coeffs(W, H)[np.array(pix, np.int64)] if pix else np.zeros((0, 6))
     return Graph(np.array(row_ptr, np.int64), cat(vids, np.int32), cat(offs, np.int16), np.array(Zs),
-                 np.full(len(pix), frame_index, np.int32), np.array(pix, np.int64), n_inv, n_drop)
+                 np.full(len(pix), frame_index, np.int32), np.array(pix, np.int64), n_inv, n_drop, coef)
 
 
 # --------------------------------------------------------------------------- B4..B6
+
+def patch_log_nu(p: Params, g: Graph):
+    """log nu of every incidence under the per-patch model (R25) -> float64[E], or None when the
+    map uses the global LUT."""
+    if p.patch is None or g.coef is None:
+        return None
+    lnu = np.zeros(g.E)
+    lib().orc_patch_log_nu(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.off_q, ctypes.c_int16),
+                           _ptr(_c(g.Z, np.float64), ctypes.c_double), _ptr(_c(g.coef, np.float64), ctypes.c_double),
+                           float(p.patch.sigma_min), _ptr(lnu, ctypes.c_double))
+    return lnu
+
+
+def _lnu_arg(p, g):
+    lnu = patch_log_nu(p, g)
+    return (_ptr(lnu, ctypes.c_double) if lnu is not None else None), lnu
+
 
 def ray_messages(c, lnu):
     """B5 core for one ray: (lpos, lneg) = log of Eq.13 / Eq.14 messages."""
@@ -348,10 +396,11 @@ def ray_pass(p: Params, g: Graph, T, lam):
     """One flooding pass (B5) in place on lam (float64[E]) from snapshot T (float64[V])."""
     T = _c(T, np.float64)
     assert lam.dtype == np.float64 and lam.flags.c_contiguous
+    le, _keep = _lnu_arg(p, g)
     lib().orc_ray_pass(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
                        _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
                        _ptr(p.lut, ctypes.c_float), p.lut.shape[0], p.lut.shape[1], _ptr(p.par, ctypes.c_double),
-                       p.L0, _ptr(T, ctypes.c_double), _ptr(lam, ctypes.c_double))
+                       p.L0, _ptr(T, ctypes.c_double), _ptr(lam, ctypes.c_double), le)
     return lam
 
 
@@ -366,10 +415,11 @@ def bp(p: Params, g: Graph, n_iter: int, lam=None):
     """B4 (lam = 0) + n flooding iterations (B5, B7) -> (lam, T)."""
     lam = np.zeros(g.E) if lam is None else _c(lam, np.float64).copy()
     T = np.zeros(p.V)
+    le, _keep = _lnu_arg(p, g)
     lib().orc_bp(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
                  _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
                  _ptr(p.lut, ctypes.c_float), p.lut.shape[0], p.lut.shape[1], _ptr(p.par, ctypes.c_double),
-                 p.L0, p.V, int(n_iter), _ptr(lam, ctypes.c_double), _ptr(T, ctypes.c_double))
+                 p.L0, p.V, int(n_iter), _ptr(lam, ctypes.c_double), _ptr(T, ctypes.c_double), le)
     return lam, T
 
 
@@ -408,11 +458,12 @@ def kf_pass(p: Params, g: Graph, lbar):
     lbar = _c(lbar, np.float64)
     F, V = lbar.shape
     lam = np.zeros(g.E)
+    le, _keep = _lnu_arg(p, g)
     lib().orc_kf_pass(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
                       _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
                       _ptr(_c(g.frame, np.int32), ctypes.c_int32), _ptr(p.lut, ctypes.c_float), p.lut.shape[0],
                       p.lut.shape[1], _ptr(p.par, ctypes.c_double), p.L0, F, V, _ptr(lbar, ctypes.c_double),
-                      _ptr(lam, ctypes.c_double))
+                      _ptr(lam, ctypes.c_double), le)
     return lam
 
 
@@ -421,11 +472,12 @@ def kf_bp(p: Params, g: Graph, n_iter: int, F: int, lbar=None):
     lbar = np.zeros((F, p.V)) if lbar is None else _c(lbar, np.float64).copy()
     lam = np.zeros(g.E)
     T = np.zeros(p.V)
+    le, _keep = _lnu_arg(p, g)
     lib().orc_kf_bp(g.n_rays, _ptr(g.row_ptr, ctypes.c_int64), _ptr(g.vid, ctypes.c_int32),
                     _ptr(g.off_q, ctypes.c_int16), _ptr(_c(g.Z, np.float64), ctypes.c_double),
                     _ptr(_c(g.frame, np.int32), ctypes.c_int32), _ptr(p.lut, ctypes.c_float), p.lut.shape[0],
                     p.lut.shape[1], _ptr(p.par, ctypes.c_double), p.L0, F, p.V, int(n_iter),
-                    _ptr(lam, ctypes.c_double), _ptr(lbar, ctypes.c_double), _ptr(T, ctypes.c_double))
+                    _ptr(lam, ctypes.c_double), _ptr(lbar, ctypes.c_double), _ptr(T, ctypes.c_double), le)
     return lam, lbar, T
 
 
@@ -460,7 +512,8 @@ def eval_pixel(p: Params, frame, u, v, xmap, k_sigma=1.5, vis_thr=0.5, mode=0):
     K = _c(frame.K, np.float64)
     T = _c(frame.T_wc, np.float64)
     xm = _c(xmap, np.float64)
-    r = lib().orc_eval_pixel(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
+    par = p.pix_par(frame.depth.shape[1], int(u), int(v))
+    r = lib().orc_eval_pixel(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(par, ctypes.c_double),
                              _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), int(u), int(v),
                              float(frame.depth[v, u]), _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr),
                              int(mode), _ptr(out, ctypes.c_double))
@@ -478,8 +531,10 @@ def eval_frame(p: Params, frame, xmap, k_sigma=1.5, vis_thr=0.5, rank=0, world=1
     K = _c(frame.K, np.float64)
     T = _c(frame.T_wc, np.float64)
     xm = _c(xmap, np.float64)
+    ps = p.pix_sigma(W, H)
     lib().orc_eval_frame(_ptr(p.dims, ctypes.c_int32), _ptr(p.geo, ctypes.c_double), _ptr(p.par, ctypes.c_double),
                          _ptr(K, ctypes.c_double), _ptr(T, ctypes.c_double), W, H, _ptr(depth, ctypes.c_float),
                          _ptr(xm, ctypes.c_double), float(k_sigma), float(vis_thr), int(mode), rank, world,
-                         _ptr(cls, ctypes.c_int8), ctypes.byref(nv), ctypes.byref(na))
+                         _ptr(cls, ctypes.c_int8), ctypes.byref(nv), ctypes.byref(na),
+                         _ptr(ps, ctypes.c_double) if ps is not None else None)
     return cls.reshape(H, W), nv.value, na.value

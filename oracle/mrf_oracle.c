@@ -22,6 +22,9 @@
  *                                                          per (keyframe, voxel) = B5 iteration
  *   orc_alloc_bricks, orc_dda_sparse  NEXT #4 sparse bricks pinned: SPEC allocation examples, full
  *                                                          mask = dense walk, skipped cells = empty
+ *   orc_patch_log_nu  NEXT #4 option: learnt per-patch noise, reading R25
+ *                                                          pinned: scipy's Gaussian log-density; equal
+ *                                                          patches = the global model's traversal
  */
 #include <math.h>
 #include <omp.h>
@@ -68,6 +71,18 @@ int orc_ray_setup(const int32_t dims[3], const double geo[4], const double par[9
     *Z_out = Z;
     *L_out = L;
     return 0;
+}
+
+/* The learnt per-patch model (NEXT #4 option, reading R25): the sigma polynomial of the pixel's
+ * 20x20 patch replaces par[6..8] (c0, c1, c2) -- the traversal margin 3 sigma(Z) of P:205 and the
+ * allocation radius then follow the pixel's own noise.  pix_sigma: [H*W][3] or NULL. */
+static void pixel_par(const double par[9], const double* pix_sigma, int64_t p, double out[9]) {
+    for (int k = 0; k < 9; ++k) out[k] = par[k];
+    if (pix_sigma) {
+        out[6] = pix_sigma[3 * p];
+        out[7] = pix_sigma[3 * p + 1];
+        out[8] = pix_sigma[3 * p + 2];
+    }
 }
 
 /* ------------------------------------------------------------------ B2 + B3: fixed-point DDA */
@@ -205,6 +220,31 @@ double orc_log_nu(const float* lut, int32_t n_z, int32_t n_off, const double par
 }
 
 /* ------------------------------------------------------------------ B5: one ray */
+/* Learnt per-patch forward model (NEXT #4 option, reading R25; "we first utilise the
+ * sensor bias to predict what the mean sensor measurement would be and then evaluate the
+ * probability of a given measurement originating from this predicted measurement and distributed
+ * using the learnt noise value"; 2nd-degree polynomials per pixel region):
+ *   log nu(Z | d) = log N(Z; d + b(d), s(d)),  b(d) = (b0 + b1 d) + b2 d^2,
+ *   s(d) = max((s0 + s1 d) + s2 d^2, sigma_min),
+ * at the voxel depth d = Z + off_q / 32768 (B3's quantised span midpoint), with the coefficients
+ * of the ray's patch (coef[r][6] = b0, b1, b2, s0, s1, s2).  Out: lnu[e] for every incidence. */
+void orc_patch_log_nu(int64_t n_rays, const int64_t* row_ptr, const int16_t* off_q, const double* Z_ray,
+                      const double* coef, double sigma_min, double* lnu) {
+    const double half_log_2pi = 0.5 * log(2.0 * 3.14159265358979323846);
+    for (int64_t r = 0; r < n_rays; ++r) {
+        const double* k = coef + 6 * r;
+        const double Z = Z_ray[r];
+        for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+            const double d = Z + (double)off_q[e] / 32768.0;
+            const double b = (k[0] + k[1] * d) + k[2] * d * d;
+            double s = (k[3] + k[4] * d) + k[5] * d * d;
+            if (s < sigma_min) s = sigma_min;
+            const double t = (Z - (d + b)) / s;
+            lnu[e] = -0.5 * t * t - log(s) - half_log_2pi;
+        }
+    }
+}
+
 static double softplus(double x) { return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
 
 static double lse(double a, double b) {
@@ -263,7 +303,7 @@ static double clip256(double x) {
  * ray reads only its own old messages).  Z_ray[r] is the ray's measured range. */
 void orc_ray_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
                   const double* Z_ray, const float* lut, int32_t n_z, int32_t n_off, const double par[9],
-                  double L0, const double* T, double* lambda) {
+                  double L0, const double* T, double* lambda, const double* lnu_e) {
 #pragma omp parallel
     {
         int64_t cap = 0;
@@ -284,7 +324,7 @@ void orc_ray_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, co
             double* work = buf + 4 * N;
             for (int64_t i = 0; i < N; ++i) {
                 c[i] = L0 + T[vid[e0 + i]] - lambda[e0 + i];
-                lnu[i] = orc_log_nu(lut, n_z, n_off, par, Z_ray[r], off_q[e0 + i]);
+                lnu[i] = lnu_e ? lnu_e[e0 + i] : orc_log_nu(lut, n_z, n_off, par, Z_ray[r], off_q[e0 + i]);
             }
             orc_ray_messages(N, c, lnu, lpos, lneg, work);
             for (int64_t i = 0; i < N; ++i) lambda[e0 + i] = clip256(lpos[i] - lneg[i]);
@@ -303,11 +343,11 @@ void orc_accumulate(int64_t E, const int32_t* vid, const double* lambda, int64_t
 /* n flooding iterations (B7) starting from lambda (in/out); T returned for the final lambda. */
 void orc_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
             const double* Z_ray, const float* lut, int32_t n_z, int32_t n_off, const double par[9],
-            double L0, int64_t V, int32_t n_iter, double* lambda, double* T) {
+            double L0, int64_t V, int32_t n_iter, double* lambda, double* T, const double* lnu_e) {
     const int64_t E = row_ptr[n_rays];
     orc_accumulate(E, vid, lambda, V, T);
     for (int32_t it = 0; it < n_iter; ++it) {
-        orc_ray_pass(n_rays, row_ptr, vid, off_q, Z_ray, lut, n_z, n_off, par, L0, T, lambda);
+        orc_ray_pass(n_rays, row_ptr, vid, off_q, Z_ray, lut, n_z, n_off, par, L0, T, lambda, lnu_e);
         orc_accumulate(E, vid, lambda, V, T);
     }
 }
@@ -360,7 +400,8 @@ void orc_kf_average(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, 
 /* One flooding pass of the variant: lambda (per incidence, out) from the snapshot lbar. */
 void orc_kf_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
                  const double* Z_ray, const int32_t* frame, const float* lut, int32_t n_z, int32_t n_off,
-                 const double par[9], double L0, int64_t F, int64_t V, const double* lbar, double* lambda) {
+                 const double par[9], double L0, int64_t F, int64_t V, const double* lbar, double* lambda,
+                 const double* lnu_e) {
     double* T = (double*)malloc(sizeof(double) * (size_t)V);
     orc_kf_beliefs(F, V, lbar, T);
 #pragma omp parallel
@@ -384,7 +425,7 @@ void orc_kf_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, con
             const double* lb = lbar + (int64_t)frame[r] * V;
             for (int64_t i = 0; i < N; ++i) {
                 c[i] = L0 + T[vid[e0 + i]] - lb[vid[e0 + i]];
-                lnu[i] = orc_log_nu(lut, n_z, n_off, par, Z_ray[r], off_q[e0 + i]);
+                lnu[i] = lnu_e ? lnu_e[e0 + i] : orc_log_nu(lut, n_z, n_off, par, Z_ray[r], off_q[e0 + i]);
             }
             orc_ray_messages(N, c, lnu, lpos, lneg, work);
             for (int64_t i = 0; i < N; ++i) lambda[e0 + i] = clip256(lpos[i] - lneg[i]);
@@ -398,9 +439,9 @@ void orc_kf_pass(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, con
 void orc_kf_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const int16_t* off_q,
                const double* Z_ray, const int32_t* frame, const float* lut, int32_t n_z, int32_t n_off,
                const double par[9], double L0, int64_t F, int64_t V, int32_t n_iter, double* lambda,
-               double* lbar, double* T) {
+               double* lbar, double* T, const double* lnu_e) {
     for (int32_t it = 0; it < n_iter; ++it) {
-        orc_kf_pass(n_rays, row_ptr, vid, off_q, Z_ray, frame, lut, n_z, n_off, par, L0, F, V, lbar, lambda);
+        orc_kf_pass(n_rays, row_ptr, vid, off_q, Z_ray, frame, lut, n_z, n_off, par, L0, F, V, lbar, lambda, lnu_e);
         orc_kf_average(n_rays, row_ptr, vid, frame, lambda, F, V, lbar);
     }
     orc_kf_beliefs(F, V, lbar, T);
@@ -415,12 +456,14 @@ void orc_kf_bp(int64_t n_rays, const int64_t* row_ptr, const int32_t* vid, const
  * within distance r of p, so "every voxel within r_alloc of a reprojected point belongs to an
  * allocated brick" holds.  All pixels count, whatever their rank (the map is global).  Returns
  * the number of newly allocated bricks. */
-int64_t orc_alloc_bricks(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+int64_t orc_alloc_bricks(const int32_t dims[3], const double geo[4], const double par_in[9], const double K[4],
                          const double Twc[12], int32_t W, int32_t H, const float* depth, int32_t B,
-                         const int32_t nb[3], uint8_t* mask) {
+                         const int32_t nb[3], uint8_t* mask, const double* pix_sigma) {
     int64_t added = 0;
     for (int32_t v = 0; v < H; ++v)
         for (int32_t u = 0; u < W; ++u) {
+            double par[9];
+            pixel_par(par_in, pix_sigma, (int64_t)v * W + u, par);
             const double z = (double)depth[(int64_t)v * W + u];
             if (!isfinite(z) || !(z > 0.0)) continue;
             const double xc = ((double)u - K[2]) / K[0];
@@ -457,10 +500,10 @@ int64_t orc_alloc_bricks(const int32_t dims[3], const double geo[4], const doubl
 /* ------------------------------------------------------------------ frames -> CSR */
 /* Pass 1 over one frame: per pixel status (0 kept, 1 invalid, 2 dropped), cell count and
  * range Z.  Only rows with v % world == rank are visited (others get status 3). */
-void orc_frame_count(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+void orc_frame_count(const int32_t dims[3], const double geo[4], const double par_in[9], const double K[4],
                      const double Twc[12], int32_t W, int32_t H, const float* depth, int32_t rank,
                      int32_t world, int8_t* status, int64_t* count, double* Z_out, double* L_out,
-                     const uint8_t* mask, int32_t B, const int32_t* nb) {
+                     const uint8_t* mask, int32_t B, const int32_t* nb, const double* pix_sigma) {
     const BrickMask bm = {mask, B, {nb ? nb[0] : 0, nb ? nb[1] : 0, nb ? nb[2] : 0}};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int32_t v = 0; v < H; ++v) {
@@ -474,7 +517,8 @@ void orc_frame_count(const int32_t dims[3], const double geo[4], const double pa
                 continue;
             }
             int64_t G0[3], G1[3];
-            double Z = 0.0, L = 0.0;
+            double Z = 0.0, L = 0.0, par[9];
+            pixel_par(par_in, pix_sigma, p, par);
             const int s = orc_ray_setup(dims, geo, par, K, Twc, u, v, depth[p], G0, G1, &Z, &L);
             status[p] = (int8_t)s;
             if (s != 0) continue;
@@ -486,9 +530,10 @@ void orc_frame_count(const int32_t dims[3], const double geo[4], const double pa
 }
 
 /* Pass 2: write vid/off_q of every kept pixel at offset[p] (offset < 0: skip). */
-void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par_in[9], const double K[4],
                     const double Twc[12], int32_t W, int32_t H, const float* depth, const int64_t* offset,
-                    int32_t* vid, int16_t* off_q, const uint8_t* mask, int32_t B, const int32_t* nb) {
+                    int32_t* vid, int16_t* off_q, const uint8_t* mask, int32_t B, const int32_t* nb,
+                    const double* pix_sigma) {
     const BrickMask bm = {mask, B, {nb ? nb[0] : 0, nb ? nb[1] : 0, nb ? nb[2] : 0}};
 #pragma omp parallel for schedule(dynamic, 4)
     for (int32_t v = 0; v < H; ++v) {
@@ -496,7 +541,8 @@ void orc_frame_fill(const int32_t dims[3], const double geo[4], const double par
             const int64_t p = (int64_t)v * W + u;
             if (offset[p] < 0) continue;
             int64_t G0[3], G1[3];
-            double Z = 0.0, L = 0.0;
+            double Z = 0.0, L = 0.0, par[9];
+            pixel_par(par_in, pix_sigma, p, par);
             if (orc_ray_setup(dims, geo, par, K, Twc, u, v, depth[p], G0, G1, &Z, &L) != 0) continue;
             dda_core(dims, G0, G1, Z, L, &bm, vid + offset[p], off_q + offset[p], NULL, NULL, INT64_MAX);
         }
@@ -599,10 +645,10 @@ int orc_eval_pixel(const int32_t dims[3], const double geo[4], const double par[
 
 /* All pixels of one frame (rows v % world == rank; others -2).  cls[H*W]; returns
  * n_valid, n_accurate through the pointers. */
-void orc_eval_frame(const int32_t dims[3], const double geo[4], const double par[9], const double K[4],
+void orc_eval_frame(const int32_t dims[3], const double geo[4], const double par_in[9], const double K[4],
                     const double Twc[12], int32_t W, int32_t H, const float* depth, const double* xmap,
                     double k_sigma, double vis_thr, int32_t mode, int32_t rank, int32_t world, int8_t* cls,
-                    int64_t* n_valid, int64_t* n_acc) {
+                    int64_t* n_valid, int64_t* n_acc, const double* pix_sigma) {
     int64_t nv = 0, na = 0;
 #pragma omp parallel for schedule(dynamic, 64) reduction(+ : nv, na)
     for (int64_t i = 0; i < (int64_t)W * H; ++i) {
@@ -611,7 +657,8 @@ void orc_eval_frame(const int32_t dims[3], const double geo[4], const double par
             cls[i] = -2;
             continue;
         }
-        double out[4];
+        double out[4], par[9];
+        pixel_par(par_in, pix_sigma, i, par);
         const int r = orc_eval_pixel(dims, geo, par, K, Twc, u, v, depth[i], xmap, k_sigma, vis_thr, mode, out);
         cls[i] = (int8_t)r;
         if (r >= 0) {

@@ -20,5 +20,9 @@ from .scenes import (  # noqa: F401
     frames30,
     frames100,
     sweep300,
+    tiny_patch,
+    frame1_patch,
+    PatchNoise,
+    patch_noise_model,
 )
 from .lut import build_log_nu_lut  # noqa: F401

@@ -61,6 +61,7 @@ class Workload:
     n_iter: int
     frames: list = field(default_factory=list)
     seed: int = 0
+    patch: "PatchNoise" = None   # learnt per-patch noise model (NEXT #4 option, reading R25); None: the LUT
 
     @property
     def n_voxels(self) -> int:
@@ -71,6 +72,44 @@ class Workload:
                     off_lo=self.off_lo, off_hi=self.off_hi,
                     margin_min=self.margin_min, margin_k=self.margin_k,
                     sigma_c=self.sigma_c)
+
+
+# --------------------------------------------------------------------------- per-patch noise
+
+@dataclass
+class PatchNoise:
+    """The paper's learnt sensor model: per 20x20-pixel patch a 2nd-degree polynomial
+    bias b(d) = b0 + b1 d + b2 d^2 and standard deviation s(d) = s0 + s1 d + s2 d^2 of the measured
+    range given the true range d ("fit a 2nd degree polynomial"; the measurement is
+    distributed around the bias-predicted mean with the learnt noise).  Synthetic here:
+    no calibration data exists; the coefficients are seeded smooth fields around the global model."""
+    patch_px: int
+    coeffs: np.ndarray          # float64 [n_py, n_px, 6]: b0, b1, b2, s0, s1, s2
+    sigma_min: float = 1e-4
+
+    def pixel_coeffs(self, W, H):
+        """[H*W, 6] per pixel (patch (u // patch_px, v // patch_px))."""
+        v, u = np.divmod(np.arange(W * H), W)
+        return self.coeffs[v // self.patch_px, u // self.patch_px].reshape(W * H, 6)
+
+
+def patch_noise_model(W, H, seed=0, patch_px=20, sigma_c=(0.0, 0.0, 0.0012), bias_amp=4e-4, sigma_spread=0.3):
+    """Seeded per-patch coefficients: s2 = c2 (1 + sigma_spread f), b2 = bias_amp g, with f, g
+    smooth fields in [-1, 1] over the patch grid (a vignetting-like pattern plus a random phase)."""
+    n_px, n_py = -(-W // patch_px), -(-H // patch_px)
+    rs = np.random.default_rng(seed + 5)
+    ph = rs.uniform(0, 2 * math.pi, 4)
+    x = (np.arange(n_px) + 0.5) / n_px - 0.5
+    y = (np.arange(n_py) + 0.5) / n_py - 0.5
+    X, Y = np.meshgrid(x, y)
+    f = np.clip(2.0 * (X * X + Y * Y) - 0.25 + 0.25 * np.sin(2 * math.pi * X + ph[0]) * np.cos(2 * math.pi * Y + ph[1]),
+                -1.0, 1.0)
+    g = np.sin(math.pi * X + ph[2]) * np.cos(math.pi * Y + ph[3])
+    c = np.zeros((n_py, n_px, 6))
+    c[..., 3], c[..., 4] = sigma_c[0], sigma_c[1]
+    c[..., 5] = sigma_c[2] * (1.0 + sigma_spread * f)
+    c[..., 2] = bias_amp * g
+    return PatchNoise(patch_px, c)
 
 
 # --------------------------------------------------------------------------- geometry
@@ -131,14 +170,20 @@ def _pixel_dirs(W, H, K):
     return Dc, rho
 
 
-def _render_frame(scene, W, H, K, R, C, sigma_c, outlier_pi, rng_noise, invalid_p, rng_invalid):
+def _render_frame(scene, W, H, K, R, C, sigma_c, outlier_pi, rng_noise, invalid_p, rng_invalid, patch=None):
     _, rho = _pixel_dirs(W, H, K)
     t = scene.render_depth(W, H, K, R, C)
     valid = np.isfinite(t)
     Z = np.where(valid, t * rho, 0.0)
-    c0, c1, c2 = sigma_c
-    sig = c0 + c1 * Z + c2 * Z * Z
-    Z = Z + rng_noise.standard_normal(Z.shape) * sig  # noise along the range (§8(d))
+    if patch is None:
+        c0, c1, c2 = sigma_c
+        sig = c0 + c1 * Z + c2 * Z * Z
+        Z = Z + rng_noise.standard_normal(Z.shape) * sig  # noise along the range (§8(d))
+    else:  # the per-patch model: bias-predicted mean, per-patch sigma
+        pc = patch.pixel_coeffs(W, H)
+        bias = pc[:, 0] + pc[:, 1] * Z + pc[:, 2] * Z * Z
+        sig = np.maximum(pc[:, 3] + pc[:, 4] * Z + pc[:, 5] * Z * Z, patch.sigma_min)
+        Z = Z + bias + rng_noise.standard_normal(Z.shape) * sig
     if outlier_pi > 0:
         out = rng_noise.random(Z.shape) < outlier_pi
         Z = np.where(out, rng_noise.uniform(OUTLIER_LO, OUTLIER_HI, Z.shape), Z)
@@ -339,3 +384,41 @@ CONFIG_NAMES = {"tiny": tiny, "frame1": single_frame, "frames30": frames30,
 
 def make_workload(name: str, seed: int = 0, **kw) -> Workload:
     return CONFIG_NAMES[name](seed=seed, **kw)
+
+
+def tiny_patch(seed: int = 0) -> Workload:
+    """The tiny config with the learnt per-patch noise model (20x20-pixel patches: 4 x 3 over 64x48)."""
+    w = tiny(seed)
+    rs = np.random.default_rng(seed)
+    scene = _tiny_scene(rs)
+    pm = patch_noise_model(64, 48, seed, 20, w.sigma_c)
+    fr = w.frames[0]
+    R = fr.T_wc.reshape(3, 4)[:, :3]
+    C = fr.T_wc.reshape(3, 4)[:, 3]
+    w.frames = [_render_frame(scene, 64, 48, tuple(fr.K), R, C, w.sigma_c, 0.0, np.random.default_rng(seed + 2), 0.1,
+                              np.random.default_rng(seed + 3), patch=pm)]
+    w.patch = pm
+    w.name = "tiny_patch"
+    return w
+
+
+def frame1_patch(seed: int = 0) -> Workload:
+    """configs[1]'s room and camera with the per-patch noise model (32 x 24 patches)."""
+    rs = np.random.default_rng(seed)
+    scene = _Scene()
+    size = (6.0, 6.0, 3.0)
+    _room(scene, size)
+    _add_boxes(scene, rs, 20, size)
+    rt = np.random.default_rng(seed + 1)
+    yaw0 = rt.uniform(0, 2 * math.pi)
+    R, C = _camera_rotation(yaw0), np.array([3.0, 3.0, 1.5])
+    sigma_c = (0.0, 0.0, 0.0012)
+    pm = patch_noise_model(640, 480, seed, 20, sigma_c)
+    fr = _render_frame(scene, 640, 480, (525.0, 525.0, 319.5, 239.5), R, C, sigma_c, 0.0,
+                       np.random.default_rng(seed + 2), 0.0, None, patch=pm)
+    lut = build_log_nu_lut(256, 256, 0.0, 9.0, -0.5, 0.5, sigma_c, 0.0)
+    return Workload("frame1_patch", (120, 120, 60), 0.05, (0.0, 0.0, 0.0), 0.1, lut, 0.0, 9.0, -0.5, 0.5,
+                    0.1, 3.0, sigma_c, 8, [fr], seed, pm)
+
+
+CONFIG_NAMES.update({"tiny_patch": tiny_patch, "frame1_patch": frame1_patch})
