@@ -271,6 +271,24 @@ mrf_status mrf_export_bricks(mrf_ctx* ctx, uint8_t* out, int64_t* n_allocated);
  * mrf_graph_sizes reports n_active_vox = -1. */
 mrf_status mrf_set_matrix_free(mrf_ctx* ctx, int32_t frames_per_chunk);
 
+/* Learnt per-patch sensor model (SURVEY §8(f) NEXT #4 option, DESIGN reading
+ * R25): the image is cut into patch_px x patch_px pixel patches, patch (i, j) = pixels
+ * u in [i patch_px, (i+1) patch_px), v in [j patch_px, (j+1) patch_px); coeffs (host, row-major
+ * [n_py][n_px][6], copied) holds per patch b0, b1, b2, s0, s1, s2: the bias b(d) = b0 + b1 d + b2 d^2
+ * and the standard deviation s(d) = max(s0 + s1 d + s2 d^2, sigma_min) of the measured range given
+ * the true range d (2nd-degree polynomials).  The forward model of Eq.4 becomes
+ * nu(d) = N(Z; d + b(d), s(d)) ("the probability of a given measurement originating from this
+ * predicted measurement and distributed using the learnt noise value"), evaluated in closed
+ * form (fp32) at each incidence's voxel depth d = Z + off_q 2^-15 instead of the table of
+ * mrf_create; the traversal margin of a pixel becomes max(margin_min, margin_k s(Z)) with its
+ * patch's s (fp64, as with sigma_c).  patch_px = 0 returns to the table (coeffs ignored).
+ * Set before the first frame (MRF_ERR_STATE otherwise); frames (and mrf_evaluate images) must fit
+ * the patch grid (W <= n_px patch_px, H <= n_py patch_px; MRF_ERR_INVALID_ARG); MRF_ERR_INVALID_ARG
+ * for non-finite coefficients, sigma_min <= 0, or a margin over the grid diagonal (the bound of
+ * mrf_create, per patch).  mrf_reset keeps the model. */
+mrf_status mrf_set_patch_noise(mrf_ctx* ctx, int32_t patch_px, int32_t n_px, int32_t n_py, const double* coeffs,
+                               double sigma_min);
+
 /* 128-byte ncclUniqueId for MRF_COMM_NCCL (call on rank 0, broadcast to the others). */
 mrf_status mrf_nccl_unique_id(unsigned char out[128]);
 

@@ -85,8 +85,11 @@ class MRFMap:
 
     @classmethod
     def from_workload(cls, w, **kw):
-        return cls(w.dims, w.res, w.origin, w.prior, w.log_nu, w.z_lo, w.z_hi, w.off_lo, w.off_hi,
-                   w.margin_min, w.margin_k, w.sigma_c, **kw)
+        m = cls(w.dims, w.res, w.origin, w.prior, w.log_nu, w.z_lo, w.z_hi, w.off_lo, w.off_hi,
+                w.margin_min, w.margin_k, w.sigma_c, **kw)
+        if getattr(w, "patch", None) is not None:  # the learnt per-patch sensor model (R25)
+            m.set_patch_noise(w.patch.patch_px, w.patch.coeffs, w.patch.sigma_min)
+        return m
 
     # ------------------------------------------------------------------ lifecycle
     def close(self):
@@ -230,6 +233,18 @@ class MRFMap:
         """mrf_set_matrix_free: keep only the messages and the tile runs; re-walk the rays of each
         chunk of frames_per_chunk frames before every message pass (0 = stored graph)."""
         self._chk(self._L.mrf_set_matrix_free(self._h, int(frames_per_chunk)))
+
+    def set_patch_noise(self, patch_px, coeffs, sigma_min=1e-4):
+        """mrf_set_patch_noise: coeffs [n_py, n_px, 6] (b0, b1, b2, s0, s1, s2 per patch of
+        patch_px x patch_px pixels); patch_px = 0 returns to the table."""
+        if int(patch_px) == 0:
+            self._chk(self._L.mrf_set_patch_noise(self._h, 0, 0, 0, None, 1.0))
+            return
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        if c.ndim != 3 or c.shape[2] != 6:
+            raise ValueError("coeffs must be [n_py, n_px, 6]")
+        self._chk(self._L.mrf_set_patch_noise(self._h, int(patch_px), int(c.shape[1]), int(c.shape[0]),
+                                              c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), float(sigma_min)))
 
     def set_sparse_bricks(self, brick=8):
         """mrf_set_sparse_bricks: brick-sparse map with B^3 bricks allocated around the

@@ -32,7 +32,8 @@ EXPORTS = ["mrf_create", "mrf_add_frame", "mrf_bp_iterate", "mrf_marginals", "mr
            "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph", "mrf_export_rays", "mrf_evaluate",
            "mrf_export_transpose", "mrf_export_messages", "mrf_import_messages", "mrf_export_beliefs",
            "mrf_bp_partial", "mrf_bp_finish", "mrf_belief_slots", "mrf_nccl_unique_id", "mrf_set_profiling",
-           "mrf_profile_read", "mrf_launch_count", "mrf_set_message_mode", "mrf_export_keyframe_average", "mrf_set_sparse_bricks", "mrf_export_bricks", "mrf_set_matrix_free"]
+           "mrf_profile_read", "mrf_launch_count", "mrf_set_message_mode", "mrf_export_keyframe_average", "mrf_set_sparse_bricks", "mrf_export_bricks", "mrf_set_matrix_free",
+           "mrf_set_patch_noise"]
 
 
 class MrfError(RuntimeError):
@@ -85,6 +86,7 @@ def load(build: bool = True):
                 "mrf_export_keyframe_average": (st, [vp, i64, vp]),
                 "mrf_set_sparse_bricks": (st, [vp, i32]),
                 "mrf_set_matrix_free": (st, [vp, i32]),
+                "mrf_set_patch_noise": (st, [vp, i32, i32, i32, P(f64), f64]),
                 "mrf_export_bricks": (st, [vp, vp, P(i64)]),
                 "mrf_export_graph": (st, [vp, vp, vp, vp, vp]),
                 "mrf_export_transpose": (st, [vp, vp, vp]),

@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS :
 // No vid / off_q / log-nu array exists: per iteration K5 moves lambda (read + write), the
 // checkpoints and the per-ray records.  Bit-identical to the stored graph (same walk, same
 // interpolation, same message arithmetic).
+constexpr int kNoIncidence = 1 << 20;  // walk_chunk: a slot past the ray's end (offsets are int16)
 template <int K>
 __device__ __forceinline__ void walk_chunk(const WalkParams& wp, const RaySeg& sg, const MsgParams& mp, int iz, float wz,
                                            int vck, bool first, int nv, int (&v)[K], int (&ln)[K]) {
@@ -458,7 +459,7 @@ __device__ __forceinline__ void walk_chunk(const WalkParams& wp, const RaySeg& s
         const double mid = __dmul_rn(__dmul_rn(0.5, __dadd_rn(w.t_in, t_out)), sg.L);
         long long q = __double2ll_rn(__dmul_rn(__dsub_rn(mid, sg.Z), 32768.0));
         q = q > 32767 ? 32767 : (q < -32767 ? -32767 : q);
-        ln[j] = __float_as_int(ok ? lut_finish(lut_fetch(mp, iz, (int)q), wz) : 0.f);
+        ln[j] = ok ? (int)q : kNoIncidence;  // log nu after the walk (table loads back to back)
         w.advance(na, da);
         w.t_in = t_out;
         // sparse bricks (g.bmask set): the next emitted cell lies past any unallocated brick, reached
@@ -466,6 +467,15 @@ __device__ __forceinline__ void walk_chunk(const WalkParams& wp, const RaySeg& s
         if (j + 1 < nv)
             while (!cell_in_map(wp.g, w.c0, w.c1, w.c2))
                 if (!w.skip_brick(wp.g) || !w.inside(wp.g)) break;
+    }
+    if (mp.pcoef) {  // per-patch noise (R25): iz = the ray's patch, wz = its range
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            ln[j] = __float_as_int(ln[j] != kNoIncidence ? patch_lnu(mp, iz, wz, ln[j]) : 0.f);
+    } else {
+#pragma unroll
+        for (int j = 0; j < K; ++j)
+            ln[j] = __float_as_int(ln[j] != kNoIncidence ? lut_finish(lut_fetch(mp, iz, ln[j]), wz) : 0.f);
     }
 }
 

@@ -21,6 +21,19 @@ constexpr unsigned kFull = 0xffffffffu;
 // All fp64 steps use explicitly rounded intrinsics (no FMA contraction), in the order
 // stated in DESIGN.md §Graph build, so the quantised end points are reproducible.
 
+// sigma(Z) = c0 + c1 Z + c2 Z^2 of the traversal margin, with the pixel's patch
+// coefficients under the per-patch model (R25)
+__device__ __forceinline__ double pixel_sigma(const NoiseDesc& n, int u, int v, double Z) {
+    double c0 = n.c0, c1 = n.c1, c2 = n.c2;
+    if (n.pcoef) {
+        const double* k = n.pcoef + 6 * pixel_patch(n, u, v) + 3;
+        c0 = k[0];
+        c1 = k[1];
+        c2 = k[2];
+    }
+    return __dadd_rn(__dadd_rn(c0, __dmul_rn(c1, Z)), __dmul_rn(__dmul_rn(c2, Z), Z));
+}
+
 // 0 = kept, 1 = invalid pixel, 2 = dropped (measured point outside the grid)
 __device__ __forceinline__ int pixel_segment(const FrameDesc& f, const GridDesc& g, const NoiseDesc& n, int u,
                                              int v, float zf, Segment& sg) {
@@ -30,7 +43,7 @@ __device__ __forceinline__ int pixel_segment(const FrameDesc& f, const GridDesc&
     const double yc = __ddiv_rn(__dsub_rn((double)v, f.cy), f.fy);
     const double rho = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xc, xc), __dmul_rn(yc, yc)), 1.0));
     const double Z = __dmul_rn(z, rho);
-    const double sig = __dadd_rn(__dadd_rn(n.c0, __dmul_rn(n.c1, Z)), __dmul_rn(__dmul_rn(n.c2, Z), Z));
+    const double sig = pixel_sigma(n, u, v, Z);
     double margin = __dmul_rn(n.margin_k, sig);
     if (margin < n.margin_min) margin = n.margin_min;
     const double L = __dadd_rn(Z, margin);
@@ -101,7 +114,12 @@ __device__ __forceinline__ void raygen_count_body(const FrameDesc& f, long long 
                             abs((int)(sg.g1[1] >> kFixShift) - w.c1) + abs((int)(sg.g1[2] >> kFixShift) - w.c2);
                 }
             }
-            // LUT row of the measured range (bin centres, clamped to the edge centres)
+            // LUT row of the measured range (bin centres, clamped to the edge centres); per-patch
+            // noise: the patch and the range
+            if (n.pcoef) {
+                rz.iz = pixel_patch(n, u, v);
+                rz.wz = (float)sg.Z;
+            } else {
             double fz = __dsub_rn(__dmul_rn(__ddiv_rn(__dsub_rn(sg.Z, n.z_lo), __dsub_rn(n.z_hi, n.z_lo)),
                                             (double)n.n_z), 0.5);
             if (fz < 0.0) fz = 0.0;
@@ -110,6 +128,7 @@ __device__ __forceinline__ void raygen_count_body(const FrameDesc& f, long long 
             if (iz > n.n_z - 2) iz = n.n_z - 2;
             rz.iz = iz;
             rz.wz = (float)(fz - (double)iz);
+            }
         }
         rz.n = 0;  // set by the fill
         n_r[f.ray_base + i] = (bound + kSegAlign - 1) & ~(kSegAlign - 1);  // segments start at multiples of 8
@@ -217,7 +236,7 @@ __global__ void brick_alloc_kernel(FrameDesc f, GridDesc g, NoiseDesc n, const f
     const double yc = __ddiv_rn(__dsub_rn((double)v, f.cy), f.fy);
     const double rho = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(xc, xc), __dmul_rn(yc, yc)), 1.0));
     const double Z = __dmul_rn(z, rho);
-    const double sig = __dadd_rn(__dadd_rn(n.c0, __dmul_rn(n.c1, Z)), __dmul_rn(__dmul_rn(n.c2, Z), Z));
+    const double sig = pixel_sigma(n, u, v, Z);
     const double r = __ddiv_rn(__dmul_rn(n.margin_k, sig), g.res);
     const double org[3] = {g.ox, g.oy, g.oz};
     const int dims[3] = {g.nx, g.ny, g.nz};
@@ -254,7 +273,14 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, int e_
         o[k] = k < nvalid ? so[k] : (short)0;
     }
 #if MRF_FILL_LNU
-    {
+    if (mp.pcoef) {  // per-patch noise (R25): iz = the ray's patch, wz = its range
+        float l[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) l[k] = k < nvalid ? patch_lnu(mp, iz, wz, o[k]) : 0.f;
+        float4* dl = reinterpret_cast<float4*>(lnu + e_chunk);
+        dl[0] = make_float4(l[0], l[1], l[2], l[3]);
+        dl[1] = make_float4(l[4], l[5], l[6], l[7]);
+    } else {
         LutFetch lf[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) lf[k] = lut_fetch(mp, iz, o[k]);
@@ -513,7 +539,8 @@ __global__ void __launch_bounds__(256) lnu_fill_kernel(long long r0, long long n
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int q = (int)(short)((ow[k >> 1] >> (16 * (k & 1))) & 0xffffu);
-            out[k] = lut_finish(lut_fetch(mp, ri.iz, q), ri.wz) * (float)(c + k < ri.n);
+            out[k] = (mp.pcoef ? patch_lnu(mp, ri.iz, ri.wz, q) : lut_finish(lut_fetch(mp, ri.iz, q), ri.wz)) *
+                     (float)(c + k < ri.n);
         }
         float4* dst = reinterpret_cast<float4*>(lnu + e0 + c);
         dst[0] = make_float4(out[0], out[1], out[2], out[3]);
@@ -583,7 +610,7 @@ __global__ void __launch_bounds__(128) eval_kernel(FrameDesc f, GridDesc g, Nois
                 w.t_in = t_out;
             }
             const double vis_inf = exp(lvis);
-            const double sig = __dadd_rn(__dadd_rn(n.c0, __dmul_rn(n.c1, Z)), __dmul_rn(__dmul_rn(n.c2, Z), Z));
+            const double sig = pixel_sigma(n, u, v, Z);
             if (vis_inf > vis_thr)
                 r = Z > s_inf;
             else if (mode == 0)

@@ -129,7 +129,15 @@ struct RunSink {
 struct NoiseDesc {
     double z_lo, z_hi, off_lo, off_hi, margin_min, margin_k, c0, c1, c2;
     int n_z, n_off;
+    // learnt per-patch noise model (NEXT #4 option, reading R25; mrf_set_patch_noise): the
+    // coefficients [patch][6] = (b0, b1, b2, s0, s1, s2) of patch (u / ppx) + pnx (v / ppx); the
+    // pixel's (s0, s1, s2) replace (c0, c1, c2) in its traversal margin.  nullptr: the global model.
+    const double* pcoef;
+    int ppx, pnx;
 };
+__host__ __device__ __forceinline__ int pixel_patch(const NoiseDesc& n, int u, int v) {
+    return (v / n.ppx) * n.pnx + u / n.ppx;
+}
 
 struct FrameDesc {
     double fx, fy, cx, cy;
@@ -144,8 +152,8 @@ struct FrameDesc {
     int bucket_stride;        // tile-run bucket of a run in tile t: index * bucket_stride + t
 };
 
-// Per-ray record: LUT row iz (<= n_z-2) and weight wz in [0,1] of the measured range, and the
-// number of incidences n.  Ray segments start at multiples of 8 in the incidence arrays
+// Per-ray record: LUT row iz (<= n_z-2) and weight wz in [0,1] of the measured range (per-patch
+// noise, R25: iz = the pixel's patch, wz = the range Z), and the number of incidences n.  Ray segments start at multiples of 8 in the incidence arrays
 // (row_ptr advances by pad8(n)), so per-lane chunks are relative to the ray start, 16-byte
 // aligned, and a ray's arithmetic never depends on where (or on which rank) it is stored.
 struct RayInfo {
@@ -168,6 +176,9 @@ struct MsgParams {
     long long qbar_vi;
     // checked build: the message slots [0, chk_lam) and belief slots [0, chk_vi) that exist
     long long chk_lam, chk_vi;
+    // per-patch noise (R25): per patch (b0, b1, b2, 0) and (s0, s1, s2, sigma_min) in fp32; a ray's
+    // RayInfo then carries iz = its patch and wz = its range Z.  nullptr: the LUT.
+    const float4* pcoef;
 };
 
 // log nu at (measured range row iz + wz, quantised offset off_q): bilinear interpolation of the
@@ -200,6 +211,20 @@ __device__ __forceinline__ float lut_finish(const LutFetch& f, float wz) {
     const float ra = fmaf(f.wo, f.ta.y - f.ta.x, f.ta.x);
     const float rb = fmaf(f.wo, f.tb.y - f.tb.x, f.tb.x);
     return fmaf(wz, rb - ra, ra) * kLnuScale;
+}
+
+// log nu of the per-patch model (reading R25) in K5's units: the measurement Z is
+// Gaussian around the bias-predicted mean d + b(d) with sigma s(d), d = Z + off_q 2^-15 the voxel
+// depth (B3's span midpoint): ln nu = -t^2 / 2 - ln s - ln(2 pi) / 2, t = (Z - d - b) / s =
+// -(off_q 2^-15 + b) / s.  fp32 (the LUT path's precision).
+__device__ __forceinline__ float patch_lnu(const MsgParams& mp, int patch, float Z, int off) {
+    const float4 b = __ldg(mp.pcoef + 2 * patch), sc = __ldg(mp.pcoef + 2 * patch + 1);
+    const float o = (float)off * (1.f / 32768.f);
+    const float d = Z + o;
+    const float bias = fmaf(b.z * d, d, fmaf(b.y, d, b.x));
+    const float sg = fmaxf(fmaf(sc.z * d, d, fmaf(sc.y, d, sc.x)), sc.w);
+    const float t = (o + bias) / sg;
+    return (fmaf(-0.5f * t, t, -logf(sg)) - 0.91893853320467274f) * kLnuScale;
 }
 
 struct RaySeg;  // walk.cuh

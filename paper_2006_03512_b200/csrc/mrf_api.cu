@@ -219,6 +219,11 @@ struct mrf_ctx {
     DBuf<uint8_t> touched;
     DBuf<long long> T_c;
     DBuf<float2> lutp;
+    // per-patch noise (R25, mrf_set_patch_noise): fp64 coefficients for the margins, fp32 pairs
+    // for log nu; the frames must lie inside the patch grid
+    DBuf<double> pcoef_d;
+    DBuf<float4> pcoef_f;
+    int patch_px = 0, patch_nx = 0, patch_ny = 0;
     DBuf<float> depth_stage, marg;
     // frames added since the last fill: the walk (K3) of all of them runs as one launch when
     // the graph is next needed (sync_fill)
@@ -1605,6 +1610,9 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
                        "sparse bricks with matrix-free walks: add every keyframe before the graph is first used");
     if (!depth || !K || !T_wc) return set_err(c, MRF_ERR_INVALID_ARG, "NULL argument");
     if (width <= 0 || height <= 0) return set_err(c, MRF_ERR_INVALID_ARG, "width/height must be > 0");
+    if (c->patch_px && ((long long)width > (long long)c->patch_px * c->patch_nx ||
+                        (long long)height > (long long)c->patch_px * c->patch_ny))
+        return set_err(c, MRF_ERR_INVALID_ARG, "image larger than the patch grid of the noise model");
     if (!finite_all(K, 4) || !(K[0] > 0) || !(K[1] > 0))
         return set_err(c, MRF_ERR_INVALID_ARG, "K must be finite with fx, fy > 0");
     if (!finite_all(T_wc, 12)) return set_err(c, MRF_ERR_INVALID_ARG, "T_wc must be finite");
@@ -1776,6 +1784,9 @@ mrf_status mrf_evaluate(mrf_ctx* ctx, const float* depth, int32_t width, int32_t
     if (width <= 0 || height <= 0) return set_err(c, MRF_ERR_INVALID_ARG, "width/height must be > 0");
     if (!(k_sigma > 0) || !(vis_threshold > 0 && vis_threshold < 1) || (mode != MRF_EVAL_SIGMA_BAND && mode != MRF_EVAL_VOXEL_BOUNDS))
         return set_err(c, MRF_ERR_INVALID_ARG, "need k_sigma > 0, 0 < vis_threshold < 1 and a known mode");
+    if (c->patch_px && ((long long)width > (long long)c->patch_px * c->patch_nx ||
+                        (long long)height > (long long)c->patch_px * c->patch_ny))
+        return set_err(c, MRF_ERR_INVALID_ARG, "image larger than the patch grid of the noise model");
     if (!finite_all(K, 4) || !(K[0] > 0) || !(K[1] > 0)) return set_err(c, MRF_ERR_INVALID_ARG, "bad K");
     if (!finite_all(T_wc, 12)) return set_err(c, MRF_ERR_INVALID_ARG, "T_wc must be finite");
     const double org[3] = {c->grid.ox, c->grid.oy, c->grid.oz};
@@ -2108,6 +2119,58 @@ mrf_status mrf_set_sparse_bricks(mrf_ctx* ctx, int32_t brick) {
     c->grid.bshift = __builtin_ctz((unsigned)brick);
     c->grid.nbx = nb[0];
     c->grid.nby = nb[1];
+    c->dirty = true;
+    return MRF_OK;
+}
+
+mrf_status mrf_set_patch_noise(mrf_ctx* ctx, int32_t patch_px, int32_t n_px, int32_t n_py, const double* coeffs,
+                               double sigma_min) {
+    ENTER(ctx);
+    if (!c->frames.empty()) return set_err(c, MRF_ERR_STATE, "the noise model is set before the first frame");
+    if (patch_px == 0) {  // back to the global model (the LUT)
+        c->noise.pcoef = nullptr;
+        c->mp.pcoef = nullptr;
+        c->patch_px = c->patch_nx = c->patch_ny = 0;
+        return MRF_OK;
+    }
+    if (!coeffs) return set_err(c, MRF_ERR_INVALID_ARG, "NULL coefficients");
+    if (patch_px < 1 || n_px < 1 || n_py < 1 || (long long)n_px * n_py > (1 << 24))
+        return set_err(c, MRF_ERR_INVALID_ARG, "need patch_px >= 1 and 1 <= n_px * n_py <= 2^24");
+    if (!std::isfinite(sigma_min) || !(sigma_min > 0)) return set_err(c, MRF_ERR_INVALID_ARG, "sigma_min must be > 0");
+    const long long np = (long long)n_px * n_py;
+    if (!finite_all(coeffs, (int)(6 * np))) return set_err(c, MRF_ERR_INVALID_ARG, "coefficients must be finite");
+    // the margin bound of mrf_create over every patch: 3 sigma stays below the grid diagonal, and
+    // the longest walk (ray_slots_max) covers the largest margin
+    const GridDesc& g = c->grid;
+    const double D = g.res * std::sqrt((double)g.nx * g.nx + (double)g.ny * g.ny + (double)g.nz * g.nz);
+    double m_max = c->noise.margin_min;
+    for (long long p = 0; p < np; ++p) {
+        const double* k = coeffs + 6 * p;
+        const double sig = std::fabs(k[3]) + std::fabs(k[4]) * D + std::fabs(k[5]) * D * D;
+        if (c->noise.margin_k * sig > D)
+            return set_err(c, MRF_ERR_INVALID_ARG, "traversal margin must stay below the grid diagonal (margin bound)");
+        m_max = std::max(m_max, c->noise.margin_k * sig);
+    }
+    const long long margin_cells = (long long)std::ceil(m_max / g.res) + 1;
+    c->ray_slots_max = std::max(c->ray_slots_max, (1 + (long long)g.nx + g.ny + g.nz + 3 * margin_cells + 7) & ~7LL);
+    std::vector<float4> f((size_t)(2 * np));
+    for (long long p = 0; p < np; ++p) {
+        const double* k = coeffs + 6 * p;
+        f[2 * p] = make_float4((float)k[0], (float)k[1], (float)k[2], 0.f);
+        f[2 * p + 1] = make_float4((float)k[3], (float)k[4], (float)k[5], (float)sigma_min);
+    }
+    CK(c->pcoef_d.ensure((size_t)(6 * np), 0, c->stream));
+    CK(c->pcoef_f.ensure((size_t)(2 * np), 0, c->stream));
+    CK(cudaMemcpyAsync(c->pcoef_d.p, coeffs, sizeof(double) * 6 * np, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->pcoef_f.p, f.data(), sizeof(float4) * 2 * np, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    c->noise.pcoef = c->pcoef_d.p;
+    c->noise.ppx = patch_px;
+    c->noise.pnx = n_px;
+    c->mp.pcoef = c->pcoef_f.p;
+    c->patch_px = patch_px;
+    c->patch_nx = n_px;
+    c->patch_ny = n_py;
     c->dirty = true;
     return MRF_OK;
 }
