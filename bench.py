@@ -157,11 +157,20 @@ def cpu_baseline(w, config, messages):
                                         f"{w.n_iter} BP iterations, fp64, 1 thread"}}
 
 
+def _workload(args):
+    import synth
+    w = synth.make_workload(args.config)
+    if args.noise == "patch":  # the learnt per-patch sensor model (R25) over the config's frames
+        H, W = w.frames[0].depth.shape
+        w.patch = synth.patch_noise_model(W, H, w.seed, 20, w.sigma_c)
+    return w
+
+
 def run_reference(args, rank, world):
     import synth
     if rank != 0:
         return
-    w = synth.make_workload(args.config)
+    w = _workload(args)
     for _ in range(args.warmup):
         _oracle_sample(w, 1, args.messages)
     tot_u = tot_t = 0.0
@@ -193,7 +202,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    w = synth.make_workload(args.config)
+    w = _workload(args)
     n_iter = w.n_iter if args.iters is None else args.iters
 
     kw = {}
@@ -331,7 +340,8 @@ def run_ours(args, rank, world, local_rank):
         try:
             d = json.load(open(prof_json))
             for name, k in d.get("kernels", {}).items():
-                if k.get("config") == args.config and k.get("E") == E_local and args.messages == "per-ray":
+                if (k.get("config") == args.config and k.get("E") == E_local and args.messages == "per-ray"
+                        and args.noise == "lut"):
                     traffic_of[name] = k.get("dram_bytes_per_launch")
         except Exception:
             pass
@@ -351,6 +361,7 @@ def run_ours(args, rank, world, local_rank):
             "data": "synthetic",
             "config": {"workload": args.config, "frames": len(w.frames), "bp_iterations": n_iter,
                        "messages": args.messages, "bricks": args.bricks, "matrix_free": args.matrix_free,
+                       "noise": args.noise,
                        "incidences": E_all, "rays": R_all, "voxels": V, "grid": list(w.dims), "res_m": w.res,
                        "parallelism": (f"rays sharded by pixel row over {world} GPU(s)" if world > 1 else
                                        f"1 GPU, {emulate} emulated ranks (device-side int64 reduce)" if emulate > 1
@@ -394,6 +405,8 @@ def main():
                     help="sparse-brick map with B^3 bricks (P:203-205; 0 = dense, the north_star graph)")
     ap.add_argument("--messages", default="per-ray", choices=["per-ray", "keyframe-avg"],
                     help="message model: exact per-ray messages (north_star) or per-keyframe averages (P:200)")
+    ap.add_argument("--noise", default="lut", choices=["lut", "patch"],
+                    help="sensor model: the global table (north_star) or learnt per-patch polynomials (P:207-230)")
     ap.add_argument("--emulate-ranks", type=int, default=None,
                     help="ranks emulated on the one GPU (default: 4 for the 0.02 m configs, else 1)")
     ap.add_argument("--dry-run", action="store_true",
