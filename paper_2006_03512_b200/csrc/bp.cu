@@ -866,7 +866,14 @@ constexpr int kK6Warps = kK6Threads / 32;
 #define MRF_K6_W 16
 #endif
 constexpr int kK6W = MRF_K6_W;  // lanes per run in the add loop
-constexpr int kK6Desc = kK6Warps * 32 * 16;  // per warp: the batch's 32 run descriptors
+// MRF_K6_STRIDES = 1: each run's step signs are turned into strides once, when its batch is staged
+// (slot of element k = s0 + dz k + (dx - dz) cx + (dy - dz) cy, three IMADs per element), and the
+// shared-memory adds are predicated instructions (no divergent block around them); 0: the round-1
+// per-element decode of the sign bits.
+#ifndef MRF_K6_STRIDES
+#define MRF_K6_STRIDES 1
+#endif
+constexpr int kK6Desc = kK6Warps * 32 * (MRF_K6_STRIDES ? 32 : 16);  // per warp: the batch's 32 run descriptors
 
 // slot -> accumulator index.  MRF_K6_SWIZZLE=1 XORs the low 5 bits with y ^ z so that y and z
 // steps (slot strides 32, 1024) change the bank (a bijection inside every 32-slot row); off by
@@ -879,6 +886,7 @@ constexpr int kK6Desc = kK6Warps * 32 * 16;  // per warp: the batch's 32 run des
 #define MRF_K6_SWIZZLE 0
 #endif
 __device__ __forceinline__ int swz(int s) { return MRF_K6_SWIZZLE ? s ^ (((s >> 5) ^ (s >> 10)) & 31) : s; }
+static_assert(!(MRF_K6_STRIDES && MRF_K6_SWIZZLE), "the stride decode needs a linear slot layout");
 // Accumulator layout of a tile's slots.  Plain (PAD = false): index = slot = x + 32 y + 1024 z, so
 // y and z steps stay in one shared-memory bank.  Padded: index = x + 35 y + 1127 z -- the bank
 // moves by 1, 3 and 7 for x, y and z steps (odd: a straight run never repeats a bank within 32
@@ -936,6 +944,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     unsigned* accm = reinterpret_cast<unsigned*>(smem + L::kSlots);  // MODE 2: min |q|
     float* accs = reinterpret_cast<float*>(smem + 2 * L::kSlots);     // MODE 3: the bucket's scales
     uint4* sdesc = reinterpret_cast<uint4*>(smem + kAccInts) + (threadIdx.x >> 5) * 32;  // this warp's batch
+    int4* sab = reinterpret_cast<int4*>(smem + kAccInts) + kK6Warps * 32 + (threadIdx.x >> 5) * 32;  // its strides
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     // items: the first per CTA by index, then dynamically (a CTA whose items ran short takes the
     // next one instead of a fixed stride, so the uneven last chunks of the tiles do not leave SMs
@@ -978,8 +987,22 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             uint4 d{0u, 0u, 0u, 0u};
             if (lane < nb) d = __ldg(reinterpret_cast<const uint4*>(runs + rb + lane));
             MRF_ASSERT(lane >= nb || (long long)d.x + ((d.y >> 14) & 63u) + 1 <= chk_lam);
+#if MRF_K6_STRIDES
+            {
+                // staged: {e, s0 | n << 16, mx, my} and {dx - dz, dy - dz, dz}, s0 the accumulator
+                // index of the first element (an empty slot of the batch: n = 0)
+                const unsigned meta = d.y;
+                const int n = lane < nb ? (int)((meta >> 14) & 63u) + 1 : 0;
+                const int s0 = L::index((int)(meta & (kTileSlots - 1)));
+                const int dx = (meta >> 20) & 1u ? -1 : 1, dy = (meta >> 21) & 1u ? -L::SY : L::SY,
+                          dz = (meta >> 22) & 1u ? -L::SZ : L::SZ;
+                d.y = (unsigned)s0 | ((unsigned)n << 16);
+                sab[lane] = int4{dx - dz, dy - dz, dz, 0};
+            }
+#else
             if constexpr (PAD)  // in-tile slot -> accumulator index, once per run
                 d.y = (unsigned)L::index((int)(d.y & (kTileSlots - 1))) | ((d.y >> 14) << L::NS);
+#endif
             sdesc[lane] = d;
             __syncwarp();
             // Lane groups of kK6W lanes (32 / kK6W runs per instruction): in round r, group g takes
@@ -992,13 +1015,45 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
                 const uint4 x = sdesc[j + NJ * hw];
+#if MRF_K6_STRIDES
+                const int n = (int)(x.y >> 16);
+#else
                 const int n = j + NJ * hw < nb ? (int)((x.y >> L::NS) & 63u) + 1 : 0;
+#endif
 #pragma unroll
                 for (int rnd = 0; rnd < NR; ++rnd) {
                     const int k = hl + kK6W * rnd;
                     q[rnd][j] = k < n ? __ldg(lam + x.x + k) : 0;
                 }
             }
+#if MRF_K6_STRIDES
+            if constexpr (MODE == 0) {
+                const unsigned acc_sh = (unsigned)__cvta_generic_to_shared(acc_lo);
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    const uint4 x = sdesc[j + NJ * hw];
+                    const int4 st = sab[j + NJ * hw];
+                    const int n = (int)(x.y >> 16);
+                    const int base = (int)(x.y & 0xffffu) + st.z * hl;
+#pragma unroll
+                    for (int rnd = 0; rnd < NR; ++rnd) {
+                        const int k = hl + kK6W * rnd;
+                        if (rnd > 0 && !__any_sync(kFull, k < n)) break;  // every run of the column ended
+                        const unsigned below_k = (1u << k) - 1u;
+                        const int si = base + st.z * (kK6W * rnd) + st.x * __popc(x.z & below_k) +
+                                       st.y * __popc(x.w & below_k);
+                        MRF_ASSERT(k >= n || (si >= 0 && si < L::kSlots));
+                        const int qv = q[rnd][j];
+                        const unsigned a = acc_sh + 4u * (unsigned)si;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.lt.s32 p, %2, %3;\n"
+                            "@p red.shared.add.u32 [%0], %1;\n@p red.shared.add.u32 [%0+%5], %4;\n}"
+                            :: "r"(a), "r"(qv & 0xffff), "r"(k), "r"(n), "r"(qv >> 16), "n"(4 * L::kSlots));
+                    }
+                }
+            } else
+#endif
+            {
 #pragma unroll
             for (int rnd = 0; rnd < NR; ++rnd) {
                 const int k = hl + kK6W * rnd;
@@ -1007,14 +1062,23 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                 for (int j = 0; j < NJ; ++j) {
                     const uint4 x = sdesc[j + NJ * hw];
                     const unsigned meta = x.y;
+#if MRF_K6_STRIDES
+                    const int n = (int)(meta >> 16);
+#else
                     const int n = j + NJ * hw < nb ? (int)((meta >> L::NS) & 63u) + 1 : 0;
+#endif
                     if (rnd > 0 && !__any_sync(kFull, k < n)) continue;  // every run of the column ended
                     if (k < n) {
                         const int cx = __popc(x.z & below_k), cy = __popc(x.w & below_k);
+#if MRF_K6_STRIDES
+                        const int4 st = sab[j + NJ * hw];
+                        const int si0 = (int)(meta & 0xffffu) + st.z * k + st.x * cx + st.y * cy;
+#else
                         const int sx = (meta >> (L::NS + 6)) & 1 ? -cx : cx, sy = (meta >> (L::NS + 7)) & 1 ? -cy : cy;
                         const int cz = k - cx - cy, sz = (meta >> (L::NS + 8)) & 1 ? -cz : cz;
-                        const int s0 = (int)(meta & ((1u << L::NS) - 1u)) + sx + L::SY * sy + L::SZ * sz;
-                        const int si = PAD ? s0 : swz(s0);
+                        const int si0 = (int)(meta & ((1u << L::NS) - 1u)) + sx + L::SY * sy + L::SZ * sz;
+#endif
+                        const int si = (PAD || MRF_K6_STRIDES) ? si0 : swz(si0);
                         MRF_ASSERT(si >= 0 && si < L::kSlots);
                         const int qv = q[rnd][j];
                         if constexpr (MODE == 0) {
@@ -1037,6 +1101,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                         }
                     }
                 }
+            }
             }
             __syncwarp();
 #if MRF_K6_WARP_DYN
