@@ -273,14 +273,10 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, int e_
         o[k] = k < nvalid ? so[k] : (short)0;
     }
 #if MRF_FILL_LNU
-    if (mp.pcoef) {  // per-patch noise (R25): iz = the ray's patch, wz = its range
-        float l[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) l[k] = k < nvalid ? patch_lnu(mp, iz, wz, o[k]) : 0.f;
-        float4* dl = reinterpret_cast<float4*>(lnu + e_chunk);
-        dl[0] = make_float4(l[0], l[1], l[2], l[3]);
-        dl[1] = make_float4(l[4], l[5], l[6], l[7]);
-    } else {
+    // (per-patch noise, R25: lnu_fill_kernel overwrites these with the closed form after the walk,
+    // which reads the table's row 0 here -- any test of the mode in this function costs the walk
+    // registers and spills in every mode)
+    {
         LutFetch lf[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) lf[k] = lut_fetch(mp, iz, o[k]);
@@ -381,7 +377,7 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                                               (int)(sg.g1[2] - sg.g0[2])},
                                              sg.Z, sg.L};
             if (MRF_FILL_LNU) {  // the depth coordinate of the table (K1)
-                s_iz[threadIdx.x] = ray_z[f.ray_base + i].iz;
+                s_iz[threadIdx.x] = mp.pcoef ? 0 : ray_z[f.ray_base + i].iz;  // (R25: iz is the patch)
                 s_wz[threadIdx.x] = ray_z[f.ray_base + i].wz;
             }
         }
@@ -1016,7 +1012,7 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
         }
 #undef MRF_FILL_LAUNCH
     }
-    if (!MRF_FILL_LNU && n_rays > 0)
+    if ((!MRF_FILL_LNU || mp.pcoef) && n_rays > 0)
         lnu_fill_kernel<<<blocks_for(n_rays, 256), 256, 0, s>>>(r0, n_rays, mp, row_ptr, ray_z, off_q, lnu);
 }
 

@@ -537,7 +537,7 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
         if (sr != MRF_OK) return sr;
         run_sink_done(c, emitted, c->mf_frame_e[f1] - c->mf_frame_e[f0]);
     }
-    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + (!MRF_FILL_LNU && r1 > r0 ? 1 : 0) + (fused && r1 > r0 ? 1 : 0));
+    CK_LAUNCH(MRF_K_DDA_FILL, (cta0.back() > 0 ? 1 : 0) + ((!MRF_FILL_LNU || c->mp.pcoef) && r1 > r0 ? 1 : 0) + (fused && r1 > r0 ? 1 : 0));
     mf_dbg(c, count ? "walk(count)" : "walk");
     return MRF_OK;
 }
@@ -673,7 +673,7 @@ mrf_status sync_fill(mrf_ctx* c, bool need_counts = true) {
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
                             c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, nullptr, c->counters.p + kClassCtr,
                             c->lam.p, c->stream);
-            CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + (!MRF_FILL_LNU && c->R > c->R_filled ? 1 : 0));
+            CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + ((!MRF_FILL_LNU || c->mp.pcoef) && c->R > c->R_filled ? 1 : 0));
         }
         if (c->grid.bmask) {  // the depth images stay: a later keyframe may grow the allocation (R24)
             c->sp_frames.insert(c->sp_frames.end(), c->pend.begin(), c->pend.end());
