@@ -948,6 +948,28 @@ struct AccLayout {
 constexpr float kKfFix = 1073741824.0f;  // 2^30
 constexpr double kKfFixInv = 1.0 / 1073741824.0;
 
+// the keyframe-average passes' per-element adds (MODE 2: counts and min |q|; MODE 3: the small
+// probability relative to the slot's scale, fixed point 2^-30 in 16-bit halves)
+template <int MODE>
+__device__ __forceinline__ void kf_accumulate(int si, int qv, int* acc_lo, int* acc_hi, int* accn, unsigned* accm,
+                                              const float* accs) {
+    if constexpr (MODE == 2) {
+        atomicAdd(accn + si, qv >= 0 ? 1 : 65536);
+        atomicMin(accm + si, qv >= 0 ? (unsigned)qv : 0u - (unsigned)qv);
+    } else if constexpr (MODE == 3) {
+        // s(|lambda|) / s(a) in fixed point (a = -1: mixed signs, absolute s)
+        const float a = accs[si];
+        const float al = (float)(qv >= 0 ? (unsigned)qv : 0u - (unsigned)qv) * (kQInv * kLog2e);
+        const float ap = fmaxf(a, 0.f) * kLog2e;
+        const float c = a < 0.f ? 1.f : 1.f + ex2(-ap);
+        const float term = ex2(ap - al) * c * __frcp_rn(1.f + ex2(-al));
+        int v = __float2int_rn(term * kKfFix);
+        if (a < 0.f && qv < 0) v = -v;
+        atomicAdd(acc_lo + si, v & 0xffff);
+        atomicAdd(acc_hi + si, v >> 16);
+    }
+}
+
 template <int MODE, bool PAD>
 __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_items, const int2* __restrict__ items,
                                                                    const long long* __restrict__ tile_ptr,
@@ -958,7 +980,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                                                                    long long chk_out_tiles, int n_tiles) {
     extern __shared__ int smem[];
     using L = AccLayout<PAD>;
-    static_assert(MODE == 0 || !PAD, "keyframe-average sums use the plain layout (shared memory)");
+    static_assert(MODE != 3 || !PAD, "the keyframe-average sums (12 B per slot) use the plain layout (shared memory)");
     constexpr int kAccInts = MODE == 3 ? 3 * L::kSlots : 2 * L::kSlots;
     int* acc_lo = smem;                 // MODE 0 / 3: sum of (v & 0xffff), at L::index(slot)
     int* acc_hi = smem + L::kSlots;     // MODE 0 / 3: sum of (v >> 16)
@@ -1049,7 +1071,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                 }
             }
 #if MRF_K6_STRIDES
-            if constexpr (MODE == 0) {
+            {
                 const unsigned acc_sh = (unsigned)__cvta_generic_to_shared(acc_lo);
 #pragma unroll
                 for (int j = 0; j < NJ; ++j) {
@@ -1066,14 +1088,19 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
                                        st.y * __popc(x.w & below_k);
                         MRF_ASSERT(k >= n || (si >= 0 && si < L::kSlots));
                         const int qv = q[rnd][j];
-                        const unsigned a = acc_sh + 4u * (unsigned)si;
-                        asm volatile(
-                            "{\n.reg .pred p;\nsetp.lt.s32 p, %2, %3;\n"
-                            "@p red.shared.add.u32 [%0], %1;\n@p red.shared.add.u32 [%0+%5], %4;\n}"
-                            :: "r"(a), "r"(qv & 0xffff), "r"(k), "r"(n), "r"(qv >> 16), "n"(4 * L::kSlots));
+                        if constexpr (MODE == 0) {
+                            const unsigned a = acc_sh + 4u * (unsigned)si;
+                            asm volatile(
+                                "{\n.reg .pred p;\nsetp.lt.s32 p, %2, %3;\n"
+                                "@p red.shared.add.u32 [%0], %1;\n@p red.shared.add.u32 [%0+%5], %4;\n}"
+                                :: "r"(a), "r"(qv & 0xffff), "r"(k), "r"(n), "r"(qv >> 16), "n"(4 * L::kSlots));
+                        } else if (k < n) {
+                            kf_accumulate<MODE>(si, qv, acc_lo, acc_hi, accn, accm, accs);
+                        }
                     }
                 }
-            } else
+            }
+            if constexpr (false)
 #endif
             {
 #pragma unroll
@@ -1152,10 +1179,11 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
             unsigned long long* Nt = static_cast<unsigned long long*>(out) + o;
             unsigned* Mt = reinterpret_cast<unsigned*>(static_cast<unsigned long long*>(out) + 2 * n_out) + o;
             for (int i = threadIdx.x; i < kTileSlots; i += kK6Threads) {
-                const unsigned cn = (unsigned)accn[swz(i)];
-                const unsigned mq = accm[swz(i)];
-                accn[swz(i)] = 0;
-                accm[swz(i)] = 0xffffffffu;
+                const int a = L::index(i);
+                const unsigned cn = (unsigned)accn[a];
+                const unsigned mq = accm[a];
+                accn[a] = 0;
+                accm[a] = 0xffffffffu;
                 if (cn) {
                     atomicAdd(Nt + i, (unsigned long long)(cn & 0xffffu) | ((unsigned long long)(cn >> 16) << 32));
                     atomicMin(Mt + i, mq);
@@ -1378,8 +1406,8 @@ void launch_kf_sums(int pass, long long n_items, const int2* items, const long l
                     long long chk_lam, cudaStream_t s) {
     if (n_items == 0) return;
     if (pass == 0)
-        launch_tile_reduce_t<2, false>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots, next, nullptr,
-                                       chk_lam, n_slots >> kTileShift, 1 << 30, s);
+        launch_tile_reduce_t<2, (bool)MRF_K6_STRIDES>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots,
+                                                      next, nullptr, chk_lam, n_slots >> kTileShift, 1 << 30, s);
     else
         launch_tile_reduce_t<3, false>(n_items, items, bucket_ptr, runs, lam, per_item, sums, n_slots, next, nullptr,
                                        chk_lam, n_slots >> kTileShift, 1 << 30, s);
