@@ -779,9 +779,15 @@ __global__ void __launch_bounds__(256) lambda_merge_kernel(long long n_rays, con
 // from the voxel slots of its first walk.  Thread per ray.
 __global__ void __launch_bounds__(256) ck_extract_kernel(long long n, const long long* __restrict__ row_ptr,
                                                          const RayInfo* __restrict__ info,
-                                                         const int32_t* __restrict__ vid, int32_t* ck) {
+                                                         const int32_t* __restrict__ vid, int32_t* ck, RaySeg* seg) {
     const long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= n) return;
+    // the segment's per-axis reciprocals RN(1 / |dg|), as Walker::start computes them (written
+    // here rather than by the fill, whose walk is register-bound)
+    RaySeg& sr = seg[r];
+    sr.y[0] = __drcp_rn((double)(sr.dg[0] ? (unsigned)abs(sr.dg[0]) : 1u));
+    sr.y[1] = __drcp_rn((double)(sr.dg[1] ? (unsigned)abs(sr.dg[1]) : 1u));
+    sr.y[2] = __drcp_rn((double)(sr.dg[2] ? (unsigned)abs(sr.dg[2]) : 1u));
     const int nr = info[r].n;
     if (nr <= 0) return;
     const int cls = ray_class(nr);
@@ -1117,9 +1123,10 @@ void launch_lambda_merge(long long n_rays, const long long* rp_old, const RayInf
 }
 
 void launch_ck_extract(long long n, const long long* row_ptr, const RayInfo* info, const int32_t* vid, int32_t* ck,
+                       RaySeg* seg,
                        cudaStream_t s) {
     if (n == 0) return;
-    ck_extract_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, row_ptr, info, vid, ck);
+    ck_extract_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, row_ptr, info, vid, ck, seg);
 }
 
 }  // namespace mrf

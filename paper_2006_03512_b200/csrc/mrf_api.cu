@@ -529,7 +529,7 @@ mrf_status mf_walk(mrf_ctx* c, const mrf_ctx::MfChunk& ch, int f0, int f1, bool 
                     count ? c->tile_runs.p : nullptr, c->counters.p + (count ? 10 : 12), sink,
                     fused ? c->ray_seg.p : nullptr, count ? c->counters.p + kClassCtr : nullptr, nullptr, st);
     if (fused) {  // K12: the first cell of every K5 chunk of these rays
-        launch_ck_extract(r1 - r0, c->row_ptr.p + r0, c->ray_z.p + r0, sv - ch.e0, c->ck.p, st);
+        launch_ck_extract(r1 - r0, c->row_ptr.p + r0, c->ray_z.p + r0, sv - ch.e0, c->ck.p, c->ray_seg.p + r0, st);
     }
     if (count) {  // the sink's count is read back per chunk walk (few chunks; first use only)
         long long emitted = 0;

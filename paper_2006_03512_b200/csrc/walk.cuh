@@ -25,6 +25,7 @@ struct RaySeg {
     int g0[3];
     int dg[3];
     double Z, L;
+    double y[3];  // RN(1 / |dg_k|) (1 for dg_k = 0): Walker::start's reciprocals, so a re-walk skips them
 };
 
 struct Walker {
@@ -91,9 +92,9 @@ struct Walker {
         axis_at(sg.g0[0], sg.dg[0], x, s0, n0, d0);
         axis_at(sg.g0[1], sg.dg[1], y, s1, n1, d1);
         axis_at(sg.g0[2], sg.dg[2], z, s2, n2, d2);
-        y0 = __drcp_rn((double)(d0 ? d0 : 1u));
-        y1 = __drcp_rn((double)(d1 ? d1 : 1u));
-        y2 = __drcp_rn((double)(d2 ? d2 : 1u));
+        y0 = sg.y[0];
+        y1 = sg.y[1];
+        y2 = sg.y[2];
         // the entry crossing: the largest (n_k - 2^16) / d_k over the axes that crossed
         int a = -1;
         unsigned pa = 0, da = 1;
@@ -225,6 +226,7 @@ void launch_ray_messages_walk(int cls, long long n_rays, const int32_t* rays, co
                               int math, cudaStream_t s);
 // the checkpoints of rays [r0, r0 + n) from the voxel slots of a walk (graph.cu)
 void launch_ck_extract(long long n, const long long* row_ptr, const RayInfo* info, const int32_t* vid, int32_t* ck,
+                       RaySeg* seg,
                        cudaStream_t s);
 
 }  // namespace mrf
