@@ -151,7 +151,12 @@ __device__ __forceinline__ float selp(bool p, float a, float b) {
     asm("{\n.reg .pred q;\nsetp.ne.u32 q, %3, 0;\nselp.f32 %0, %1, %2, q;\n}" : "=f"(r) : "f"(a), "f"(b), "r"((unsigned)p));
     return r;
 }
-template <int M>
+// MASK_ALL = false (the class kernels, whose lane scans carry only b parts): only w is masked.
+// An element past the ray's end then keeps its la and l, which are harmless there: it lies after
+// every element of the ray, so its la only scales suffix values that are log 0 (R beyond the ray),
+// enters its own lane's a part (unused without carries) and the prefix maps of lanes past the ray,
+// and its l only its own (discarded) output -- while w = log 0 keeps it out of every sum.
+template <int M, bool MASK_ALL = true>
 __device__ __forceinline__ void elem_terms(long long t, int q, float lnu, float L0, bool ok, float& la, float& w,
                                            float& l) {
 #if MRF_K5_I2F_SPLIT
@@ -166,9 +171,14 @@ __device__ __forceinline__ void elem_terms(long long t, int q, float lnu, float 
     const float y = expn(-fabsf(c));
     const float L1 = M >= 2 ? log1pf_abs(y) : log1pn(y);  // ln(1 + e^-|c|)
     // lnu arrives in working units (the fill stores log nu * kLnuScale, internal.cuh)
-    la = selp(ok, -(fmaxf(c, 0.f) + L1), 0.f);
+    if constexpr (MASK_ALL) {
+        la = selp(ok, -(fmaxf(c, 0.f) + L1), 0.f);
+        l = selp(ok, lnu, kNeg);
+    } else {
+        la = -(fmaxf(c, 0.f) + L1);
+        l = lnu;
+    }
     w = selp(ok, lnu - (fmaxf(-c, 0.f) + L1), kNeg);
-    l = selp(ok, lnu, kNeg);
 }
 
 // Chunk composite of the suffix maps R -> e^{la} R + e^{w} (first applied last):
@@ -388,6 +398,9 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
 #ifndef MRF_K5_WALK_MIN_BLOCKS
 #define MRF_K5_WALK_MIN_BLOCKS 5
 #endif
+#ifndef MRF_K5_MASK_ALL
+#define MRF_K5_MASK_ALL 0
+#endif
 template <int G, int K, int M, bool AVG>
 __global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS : MRF_K5_MIN_BLOCKS_SMALL))) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
                                                          const long long* __restrict__ row_ptr,
@@ -436,7 +449,8 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS :
             t[j] = __ldg(T + v[j]);
         }
 #pragma unroll
-        for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
+        for (int j = 0; j < K; ++j)
+            elem_terms<M, MRF_K5_MASK_ALL>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
     }
     MRF_ASSERT(!AVG && nv > 0 ? (long long)s + nv <= mp.chk_lam : true);
     float aB, bB, Rin, Qin;
@@ -565,7 +579,8 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : MRF_K5_WALK_MIN_BLOCKS)) ray
             t[j] = __ldg(T + v[j]);
         }
 #pragma unroll
-        for (int j = 0; j < K; ++j) elem_terms<M>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
+        for (int j = 0; j < K; ++j)
+            elem_terms<M, MRF_K5_MASK_ALL>(t[j], q[j], __int_as_float(ln[j]), mp.L0, j < nv, la[j], w[j], l[j]);
     }
     MRF_ASSERT(!AVG && nv > 0 ? (long long)s + nv <= mp.chk_lam : true);
     float aB, bB, Rin, Qin;
