@@ -324,7 +324,11 @@ def run_ours(args, rank, world, local_rank):
     bytes_k5 = 14 * E_local + 8 * V
     bytes_k6 = 8 * E_local + 8 * V
     dbytes_k5 = 16 * E_local + 8 * V             # this design
-    dbytes_k6 = 4 * E_local + 16 * n_runs + 8 * V
+    # K6 path: the pixel-block hash reduction (K6b, default for per-ray messages over a stored
+    # graph: vid + lambda of every slot of the rows, padding included) or the tile-run K6
+    k6_path = ("block" if os.environ.get("MRF_K6", "block") == "block" and args.messages == "per-ray"
+               and not args.matrix_free else "tile")
+    dbytes_k6 = (8 * lay["n_slots"] + 8 * V) if k6_path == "block" else (4 * E_local + 16 * n_runs + 8 * V)
     gbs = lambda b, t: b / (t / 1e3) / 1e9 if t > 0 else 0.0
     ach_k5, ach_k6 = gbs(bytes_k5, per_iter_k5), gbs(bytes_k6, per_iter_k6)
     ach_bp = gbs(bytes_k5 + bytes_k6, per_iter_k5 + per_iter_k6)
@@ -375,8 +379,11 @@ def run_ours(args, rank, world, local_rank):
                          "algorithmic_bytes_per_launch": bytes_k5 if dominant == "ray_messages" else bytes_k6,
                          "k5_frac": ach_k5 / peak, "k6_frac": ach_k6 / peak,
                          "bp_iteration_frac": ach_bp / peak,
-                         "design_bytes": {"model": "K5 16 B/incidence (log nu stored) + 8 B/voxel; "
-                                                   "K6 4 B/incidence + 16 B/tile run + 8 B/voxel",
+                         "k6_path": k6_path,
+                         "design_bytes": {"model": "K5 16 B/incidence (log nu stored) + 8 B/voxel; " +
+                                                   ("K6b 8 B/slot (vid + lambda, padding included) + 8 B/voxel"
+                                                    if k6_path == "block" else
+                                                    "K6 4 B/incidence + 16 B/tile run + 8 B/voxel"),
                                           "k5_frac": dach_k5 / peak, "k6_frac": dach_k6 / peak,
                                           "bp_iteration_frac": dach_bp / peak},
                          "ms_k5": per_iter_k5, "ms_k6": per_iter_k6, "tile_runs": n_runs, **dram},

@@ -20,8 +20,8 @@ if [[ $what == ncu || $what == all ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/launches.csv $C > gpurun_out/ncu_launch.log 2>&1
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-      -k regex:'ray_msg|tile_reduce' -o gpurun_out/traffic -f $C > gpurun_out/ncu_traffic.log 2>&1
+      -k regex:'ray_msg|tile_reduce|block_reduce' -o gpurun_out/traffic -f $C > gpurun_out/ncu_traffic.log 2>&1
   timeout 1200 ncu --set full --clock-control none --import-source on \
-      --kernel-name-base demangled -k regex:'ray_msg_kernel<\(int\)16, \(int\)6|tile_reduce' -s 2 -c 2 -o gpurun_out/prof -f $C > gpurun_out/ncu_full.log 2>&1
+      --kernel-name-base demangled -k regex:'ray_msg_kernel<\(int\)16, \(int\)6|tile_reduce|block_reduce' -s 2 -c 2 -o gpurun_out/prof -f $C > gpurun_out/ncu_full.log 2>&1
   tail -1 gpurun_out/ncu_full.log; du -sh gpurun_out
 fi

@@ -1225,6 +1225,194 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
     }
 }
 
+// ---------------------------------------------------------------- K6b: pixel-block reduction
+// The voxel sums T_v = sum of the messages of every incidence on v (Eq.6's belief), read
+// in the messages' own (ray-major) order instead of through a transpose.  A work item is a block
+// of neighbouring pixels of one frame (kBlkCols columns x kBlkRows owned rows): their rays fan out
+// through nearly the same voxels (frames30: 43.6 k incidences per 32 x 16 block fall on 400-900
+// distinct voxels, a factor of ~100), so a CTA sums the block's messages into a small shared hash
+// table keyed by the belief slot and then adds each entry to T with one int64 global atomic.
+// Per incidence the kernel reads vid and lambda once, coalesced and contiguous (SURVEY §8(d)'s
+// 8 B), and needs no tile runs, bucket pass or work list beyond the block list.
+//   * a warp takes the block's rows from a shared counter and streams each row's slots -- its 32
+//     rays' segments are contiguous -- with 16-byte loads, 4 slots per lane (the 4 adds of an
+//     element index k touch slots 4 apart: distinct voxels unless two rays meet by chance);
+//   * table: open addressing, multiplicative hash, linear probing, 16-bit halves of q in two int32
+//     arrays (a slot gets at most one message per ray, <= 512 per block: no overflow);
+//   * fast path: ONE probe, branch-free -- an element whose key sits at its home slot (almost all:
+//     each voxel recurs ~100 times per block) adds there at once; the others (a key's first
+//     occurrence, or a key displaced by probing) go to a per-warp queue that is drained 32 at a
+//     time by the full probe loop (claim by CAS), so the loop's divergence is paid by full warps
+//     of misses instead of by every warp holding one (a per-element probe loop ran 3-4 iterations
+//     per warp instruction: the longest of 32 lanes' probe sequences);
+//   * an element whose probe sequence exceeds max_probe (64; a table filled by an unusually
+//     scattered block) goes straight to T with a global atomic: exact either way;
+//   * integer sums: T is bit-identical to the tile-run K6 for any block shape or order.
+constexpr int kBlkThreads = 256;
+constexpr int kBlkWarps = kBlkThreads / 32;
+constexpr int kBlkTableLog = 11;  // 2048 entries
+constexpr int kBlkQueue = 64;     // per-warp ring of deferred (v, q)
+#ifndef MRF_BLK_CTAS
+#define MRF_BLK_CTAS 6
+#endif
+constexpr int kBlkMinCtas = MRF_BLK_CTAS;  // resident CTAs per SM (registers: 65536 / (256 x 6) = 42)
+template <int S_LOG>
+__global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(long long n_blocks, const int4* __restrict__ blocks,
+                                                                     const long long* __restrict__ row_ptr,
+                                                                     const RayInfo* __restrict__ ray_z,
+                                                                     const int32_t* __restrict__ vid,
+                                                                     const int32_t* __restrict__ lam, long long* T,
+                                                                     unsigned* next, const int32_t* __restrict__ tile_map,
+                                                                     int max_probe, long long chk_lam, long long chk_out) {
+    constexpr int S = 1 << S_LOG;
+    __shared__ int key[S];
+    __shared__ int acc[2 * S];  // [0, S): sum of (q & 0xffff); [S, 2S): sum of (q >> 16)
+    __shared__ int2 queue[kBlkWarps][kBlkQueue];
+    __shared__ int s_row;
+    __shared__ long long s_blk;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int i = threadIdx.x; i < S; i += kBlkThreads) {
+        key[i] = -1;
+        acc[i] = 0;
+        acc[S + i] = 0;
+    }
+    if (threadIdx.x == 0) s_row = 0;
+    __syncthreads();
+    const unsigned acc_sh = (unsigned)__cvta_generic_to_shared(acc);
+    volatile int* vkey = key;
+    int2* wq = queue[wid];
+    int qh = 0, qt = 0;  // the warp's ring: entries [qh, qt) (warp-uniform)
+    auto to_T = [&](int v) -> long long {
+        return tile_map ? ((long long)__ldg(tile_map + (v >> kTileShift)) << kTileShift) | (v & (kTileSlots - 1))
+                        : (long long)v;
+    };
+    auto hash = [](int v) { return ((unsigned)v * 0x9E3779B1u) >> (32 - S_LOG); };
+    auto red2 = [&](unsigned h, int q) {
+        const unsigned a = acc_sh + 4u * h;
+        asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.add.u32 [%0+%3], %2;" ::"r"(a), "r"(q & 0xffff),
+                     "r"(q >> 16), "n"(4 * S));
+    };
+    // the full probe loop (queued elements): find or claim v's slot, else T directly
+    auto slow = [&](int v, int q) {
+        unsigned h = hash(v);
+        int p = max_probe < 0 ? max_probe : 0;  // (< 0: every element to T directly, a test knob)
+        for (; p >= 0; ++p) {
+            const int k = vkey[h];
+            if (k == v) break;
+            if (k < 0) {
+                const int old = atomicCAS(key + h, -1, v);
+                if (old < 0 || old == v) break;
+            }
+            h = (h + 1) & (S - 1);
+            if (p == max_probe) break;
+        }
+        if (p >= 0 && p < max_probe) {
+            red2(h, q);
+        } else {
+            const long long t = to_T(v);
+            MRF_ASSERT(t >= 0 && t < chk_out);
+            atomicAdd(reinterpret_cast<unsigned long long*>(T + t), (unsigned long long)(long long)q);
+        }
+    };
+    auto drain = [&](int cnt) {  // the first cnt queued entries, one per lane
+        __syncwarp();
+        if (lane < cnt) {
+            const int2 e = wq[(qh + lane) & (kBlkQueue - 1)];
+            slow(e.x, e.y);
+        }
+        qh += cnt;
+        __syncwarp();
+    };
+    // fast path for all 32 lanes (valid: this lane holds an element)
+    // fast path for one lane's 4 slots (q = 0: nothing to add -- padding, or a zero message):
+    // 4 independent probes of the home slots, the adds predicated on a hit, misses queued
+    const unsigned key_sh = (unsigned)__cvta_generic_to_shared(key);
+    const bool fast = max_probe >= 0;
+    auto add4 = [&](const int4& v4, const int4& q4) {
+        const int vv[4] = {v4.x, v4.y, v4.z, v4.w}, qq[4] = {q4.x, q4.y, q4.z, q4.w};
+        unsigned hh[4];
+        int kk[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            hh[k] = hash(vv[k]);
+            asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kk[k]) : "r"(key_sh + 4u * hh[k]));
+        }
+        bool miss[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool hit = fast && qq[k] != 0 && kk[k] == vv[k];
+            asm volatile(
+                "{\n.reg .pred p;\nsetp.ne.u32 p, %3, 0;\n"
+                "@p red.shared.add.u32 [%0], %1;\n@p red.shared.add.u32 [%0+%4], %2;\n}" ::"r"(acc_sh + 4u * hh[k]),
+                "r"(qq[k] & 0xffff), "r"(qq[k] >> 16), "r"((unsigned)hit), "n"(4 * S));
+            miss[k] = qq[k] != 0 && !hit;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const unsigned mm = __ballot_sync(kFull, miss[k]);
+            if (mm) {
+                if (miss[k]) wq[(qt + __popc(mm & lt)) & (kBlkQueue - 1)] = make_int2(vv[k], qq[k]);
+                qt += __popc(mm);
+                if (qt - qh >= 32) drain(32);
+            }
+        }
+    };
+    for (long long bi = blockIdx.x; bi < n_blocks;) {
+        const int4 b = __ldg(blocks + bi);  // {first ray, ncols | nrows << 16, row stride (rays), -}
+        const int ncols = b.y & 0xffff, nrows = b.y >> 16;
+        for (;;) {
+            int r = 0;
+            if (lane == 0) r = atomicAdd(&s_row, 1);
+            r = __shfl_sync(kFull, r, 0);
+            if (r >= nrows) break;
+            // the row's rays are contiguous slots [A, B) (their segments, 8-aligned, in pixel order);
+            // slots past a ray's end are padding with lambda = 0 (the fill writes it, K5 never
+            // writes a slot past n, import and re-layout fill it with 0), skipped like any zero
+            const long long ray = (long long)b.x + (long long)r * b.z;
+            const int A = (int)__ldg(row_ptr + ray), B = (int)__ldg(row_ptr + ray + ncols);
+            for (int e = A + 4 * lane; e - 4 * lane < B; e += 256) {  // (warp-uniform trip count)
+                int4 v0 = {0, 0, 0, 0}, q0 = {0, 0, 0, 0}, v1 = {0, 0, 0, 0}, q1 = {0, 0, 0, 0};
+                MRF_ASSERT(e >= B || e + 3 < chk_lam);
+                if (e < B) {
+                    v0 = __ldg(reinterpret_cast<const int4*>(vid + e));
+                    q0 = __ldg(reinterpret_cast<const int4*>(lam + e));
+                }
+                if (e + 128 < B) {
+                    v1 = __ldg(reinterpret_cast<const int4*>(vid + e + 128));
+                    q1 = __ldg(reinterpret_cast<const int4*>(lam + e + 128));
+                }
+                // (B is a multiple of 8 and e of 4: a lane's 4 slots lie all inside [A, B) or all past it)
+                add4(v0, q0);
+                if (e - 4 * lane + 128 < B) add4(v1, q1);  // (warp-uniform)
+            }
+        }
+        if (qt > qh) drain(qt - qh);
+        __syncthreads();
+        // flush: every claimed entry to T (one int64 atomic), and clear it for the next block
+        for (int i = threadIdx.x; i < S; i += kBlkThreads) {
+            const int v = key[i];
+            if (v >= 0) {
+                const long long sum = (long long)acc[S + i] * 65536 + (long long)acc[i];
+                key[i] = -1;
+                acc[i] = 0;
+                acc[S + i] = 0;
+                if (sum) {
+                    const long long t = to_T(v);
+                    MRF_ASSERT(t >= 0 && t < chk_out);
+                    atomicAdd(reinterpret_cast<unsigned long long*>(T + t), (unsigned long long)sum);
+                }
+            }
+        }
+        if (threadIdx.x == 0) {
+            s_row = 0;
+            s_blk = (long long)gridDim.x + atomicAdd(next, 1u);
+        }
+        __syncthreads();
+        bi = s_blk;
+    }
+}
+
 // ---------------------------------------------------------------- K8
 __global__ void marginals_kernel(GridDesc g, const long long* __restrict__ T, double L0, float* out) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1414,6 +1602,18 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
     else
         launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, chk_lam,
                                        chk_out_tiles, n_tiles, s);
+}
+
+void launch_block_reduce(long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,
+                         const int32_t* vid, const int32_t* lam, long long* T, unsigned* next, const int32_t* tile_map,
+                         int max_probe, long long chk_lam, long long chk_out, cudaStream_t s) {
+    if (n_blocks == 0) return;
+    DevCfg& dc = dev_cfg();
+    const long long cap = (long long)dc.sms * kBlkMinCtas;
+    const long long grid = n_blocks < cap ? n_blocks : cap;
+    cudaMemsetAsync(next, 0, sizeof(unsigned), s);
+    block_reduce_kernel<kBlkTableLog><<<(unsigned)grid, kBlkThreads, 0, s>>>(n_blocks, blocks, row_ptr, ray_z, vid, lam, T,
+                                                                              next, tile_map, max_probe, chk_lam, chk_out);
 }
 
 void launch_kf_sums(int pass, long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,

@@ -371,6 +371,14 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
                          const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, int math, cudaStream_t s);
+// K6b (default for per-ray messages with a stored graph): blocks = {first ray, ncols | nrows << 16,
+// row stride in rays, 0} of neighbouring pixels; max_probe: the hash table's probe limit (64; < 0:
+// every element straight to T, a test knob); T (or the compacted tiles through tile_map)
+// accumulates with int64 atomics (zero it first); next: a device counter (zeroed here).
+constexpr int kBlkCols = 32, kBlkRows = 16;
+void launch_block_reduce(long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,
+                         const int32_t* vid, const int32_t* lam, long long* T, unsigned* next, const int32_t* tile_map,
+                         int max_probe, long long chk_lam, long long chk_out, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 // tile_map (nullable): tile -> position among the tiles written (world > 1: the tiles some rank

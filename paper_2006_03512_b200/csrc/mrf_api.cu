@@ -84,6 +84,11 @@ struct mrf_ctx {
     long long VI = 0;  // internal belief slots: tiles * 16384 (tile-major, DESIGN.md §Data layout)
     long long NT = 0;  // tiles
     bool k6_voxel = false;  // ablation: per-voxel transpose K6 instead of the tile-run K6 (MRF_K6=voxel)
+    // K6b (default): the pixel-block hash reduction over the stored graph (no tile runs); MRF_K6=tile:
+    // the tile-run K6.  The modes without stored vid (matrix-free) or with per-(frame, slot) sums
+    // (keyframe averages) always use the tile runs.
+    bool k6_block = true;
+    int blk_max_probe = 64;  // (MRF_BLK_PROBE: < 0 sends every element to T directly, for tests)
     int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1)
     int k6_item = 8192;       // runs per K6 work item (set per graph unless MRF_K6_ITEM fixes it)
     bool k6_item_fixed = false;
@@ -139,6 +144,7 @@ struct mrf_ctx {
     // with MRF_K6_FRAMES=1 (K6 items then cover one frame's rays of a tile)
     bool frame_buckets = false;
     bool fb() const { return kf_avg || frame_buckets; }
+    bool use_block() const { return k6_block && !k6_voxel && !kf_avg && !mf && !frame_buckets; }
     long long n_bucket_groups() const { return fb() ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
@@ -204,6 +210,9 @@ struct mrf_ctx {
     double run_ratio = 0.125;        // (MRF_RUN_RATIO: the first estimate; tests force an overflow)
     long long run_slack = 65536;     // (MRF_RUN_SLACK)
     DBuf<int2> bitems;
+    DBuf<int4> blk;             // K6b pixel blocks (build_blocks)
+    std::vector<int4> h_blk;
+    long long n_blk = 0;
     std::vector<int2> h_items;  // host copy of the K6 work list
     long long n_runs = 0, n_bitems = 0;
     DBuf<long long> T, T_part;
@@ -470,6 +479,10 @@ mrf_status mf_rechunk(mrf_ctx* c) {
 // The sink of the next fill over new_slots incidence slots (capacity from run_ratio; see runs_ok).
 mrf_status run_sink(mrf_ctx* c, long long new_slots, RunSink& sink) {
     sink = RunSink{nullptr, nullptr, nullptr, 0};
+    if (c->use_block()) {  // K6b needs no tile runs (a later tile-run K6 would re-read vid)
+        c->runs_ok = false;
+        return MRF_OK;
+    }
     if (c->run_fill_forced || !c->runs_ok) return MRF_OK;
     const long long need = c->runs_emitted + (long long)std::ceil((double)new_slots * c->run_ratio) + c->run_slack;
     if (need > c->runs_cap) {
@@ -879,6 +892,34 @@ mrf_status build_active_tiles(mrf_ctx* c) {
     return MRF_OK;
 }
 
+// K6b: the pixel blocks of every frame (kBlkCols x kBlkRows owned rows), and the runs per tile
+// the fills counted (touched tiles for the compacted all-reduce; their sum is n_runs)
+mrf_status build_blocks(mrf_ctx* c) {
+    mrf_status st;
+    std::vector<int4>& bl = c->h_blk;  // (kept: the copy below is asynchronous)
+    bl.clear();
+    for (const FrameRec& f : c->frames)
+        for (int r0 = 0; r0 < f.rows_owned; r0 += kBlkRows)
+            for (int u0 = 0; u0 < f.W; u0 += kBlkCols)
+                bl.push_back(make_int4((int)(f.ray_base + (long long)r0 * f.W + u0),
+                                       std::min(kBlkCols, f.W - u0) | (std::min(kBlkRows, f.rows_owned - r0) << 16),
+                                       f.W, 0));
+    c->n_blk = (long long)bl.size();
+    CK(c->blk.ensure((size_t)std::max(1LL, c->n_blk), 0, c->stream));
+    if (c->n_blk)
+        CK(cudaMemcpyAsync(c->blk.p, bl.data(), sizeof(int4) * bl.size(), cudaMemcpyHostToDevice, c->stream));
+    const long long NT = c->NT;
+    std::vector<int32_t> nr((size_t)NT);
+    CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if ((st = fill_readback(c)) != MRF_OK) return st;  // (already here: no further wait)
+    c->n_runs = 0;
+    for (int32_t x : nr) c->n_runs += x;
+    c->tile_nr = nr;
+    c->n_bitems = 0;
+    return MRF_OK;
+}
+
 // Build the transpose used by K6, its work list and the K5 length classes (on graph change).
 mrf_status prepare(mrf_ctx* c) {
     if (!c->dirty) return MRF_OK;
@@ -887,6 +928,8 @@ mrf_status prepare(mrf_ctx* c) {
     c->vtr_valid = false;
     if (c->k6_voxel) {
         if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
+    } else if (c->use_block()) {
+        if ((st = build_blocks(c)) != MRF_OK) return st;
     } else {
         if ((st = build_tile_runs(c)) != MRF_OK) return st;
     }
@@ -1037,6 +1080,11 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
     if (c->k6_voxel) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
+    } else if (c->use_block()) {
+        launch_block_reduce(c->n_blk, c->blk.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lam.p, out,
+                            reinterpret_cast<unsigned*>(c->counters.p + 18), compact ? c->tile_map.p : nullptr,
+                            c->blk_max_probe, (long long)c->lam.cap, (compact ? c->n_act_tiles : c->NT) * kTileSlots, c->stream);
+        CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_blk > 0 ? 1 : 0);
     } else {
         launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
                            c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->k6_pad,
@@ -1377,7 +1425,11 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     c->NT = (long long)c->grid.ntx * c->grid.nty * c->grid.ntz;
     c->VI = c->NT * kTileSlots;
     c->ray_slots_max = (1 + (long long)dims[0] + dims[1] + dims[2] + 3 * margin_cells + 7) & ~7LL;
-    if (const char* k6 = getenv("MRF_K6")) c->k6_voxel = strcmp(k6, "voxel") == 0;
+    if (const char* k6 = getenv("MRF_K6")) {
+        c->k6_voxel = strcmp(k6, "voxel") == 0;
+        c->k6_block = strcmp(k6, "block") == 0;
+    }
+    if (const char* bp = getenv("MRF_BLK_PROBE")) c->blk_max_probe = atoi(bp);
     if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
     if (const char* ki = getenv("MRF_K6_ITEM")) {
         c->k6_item = std::min(std::max(atoi(ki), 1024), kRunsPerItem);

@@ -547,6 +547,41 @@ def test_runs_from_fill_match_run_fill(mode, monkeypatch):
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
 
 
+@pytest.mark.parametrize("mode", ["dense", "sparse", "compact", "fallback", "patch"])
+def test_block_k6_matches_tile_k6(mode, monkeypatch):
+    """K6b (the pixel-block hash reduction, default) against the tile-run K6 (MRF_K6=tile): beliefs
+    and messages bit-identical (exact integer sums in any order), with a warm start (a frame added
+    after iterating), in sparse-brick mode, through the compacted multi-GPU reduction (MRF_COMPACT),
+    with every element sent through the global fallback (MRF_BLK_PROBE=-1) and with the per-patch
+    sensor model."""
+    w = synth.frame1_patch() if mode == "patch" else (synth.single_frame() if mode != "sparse" else synth.tiny_frames(n_frames=4))
+    if mode == "compact":
+        monkeypatch.setenv("MRF_COMPACT", "1")
+    outs = []
+    for k6 in ("tile", "block"):
+        monkeypatch.setenv("MRF_K6", k6)
+        monkeypatch.setenv("MRF_BLK_PROBE", "-1" if mode == "fallback" else "64")
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        if mode == "sparse":
+            m.set_sparse_bricks(8)
+        with m:
+            fr0 = w.frames[0]
+            if mode in ("dense", "compact", "fallback", "patch"):
+                # the single frame twice (a second pose): a warm start appends a frame's rays
+                m.add_frame(fr0.depth, fr0.K, fr0.T_wc)
+                m.bp_iterate(2)
+                T2 = np.array(fr0.T_wc, np.float64).reshape(3, 4).copy()
+                T2[0, 3] += 0.07
+                m.add_frame(fr0.depth, fr0.K, T2.reshape(-1))
+            else:
+                for fr in w.frames:
+                    m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(2)
+            outs.append((m.export_beliefs(), m.export_messages()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
 def _single_cell_rays():
     """1 m voxels, camera at a cell centre looking +x, every depth 0.2 m (+ the 0.1 m margin): every
     ray ends inside the camera's cell -- rays of ONE incidence (N = 1: Eq.14's message has no
