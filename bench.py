@@ -326,8 +326,7 @@ def run_ours(args, rank, world, local_rank):
     dbytes_k5 = 16 * E_local + 8 * V             # this design
     # K6 path: the pixel-block hash reduction (K6b, default for per-ray messages over a stored
     # graph: vid + lambda of every slot of the rows, padding included) or the tile-run K6
-    k6_path = ("block" if os.environ.get("MRF_K6", "block") == "block" and args.messages == "per-ray"
-               and not args.matrix_free else "tile")
+    k6_path = m.k6_path()
     dbytes_k6 = (8 * lay["n_slots"] + 8 * V) if k6_path == "block" else (4 * E_local + 16 * n_runs + 8 * V)
     gbs = lambda b, t: b / (t / 1e3) / 1e9 if t > 0 else 0.0
     ach_k5, ach_k6 = gbs(bytes_k5, per_iter_k5), gbs(bytes_k6, per_iter_k6)

@@ -162,6 +162,13 @@ mrf_status mrf_evaluate(mrf_ctx* ctx, const float* depth, int32_t width, int32_t
  * transpose if the graph changed.  Any pointer may be NULL.  Synchronises. */
 mrf_status mrf_layout_sizes(mrf_ctx* ctx, int64_t* n_slots, int64_t* n_runs, int64_t* n_belief_slots);
 
+/* Which voxel aggregation (Eq.6's T_v = sum of the messages on v) the next iteration
+ * runs: *path = 1 for the pixel-block hash reduction over the messages in ray order
+ * (K6b), 0 for the reduction over the tile-run transpose (K6).  Builds the layout if the graph
+ * changed; a ctx whose blocks shared too few voxels in their first K6b reports 0 afterwards.
+ * path must not be NULL.  Synchronises. */
+mrf_status mrf_k6_path(mrf_ctx* ctx, int32_t* path);
+
 /* Copy this rank's graph to host buffers in canonical order: ray_pixel[n_rays] = frame*2^32 +
  * (v*W + u) of each kept ray, row_ptr[n_rays+1], vid[E], off_q[E] (metres * 32768).  Any pointer
  * may be NULL.  Synchronises. */

@@ -158,6 +158,12 @@ class MRFMap:
         self._chk(self._L.mrf_layout_sizes(self._h, *(ctypes.byref(x) for x in v)))
         return dict(n_slots=v[0].value, n_runs=v[1].value, n_belief_slots=v[2].value)
 
+    def k6_path(self) -> str:
+        """mrf_k6_path: "block" (K6b, the pixel-block hash reduction) or "tile" (tile runs)."""
+        v = ctypes.c_int32()
+        self._chk(self._L.mrf_k6_path(self._h, ctypes.byref(v)))
+        return "block" if v.value == 1 else "tile"
+
     def evaluate(self, depth, K, T_wc, k_sigma=1.5, vis_threshold=0.5, mode=0):
         """mrf_evaluate: §III.D generating-surface accuracy of one posed depth image against the
         current beliefs -> (cls[H, W] int8, n_valid, n_accurate) for this rank's rows.

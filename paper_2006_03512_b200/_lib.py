@@ -29,7 +29,7 @@ MRF_K_COUNT = len(KERNEL_NAMES)
 
 # every symbol include/mrf.h declares
 EXPORTS = ["mrf_create", "mrf_add_frame", "mrf_bp_iterate", "mrf_marginals", "mrf_destroy", "mrf_last_error",
-           "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_export_graph", "mrf_export_rays", "mrf_evaluate",
+           "mrf_set_stream", "mrf_reset", "mrf_reserve", "mrf_graph_sizes", "mrf_layout_sizes", "mrf_k6_path", "mrf_export_graph", "mrf_export_rays", "mrf_evaluate",
            "mrf_export_transpose", "mrf_export_messages", "mrf_import_messages", "mrf_export_beliefs",
            "mrf_bp_partial", "mrf_bp_finish", "mrf_belief_slots", "mrf_nccl_unique_id", "mrf_set_profiling",
            "mrf_profile_read", "mrf_launch_count", "mrf_set_message_mode", "mrf_export_keyframe_average", "mrf_set_sparse_bricks", "mrf_export_bricks", "mrf_set_matrix_free",
@@ -80,6 +80,7 @@ def load(build: bool = True):
                 "mrf_reserve": (st, [vp, i64, i64]),
                 "mrf_graph_sizes": (st, [vp, P(i64), P(i64), P(i64), P(i64), P(i64)]),
                 "mrf_layout_sizes": (st, [vp, P(i64), P(i64), P(i64)]),
+                "mrf_k6_path": (st, [vp, P(i32)]),
                 "mrf_export_rays": (st, [vp, i64, vp, vp, i64, vp, vp, vp, vp]),
                 "mrf_evaluate": (st, [vp, vp, i32, i32, P(f64), P(f64), i32, f64, f64, vp, P(i64), P(i64)]),
                 "mrf_set_message_mode": (st, [vp, i32]),

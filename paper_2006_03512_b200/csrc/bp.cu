@@ -1245,8 +1245,11 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
 //     time by the full probe loop (claim by CAS), so the loop's divergence is paid by full warps
 //     of misses instead of by every warp holding one (a per-element probe loop ran 3-4 iterations
 //     per warp instruction: the longest of 32 lanes' probe sequences);
-//   * an element whose probe sequence exceeds max_probe (64; a table filled by an unusually
-//     scattered block) goes straight to T with a global atomic: exact either way;
+//   * a block claims at most half the table (linear probing stays short); an element whose key
+//     finds no room, or whose probe sequence exceeds max_probe (64), goes straight to T with a
+//     global atomic: exact either way.  The claims and direct adds are counted (stats) so that
+//     the host can drop K6b where blocks share too little (interleaved rows of several ranks,
+//     fine grids: DESIGN §5 K6b);
 //   * integer sums: T is bit-identical to the tile-run K6 for any block shape or order.
 constexpr int kBlkThreads = 256;
 constexpr int kBlkWarps = kBlkThreads / 32;
@@ -1262,13 +1265,15 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
                                                                      const RayInfo* __restrict__ ray_z,
                                                                      const int32_t* __restrict__ vid,
                                                                      const int32_t* __restrict__ lam, long long* T,
-                                                                     unsigned* next, const int32_t* __restrict__ tile_map,
+                                                                     unsigned* next, unsigned long long* stats,
+                                                                     const int32_t* __restrict__ tile_map,
                                                                      int max_probe, long long chk_lam, long long chk_out) {
     constexpr int S = 1 << S_LOG;
     __shared__ int key[S];
     __shared__ int acc[2 * S];  // [0, S): sum of (q & 0xffff); [S, 2S): sum of (q >> 16)
     __shared__ int2 queue[kBlkWarps][kBlkQueue];
     __shared__ int s_row;
+    __shared__ int s_used, s_fall;  // this block's claimed entries, elements sent to T directly
     __shared__ long long s_blk;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned lt = (1u << lane) - 1u;
@@ -1277,8 +1282,13 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
         acc[i] = 0;
         acc[S + i] = 0;
     }
-    if (threadIdx.x == 0) s_row = 0;
+    if (threadIdx.x == 0) {
+        s_row = 0;
+        s_used = 0;
+        s_fall = 0;
+    }
     __syncthreads();
+    volatile int* vused = &s_used;
     const unsigned acc_sh = (unsigned)__cvta_generic_to_shared(acc);
     volatile int* vkey = key;
     int2* wq = queue[wid];
@@ -1300,9 +1310,17 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
         for (; p >= 0; ++p) {
             const int k = vkey[h];
             if (k == v) break;
-            if (k < 0) {
+            if (k < 0) {  // v is absent (no deletions): claim this slot, unless the table is half full
+                if (*vused >= S / 2) {
+                    p = max_probe;
+                    break;
+                }
                 const int old = atomicCAS(key + h, -1, v);
-                if (old < 0 || old == v) break;
+                if (old < 0) {
+                    atomicAdd(&s_used, 1);
+                    break;
+                }
+                if (old == v) break;
             }
             h = (h + 1) & (S - 1);
             if (p == max_probe) break;
@@ -1313,6 +1331,7 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
             const long long t = to_T(v);
             MRF_ASSERT(t >= 0 && t < chk_out);
             atomicAdd(reinterpret_cast<unsigned long long*>(T + t), (unsigned long long)(long long)q);
+            atomicAdd(&s_fall, 1);
         }
     };
     auto drain = [&](int cnt) {  // the first cnt queued entries, one per lane
@@ -1405,7 +1424,15 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
             }
         }
         if (threadIdx.x == 0) {
+            // stats[0]: claimed entries (distinct voxels per block, summed), stats[1]: elements
+            // sent to T directly -- the host's check that the blocks share voxels (mrf_api.cu)
+            if (stats) {
+                atomicAdd(stats, (unsigned long long)s_used);
+                if (s_fall) atomicAdd(stats + 1, (unsigned long long)s_fall);
+            }
             s_row = 0;
+            s_used = 0;
+            s_fall = 0;
             s_blk = (long long)gridDim.x + atomicAdd(next, 1u);
         }
         __syncthreads();
@@ -1605,15 +1632,16 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
 }
 
 void launch_block_reduce(long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,
-                         const int32_t* vid, const int32_t* lam, long long* T, unsigned* next, const int32_t* tile_map,
-                         int max_probe, long long chk_lam, long long chk_out, cudaStream_t s) {
+                         const int32_t* vid, const int32_t* lam, long long* T, unsigned* next,
+                         unsigned long long* stats, const int32_t* tile_map, int max_probe, long long chk_lam,
+                         long long chk_out, cudaStream_t s) {
     if (n_blocks == 0) return;
     DevCfg& dc = dev_cfg();
     const long long cap = (long long)dc.sms * kBlkMinCtas;
     const long long grid = n_blocks < cap ? n_blocks : cap;
     cudaMemsetAsync(next, 0, sizeof(unsigned), s);
     block_reduce_kernel<kBlkTableLog><<<(unsigned)grid, kBlkThreads, 0, s>>>(n_blocks, blocks, row_ptr, ray_z, vid, lam, T,
-                                                                              next, tile_map, max_probe, chk_lam, chk_out);
+                                                                              next, stats, tile_map, max_probe, chk_lam, chk_out);
 }
 
 void launch_kf_sums(int pass, long long n_items, const int2* items, const long long* bucket_ptr, const Run* runs,

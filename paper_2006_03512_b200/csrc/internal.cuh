@@ -373,12 +373,16 @@ void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const l
                          int n_warps_long, int math, cudaStream_t s);
 // K6b (default for per-ray messages with a stored graph): blocks = {first ray, ncols | nrows << 16,
 // row stride in rays, 0} of neighbouring pixels; max_probe: the hash table's probe limit (64; < 0:
-// every element straight to T, a test knob); T (or the compacted tiles through tile_map)
+// every element straight to T, a test knob); stats (nullable): += {distinct voxels summed over the
+// blocks, elements sent to T directly}; T (or the compacted tiles through tile_map)
 // accumulates with int64 atomics (zero it first); next: a device counter (zeroed here).
 constexpr int kBlkCols = 32, kBlkRows = 16;
+constexpr double kBlkMinPpv = 6.0;   // auto K6b: a voxel spans >= 6 pixels at 3 m (mrf_api.cu)
+constexpr long long kBlkMinShare = 16;  // ... and the blocks' incidences per distinct voxel >= 16
 void launch_block_reduce(long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,
-                         const int32_t* vid, const int32_t* lam, long long* T, unsigned* next, const int32_t* tile_map,
-                         int max_probe, long long chk_lam, long long chk_out, cudaStream_t s);
+                         const int32_t* vid, const int32_t* lam, long long* T, unsigned* next,
+                         unsigned long long* stats, const int32_t* tile_map, int max_probe, long long chk_lam,
+                         long long chk_out, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 // tile_map (nullable): tile -> position among the tiles written (world > 1: the tiles some rank

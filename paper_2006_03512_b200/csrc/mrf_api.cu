@@ -87,7 +87,19 @@ struct mrf_ctx {
     // K6b (default): the pixel-block hash reduction over the stored graph (no tile runs); MRF_K6=tile:
     // the tile-run K6.  The modes without stored vid (matrix-free) or with per-(frame, slot) sums
     // (keyframe averages) always use the tile runs.
+    // MRF_K6: unset = auto, "block" = always K6b, anything else = the tile runs.  Auto takes K6b
+    // when the blocks can share voxels: one rank (interleaved rows of world > 1 share few), and a
+    // voxel spanning >= kBlkMinPpv pixels at a nominal 3 m (min over the frames of f res / 3 m:
+    // frames30 8.75, the 0.02 m configs 3.5 -- measured: K6b loses to the tile runs at 2, 4, 8
+    // emulated ranks and on frames100, profiles/r02x_k6_paths.log).  The first K6b after a graph
+    // change also checks what the blocks shared (blk_check): too little, and this ctx demotes
+    // itself to the tile runs for good.
     bool k6_block = true;
+    int k6_force = 0;           // 1: K6b always, 2: tile runs always (MRF_K6)
+    bool k6_demoted = false;
+    bool blk_check = false;     // check the next K6b's stats (after build_blocks)
+    double ppv_min = 1e30;      // min over the frames of min(fx, fy) res / 3 m
+    long long blk_min_share = kBlkMinShare;  // (MRF_BLK_SHARE: a test forces the demotion)
     int blk_max_probe = 64;  // (MRF_BLK_PROBE: < 0 sends every element to T directly, for tests)
     int k5_math = 1;        // K5 math level (bp.cu; MRF_K5_MATH=0|1)
     int k6_item = 8192;       // runs per K6 work item (set per graph unless MRF_K6_ITEM fixes it)
@@ -144,7 +156,10 @@ struct mrf_ctx {
     // with MRF_K6_FRAMES=1 (K6 items then cover one frame's rays of a tile)
     bool frame_buckets = false;
     bool fb() const { return kf_avg || frame_buckets; }
-    bool use_block() const { return k6_block && !k6_voxel && !kf_avg && !mf && !frame_buckets; }
+    bool use_block() const {
+        const bool want = k6_force == 1 || (k6_force == 0 && world == 1 && ppv_min >= kBlkMinPpv && !k6_demoted);
+        return want && !k6_voxel && !kf_avg && !mf && !frame_buckets;
+    }
     long long n_bucket_groups() const { return fb() ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
@@ -917,6 +932,7 @@ mrf_status build_blocks(mrf_ctx* c) {
     for (int32_t x : nr) c->n_runs += x;
     c->tile_nr = nr;
     c->n_bitems = 0;
+    c->blk_check = !c->k6_demoted && c->E_real > 0;
     return MRF_OK;
 }
 
@@ -1081,10 +1097,23 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
         launch_voxel_reduce(c->n_items_total, c->items.p, c->col_ptr.p, c->tr.p, c->lam.p, out, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_items_total > 0 ? 1 : 0);
     } else if (c->use_block()) {
+        unsigned long long* stats = c->blk_check ? c->counters.p + 20 : nullptr;
+        if (stats) CK(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), c->stream));
         launch_block_reduce(c->n_blk, c->blk.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lam.p, out,
-                            reinterpret_cast<unsigned*>(c->counters.p + 18), compact ? c->tile_map.p : nullptr,
+                            reinterpret_cast<unsigned*>(c->counters.p + 18), stats, compact ? c->tile_map.p : nullptr,
                             c->blk_max_probe, (long long)c->lam.cap, (compact ? c->n_act_tiles : c->NT) * kTileSlots, c->stream);
         CK_LAUNCH(MRF_K_VOXEL_SUM, c->n_blk > 0 ? 1 : 0);
+        if (stats) {  // did the blocks share voxels?  (one round trip per graph change)
+            c->blk_check = false;
+            CK(cudaMemcpyAsync(c->pinned + 60, stats, 2 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            const long long distinct = c->pinned[60], direct = c->pinned[61];
+            if (c->k6_force == 0 && (distinct * c->blk_min_share > c->E_real || direct * 200 > c->E_real)) {
+                c->k6_demoted = true;  // the next K6 runs over tile runs (built from vid: runs_ok is false)
+                c->dirty = true;
+                return prepare(c);
+            }
+        }
     } else {
         launch_tile_reduce(c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, out,
                            c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 14) : nullptr, c->k6_pad,
@@ -1427,9 +1456,10 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     c->ray_slots_max = (1 + (long long)dims[0] + dims[1] + dims[2] + 3 * margin_cells + 7) & ~7LL;
     if (const char* k6 = getenv("MRF_K6")) {
         c->k6_voxel = strcmp(k6, "voxel") == 0;
-        c->k6_block = strcmp(k6, "block") == 0;
+        c->k6_force = strcmp(k6, "block") == 0 ? 1 : 2;
     }
     if (const char* bp = getenv("MRF_BLK_PROBE")) c->blk_max_probe = atoi(bp);
+    if (const char* bs = getenv("MRF_BLK_SHARE")) c->blk_min_share = atoll(bs);
     if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
     if (const char* ki = getenv("MRF_K6_ITEM")) {
         c->k6_item = std::min(std::max(atoi(ki), 1024), kRunsPerItem);
@@ -1758,6 +1788,7 @@ mrf_status mrf_add_frame(mrf_ctx* ctx, const float* depth, int32_t width, int32_
     if (Rf > 0) c->pend.push_back(f);
     if (frame_id_out) *frame_id_out = (int64_t)c->frames.size();
     c->frames.push_back({width, height, rows_owned, c->R, Rf});
+    c->ppv_min = std::min(c->ppv_min, std::min(K[0], K[1]) * c->grid.res / 3.0);
     c->R += Rf;
     if (fast) {
         c->E_unresolved = true;
@@ -1892,6 +1923,15 @@ mrf_status mrf_layout_sizes(mrf_ctx* ctx, int64_t* n_slots, int64_t* n_runs, int
     if (n_slots) *n_slots = c->E;
     if (n_runs) *n_runs = c->n_runs;
     if (n_belief_slots) *n_belief_slots = c->VI;
+    return MRF_OK;
+}
+
+mrf_status mrf_k6_path(mrf_ctx* ctx, int32_t* path) {
+    ENTER(ctx);
+    if (!path) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
+    mrf_status st;
+    if ((st = prepare(c)) != MRF_OK) return st;
+    *path = c->use_block() ? 1 : 0;
     return MRF_OK;
 }
 

@@ -88,6 +88,10 @@ class EmulatedRanks:
         return dict(n_slots=sum(x["n_slots"] for x in s), n_runs=sum(x["n_runs"] for x in s),
                     n_belief_slots=s[0]["n_belief_slots"])
 
+    def k6_path(self):
+        paths = {m.k6_path() for m in self.maps}
+        return paths.pop() if len(paths) == 1 else "mixed"
+
     def set_profiling(self, on=True):
         for m in self.maps:
             m.set_profiling(on)

@@ -166,6 +166,7 @@ def test_k6_accumulator_layouts_agree(frame1, monkeypatch):
     mrf_create) give identical beliefs: the sums are exact integers, the layout only moves the
     accumulator slots."""
     outs = []
+    monkeypatch.setenv("MRF_K6", "tile")
     for pad in ("1", "0"):
         monkeypatch.setenv("MRF_K6_PAD", pad)
         with _gpu_map(frame1) as m:
@@ -522,6 +523,7 @@ def test_runs_from_fill_match_run_fill(mode, monkeypatch):
     vid re-read (MRF_RUN_FILL=1): same run count, beliefs and messages bit-identical (exact integer
     sums; the order of runs inside a tile is free)."""
     w = synth.single_frame() if mode == "dense" else synth.tiny_frames(n_frames=4)
+    monkeypatch.setenv("MRF_K6", "tile")  # (the runs exist for the tile-run K6)
     outs = []
     for forced in ("0", "1"):
         monkeypatch.setenv("MRF_RUN_FILL", forced)
@@ -547,19 +549,24 @@ def test_runs_from_fill_match_run_fill(mode, monkeypatch):
     assert np.array_equal(outs[0][1], outs[1][1]) and np.array_equal(outs[0][2], outs[1][2])
 
 
-@pytest.mark.parametrize("mode", ["dense", "sparse", "compact", "fallback", "patch"])
+@pytest.mark.parametrize("mode", ["dense", "sparse", "compact", "fallback", "patch", "demote"])
 def test_block_k6_matches_tile_k6(mode, monkeypatch):
-    """K6b (the pixel-block hash reduction, default) against the tile-run K6 (MRF_K6=tile): beliefs
-    and messages bit-identical (exact integer sums in any order), with a warm start (a frame added
+    """K6b (the pixel-block hash reduction) against the tile-run K6 (MRF_K6=tile): beliefs and
+    messages bit-identical (exact integer sums in any order), with a warm start (a frame added
     after iterating), in sparse-brick mode, through the compacted multi-GPU reduction (MRF_COMPACT),
-    with every element sent through the global fallback (MRF_BLK_PROBE=-1) and with the per-patch
-    sensor model."""
+    with every element sent through the global fallback (MRF_BLK_PROBE=-1), with the per-patch
+    sensor model, and in auto mode when the first K6b demotes the ctx to the tile runs
+    (MRF_BLK_SHARE: a sharing threshold no block meets)."""
     w = synth.frame1_patch() if mode == "patch" else (synth.single_frame() if mode != "sparse" else synth.tiny_frames(n_frames=4))
     if mode == "compact":
         monkeypatch.setenv("MRF_COMPACT", "1")
     outs = []
     for k6 in ("tile", "block"):
-        monkeypatch.setenv("MRF_K6", k6)
+        if mode == "demote" and k6 == "block":
+            monkeypatch.delenv("MRF_K6", raising=False)  # auto: K6b for frame1 (a voxel spans 8.75 px at 3 m)
+            monkeypatch.setenv("MRF_BLK_SHARE", "1000000000")
+        else:
+            monkeypatch.setenv("MRF_K6", k6)
         monkeypatch.setenv("MRF_BLK_PROBE", "-1" if mode == "fallback" else "64")
         m = pkg.MRFMap.from_workload(w)
         m.set_stream(torch.cuda.current_stream().cuda_stream)
@@ -577,9 +584,30 @@ def test_block_k6_matches_tile_k6(mode, monkeypatch):
             else:
                 for fr in w.frames:
                     m.add_frame(fr.depth, fr.K, fr.T_wc)
+            if mode == "demote" and k6 == "block":
+                assert m.k6_path() == "block"
             m.bp_iterate(2)
+            assert m.k6_path() == ("tile" if mode in ("demote",) or k6 == "tile" else "block")
             outs.append((m.export_beliefs(), m.export_messages()))
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_k6_auto_path(monkeypatch):
+    """Auto K6 choice (DESIGN §5 K6b): the pixel blocks for one rank at 0.05 m with Kinect optics
+    (frame1: a voxel spans 8.75 px at 3 m), the tile runs for the tiny camera (1 px per voxel),
+    for ranks of a sharded map (interleaved rows) and for the matrix-free walks (no stored vid)."""
+    monkeypatch.delenv("MRF_K6", raising=False)
+    w1, wt = synth.single_frame(), synth.tiny()
+    for w, kw, expect in ((w1, {}, "block"), (wt, {}, "tile"), (w1, dict(rank=0, world=2, comm=pkg.MRF_COMM_EXTERNAL), "tile"),
+                          (w1, "mf", "tile")):
+        m = pkg.MRFMap.from_workload(w, **(kw if isinstance(kw, dict) else {}))
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        if kw == "mf":
+            m.set_matrix_free(1)
+        with m:
+            fr = w.frames[0]
+            m.add_frame(fr.depth, fr.K, fr.T_wc)
+            assert m.k6_path() == expect
 
 
 def _single_cell_rays():
@@ -667,6 +695,7 @@ def test_run_sink_overflow_falls_back(frame1, monkeypatch):
     transpose falls back to the vid re-read and the beliefs are the same; the next graph (after a
     reset) gets a sink sized from the observed runs per slot and uses it."""
     w = frame1
+    monkeypatch.setenv("MRF_K6", "tile")  # (the run sink feeds the tile-run K6)
     with _gpu_map(w) as m:
         m.bp_iterate(2)
         ref = (m.export_beliefs(), m.export_messages())
