@@ -312,7 +312,7 @@ __device__ __forceinline__ void flush_chunk(int32_t* vid, int16_t* off_q, int e_
 #endif
 // One launch fills every frame added since the last fill (frames[k] owns the CTAs
 // [cta0[k], cta0[k+1])): one wave-quantisation tail per batch instead of per frame.
-template <bool SPARSE, bool RUNS>
+template <bool SPARSE, bool RUNS, bool COUNT = true>
 __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS : MRF_FILL_MIN_BLOCKS) dda_fill_kernel(const FrameDesc* __restrict__ frames,
                                                        const int* __restrict__ cta0, int n_frames, GridDesc g,
                                                        NoiseDesc n, const float* __restrict__ depth_all,
@@ -407,12 +407,14 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
                 if ((e & 7) == 7)
                     flush_chunk(vid, off_q, e - 7, 8, sv, so, lnu, mp, s_iz[threadIdx.x], s_wz[threadIdx.x], lam0);
                 // K4b: runs per tile (a warp's concurrent run starts in one tile share an atomic);
-                // a run that ends here goes to the sink
+                // a run that ends here goes to the sink.  COUNT = false (the pixel-block K6b needs
+                // no transpose): no run state at all
                 b = vx >> kTileShift;
                 const int l = vx & (kTileSlots - 1);
                 const int ad = abs(l - run_prev);
-                start = !run_extends(b, l, run_tile, run_n, run_prev);
-                if (start) {
+                if (COUNT) start = !run_extends(b, l, run_tile, run_n, run_prev);
+                if (!COUNT) {
+                } else if (start) {
                     if (RUNS && run_tile >= 0) {  // the run that ends here waits in shared memory
                         s_done[threadIdx.x] = Run{s_run_e[threadIdx.x],
                                                   s_run_slot0[threadIdx.x] | ((unsigned)(run_n - 1) << 14) | run_neg,
@@ -446,8 +448,8 @@ __global__ void __launch_bounds__(kFillThreads, RUNS ? MRF_FILL_MIN_BLOCKS_RUNS 
             } else {  // empty skip: past the unallocated brick in one step (sparse bricks)
                 alive = w.skip_brick(g) && w.inside(g);
             }
-            const unsigned sm = __ballot_sync(am, start);
-            if (start && tile_runs) {  // (no counting on the matrix-free re-walks)
+            const unsigned sm = COUNT ? __ballot_sync(am, start) : 0u;
+            if (COUNT && start && tile_runs) {  // (no counting on the matrix-free re-walks)
                 const int key = bucket0 + b;  // (frame, tile) bucket; the tile itself in per-ray mode
                 const unsigned peers = __match_any_sync(sm, key);
                 if (lane == __ffs(peers) - 1) atomicAdd(&tile_runs[key], __popc(peers));
@@ -724,7 +726,7 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
             const bool ext = !at_end && nb.extend(b, l);
             const bool emit = rb.tile >= 0 && !ext;  // the current run ends before e
             const unsigned em = __ballot_sync(am, emit);
-            if (emit) {
+            if (emit) {  // (runs == nullptr: only count the runs per bucket, into cursor)
                 const int cur = bucket0 + rb.tile;
                 const unsigned peers = __match_any_sync(em, cur);
                 const int leader = __ffs(peers) - 1;
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(256) run_fill_kernel(long long n_rays, const l
                 if (lane == leader) base = atomicAdd(&cursor[cur], __popc(peers));
                 base = __shfl_sync(peers, base, leader);
                 const int rank = __popc(peers & ((1u << lane) - 1u));
-                runs[tile_ptr[cur] + base + rank] = rb.make();
+                if (runs) runs[tile_ptr[cur] + base + rank] = rb.make();
             }
             if (at_end) {
                 alive = false;
@@ -1032,14 +1034,19 @@ void launch_dda_fill(const FrameDesc* frames, const int* cta0, int n_frames, int
                      const RunSink& sink, RaySeg* seg, unsigned long long* class_counts, int32_t* lam0,
                      cudaStream_t s) {
     if (n_ctas > 0) {
-#define MRF_FILL_LAUNCH(SP, RU)                                                                                     \
-    dda_fill_kernel<SP, RU><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, \
-                                                            off_q, tile_runs, ray_z, counters, mp, lnu, sink, seg, \
-                                                            class_counts, lam0)
+#define MRF_FILL_LAUNCH(SP, RU, CO)                                                                                 \
+    dda_fill_kernel<SP, RU, CO><<<n_ctas, kFillThreads, 0, s>>>(frames, cta0, n_frames, g, n, depth_all, row_ptr, vid, \
+                                                                off_q, tile_runs, ray_z, counters, mp, lnu, sink, seg, \
+                                                                class_counts, lam0)
+        // tile_runs == nullptr without a sink: no run tracking at all (matrix-free re-walks, K6b)
         if (g.bmask) {
-            if (sink.runs) MRF_FILL_LAUNCH(true, true); else MRF_FILL_LAUNCH(true, false);
+            if (sink.runs) MRF_FILL_LAUNCH(true, true, true);
+            else if (tile_runs) MRF_FILL_LAUNCH(true, false, true);
+            else MRF_FILL_LAUNCH(true, false, false);
         } else {
-            if (sink.runs) MRF_FILL_LAUNCH(false, true); else MRF_FILL_LAUNCH(false, false);
+            if (sink.runs) MRF_FILL_LAUNCH(false, true, true);
+            else if (tile_runs) MRF_FILL_LAUNCH(false, false, true);
+            else MRF_FILL_LAUNCH(false, false, false);
         }
 #undef MRF_FILL_LAUNCH
     }

@@ -98,6 +98,7 @@ struct mrf_ctx {
     int k6_force = 0;           // 1: K6b always, 2: tile runs always (MRF_K6)
     bool k6_demoted = false;
     bool blk_check = false;     // check the next K6b's stats (after build_blocks)
+    bool tile_counts_ok = true; // tile_runs holds the runs per bucket of every ray walked so far
     double ppv_min = 1e30;      // min over the frames of min(fx, fy) res / 3 m
     long long blk_min_share = kBlkMinShare;  // (MRF_BLK_SHARE: a test forces the demotion)
     int blk_max_probe = 64;  // (MRF_BLK_PROBE: < 0 sends every element to T directly, for tests)
@@ -695,11 +696,13 @@ mrf_status sync_fill(mrf_ctx* c, bool need_counts = true) {
             if (ss != MRF_OK) return ss;
         }
         new_slots = c->E - c->E_filled;
+        if (c->use_block()) c->tile_counts_ok = false;  // (K6b: the fill tracks no tile runs)
         {
             ProfScope ps(c, MRF_K_DDA_FILL);
             launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
-                            c->lnu.p, c->tile_runs.p, c->counters.p + 10, sink, nullptr, c->counters.p + kClassCtr,
+                            c->lnu.p, c->use_block() ? nullptr : c->tile_runs.p, c->counters.p + 10, sink, nullptr,
+                            c->counters.p + kClassCtr,
                             c->lam.p, c->stream);
             CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + ((!MRF_FILL_LNU || c->mp.pcoef) && c->R > c->R_filled ? 1 : 0));
         }
@@ -785,10 +788,28 @@ mrf_status build_voxel_transpose(mrf_ctx* c) {
 
 // Tile-run transpose (runs grouped by tile) + its K6 work list.  The runs per tile were counted
 // by the DDA fills.
+// The runs per tile bucket, counted from vid (run_fill without placing) when the fills did not
+// count them (K6b mode; needed after a demotion to the tile runs, or for the touched tiles of the
+// compacted reduction).
+mrf_status ensure_tile_counts(mrf_ctx* c) {
+    if (c->tile_counts_ok) return MRF_OK;
+    const long long NT = c->NT * c->n_bucket_groups();
+    CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * (size_t)NT, c->stream));
+    {
+        ProfScope ps(c, MRF_K_TRANSPOSE);
+        launch_run_fill(c->R, c->row_ptr.p, c->ray_z.p, c->vid.p, nullptr, c->tile_runs.p, c->fb() ? (int)c->NT : 0,
+                        nullptr, c->stream);
+        CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    }
+    c->tile_counts_ok = true;
+    return MRF_OK;
+}
+
 mrf_status build_tile_runs(mrf_ctx* c) {
     // buckets: the tiles (per-ray mode), or (frame, tile) pairs frame-major (keyframe averages)
     const long long NT = c->NT * c->n_bucket_groups();
     mrf_status st;
+    if ((st = ensure_tile_counts(c)) != MRF_OK) return st;
     CK(c->tile_ptr.ensure((size_t)NT + 1, 0, c->stream));
     CK(c->tile_cursor.ensure((size_t)NT, 0, c->stream));
     if ((st = scan(c, c->tile_runs.p, c->tile_ptr.p, NT, 0)) != MRF_OK) return st;
@@ -923,12 +944,17 @@ mrf_status build_blocks(mrf_ctx* c) {
     CK(c->blk.ensure((size_t)std::max(1LL, c->n_blk), 0, c->stream));
     if (c->n_blk)
         CK(cudaMemcpyAsync(c->blk.p, bl.data(), sizeof(int4) * bl.size(), cudaMemcpyHostToDevice, c->stream));
+    // the touched tiles of the compacted reduction (one rank: the MRF_COMPACT / one-rank NCCL
+    // tests) come from the runs per tile, which the fills did not count here
+    const bool need_tiles = c->force_compact || c->comm;
+    if (need_tiles && (st = ensure_tile_counts(c)) != MRF_OK) return st;
     const long long NT = c->NT;
-    std::vector<int32_t> nr((size_t)NT);
-    CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<int32_t> nr(need_tiles ? (size_t)NT : 0);
+    if (need_tiles)
+        CK(cudaMemcpyAsync(nr.data(), c->tile_runs.p, sizeof(int32_t) * NT, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if ((st = fill_readback(c)) != MRF_OK) return st;  // (already here: no further wait)
-    c->n_runs = 0;
+    c->n_runs = 0;  // (no transpose in K6b mode; the count only when the tiles were counted)
     for (int32_t x : nr) c->n_runs += x;
     c->tile_nr = nr;
     c->n_bitems = 0;
@@ -1677,6 +1703,7 @@ mrf_status mrf_reset(mrf_ctx* ctx) {
     c->n_invalid = c->n_dropped = c->n_kept = 0;
     c->frames.clear();
     CK(cudaMemsetAsync(c->tile_runs.p, 0, sizeof(int32_t) * c->NT, c->stream));
+    c->tile_counts_ok = true;
     CK(cudaMemsetAsync(c->T.p, 0, sizeof(long long) * c->VI, c->stream));
     CK(cudaMemsetAsync(c->row_ptr.p, 0, sizeof(long long), c->stream));
     c->dirty = true;
