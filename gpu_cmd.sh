@@ -1,7 +1,8 @@
 #!/bin/bash
 # One gpurun call: GPU parity tests + smoke, the default bench line, the ncu launch list, the
 # per-launch DRAM traffic of one BP iteration (K5 classes + K6) and one --set full capture of the
-# largest K5 class kernel and of K6.   gpurun --timeout 3000 -- 'bash gpu_cmd.sh [tests|bench|ncu|all]'
+# largest K5 class kernel and of K6 / K6b; "modes": every mode's bench line.
+#   gpurun --timeout 3000 -- 'bash gpu_cmd.sh [tests|bench|ncu|modes|all]'
 mkdir -p gpurun_out
 what=${1:-all}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
@@ -24,4 +25,12 @@ if [[ $what == ncu || $what == all ]]; then
   timeout 1200 ncu --set full --clock-control none --import-source on \
       --kernel-name-base demangled -k regex:'ray_msg_kernel<\(int\)16, \(int\)6|tile_reduce|block_reduce' -s 2 -c 2 -o gpurun_out/prof -f $C > gpurun_out/ncu_full.log 2>&1
   tail -1 gpurun_out/ncu_full.log; du -sh gpurun_out
+fi
+if [[ $what == modes || $what == all ]]; then
+  # every mode's bench line (frames30 unless named), and the 0.02 m config on 4 emulated ranks
+  for m in "sparse:--bricks 8" "patch:--noise patch" "kfavg:--messages keyframe-avg" "mf:--matrix-free 5" "frames100:--config frames100 --steps 2 --warmup 3"; do
+    n=${m%%:*}; a=${m#*:}
+    timeout 900 python bench.py --no-cpu-baseline $a > gpurun_out/bench_$n.log 2>&1
+    echo "$n $(tail -1 gpurun_out/bench_$n.log | cut -c1-160)"
+  done
 fi
