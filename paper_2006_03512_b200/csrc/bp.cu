@@ -1254,7 +1254,7 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
 constexpr int kBlkThreads = 256;
 constexpr int kBlkWarps = kBlkThreads / 32;
 constexpr int kBlkTableLog = 11;  // 2048 entries
-constexpr int kBlkQueue = 64;     // per-warp ring of deferred (v, q)
+constexpr int kBlkQueue = 160;    // per-warp ring of deferred (v, q): < 32 left + 4 x 32 appended
 #ifndef MRF_BLK_CTAS
 #define MRF_BLK_CTAS 6
 #endif
@@ -1276,7 +1276,6 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
     __shared__ int s_used, s_fall;  // this block's claimed entries, elements sent to T directly
     __shared__ long long s_blk;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
     for (int i = threadIdx.x; i < S; i += kBlkThreads) {
         key[i] = -1;
         acc[i] = 0;
@@ -1337,13 +1336,17 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
     auto drain = [&](int cnt) {  // the first cnt queued entries, one per lane
         __syncwarp();
         if (lane < cnt) {
-            const int2 e = wq[(qh + lane) & (kBlkQueue - 1)];
+            const int j = qh + lane;
+            const int2 e = wq[j >= kBlkQueue ? j - kBlkQueue : j];
             slow(e.x, e.y);
         }
         qh += cnt;
+        if (qh >= kBlkQueue) {  // (keeps the ring positions below 2 x kBlkQueue)
+            qh -= kBlkQueue;
+            qt -= kBlkQueue;
+        }
         __syncwarp();
     };
-    // fast path for all 32 lanes (valid: this lane holds an element)
     // fast path for one lane's 4 slots (q = 0: nothing to add -- padding, or a zero message):
     // 4 independent probes of the home slots, the adds predicated on a hit, misses queued
     const unsigned key_sh = (unsigned)__cvta_generic_to_shared(key);
@@ -1360,6 +1363,8 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
         bool miss[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
+            // the adds predicated on a hit (a miss lane adding 0 instead costs more bank conflicts
+            // in this L1-bound kernel: measured)
             const bool hit = fast && qq[k] != 0 && kk[k] == vv[k];
             asm volatile(
                 "{\n.reg .pred p;\nsetp.ne.u32 p, %3, 0;\n"
@@ -1367,15 +1372,17 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
                 "r"(qq[k] & 0xffff), "r"(qq[k] >> 16), "r"((unsigned)hit), "n"(4 * S));
             miss[k] = qq[k] != 0 && !hit;
         }
+        // the misses to the ring (room for 4 x 32 more: drained below 32 before each add4)
+        unsigned ltm;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const unsigned mm = __ballot_sync(kFull, miss[k]);
-            if (mm) {
-                if (miss[k]) wq[(qt + __popc(mm & lt)) & (kBlkQueue - 1)] = make_int2(vv[k], qq[k]);
-                qt += __popc(mm);
-                if (qt - qh >= 32) drain(32);
-            }
+            const int j = qt + __popc(mm & ltm);  // (qt < qh + 160 <= 320)
+            if (miss[k]) wq[j >= kBlkQueue ? j - kBlkQueue : j] = make_int2(vv[k], qq[k]);
+            qt += __popc(mm);
         }
+        while (qt - qh >= 32) drain(32);
     };
     for (long long bi = blockIdx.x; bi < n_blocks;) {
         const int4 b = __ldg(blocks + bi);  // {first ray, ncols | nrows << 16, row stride (rays), -}
