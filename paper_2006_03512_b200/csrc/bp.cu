@@ -1396,10 +1396,11 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
             // slots past a ray's end are padding with lambda = 0 (the fill writes it, K5 never
             // writes a slot past n, import and re-layout fill it with 0), skipped like any zero
             const long long ray = (long long)b.x + (long long)r * b.z;
-            const int A = (int)__ldg(row_ptr + ray), B = (int)__ldg(row_ptr + ray + ncols);
-            for (int e = A + 4 * lane; e - 4 * lane < B; e += 256) {  // (warp-uniform trip count)
+            // (unsigned: e runs up to 383 slots past B, which may lie just below 2^31)
+            const unsigned A = (unsigned)__ldg(row_ptr + ray), B = (unsigned)__ldg(row_ptr + ray + ncols);
+            for (unsigned e = A + 4 * lane; e - 4 * lane < B; e += 256) {  // (warp-uniform trip count)
                 int4 v0 = {0, 0, 0, 0}, q0 = {0, 0, 0, 0}, v1 = {0, 0, 0, 0}, q1 = {0, 0, 0, 0};
-                MRF_ASSERT(e >= B || e + 3 < chk_lam);
+                MRF_ASSERT(e >= B || (long long)e + 3 < chk_lam);
                 if (e < B) {
                     v0 = __ldg(reinterpret_cast<const int4*>(vid + e));
                     q0 = __ldg(reinterpret_cast<const int4*>(lam + e));
