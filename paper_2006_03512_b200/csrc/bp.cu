@@ -1448,6 +1448,221 @@ __global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_reduce_kernel(
     }
 }
 
+// ---------------------------------------------------------------- K6b for the keyframe averages
+// The two integer passes of the keyframe-average sums (MODE 2: counts + min |q|; MODE 3: the
+// fixed-point small probabilities relative to the slot's scale -- see kf_accumulate above) over
+// pixel blocks instead of (frame, tile) run buckets: a block lies in one frame (b.w), so its
+// hash-table entries are (frame, slot) sums already.  Unlike the belief sums a zero message
+// counts here, so an element's validity comes from its ray (slots past a ray's end are padding):
+// the lane finds the ray of its 4 slots among the row's 32 by a shuffle binary search.
+// Integer sums (and min) in any order: bit-identical to the tile-run passes.
+template <int MODE>
+__global__ void __launch_bounds__(kBlkThreads, kBlkMinCtas) block_kf_kernel(long long n_blocks, const int4* __restrict__ blocks,
+                                                                          const long long* __restrict__ row_ptr,
+                                                                          const RayInfo* __restrict__ ray_z,
+                                                                          const int32_t* __restrict__ vid,
+                                                                          const int32_t* __restrict__ lam,
+                                                                          long long* out, long long n_out, long long VI,
+                                                                          unsigned* next, long long chk_lam) {
+    constexpr int S = 1 << kBlkTableLog;
+    constexpr int kMaxProbe = 64;
+    __shared__ int key[S];
+    __shared__ int a0[S];  // MODE 2: packed counts n_pos + 65536 n_neg; MODE 3: sum of (v & 0xffff)
+    __shared__ int a1[S];  // MODE 2: min |q| (unsigned); MODE 3: sum of (v >> 16)
+    __shared__ int2 queue[kBlkWarps][kBlkQueue];
+    __shared__ int s_row, s_used;
+    __shared__ long long s_blk;
+    const int lane = threadIdx.x & 31;
+    unsigned long long* N = reinterpret_cast<unsigned long long*>(out);
+    long long* D = out + n_out;
+    unsigned* M = reinterpret_cast<unsigned*>(out + 2 * n_out);
+    const float* A = reinterpret_cast<const float*>(out + 2 * n_out);
+    for (int i = threadIdx.x; i < S; i += kBlkThreads) {
+        key[i] = -1;
+        a0[i] = 0;
+        a1[i] = MODE == 2 ? -1 : 0;
+    }
+    if (threadIdx.x == 0) {
+        s_row = 0;
+        s_used = 0;
+    }
+    __syncthreads();
+    volatile int* vkey = key;
+    volatile int* vused = &s_used;
+    auto hash = [](int v) { return ((unsigned)v * 0x9E3779B1u) >> (32 - kBlkTableLog); };
+    // the element's term: MODE 2 (count word, |q|), MODE 3 the fixed-point value (kf_accumulate)
+    auto term3a = [&](float a, int qv) {
+        const float al = (float)(qv >= 0 ? (unsigned)qv : 0u - (unsigned)qv) * (kQInv * kLog2e);
+        const float ap = fmaxf(a, 0.f) * kLog2e;
+        const float c = a < 0.f ? 1.f : 1.f + ex2(-ap);
+        const float t = ex2(ap - al) * c * __frcp_rn(1.f + ex2(-al));
+        int r = __float2int_rn(t * kKfFix);
+        if (a < 0.f && qv < 0) r = -r;
+        return r;
+    };
+    auto term3 = [&](long long fb, int v, int qv) { return term3a(__ldg(A + fb + v), qv); };
+    auto add = [&](long long fb, int v, int qv) {
+        unsigned h = hash(v);
+        int p = 0;
+        for (; p < kMaxProbe; ++p) {
+            const int k = vkey[h];
+            if (k == v) break;
+            if (k < 0) {
+                if (*vused >= S / 2) {
+                    p = kMaxProbe;
+                    break;
+                }
+                const int old = atomicCAS(key + h, -1, v);
+                if (old < 0) {
+                    atomicAdd(&s_used, 1);
+                    break;
+                }
+                if (old == v) break;
+            }
+            h = (h + 1) & (S - 1);
+        }
+        const unsigned aq = qv >= 0 ? (unsigned)qv : 0u - (unsigned)qv;
+        if (p < kMaxProbe) {
+            if constexpr (MODE == 2) {
+                atomicAdd(a0 + h, qv >= 0 ? 1 : 65536);
+                atomicMin(reinterpret_cast<unsigned*>(a1) + h, aq);
+            } else {
+                const int t = term3(fb, v, qv);
+                atomicAdd(a0 + h, t & 0xffff);
+                atomicAdd(a1 + h, t >> 16);
+            }
+        } else {  // straight to the (frame, slot) sums
+            if constexpr (MODE == 2) {
+                atomicAdd(N + fb + v, qv >= 0 ? 1ull : (1ull << 32));
+                atomicMin(M + fb + v, aq);
+            } else {
+                atomicAdd(reinterpret_cast<unsigned long long*>(D + fb + v), (unsigned long long)(long long)term3(fb, v, qv));
+            }
+        }
+    };
+    // the misses of the fast path, per warp (as in block_reduce_kernel)
+    int2* wq = queue[threadIdx.x >> 5];
+    int qh = 0, qt = 0;
+    const unsigned key_sh = (unsigned)__cvta_generic_to_shared(key);
+    auto drain = [&](long long fb, int cnt) {
+        __syncwarp();
+        if (lane < cnt) {
+            const int j = qh + lane;
+            const int2 q2 = wq[j >= kBlkQueue ? j - kBlkQueue : j];
+            add(fb, q2.x, q2.y);
+        }
+        qh += cnt;
+        if (qh >= kBlkQueue) {
+            qh -= kBlkQueue;
+            qt -= kBlkQueue;
+        }
+        __syncwarp();
+    };
+    for (long long bi = blockIdx.x; bi < n_blocks;) {
+        const int4 b = __ldg(blocks + bi);  // {first ray, ncols | nrows << 16, row stride (rays), frame}
+        const int ncols = b.y & 0xffff, nrows = b.y >> 16;
+        const long long fb = (long long)b.w * VI;
+        for (;;) {
+            int r = 0;
+            if (lane == 0) r = atomicAdd(&s_row, 1);
+            r = __shfl_sync(kFull, r, 0);
+            if (r >= nrows) break;
+            const long long ray = (long long)b.x + (long long)r * b.z;
+            // lane j: ray j's first slot and length (past the row: never <= a slot)
+            unsigned rp = 0xffffffffu;
+            int nr = 0;
+            if (lane < ncols) {
+                rp = (unsigned)__ldg(row_ptr + ray + lane);
+                nr = __ldg(&ray_z[ray + lane].n);
+            }
+            const unsigned A0 = __shfl_sync(kFull, rp, 0);
+            const unsigned B = (unsigned)__ldg(row_ptr + ray + ncols);
+            for (unsigned e = A0 + 4 * lane; e - 4 * lane < B; e += 128) {  // (warp-uniform trip count)
+                int4 v4 = {0, 0, 0, 0}, q4 = {0, 0, 0, 0};
+                const bool in = e < B;
+                if (in) {
+                    MRF_ASSERT((long long)e + 3 < chk_lam);
+                    v4 = __ldg(reinterpret_cast<const int4*>(vid + e));
+                    q4 = __ldg(reinterpret_cast<const int4*>(lam + e));
+                }
+                // the ray of slots e..e+3 (one ray: segments are 8-aligned): the largest j with rp_j <= e
+                int j = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const unsigned rc = __shfl_sync(kFull, rp, (j + st) & 31);
+                    if (j + st < 32 && rc <= e) j += st;
+                }
+                const unsigned s0 = __shfl_sync(kFull, rp, j);
+                const int nj = __shfl_sync(kFull, nr, j);
+                const int vv[4] = {v4.x, v4.y, v4.z, v4.w}, qq[4] = {q4.x, q4.y, q4.z, q4.w};
+                // fast path: the 4 home slots probed at once, hits added there, misses queued
+                unsigned hh[4];
+                int kk[4];
+                float sa[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    hh[k] = hash(vv[k]);
+                    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(kk[k]) : "r"(key_sh + 4u * hh[k]));
+                    if constexpr (MODE == 3) sa[k] = in ? __ldg(A + fb + vv[k]) : 0.f;
+                }
+                bool miss[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool ok = in && (int)(e + k - s0) < nj;
+                    const bool hit = ok && kk[k] == vv[k];
+                    if (hit) {
+                        if constexpr (MODE == 2) {
+                            atomicAdd(a0 + hh[k], qq[k] >= 0 ? 1 : 65536);
+                            atomicMin(reinterpret_cast<unsigned*>(a1) + hh[k],
+                                      qq[k] >= 0 ? (unsigned)qq[k] : 0u - (unsigned)qq[k]);
+                        } else {
+                            const int t = term3a(sa[k], qq[k]);
+                            atomicAdd(a0 + hh[k], t & 0xffff);
+                            atomicAdd(a1 + hh[k], t >> 16);
+                        }
+                    }
+                    miss[k] = ok && !hit;
+                }
+                unsigned ltm;
+                asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const unsigned mm = __ballot_sync(kFull, miss[k]);
+                    const int jq = qt + __popc(mm & ltm);
+                    if (miss[k]) wq[jq >= kBlkQueue ? jq - kBlkQueue : jq] = make_int2(vv[k], qq[k]);
+                    qt += __popc(mm);
+                }
+                while (qt - qh >= 32) drain(fb, 32);
+            }
+        }
+        if (qt > qh) drain(fb, qt - qh);
+        __syncthreads();
+        for (int i = threadIdx.x; i < S; i += kBlkThreads) {
+            const int v = key[i];
+            if (v >= 0) {
+                if constexpr (MODE == 2) {
+                    const unsigned cn = (unsigned)a0[i];
+                    atomicAdd(N + fb + v, (unsigned long long)(cn & 0xffffu) | ((unsigned long long)(cn >> 16) << 32));
+                    atomicMin(M + fb + v, (unsigned)a1[i]);
+                } else {
+                    const long long sum = (long long)a1[i] * 65536 + (long long)a0[i];
+                    if (sum) atomicAdd(reinterpret_cast<unsigned long long*>(D + fb + v), (unsigned long long)sum);
+                }
+                key[i] = -1;
+                a0[i] = 0;
+                a1[i] = MODE == 2 ? -1 : 0;
+            }
+        }
+        if (threadIdx.x == 0) {
+            s_row = 0;
+            s_used = 0;
+            s_blk = (long long)gridDim.x + atomicAdd(next, 1u);
+        }
+        __syncthreads();
+        bi = s_blk;
+    }
+}
+
 // ---------------------------------------------------------------- K8
 __global__ void marginals_kernel(GridDesc g, const long long* __restrict__ T, double L0, float* out) {
     const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1637,6 +1852,22 @@ void launch_tile_reduce(long long n_items, const int2* items, const long long* t
     else
         launch_tile_reduce_t<0, false>(n_items, items, tile_ptr, runs, lam, per_item, T, 0, next, tile_map, chk_lam,
                                        chk_out_tiles, n_tiles, s);
+}
+
+void launch_block_kf(int pass, long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,
+                     const int32_t* vid, const int32_t* lam, long long* sums, long long n_slots, long long VI,
+                     unsigned* next, long long chk_lam, cudaStream_t s) {
+    if (n_blocks == 0) return;
+    DevCfg& dc = dev_cfg();
+    const long long cap = (long long)dc.sms * kBlkMinCtas;
+    const unsigned grid = (unsigned)(n_blocks < cap ? n_blocks : cap);
+    cudaMemsetAsync(next, 0, sizeof(unsigned), s);
+    if (pass == 0)
+        block_kf_kernel<2><<<grid, kBlkThreads, 0, s>>>(n_blocks, blocks, row_ptr, ray_z, vid, lam, sums, n_slots, VI,
+                                                        next, chk_lam);
+    else
+        block_kf_kernel<3><<<grid, kBlkThreads, 0, s>>>(n_blocks, blocks, row_ptr, ray_z, vid, lam, sums, n_slots, VI,
+                                                        next, chk_lam);
 }
 
 void launch_block_reduce(long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,

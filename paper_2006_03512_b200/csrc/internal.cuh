@@ -383,6 +383,11 @@ void launch_block_reduce(long long n_blocks, const int4* blocks, const long long
                          const int32_t* vid, const int32_t* lam, long long* T, unsigned* next,
                          unsigned long long* stats, const int32_t* tile_map, int max_probe, long long chk_lam,
                          long long chk_out, cudaStream_t s);
+// K6b for the keyframe averages (pass 0: counts + min |q|, pass 1: the fixed-point sums; the
+// blocks' .w is their frame): the same outputs as launch_kf_sums over (frame, tile) runs
+void launch_block_kf(int pass, long long n_blocks, const int4* blocks, const long long* row_ptr, const RayInfo* ray_z,
+                     const int32_t* vid, const int32_t* lam, long long* sums, long long n_slots, long long VI,
+                     unsigned* next, long long chk_lam, cudaStream_t s);
 void launch_voxel_reduce(long long n_items, const int2* items, const long long* col_ptr, const int32_t* tr,
                          const int32_t* lam, long long* T, cudaStream_t s);
 // tile_map (nullable): tile -> position among the tiles written (world > 1: the tiles some rank

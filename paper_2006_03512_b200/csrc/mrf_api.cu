@@ -99,6 +99,9 @@ struct mrf_ctx {
     bool k6_demoted = false;
     bool blk_check = false;     // check the next K6b's stats (after build_blocks)
     bool tile_counts_ok = true; // tile_runs holds the runs per bucket of every ray walked so far
+    // MRF_KF_BLOCK=1: the keyframe-average passes over pixel blocks too (bit-identical, but slower
+    // than the (frame, tile) runs at frames30: 69.4 vs 54.2 ms of K6' per step -- off)
+    bool kf_blk_on = false;
     double ppv_min = 1e30;      // min over the frames of min(fx, fy) res / 3 m
     long long blk_min_share = kBlkMinShare;  // (MRF_BLK_SHARE: a test forces the demotion)
     int blk_max_probe = 64;  // (MRF_BLK_PROBE: < 0 sends every element to T directly, for tests)
@@ -157,10 +160,13 @@ struct mrf_ctx {
     // with MRF_K6_FRAMES=1 (K6 items then cover one frame's rays of a tile)
     bool frame_buckets = false;
     bool fb() const { return kf_avg || frame_buckets; }
-    bool use_block() const {
-        const bool want = k6_force == 1 || (k6_force == 0 && world == 1 && ppv_min >= kBlkMinPpv && !k6_demoted);
-        return want && !k6_voxel && !kf_avg && !mf && !frame_buckets;
+    bool want_block() const {
+        return k6_force == 1 || (k6_force == 0 && world == 1 && ppv_min >= kBlkMinPpv && !k6_demoted);
     }
+    bool use_block() const { return want_block() && !k6_voxel && !kf_avg && !mf && !frame_buckets; }
+    // the keyframe-average sums over pixel blocks (stored graph only)
+    bool kf_block() const { return want_block() && kf_avg && !mf && !k6_voxel && kf_blk_on; }
+    bool any_block() const { return use_block() || kf_block(); }
     long long n_bucket_groups() const { return fb() ? std::max<long long>(1, (long long)frames.size()) : 1; }     // runs per K6 work item (MRF_K6_ITEM, <= kRunsPerItem)
     bool k5_staged = false; // K5 over TMA-staged ray stages (MRF_K5=staged); default: per-class warp kernels
     bool vtr_valid = false; // per-voxel transpose built for the current graph
@@ -495,7 +501,7 @@ mrf_status mf_rechunk(mrf_ctx* c) {
 // The sink of the next fill over new_slots incidence slots (capacity from run_ratio; see runs_ok).
 mrf_status run_sink(mrf_ctx* c, long long new_slots, RunSink& sink) {
     sink = RunSink{nullptr, nullptr, nullptr, 0};
-    if (c->use_block()) {  // K6b needs no tile runs (a later tile-run K6 would re-read vid)
+    if (c->any_block()) {  // K6b needs no tile runs (a later tile-run K6 would re-read vid)
         c->runs_ok = false;
         return MRF_OK;
     }
@@ -696,12 +702,12 @@ mrf_status sync_fill(mrf_ctx* c, bool need_counts = true) {
             if (ss != MRF_OK) return ss;
         }
         new_slots = c->E - c->E_filled;
-        if (c->use_block()) c->tile_counts_ok = false;  // (K6b: the fill tracks no tile runs)
+        if (c->any_block()) c->tile_counts_ok = false;  // (K6b: the fill tracks no tile runs)
         {
             ProfScope ps(c, MRF_K_DDA_FILL);
             launch_dda_fill(c->d_frames.p, c->d_cta0.p, nf, cta0[nf], c->R_filled, c->R - c->R_filled, c->grid,
                             c->noise, c->mp, c->depth_all.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->off_q.p,
-                            c->lnu.p, c->use_block() ? nullptr : c->tile_runs.p, c->counters.p + 10, sink, nullptr,
+                            c->lnu.p, c->any_block() ? nullptr : c->tile_runs.p, c->counters.p + 10, sink, nullptr,
                             c->counters.p + kClassCtr,
                             c->lam.p, c->stream);
             CK_LAUNCH(MRF_K_DDA_FILL, (cta0[nf] > 0 ? 1 : 0) + ((!MRF_FILL_LNU || c->mp.pcoef) && c->R > c->R_filled ? 1 : 0));
@@ -934,12 +940,14 @@ mrf_status build_blocks(mrf_ctx* c) {
     mrf_status st;
     std::vector<int4>& bl = c->h_blk;  // (kept: the copy below is asynchronous)
     bl.clear();
-    for (const FrameRec& f : c->frames)
+    for (size_t fi = 0; fi < c->frames.size(); ++fi) {
+        const FrameRec& f = c->frames[fi];
         for (int r0 = 0; r0 < f.rows_owned; r0 += kBlkRows)
             for (int u0 = 0; u0 < f.W; u0 += kBlkCols)
                 bl.push_back(make_int4((int)(f.ray_base + (long long)r0 * f.W + u0),
                                        std::min(kBlkCols, f.W - u0) | (std::min(kBlkRows, f.rows_owned - r0) << 16),
-                                       f.W, 0));
+                                       f.W, (int)fi));
+    }
     c->n_blk = (long long)bl.size();
     CK(c->blk.ensure((size_t)std::max(1LL, c->n_blk), 0, c->stream));
     if (c->n_blk)
@@ -970,7 +978,7 @@ mrf_status prepare(mrf_ctx* c) {
     c->vtr_valid = false;
     if (c->k6_voxel) {
         if ((st = build_voxel_transpose(c)) != MRF_OK) return st;
-    } else if (c->use_block()) {
+    } else if (c->any_block()) {
         if ((st = build_blocks(c)) != MRF_OK) return st;
     } else {
         if ((st = build_tile_runs(c)) != MRF_OK) return st;
@@ -1108,6 +1116,17 @@ mrf_status voxel_sums(mrf_ctx* c, long long* out, bool compact = false) {
         CK(cudaMemsetAsync(c->kf_sums.p, 0, 2 * sizeof(long long) * (size_t)n, c->stream));
         CK(cudaMemsetAsync(c->kf_sums.p + 2 * n, 0xff, sizeof(unsigned) * (size_t)n, c->stream));
         unsigned* nxt = c->k6_dynamic ? reinterpret_cast<unsigned*>(c->counters.p + 15) : nullptr;
+        if (c->kf_block()) {  // K6b: the two passes over pixel blocks (one frame each)
+            unsigned* bn = reinterpret_cast<unsigned*>(c->counters.p + 18);
+            launch_block_kf(0, c->n_blk, c->blk.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lam.p, c->kf_sums.p, n, c->VI,
+                            bn, (long long)c->lam.cap, c->stream);
+            launch_kf_scale(n, 0, n, c->kf_sums.p, c->stream);
+            launch_block_kf(1, c->n_blk, c->blk.p, c->row_ptr.p, c->ray_z.p, c->vid.p, c->lam.p, c->kf_sums.p, n, c->VI,
+                            bn, (long long)c->lam.cap, c->stream);
+            launch_kf_finalize(F, c->VI, c->kf_sums.p, c->qbar.p, out, c->stream);
+            CK_LAUNCH(MRF_K_VOXEL_SUM, (c->n_blk > 0 ? 2 : 0) + 2);
+            return MRF_OK;
+        }
         launch_kf_sums(0, c->n_bitems, c->bitems.p, c->tile_ptr.p, c->runs.p, c->lam.p, c->k6_item, c->kf_sums.p, n,
                        nxt, (long long)c->lam.cap, c->stream);
         launch_kf_scale(n, 0, n, c->kf_sums.p, c->stream);
@@ -1486,6 +1505,7 @@ mrf_status mrf_create(const int32_t dims[3], double resolution_m, const double o
     }
     if (const char* bp = getenv("MRF_BLK_PROBE")) c->blk_max_probe = atoi(bp);
     if (const char* bs = getenv("MRF_BLK_SHARE")) c->blk_min_share = atoll(bs);
+    if (const char* kb = getenv("MRF_KF_BLOCK")) c->kf_blk_on = atoi(kb) != 0;
     if (const char* km = getenv("MRF_K5_MATH")) c->k5_math = atoi(km);
     if (const char* ki = getenv("MRF_K6_ITEM")) {
         c->k6_item = std::min(std::max(atoi(ki), 1024), kRunsPerItem);
@@ -1958,7 +1978,7 @@ mrf_status mrf_k6_path(mrf_ctx* ctx, int32_t* path) {
     if (!path) return set_err(c, MRF_ERR_INVALID_ARG, "NULL output");
     mrf_status st;
     if ((st = prepare(c)) != MRF_OK) return st;
-    *path = c->use_block() ? 1 : 0;
+    *path = c->any_block() ? 1 : 0;
     return MRF_OK;
 }
 

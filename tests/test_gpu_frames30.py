@@ -119,3 +119,27 @@ def test_frames30_full_trajectory_count_rule(run30, n):
     gpu, noisy = run30[n]["gpu"], run30[n]["noisy"]
     assert gpu["p9999"] <= traj.MARG_TOL, gpu
     assert gpu["over"] <= traj.count_bar([x["over"] for x in noisy]), (gpu, noisy)
+
+
+def test_frames30_block_k6_bit_identical_to_tile_runs(monkeypatch):
+    """At the headline config, K6b (the pixel-block hash reduction the one-GPU path uses here)
+    and the tile-run K6 give bit-identical beliefs after each of 3 iterations (exact integer sums
+    in any order): the hash table's miss ring, probe loop and flush carry every message of all
+    847 M incidences exactly, with the tables as full as real blocks make them."""
+    w = synth.frames30()
+    depth = [torch.from_numpy(fr.depth).cuda() for fr in w.frames]
+    outs = {}
+    for k6 in ("tile", "block"):
+        monkeypatch.setenv("MRF_K6", k6)
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        with m:
+            for fr, d in zip(w.frames, depth):
+                m.add_frame(d, fr.K, fr.T_wc)
+            assert m.k6_path() == k6
+            outs[k6] = []
+            for _ in range(3):
+                m.bp_iterate(1)
+                outs[k6].append(m.export_beliefs())
+    for a, b in zip(outs["tile"], outs["block"]):
+        assert np.array_equal(a, b)

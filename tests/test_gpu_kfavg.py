@@ -191,3 +191,31 @@ def test_kfavg_deterministic(tf4, mf):
     for other in runs[1:]:
         for (a, ta), (b, tb) in zip(runs[0], other):
             assert np.array_equal(a, b) and np.array_equal(ta, tb)
+
+
+@pytest.mark.parametrize("scene", ["tiny4", "room3"])
+def test_kfavg_block_passes_bit_identical(scene, monkeypatch):
+    """The keyframe-average sums over pixel blocks (K6b passes: MRF_K6=block + MRF_KF_BLOCK=1, an
+    option -- slower than the runs at frames30) against the passes over (frame, tile) runs (MRF_K6=tile):
+    keyframe averages, messages and beliefs bit-identical (integer counts, minima and fixed-point
+    sums in any order), with a frame added after iterating (warm start)."""
+    w = synth.tiny_frames(n_frames=4) if scene == "tiny4" else synth.frames30(n_frames=3)
+    monkeypatch.setenv("MRF_KF_BLOCK", "1")
+    outs = {}
+    for k6 in ("tile", "block"):
+        monkeypatch.setenv("MRF_K6", k6)
+        m = pkg.MRFMap.from_workload(w)
+        m.set_stream(torch.cuda.current_stream().cuda_stream)
+        m.set_message_mode(pkg.MRF_MSG_KEYFRAME_AVG)
+        with m:
+            for fr in w.frames[:-1]:
+                m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(2)
+            fr = w.frames[-1]
+            m.add_frame(fr.depth, fr.K, fr.T_wc)
+            m.bp_iterate(2)
+            assert m.k6_path() == k6
+            outs[k6] = [m.export_keyframe_average(f) for f in range(len(w.frames))] + [m.export_messages(),
+                                                                                      m.export_beliefs()]
+    for a, b in zip(outs["tile"], outs["block"]):
+        assert np.array_equal(a, b)
