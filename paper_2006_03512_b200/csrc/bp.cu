@@ -1226,7 +1226,8 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
 }
 
 // ---------------------------------------------------------------- K6b: pixel-block reduction
-// The voxel sums T_v = sum of the messages of every incidence on v (Eq.6's belief), read
+// The voxel sums T_v = sum of the messages of every incidence on v (Eq.6; "accumulated to
+// obtain the current incoming belief"), read
 // in the messages' own (ray-major) order instead of through a transpose.  A work item is a block
 // of neighbouring pixels of one frame (kBlkCols columns x kBlkRows owned rows): their rays fan out
 // through nearly the same voxels (frames30: 43.6 k incidences per 32 x 16 block fall on 400-900
@@ -1241,8 +1242,9 @@ __global__ void __launch_bounds__(kK6Threads, 1) tile_reduce_kernel(long long n_
 //     arrays (a slot gets at most one message per ray, <= 512 per block: no overflow);
 //   * fast path: ONE probe, branch-free -- an element whose key sits at its home slot (almost all:
 //     each voxel recurs ~100 times per block) adds there at once; the others (a key's first
-//     occurrence, or a key displaced by probing) go to a per-warp queue that is drained 32 at a
-//     time by the full probe loop (claim by CAS), so the loop's divergence is paid by full warps
+//     occurrence, or a key displaced by probing) go to a per-warp ring (room for a lane group's
+//     4 x 32 misses) that is drained 32 at a time by the full probe loop (claim by CAS), so the
+//     loop's divergence is paid by full warps
 //     of misses instead of by every warp holding one (a per-element probe loop ran 3-4 iterations
 //     per warp instruction: the longest of 32 lanes' probe sequences);
 //   * a block claims at most half the table (linear probing stays short); an element whose key
