@@ -402,9 +402,7 @@ __device__ __forceinline__ void lane_out(const float (&l)[K], const float (&lR)[
 #define MRF_K5_MASK_ALL 0
 #endif
 template <int G, int K, int M, bool AVG>
-__global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS : MRF_K5_MIN_BLOCKS_SMALL))) ray_msg_kernel(long long n, const int32_t* __restrict__ rays,
-                                                         const long long* __restrict__ row_ptr,
-                                                         const RayInfo* __restrict__ ray_z,
+__global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS : MRF_K5_MIN_BLOCKS_SMALL))) ray_msg_kernel(long long n, const int4* __restrict__ desc,
                                                          const int32_t* __restrict__ vid,
                                                          const float* __restrict__ lnu, int32_t* lam,
                                                          const long long* __restrict__ T, MsgParams mp) {
@@ -418,10 +416,12 @@ __global__ void __launch_bounds__(256, (K > 8 ? 2 : (K > 6 ? MRF_K5_MIN_BLOCKS :
     // matrix-free mode, is a scratch holding only the current chunk's slots
     int nr = 0, e0 = 0, fr = 0;
     {
-        const int r = __ldg(rays + (ri < n ? ri : n - 1));
-        if (ri < n) nr = ray_z[r].n;
-        e0 = (int)__ldg(row_ptr + r);
-        if constexpr (AVG) fr = ray_z[r].frame;
+        // {row_ptr[r], n, frame, r} of the class list's ray (launch_class_desc): one load, where
+        // the ray id, then its record and row pointer were two dependent ones
+        const int4 d = __ldg(desc + (ri < n ? ri : n - 1));
+        if (ri < n) nr = d.y;
+        e0 = d.x;
+        if constexpr (AVG) fr = d.z;
     }
     const int s = e0 + sl * K;
     const int nv = min(max(nr - sl * K, 0), K);  // valid incidences of this lane's chunk
@@ -1702,27 +1702,26 @@ DevCfg& dev_cfg() {
 
 
 template <int M, bool AVG, int k>
-void launch_class_k(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr, const RayInfo* ray_z,
-                    const int32_t* vid, const float* lnu, int32_t* lam, const long long* T, const MsgParams& mp,
-                    cudaStream_t s) {
+void launch_class_k(int cls, long long n_rays, const int4* desc, const int32_t* vid, const float* lnu, int32_t* lam,
+                    const long long* T, const MsgParams& mp, cudaStream_t s) {
     if constexpr (k < kNumShort) {
         if (cls == k) {
             constexpr int G = class_G(k), K = class_K(k);
             const unsigned grid = blocks_for((n_rays + 32 / G - 1) / (32 / G) * 32, 256);
-            ray_msg_kernel<G, K, M, AVG><<<grid, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp);
+            ray_msg_kernel<G, K, M, AVG><<<grid, 256, 0, s>>>(n_rays, desc, vid, lnu, lam, T, mp);
             return;
         }
-        launch_class_k<M, AVG, k + 1>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
+        launch_class_k<M, AVG, k + 1>(cls, n_rays, desc, vid, lnu, lam, T, mp, s);
     }
 }
 
 template <int M, bool AVG>
-void launch_ray_messages_m(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+void launch_ray_messages_m(int cls, long long n_rays, const int32_t* rays, const int4* desc, const long long* row_ptr,
                            const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
                            const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                            int n_warps_long, cudaStream_t s) {
     if (cls < kNumShort) {
-        launch_class_k<M, AVG, 0>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, s);
+        launch_class_k<M, AVG, 0>(cls, n_rays, desc, vid, lnu, lam, T, mp, s);
     } else {
         const unsigned g = blocks_for((long long)n_warps_long * 32, 256);
         ray_msg_long_kernel<M, AVG, false><<<g, 256, 0, s>>>(n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
@@ -1775,19 +1774,35 @@ void launch_staged_m(long long n_stages, const Stage* stages, const long long* r
 
 }  // namespace
 
-void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+namespace {
+__global__ void class_desc_kernel(long long n, const int32_t* __restrict__ rays, const long long* __restrict__ row_ptr,
+                                  const RayInfo* __restrict__ info, int4* desc) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int r = rays[i];
+    desc[i] = make_int4((int)row_ptr[r], info[r].n, info[r].frame, r);
+}
+}  // namespace
+
+void launch_class_desc(long long n, const int32_t* rays, const long long* row_ptr, const RayInfo* info, int4* desc,
+                       cudaStream_t s) {
+    if (n == 0) return;
+    class_desc_kernel<<<blocks_for(n, 256), 256, 0, s>>>(n, rays, row_ptr, info, desc);
+}
+
+void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const int4* desc, const long long* row_ptr,
                          const RayInfo* ray_z, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, int math, cudaStream_t s) {
     if (n_rays == 0) return;
     if (mp.qbar)  // keyframe-average mode (math level 1)
-        launch_ray_messages_m<1, true>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+        launch_ray_messages_m<1, true>(cls, n_rays, rays, desc, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
                                        scratch_per_warp, n_warps_long, s);
     else if (math == 0)
-        launch_ray_messages_m<0, false>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+        launch_ray_messages_m<0, false>(cls, n_rays, rays, desc, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
                                         scratch_per_warp, n_warps_long, s);
     else
-        launch_ray_messages_m<1, false>(cls, n_rays, rays, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
+        launch_ray_messages_m<1, false>(cls, n_rays, rays, desc, row_ptr, ray_z, vid, lnu, lam, T, mp, scratch,
                                         scratch_per_warp, n_warps_long, s);
 }
 

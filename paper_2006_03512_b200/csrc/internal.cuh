@@ -367,7 +367,12 @@ void launch_class_scatter_mf(long long n_rays, const RayInfo* info, int fpc, con
                              unsigned long long* cursor, int32_t* out, cudaStream_t s);
 void launch_class_scatter(long long n_rays, const RayInfo* info, const ClassOffsets& off, unsigned long long* cursor,
                           int32_t* out, cudaStream_t s);
-void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const long long* row_ptr,
+// K5 class-list descriptors: desc[i] = {row_ptr[r] (int32), n, frame, r} for r = rays[i], so a
+// class kernel's warp reaches its ray's incidences with one load instead of two dependent ones
+// (rebuilt with the class lists, once per graph change)
+void launch_class_desc(long long n, const int32_t* rays, const long long* row_ptr, const RayInfo* info, int4* desc,
+                       cudaStream_t s);
+void launch_ray_messages(int cls, long long n_rays, const int32_t* rays, const int4* desc, const long long* row_ptr,
                          const RayInfo* info, const int32_t* vid, const float* lnu, int32_t* lam,
                          const long long* T, const MsgParams& mp, float* scratch, long long scratch_per_warp,
                          int n_warps_long, int math, cudaStream_t s);

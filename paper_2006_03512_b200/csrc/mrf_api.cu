@@ -275,6 +275,7 @@ struct mrf_ctx {
     DBuf<long long> scan_scratch;
     DBuf<unsigned long long> counters;
     DBuf<int32_t> class_all;                 // ray ids grouped by K5 class
+    DBuf<int4> class_desc;                   // per class_all entry: {row_ptr, n, frame, ray id} (launch_class_desc)
     DBuf<unsigned long long> class_cnt;      // [counts | cursors] per class
     long long class_off[kNumClasses] = {};
     DBuf<Stage> stages;
@@ -1024,6 +1025,8 @@ mrf_status prepare(mrf_ctx* c) {
         CK(c->class_all.ensure((size_t)std::max(1LL, tot), 0, c->stream));
         launch_class_scatter_mf(c->R, c->ray_z.p, c->mf, c->mf_cls_off_d.p, c->class_cnt.p + NK, c->class_all.p,
                                 c->stream);
+        CK(c->class_desc.ensure((size_t)std::max(1LL, tot), 0, c->stream));
+        launch_class_desc(tot, c->class_all.p, c->row_ptr.p, c->ray_z.p, c->class_desc.p, c->stream);
         CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
         const int kl = kNumClasses - 1;
         long long n_long = 0;
@@ -1073,6 +1076,9 @@ mrf_status prepare(mrf_ctx* c) {
     CK(c->class_all.ensure((size_t)std::max(1LL, tot), 0, c->stream));
     launch_class_scatter(c->R, c->ray_z.p, off, c->class_cnt.p + kNumClasses, c->class_all.p, c->stream);
     CK_LAUNCH(MRF_K_TRANSPOSE, c->R > 0 ? 1 : 0);
+    CK(c->class_desc.ensure((size_t)std::max(1LL, tot), 0, c->stream));
+    launch_class_desc(tot, c->class_all.p, c->row_ptr.p, c->ray_z.p, c->class_desc.p, c->stream);
+    CK_LAUNCH(MRF_K_TRANSPOSE, tot > 0 ? 1 : 0);
     // scratch for the tiled long-ray kernel
     const int kl = kNumClasses - 1;
     if (c->class_n[kl] > 0) {
@@ -1242,7 +1248,8 @@ mrf_status ray_messages(mrf_ctx* c) {
             for (int k = 0; k < kNumClasses; ++k) {
                 const long long key = (long long)ci * kNumClasses + k;
                 if (c->mf_cls_n[key] == 0) continue;
-                launch_ray_messages(k, c->mf_cls_n[key], c->class_all.p + c->mf_cls_off[key], c->row_ptr.p,
+                launch_ray_messages(k, c->mf_cls_n[key], c->class_all.p + c->mf_cls_off[key],
+                                    c->class_desc.p + c->mf_cls_off[key], c->row_ptr.p,
                                     c->ray_z.p, sv - ch.e0, sl - ch.e0, c->lam.p, c->T.p, c->mp, c->long_scratch.p,
                                     c->long_scratch_per_warp, c->n_warps_long, c->k5_math, B);
                 CK_LAUNCH(MRF_K_RAY_MSG, 1);
@@ -1281,7 +1288,8 @@ mrf_status ray_messages(mrf_ctx* c) {
         for (int j = 1; j < ns; ++j)
             if (load[j] < load[si]) si = j;
         load[si] += work(k);
-        launch_ray_messages(k, c->class_n[k], c->class_all.p + c->class_off[k], c->row_ptr.p, c->ray_z.p, c->vid.p,
+        launch_ray_messages(k, c->class_n[k], c->class_all.p + c->class_off[k], c->class_desc.p + c->class_off[k],
+                            c->row_ptr.p, c->ray_z.p, c->vid.p,
                             c->lnu.p, c->lam.p, c->T.p, c->mp, c->long_scratch.p, c->long_scratch_per_warp,
                             c->n_warps_long, c->k5_math, ns > 1 ? c->side[si] : c->stream);
         CK_LAUNCH(MRF_K_RAY_MSG, 1);
@@ -1650,6 +1658,7 @@ mrf_status mrf_destroy(mrf_ctx* ctx) {
     c->ray_seg.release(); c->ck.release(); c->lam_chunk.release();
     c->d_k1_frames.release(); c->d_k1_cta0.release();
     c->class_all.release();
+    c->class_desc.release();
     c->class_cnt.release();
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
